@@ -1,0 +1,360 @@
+"""Benchmark: RGS-QR columns/s on BASELINE config 1 (and other configs on request).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1]
+    python bench.py --impl reference ...        # CPU reference arm (oracle port)
+    torchrun --nproc-per-node N bench.py --gpus N   # row-sharded, NCCL all-reduce
+
+A step is one full randomized Gram-Schmidt factorisation of the config's W
+(n x m) already resident in HBM (``value``), or through the public API from
+pinned host memory with the factors copied back (``e2e``).  Rank 0 prints one
+JSON line.  W and Q (2 GB each at c1) exceed the 126 MB L2, so no flush is
+needed between steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def qr_alg_bytes(n, m, bq, bw, k=0, gaussian=False):
+    """n b_Q m(m+1)/2 + 2 n b_W m (+ (m+1) k n 8 for Gaussian)."""
+    b = n * bq * m * (m + 1) / 2 + 2 * n * bw * m
+    if gaussian:
+        b += (m + 1) * k * n * 8
+    return b
+
+
+def update_alg_bytes(n, i, bq, bw):
+    """One sgs_rgs_update launch for column i: read Q[:, :i], read w, write q'_i,
+    write the normalised q_{i-1} (i > 0)."""
+    return n * bq * i + n * bw + n * bq + (n * bq if i > 0 else 0)
+
+
+# ---------------------------------------------------------------------------
+def cpu_sample(cfg, n_cols, threads):
+    """Time the oracle port (the reference's algorithm, reference numerics) on
+    the first n_cols columns of a config-shaped problem."""
+    from threadpoolctl import threadpool_limits
+    from oracle import OracleRgs, OracleSketch
+    from paper_2011_05090_b200.workloads import make_w
+    n, k = cfg["n"], cfg["k"]
+    W = make_w(n, n_cols, cfg["sigma_min"], 0,
+               dtype=np.float32 if cfg["policy"] == "mixed" else np.float64)
+    th = OracleSketch(cfg["kind"], k, n, 0, **({"block_log2": cfg["block_log2"]}
+                                               if "block_log2" in cfg else {}))
+    with threadpool_limits(limits=threads):
+        st = OracleRgs(th, cfg["policy"], cfg["breakdown_factor"], capacity=n_cols)
+        t0 = time.perf_counter()
+        for j in range(n_cols):
+            st.push(W[:, j])
+        dt = time.perf_counter() - t0
+    return n_cols / dt, dt
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args, cfg_name):
+    import torch  # noqa: F401  (keeps the import cost out of the timed region)
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2011_05090_b200.workloads import CONFIGS
+    cfg = CONFIGS[cfg_name]
+    threads = os.cpu_count() or 1
+    ncols = args.cpu_cols
+    vals = []
+    for _ in range(args.warmup):
+        cpu_sample(cfg, max(2, ncols // 4), threads)
+    for _ in range(args.steps):
+        v, _ = cpu_sample(cfg, ncols, threads)
+        vals.append(v)
+    v = statistics.mean(vals)
+    sample = (f"first {ncols} columns of a {cfg_name}-shaped RGS-QR (n={cfg['n']}, k={cfg['k']} "
+              f"{cfg['kind']}, {cfg['policy']}), oracle port of sketchgs, numpy/OpenBLAS")
+    print(json.dumps({
+        "impl": "reference", "metric": "RGS-QR columns/s", "value": v, "unit": "columns/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * ncols / v, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32/f64" if cfg["policy"] == "mixed" else "f64",
+        "data": "synthetic", "config": {"workload": cfg_name, **_cfg_public(cfg)},
+        "cpu_baseline": {"value": v, "unit": "columns/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "columns/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def _cfg_public(cfg):
+    return {k: v for k, v in cfg.items()}
+
+
+# ---------------------------------------------------------------------------
+def run_qr(args, cfg_name):
+    import torch
+    import paper_2011_05090_b200 as sg
+    from paper_2011_05090_b200 import _lib
+    from paper_2011_05090_b200.distributed import init_from_env
+    from paper_2011_05090_b200.workloads import CONFIGS, make_w_device, shard_rows
+
+    comm = init_from_env("nccl")
+    rank = comm.rank if comm else 0
+    world = comm.world if comm else 1
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = CONFIGS[cfg_name]
+    n, m, k = cfg["n"], cfg["m"], cfg["k"]
+    pol = sg.policy_from_name(cfg["policy"])
+    bf = cfg["breakdown_factor"]
+    kw = {"block_log2": cfg["block_log2"]} if "block_log2" in cfg else {}
+    th = sg.make_sketch(sg.SketchKind(cfg["kind"]), k, n, 0, **kw)
+    row0, n_loc = (0, n) if world == 1 else shard_rows(n, world, rank, th.row_align())
+    wdt = torch.float32 if pol.coarse_dtype == np.float32 else torch.float64
+    Wt = make_w_device(n, m, cfg["sigma_min"], 0, wdt, dev, row0=row0, n_local=n_loc)
+    ldw = Wt.shape[1]
+    th.device_data(dev)
+    torch.cuda.synchronize()
+
+    def step():
+        st = sg.RgsState(th, pol, capacity=m + 1, breakdown_factor=bf, comm=comm, row0=row0,
+                         n_local=n_loc)
+        st.factorize_columns(Wt, ldw, m)
+        return st
+
+    def barrier():
+        torch.cuda.synchronize()
+        if comm:
+            torch.distributed.barrier()
+            torch.cuda.synchronize()
+
+    # state allocation is part of a step (RgsState buffers), sync at the end is too
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    lc0 = _lib.launch_count()
+    clocks = Clocks(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    barrier()
+    clk = clocks.stop()
+    launches = _lib.launch_count() - lc0
+    ms = e0.elapsed_time(e1) / args.steps
+    if comm:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t)
+    value = m / (ms / 1e3)
+    bq = 4 if pol.coarse_dtype == np.float32 else 8
+    bw = bq
+    alg = qr_alg_bytes(n, m, bq, bw, k, cfg["kind"] == "gaussian")
+    hbm_gbs = alg / (ms / 1e3) / 1e9
+
+    # ---- roofline of the dominant kernel (sgs_rgs_update), CUDA events per launch
+    peak, peak_kind = _peaks()
+    roof = None
+    if rank == 0:
+        import paper_2011_05090_b200.gram_schmidt as gsm
+        evs = []
+        orig = gsm.RgsState._update
+
+        def timed_update(self, i, w_ptr, w_code, normalize_prev):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            orig(self, i, w_ptr, w_code, normalize_prev)
+            b.record()
+            evs.append((i, a, b))
+
+        gsm.RgsState._update = timed_update
+        try:
+            step()
+        finally:
+            gsm.RgsState._update = orig
+        torch.cuda.synchronize()
+        tot_ms = sum(a.elapsed_time(b) for _, a, b in evs)
+        tot_b = sum(update_alg_bytes(n_loc, i, bq, bw) for i, _, _ in evs)
+        ach = tot_b / (tot_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": None, "kernel": "rgs_update_kernel",
+                "peak_source": peak_kind,
+                "share_of_step": round(tot_ms / ms, 4),
+                "launches": len(evs), "avg_launch_us": round(1e3 * tot_ms / len(evs), 2)}
+
+    # ---- e2e through the public API (pinned host W -> factors on the host)
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        pin = torch.empty((m, n), dtype=wdt, pin_memory=True)
+        pin.copy_(Wt[:, :n])
+        Wh = pin.numpy().T  # (n, m) Fortran-ordered numpy view of pinned memory
+        for _ in range(1):
+            sg.rgs_factorize(Wh, th, pol, with_certificate=False, breakdown_factor=bf)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ne = max(1, min(args.steps, 3))
+        for _ in range(ne):
+            f, _ = sg.rgs_factorize(Wh, th, pol, with_certificate=False, breakdown_factor=bf)
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / ne
+        fb = np.dtype(pol.fine_dtype).itemsize
+        e2e = {"value": m / dt, "unit": "columns/s", "h2d_bytes_per_step": n * m * bq,
+               "d2h_bytes_per_step": n * m * bq + m * m * 8 + 2 * k * m * fb,
+               "ms_per_step": 1e3 * dt}
+        del pin, Wh, f
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        v, dt = cpu_sample(cfg, args.cpu_cols, threads)
+        cpu = {"value": v, "unit": "columns/s", "cores": threads, "kind": "port",
+               "sample": f"first {args.cpu_cols} columns of a {cfg_name}-shaped problem "
+                         f"(n={n}, k={k} {cfg['kind']}, {cfg['policy']}), oracle port, "
+                         f"{dt:.1f} s"}
+    if rank == 0:
+        print(json.dumps({
+            "metric": "RGS-QR columns/s", "value": value, "unit": "columns/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f32 (Q, update) / f64 (sketch, LS)" if cfg["policy"] == "mixed" else "f64",
+            "data": "synthetic (W = G diag(sigma) V^T generated on device, seeded)",
+            "config": {"workload": cfg_name, "n": n, "m": m, "k": k, "sketch": cfg["kind"],
+                       "policy": cfg["policy"], "breakdown_factor": bf,
+                       "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (W, Q >> 126 MB)"},
+            "hbm_gbs_whole_step": round(hbm_gbs, 1),
+            "hbm_frac_whole_step": round(hbm_gbs / peak, 4),
+            "alg_bytes_per_step": alg,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk,
+        }), flush=True)
+    if comm:
+        torch.distributed.destroy_process_group()
+
+
+def run_gmres(args):
+    import torch
+    import paper_2011_05090_b200 as sg
+    from paper_2011_05090_b200 import _lib
+    from paper_2011_05090_b200.workloads import CONFIGS, convdiff3d, rhs_gaussian
+    cfg = CONFIGS["c3"]
+    N = cfg["grid"]
+    rp, ci, va = convdiff3d(N, (cfg["beta"],) * 3)
+    A = sg.SparseMatrix(n=N ** 3, row_ptr=rp, col_idx=ci, values=va)
+    A.device_arrays()
+    b = torch.from_numpy(rhs_gaussian(A.n, 0)).cuda()
+    th = sg.make_sketch(sg.SketchKind.PSRHT, cfg["k"], A.n, 0)
+    th.device_data()
+    out = {}
+    for pname in ("f64", "mixed"):
+        pol = sg.policy_from_name(pname)
+        for _ in range(args.warmup):
+            sg.gmres_restarted(A, b, th, pol, cfg["restart"], cfg["max_iters"], cfg["tol"])
+        torch.cuda.synchronize()
+        lc0 = _lib.launch_count()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        its = 0
+        for _ in range(args.steps):
+            res = sg.gmres_restarted(A, b, th, pol, cfg["restart"], cfg["max_iters"], cfg["tol"])
+            its += res.iterations
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        out[pname] = {"steps_per_s": its / (ms / 1e3), "iterations": res.iterations,
+                      "cycles": res.cycles, "relres": res.final_residual,
+                      "ms_per_solve": ms / args.steps,
+                      "gpu_launches": _lib.launch_count() - lc0}
+    print(json.dumps({"metric": "RGMRES Arnoldi steps/s", "value": out["f64"]["steps_per_s"],
+                      "unit": "steps/s", "n_gpus": 1, "steps": args.steps,
+                      "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+                      "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                      "config": {"workload": "c3", **cfg}, "results": out}), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c1")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-cols", type=int, default=24)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args, args.config if args.config != "c3" else "c1")
+        return
+    if args.config == "c3":
+        run_gmres(args)
+        return
+    run_qr(args, args.config)
+
+
+if __name__ == "__main__":
+    main()

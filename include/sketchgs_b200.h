@@ -1,0 +1,214 @@
+/*
+ * sketchgs_b200.h -- C ABI of the B200 (sm_100a) randomized Gram-Schmidt /
+ * randomized-GMRES hot path.
+ *
+ * Every entry point takes plain device pointers, sizes and a cudaStream_t
+ * passed as `void*`; no torch or numpy types cross this boundary.  All calls
+ * are asynchronous on the given stream and return 0 on success or a negative
+ * SGS_E* code (details in sgs_last_error()).  Numerical outcomes that the
+ * reference reports by raising (BreakdownError, LinAlgError) are recorded in
+ * the device-resident `sgs_status` block and read back by the host at sync
+ * points; once a status code is set every later kernel that is handed the
+ * same block returns immediately, so a host may enqueue ahead.
+ *
+ * The reference (`sketchgs`, pure Python) has no native boundary; each entry
+ * point below replaces the reference function cited next to it
+ * (paths relative to the reference's pkg/src/sketchgs/).
+ *
+ * Layouts (all column-major, "ld" = elements between consecutive columns):
+ *   X, W, Q        n x ncols, ld >= n (ld % 4 == 0 for the vectorised kernels)
+ *   S, P           k x cap  (fine dtype)
+ *   R              cap x cap fp64, upper triangular
+ *   Theta^T        n x ldt fp64 row-major (= Theta column-major), dense kinds
+ *   sign_bits      one bit per local row, bit set = +1 (LSB-first in uint32)
+ *   samples        nblocks x k int32, sorted ascending within each block
+ */
+#ifndef SKETCHGS_B200_H
+#define SKETCHGS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SGS_ABI_VERSION 1
+
+/* dtype codes */
+#define SGS_F32 0
+#define SGS_F64 1
+
+/* return codes */
+#define SGS_OK 0
+#define SGS_EINVAL (-1)
+#define SGS_ECUDA (-2)
+#define SGS_ENOMEM (-3)
+
+/* sgs_status.code values (device-side outcomes) */
+#define SGS_ST_OK 0
+#define SGS_ST_BREAKDOWN 1   /* reference: gram_schmidt.BreakdownError (gram_schmidt.py:323-326) */
+#define SGS_ST_RANK 2        /* reference: np.linalg.LinAlgError (gram_schmidt.py:186-189) */
+#define SGS_ST_CONVERGED 3   /* reference: gmres early exit est <= tol (krylov.py:300-301) */
+#define SGS_ST_NONFINITE 4   /* non-finite sketched norm */
+
+/* Device-resident status block (64 bytes, 8-byte aligned). */
+typedef struct sgs_status {
+  int64_t code;      /* SGS_ST_* */
+  int64_t column;    /* 1-based column the code refers to */
+  int64_t ncols;     /* columns committed to Q/R/S (RgsState.m) */
+  int64_t iters;     /* GMRES iterations completed in this cycle */
+  double r_ii;       /* last diagonal (or offending r_ii on breakdown) */
+  double tol;        /* breakdown tolerance that was compared against */
+  double diag_max;   /* running max |diag R_S| of the sketched-basis QR */
+  double diag_min;   /* running min |diag R_S| */
+} sgs_status;
+
+/* ---- library ------------------------------------------------------------ */
+int sgs_abi_version(void);
+const char* sgs_last_error(void);
+/* number of kernels this library has launched (process-wide counter) */
+uint64_t sgs_launch_count(void);
+int sgs_device_sm_count(int device);
+int sgs_status_init(sgs_status* st, void* stream);
+
+/* ---- sketch operators ----------------------------------------------------
+ * Replaces SketchOperator.apply / apply_block (sketch.py:168-198) and fwht
+ * (sketch.py:90-109).  A P-SRHT of the reference is nblocks=1 with
+ * log2_block = log2(next_pow2(n)); a block-SRHT is nblocks contiguous
+ * 2^log2_block-row blocks each with its own signs/samples.  Partials are
+ * per-CTA unscaled k-vectors: partials[(c*nparts + p)*k + j].  The number of
+ * parts is a pure function of (n_local, log2_block) so every caller that
+ * sketches the same vector gets bit-identical results. */
+int sgs_srht_nparts(int64_t n_local, int log2_block);
+int sgs_srht_partials(const void* X, int x_dtype, int64_t ldx, int ncols,
+                      int64_t n_local, int64_t row0, int log2_block,
+                      const uint32_t* sign_bits, const int32_t* samples, int k,
+                      double* partials, const sgs_status* st, void* stream);
+
+/* Dense sketch (Gaussian / materialised Rademacher, absent from the
+ * reference's SketchKind; duck-typed in through sketch.py:120-206):
+ * partials of Theta^T' X over nparts fixed row chunks. ncols==1 is a GEMV,
+ * ncols>1 a split-K GEMM; both accumulate each chunk in ascending row order,
+ * so apply_block is bit-identical to apply. */
+int sgs_dense_nparts(int64_t n);
+int sgs_dense_partials(const double* thetaT, int64_t ldt, int k,
+                       const void* X, int x_dtype, int64_t ldx, int ncols,
+                       int64_t n, double* partials, const sgs_status* st,
+                       void* stream);
+
+/* Y[:, c] = cast(scale * sum_p partials[c][p][:]) in fixed p order. */
+int sgs_partials_reduce(const double* partials, int nparts, int k, int ncols,
+                        double scale, void* Y, int y_dtype, int64_t ldy,
+                        const sgs_status* st, void* stream);
+
+/* Unnormalised Sylvester FWHT along axis 0 of a power-of-two length vector,
+ * batched over columns (sketch.py:90-109). */
+int sgs_fwht(double* X, int64_t s, int ncols, int64_t ldx, void* stream);
+
+/* ---- RGS column step -----------------------------------------------------
+ * Step 3 of RgsState.push (gram_schmidt.py:316-319):
+ *   Q[:, i] = cast_crs(w) - Q[:, :i] @ r_crs        (coarse arithmetic)
+ * When normalize_prev != 0 column i-1 holds the unnormalised q'_{i-1} and is
+ * first normalised in place, Q[:, i-1] = cast_crs(q'_{i-1} / R[i-1, i-1])
+ * (step 7, gram_schmidt.py:329), inside the same pass.  i == 0 stores
+ * cast_crs(w) (gram_schmidt.py:307-310). */
+int sgs_rgs_update(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
+                   const void* w, int w_dtype, const void* r_crs,
+                   int normalize_prev, const double* R, int64_t ldr,
+                   const sgs_status* st, void* stream);
+
+/* Q[:, col] = cast_crs(Q[:, col] / R[col, col])   (gram_schmidt.py:329) */
+int sgs_normalize_column(void* Q, int q_dtype, int64_t ldq, int64_t n,
+                         int col, const double* R, int64_t ldr,
+                         const sgs_status* st, void* stream);
+
+/* z = A_crs[:, :ncols] @ y in fp64 (A upcast), optionally z *= scale_num/scale_den[0]
+ * (krylov.py:308-310: z = Q[:, :k].astype(f64) @ y; x = (b_norm/alpha) z). */
+int sgs_gemv_f64(const void* A, int a_dtype, int64_t lda, int64_t n, int ncols,
+                 const double* y, double* z, void* stream);
+
+/* ---- sketched least squares (steps 2, 5, 6 and the LS append) ------------
+ * One launch of a thread-block cluster that replicates the k-dimensional
+ * work of RgsState.push (gram_schmidt.py:303-337) on device:
+ *   finalize: s' = scale*sum(partials) (or P[:,0] for column 0), r_ii = ||s'||,
+ *             breakdown guard, S[:, i] = s'/r_ii, R[i,i] = r_ii, and append
+ *             s_i to an incrementally maintained QR of S (orthonormal factor
+ *             Qs, explicit inverse Rinv of R_S), which replaces
+ *             _IncrementalHouseholderQR.append (gram_schmidt.py:148-171).
+ *   solve:    r = argmin ||S[:, :i] r - p|| = Rinv Qs^T p with the reference's
+ *             rank check (gram_schmidt.py:180-190); writes R[:i, col] and the
+ *             coarse copy r_crs used by sgs_rgs_update.
+ * Fine dtype is fp64 (UNIFIED64, MIXED32_64) or fp32 (UNIFIED32). */
+typedef struct sgs_ls_args {
+  int k;                 /* sketch rows */
+  int cap;               /* allocated columns of S/P/Qs/Rinv/R */
+  int fine_dtype;        /* SGS_F32 / SGS_F64 */
+  int coarse_dtype;      /* dtype of r_crs */
+  int do_finalize;       /* finalize + append column `col_fin` */
+  int col_fin;
+  const double* s_partials; int s_nparts; double s_scale;
+  int do_solve;          /* solve for column `col_sol` (uses col_sol columns) */
+  int col_sol;
+  const double* p_partials; int p_nparts; double p_scale; /* NULL: P[:,col_sol] is already stored */
+  double bf_ucrs;        /* breakdown_factor * u_crs */
+  void* S; void* P;      /* k x cap, fine, ld = k */
+  double* R;             /* cap x cap, ld = cap */
+  void* Qs; void* Rinv;  /* k x cap and cap x cap, fine */
+  double* scratch;       /* sgs_ls_scratch_elems(k, cap) doubles */
+  void* r_crs;           /* cap, coarse */
+  sgs_status* st;
+} sgs_ls_args;
+
+int64_t sgs_ls_scratch_elems(int k, int cap);
+int sgs_ls_cluster_size(int k);
+int sgs_ls_step(const sgs_ls_args* a, void* stream);
+
+/* ---- Krylov ---------------------------------------------------------------
+ * SparseMatrix.matvec (krylov.py:81-83) fused with the 1/alpha scaling of
+ * gmres (krylov.py:276): y = (A x) / alpha[0] (alpha == NULL: no scaling).
+ * x is fp64 or a coarse column of Q. CSR with int32 indices, fp64 values. */
+int sgs_csr_spmv(int64_t n, const int32_t* row_ptr, const int32_t* col_idx,
+                 const double* vals, const void* x, int x_dtype,
+                 const double* alpha, double* y, const sgs_status* st,
+                 void* stream);
+
+/* deterministic ||x||_2 (fp64 or fp32 input, fp64 result on device) */
+int sgs_norm2(const void* x, int x_dtype, int64_t n, double* out, double* work,
+              void* stream);
+int64_t sgs_norm2_work_elems(int64_t n);
+/* divide != 0: y = x / den[0];  else y = x * (num / den[0]) (den == NULL: x * num).
+ * fp64; mirrors `v / nw` (krylov.py:224) and `(b_norm / alpha) * z` (krylov.py:309). */
+int sgs_scale(const double* x, double num, const double* den, int divide, double* y,
+              int64_t n, void* stream);
+/* y = b - y (fp64), in place (residual r = b - A x of the restart wrapper) */
+int sgs_rsub(const double* b, double* y, int64_t n, void* stream);
+/* dst = cast(src / den[0]) (den == NULL: plain cast); e.g. push(b / b_norm) */
+int sgs_cast_div(const void* src, int src_dtype, void* dst, int dst_dtype,
+                 const double* den, int64_t n, void* stream);
+/* v[r] = cos(r + 1): start vector of _operator_norm_estimate (krylov.py:218) */
+int sgs_cos_init(double* v, int64_t n, void* stream);
+
+/* Power-iteration step of _operator_norm_estimate (krylov.py:213-226):
+ * given w = A v and ||w|| in nrm[0], sets v = w / ||w|| and sigma[0] = ||w||;
+ * a zero norm freezes sigma at -1 (the reference returns 0.0). */
+int sgs_power_step(const double* w, const double* nrm, double* v,
+                   double* sigma, int64_t n, void* stream);
+
+/* Progressive Givens step of gmres (krylov.py:282-301) on device:
+ * hcol = R[:i+2, i+1] rotated by the previous i rotations (cs/sn), new
+ * rotation, T[:i+2, i] = hcol, g update, est = |g[i+1]|/beta appended to
+ * hist[i]; sets st->code = SGS_ST_CONVERGED when tol > 0 and est <= tol and
+ * advances st->iters. */
+int sgs_givens_step(const double* R, int64_t ldr, int i, double* cs,
+                    double* sn, double* g, double* T, int64_t ldt,
+                    double* hist, double tol, sgs_status* st, void* stream);
+
+/* Column-major transpose for staging host row-major inputs:
+ * dst[c*ldd + r] = src[r*lds + c], r < rows, c < cols. */
+int sgs_transpose(const void* src, int64_t lds, void* dst, int64_t ldd,
+                  int64_t rows, int64_t cols, int dtype, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKETCHGS_B200_H */

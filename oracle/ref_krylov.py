@@ -1,0 +1,130 @@
+"""Oracle RGS-Arnoldi / RGS-GMRES (TEST INFRASTRUCTURE ONLY, see oracle/__init__.py).
+
+Restates reference krylov.py: SparseMatrix.matvec (:81-83, scipy CSR),
+_operator_norm_estimate (:213-226), arnoldi (:176-199), gmres (:229-319,
+unpreconditioned), and the restart wrapper BASELINE config 3 needs
+(identical definition to paper_2011_05090_b200.gmres_restarted).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import scipy.linalg
+import scipy.sparse
+
+from .ref_rgs import OracleBreakdown, OracleRgs
+
+
+def csr_matvec(row_ptr, col_idx, values, n, x):
+    A = scipy.sparse.csr_matrix((values, col_idx, row_ptr), shape=(n, n))
+    return A @ np.asarray(x, dtype=np.float64)
+
+
+def power_norm_estimate(matvec, n: int, iters: int = 20) -> float:
+    v = np.cos(np.arange(n, dtype=np.float64) + 1.0)
+    v /= np.linalg.norm(v)
+    sigma = 1.0
+    for _ in range(iters):
+        w = matvec(v)
+        nw = np.linalg.norm(w)
+        if nw == 0.0:
+            return 0.0
+        sigma = nw
+        v = w / nw
+    return float(sigma)
+
+
+def oracle_arnoldi(matvec, n, b, m, theta, policy="mixed"):
+    st = OracleRgs(theta, policy, capacity=16)
+    st.push(np.asarray(b, dtype=np.float64))
+    broke = False
+    for i in range(m):
+        w = matvec(st.Q[:, i].astype(np.float64))
+        try:
+            st.push(w)
+        except OracleBreakdown:
+            broke = True
+            break
+    R = st.R.copy()
+    return {"Q": st.Q.copy(), "H": R[:, 1:].copy(), "R": R, "beta": float(R[0, 0]),
+            "breakdown": broke}
+
+
+def oracle_gmres(matvec, n, b, m, theta, policy="mixed", tol=None):
+    b = np.asarray(b, dtype=np.float64)
+    b_norm = float(np.linalg.norm(b))
+    if b_norm == 0.0:
+        return {"x": np.zeros(n), "history": np.zeros(0), "final_residual": 0.0,
+                "iterations": 0, "converged": True, "breakdown": False}
+    alpha = power_norm_estimate(matvec, n)
+    if alpha == 0.0:
+        raise np.linalg.LinAlgError("operator norm estimate is zero")
+    st = OracleRgs(theta, policy, capacity=16)
+    st.push(b / b_norm)
+    beta = float(st.R[0, 0])
+    g = np.zeros(m + 1)
+    g[0] = beta
+    T = np.zeros((m + 1, m))
+    cs, sn = np.zeros(m), np.zeros(m)
+    hist, broke, iters = [], False, 0
+    for i in range(m):
+        w = matvec(st.Q[:, i].astype(np.float64)) / alpha
+        try:
+            st.push(w)
+        except OracleBreakdown:
+            broke = True
+            break
+        iters = i + 1
+        h = st.R[:i + 2, i + 1].copy()
+        for j in range(i):
+            t = cs[j] * h[j] + sn[j] * h[j + 1]
+            h[j + 1] = -sn[j] * h[j] + cs[j] * h[j + 1]
+            h[j] = t
+        rr = np.hypot(h[i], h[i + 1])
+        if rr == 0.0:
+            cs[i], sn[i] = 1.0, 0.0
+        else:
+            cs[i], sn[i] = h[i] / rr, h[i + 1] / rr
+        h[i], h[i + 1] = rr, 0.0
+        T[:i + 2, i] = h
+        g[i + 1] = -sn[i] * g[i]
+        g[i] = cs[i] * g[i]
+        est = abs(g[i + 1]) / beta
+        hist.append(est)
+        if tol is not None and est <= tol:
+            break
+    k = iters
+    if k == 0:
+        x = np.zeros(n)
+    else:
+        y = scipy.linalg.solve_triangular(T[:k, :k], g[:k], lower=False)
+        x = (b_norm / alpha) * (st.Q[:, :k].astype(np.float64) @ y)
+    res = float(np.linalg.norm(b - matvec(x)) / b_norm)
+    conv = (res <= max(tol, 0.0)) if tol is not None else False
+    return {"x": x, "history": np.asarray(hist), "final_residual": res, "iterations": k,
+            "converged": conv or broke, "breakdown": broke, "R": st.R.copy(),
+            "Q": st.Q.copy(), "alpha": alpha}
+
+
+def oracle_gmres_restarted(matvec, n, b, theta, policy="mixed", restart=300,
+                           max_iters=3000, tol=1e-8, max_cycles=None):
+    b = np.asarray(b, dtype=np.float64)
+    b_norm = float(np.linalg.norm(b))
+    x = np.zeros(n)
+    r = b.copy()
+    r_norm = b_norm
+    its, cycles = 0, []
+    while not (b_norm == 0.0 or r_norm / b_norm <= tol or its >= max_iters):
+        if max_cycles is not None and len(cycles) >= max_cycles:
+            break
+        out = oracle_gmres(matvec, n, r, min(restart, max_iters - its), theta, policy,
+                           tol=tol * b_norm / r_norm)
+        cycles.append(out["iterations"])
+        its += out["iterations"]
+        x = x + out["x"]
+        r = b - matvec(x)
+        r_norm = float(np.linalg.norm(r))
+        if out["iterations"] == 0:
+            break
+    rel = r_norm / b_norm if b_norm else 0.0
+    return {"x": x, "iterations": its, "cycles": cycles, "final_residual": rel}

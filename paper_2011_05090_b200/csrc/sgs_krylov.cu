@@ -1,0 +1,296 @@
+// RGMRES support kernels on sm_100a: CSR SpMV with the gmres 1/alpha scaling
+// (krylov.py:81-83, :276), deterministic norms, the power-iteration step of
+// _operator_norm_estimate (krylov.py:213-226) and the progressive Givens
+// update (krylov.py:282-301) so the Arnoldi loop never waits on the host.
+
+#include "sgs_common.cuh"
+
+namespace sgs {
+
+std::atomic<uint64_t> g_launches{0};
+
+static thread_local char g_err[512] = {0};
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int sm_count() {
+  static int cached = 0;
+  if (cached == 0) {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached = v > 0 ? v : kMaxSMs;
+  }
+  return cached;
+}
+
+template <typename TX>
+__global__ void __launch_bounds__(256)
+csr_spmv_kernel(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                const double* __restrict__ vals, const TX* __restrict__ x,
+                const double* __restrict__ alpha, double* __restrict__ y, const sgs_status* st) {
+  if (status_stopped(st)) return;
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int b = __ldg(rp + r), e = __ldg(rp + r + 1);
+  double acc = 0.0;
+  for (int q = b; q < e; ++q) acc = fma(__ldg(vals + q), (double)__ldg(x + __ldg(ci + q)), acc);
+  y[r] = alpha ? acc / __ldg(alpha) : acc;
+}
+
+constexpr int kNormBlocks = 296;
+
+template <typename TX>
+__global__ void __launch_bounds__(256)
+norm_partial_kernel(const TX* __restrict__ x, int64_t n, double* __restrict__ work) {
+  __shared__ double red[8];
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t b = per * blockIdx.x, e = min(n, b + per);
+  double acc = 0.0;
+  for (int64_t r = b + threadIdx.x; r < e; r += blockDim.x) {
+    const double v = (double)x[r];
+    acc = fma(v, v, acc);
+  }
+  const double s = block_sum(acc, red);
+  if (threadIdx.x == 0) work[blockIdx.x] = s;
+}
+
+__global__ void norm_final_kernel(const double* __restrict__ work, int nb, double* out) {
+  __shared__ double red[8];
+  double acc = 0.0;
+  for (int q = threadIdx.x; q < nb; q += blockDim.x) acc += work[q];
+  const double s = block_sum(acc, red);
+  if (threadIdx.x == 0) out[0] = sqrt(s);
+}
+
+__global__ void scale_kernel(const double* __restrict__ x, double num, const double* den,
+                             int divide, double* __restrict__ y, int64_t n) {
+  double f;
+  if (divide) f = *den;
+  else f = den ? num / *den : num;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    y[r] = divide ? x[r] / f : f * x[r];
+}
+
+__global__ void rsub_kernel(const double* __restrict__ b, double* __restrict__ y, int64_t n) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    y[r] = b[r] - y[r];
+}
+
+template <typename TS, typename TD>
+__global__ void cast_div_kernel(const TS* __restrict__ x, const double* den, TD* __restrict__ y,
+                                int64_t n) {
+  const double d = den ? *den : 1.0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const double v = den ? (double)x[r] / d : (double)x[r];
+    y[r] = from_double<TD>(v);
+  }
+}
+
+__global__ void power_step_kernel(const double* __restrict__ w, const double* nrm,
+                                  double* __restrict__ v, double* sigma, int64_t n) {
+  const double nw = *nrm;
+  // sigma < 0 marks "frozen": a zero norm was seen, estimate is 0 (krylov.py:220-221)
+  if (*sigma < 0.0) return;
+  if (nw == 0.0) {
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) *sigma = -1.0;
+    return;
+  }
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    v[r] = w[r] / nw;
+}
+
+__global__ void power_commit_kernel(const double* nrm, double* sigma) {
+  if (*sigma < 0.0) return;
+  if (*nrm != 0.0) *sigma = *nrm;
+}
+
+__global__ void cos_init_kernel(double* v, int64_t n) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    v[r] = cos((double)r + 1.0);
+}
+
+// One progressive Givens step. Sequential over the previous rotations (O(i)
+// single-thread work); products and sums are not contracted so the rotation
+// arithmetic matches numpy's scalar expressions.
+__global__ void givens_step_kernel(const double* __restrict__ R, int64_t ldr, int i,
+                                   double* cs, double* sn, double* g, double* T, int64_t ldt,
+                                   double* hist, double tol, sgs_status* st) {
+  if (status_stopped(st)) return;
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double beta = R[0];
+  if (i == 0) g[0] = beta;
+  double* h = T + (int64_t)i * ldt;
+  const double* rc = R + (int64_t)(i + 1) * ldr;
+  for (int j = 0; j < i + 2; ++j) h[j] = rc[j];
+  for (int j = 0; j < i; ++j) {
+    const double t = __dadd_rn(__dmul_rn(cs[j], h[j]), __dmul_rn(sn[j], h[j + 1]));
+    h[j + 1] = __dadd_rn(__dmul_rn(-sn[j], h[j]), __dmul_rn(cs[j], h[j + 1]));
+    h[j] = t;
+  }
+  const double r = hypot(h[i], h[i + 1]);
+  double c, s;
+  if (r == 0.0) { c = 1.0; s = 0.0; }
+  else { c = h[i] / r; s = h[i + 1] / r; }
+  cs[i] = c;
+  sn[i] = s;
+  h[i] = r;
+  h[i + 1] = 0.0;
+  g[i + 1] = __dmul_rn(-s, g[i]);
+  g[i] = __dmul_rn(c, g[i]);
+  const double est = fabs(g[i + 1]) / beta;
+  hist[i] = est;
+  st->iters = i + 1;
+  if (tol >= 0.0 && est <= tol) {
+    st->code = SGS_ST_CONVERGED;
+    st->column = i + 1;
+  }
+}
+
+__global__ void status_init_kernel(sgs_status* st) {
+  st->code = 0;
+  st->column = 0;
+  st->ncols = 0;
+  st->iters = 0;
+  st->r_ii = 0.0;
+  st->tol = 0.0;
+  st->diag_max = 0.0;
+  st->diag_min = 0.0;
+}
+
+static unsigned grid_for(int64_t n, int threads = 256) {
+  int64_t b = (n + threads - 1) / threads;
+  const int64_t cap = (int64_t)sm_count() * 8;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+}  // namespace sgs
+
+using namespace sgs;
+
+extern "C" int sgs_abi_version(void) { return SGS_ABI_VERSION; }
+extern "C" const char* sgs_last_error(void) { return g_err; }
+extern "C" uint64_t sgs_launch_count(void) { return g_launches.load(); }
+
+extern "C" int sgs_device_sm_count(int device) {
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
+    set_error("cudaDeviceGetAttribute failed");
+    return SGS_ECUDA;
+  }
+  return v;
+}
+
+extern "C" int sgs_status_init(sgs_status* st, void* stream) {
+  SGS_REQUIRE(st, "status_init: null");
+  status_init_kernel<<<1, 1, 0, as_stream(stream)>>>(st);
+  return check_launch("status_init_kernel");
+}
+
+extern "C" int sgs_csr_spmv(int64_t n, const int32_t* row_ptr, const int32_t* col_idx,
+                            const double* vals, const void* x, int x_dtype, const double* alpha,
+                            double* y, const sgs_status* st, void* stream) {
+  SGS_REQUIRE(n >= 1 && row_ptr && col_idx && vals && x && y, "spmv: bad args");
+  cudaStream_t s = as_stream(stream);
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  if (x_dtype == SGS_F32)
+    csr_spmv_kernel<float><<<blocks, 256, 0, s>>>(n, row_ptr, col_idx, vals,
+                                                  static_cast<const float*>(x), alpha, y, st);
+  else
+    csr_spmv_kernel<double><<<blocks, 256, 0, s>>>(n, row_ptr, col_idx, vals,
+                                                   static_cast<const double*>(x), alpha, y, st);
+  return check_launch("csr_spmv_kernel");
+}
+
+extern "C" int64_t sgs_norm2_work_elems(int64_t n) { (void)n; return kNormBlocks; }
+
+extern "C" int sgs_norm2(const void* x, int x_dtype, int64_t n, double* out, double* work,
+                         void* stream) {
+  SGS_REQUIRE(x && out && work && n >= 0, "norm2: bad args");
+  cudaStream_t s = as_stream(stream);
+  const int nb = kNormBlocks;
+  if (x_dtype == SGS_F32)
+    norm_partial_kernel<float><<<nb, 256, 0, s>>>(static_cast<const float*>(x), n, work);
+  else
+    norm_partial_kernel<double><<<nb, 256, 0, s>>>(static_cast<const double*>(x), n, work);
+  int rc = check_launch("norm_partial_kernel");
+  if (rc) return rc;
+  norm_final_kernel<<<1, 256, 0, s>>>(work, nb, out);
+  return check_launch("norm_final_kernel");
+}
+
+extern "C" int sgs_scale(const double* x, double num, const double* den, int divide, double* y,
+                         int64_t n, void* stream) {
+  SGS_REQUIRE(x && y && n >= 0 && (!divide || den), "scale: bad args");
+  if (n == 0) return SGS_OK;
+  scale_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(x, num, den, divide, y, n);
+  return check_launch("scale_kernel");
+}
+
+extern "C" int sgs_rsub(const double* b, double* y, int64_t n, void* stream) {
+  SGS_REQUIRE(b && y && n >= 0, "rsub: bad args");
+  if (n == 0) return SGS_OK;
+  rsub_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(b, y, n);
+  return check_launch("rsub_kernel");
+}
+
+extern "C" int sgs_cast_div(const void* src, int src_dtype, void* dst, int dst_dtype,
+                            const double* den, int64_t n, void* stream) {
+  SGS_REQUIRE(src && dst && n >= 0, "cast_div: bad args");
+  if (n == 0) return SGS_OK;
+  cudaStream_t s = as_stream(stream);
+  const unsigned g = grid_for(n);
+  if (src_dtype == SGS_F64 && dst_dtype == SGS_F64)
+    cast_div_kernel<double, double><<<g, 256, 0, s>>>(static_cast<const double*>(src), den,
+                                                       static_cast<double*>(dst), n);
+  else if (src_dtype == SGS_F64 && dst_dtype == SGS_F32)
+    cast_div_kernel<double, float><<<g, 256, 0, s>>>(static_cast<const double*>(src), den,
+                                                      static_cast<float*>(dst), n);
+  else if (src_dtype == SGS_F32 && dst_dtype == SGS_F64)
+    cast_div_kernel<float, double><<<g, 256, 0, s>>>(static_cast<const float*>(src), den,
+                                                      static_cast<double*>(dst), n);
+  else
+    cast_div_kernel<float, float><<<g, 256, 0, s>>>(static_cast<const float*>(src), den,
+                                                     static_cast<float*>(dst), n);
+  return check_launch("cast_div_kernel");
+}
+
+extern "C" int sgs_cos_init(double* v, int64_t n, void* stream) {
+  SGS_REQUIRE(v && n >= 0, "cos_init: bad args");
+  if (n == 0) return SGS_OK;
+  cos_init_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(v, n);
+  return check_launch("cos_init_kernel");
+}
+
+extern "C" int sgs_power_step(const double* w, const double* nrm, double* v, double* sigma,
+                              int64_t n, void* stream) {
+  SGS_REQUIRE(w && nrm && v && sigma && n >= 1, "power_step: bad args");
+  cudaStream_t s = as_stream(stream);
+  power_commit_kernel<<<1, 1, 0, s>>>(nrm, sigma);
+  int rc = check_launch("power_commit_kernel");
+  if (rc) return rc;
+  power_step_kernel<<<grid_for(n), 256, 0, s>>>(w, nrm, v, sigma, n);
+  return check_launch("power_step_kernel");
+}
+
+extern "C" int sgs_givens_step(const double* R, int64_t ldr, int i, double* cs, double* sn,
+                               double* g, double* T, int64_t ldt, double* hist, double tol,
+                               sgs_status* st, void* stream) {
+  SGS_REQUIRE(R && cs && sn && g && T && hist && st && i >= 0 && ldr >= i + 2 && ldt >= i + 2,
+              "givens: bad args");
+  givens_step_kernel<<<1, 32, 0, as_stream(stream)>>>(R, ldr, i, cs, sn, g, T, ldt, hist, tol, st);
+  return check_launch("givens_step_kernel");
+}

@@ -1,0 +1,499 @@
+// Sketch operators Theta x on sm_100a.
+//
+// P-SRHT / block-SRHT (reference: SketchOperator.apply, sketch.py:168-184,
+// fwht sketch.py:90-109).  The reference pads d∘x to s = 2^L, runs a full
+// Sylvester FWHT and keeps k sampled rows.  Here the Hadamard matrix is
+// factorised by bits, H_s = H_{s/T} (x) H_T with T = 2^LOGT the tile size
+// (high bits outer), so sampled row r = (r_h, r_l) of H_s (d∘x) equals
+//     sum_h (-1)^{popcount(r_h & h)} * FWHT_T(tile_h)[r_l].
+// Each CTA transforms its tiles in shared memory (radix-8 register passes),
+// gathers only the k sampled low-bit rows, applies the high-bit sign and
+// accumulates into a per-CTA k-vector in shared memory.  One partial per CTA
+// is written; a fixed-order reduction produces y.  Padding tiles are never
+// read.  Deterministic for a fixed (n_local, log2_block).
+
+#include "sgs_common.cuh"
+
+namespace sgs {
+
+// padded shared-memory index: one spare slot per 8 doubles keeps the
+// radix-8 passes free of bank conflicts beyond the inherent 2 wavefronts.
+__device__ __forceinline__ int pidx(int e) { return e + (e >> 3); }
+
+template <int NB>
+__device__ __forceinline__ void fwht_reg(double* v) {
+  // in-register Sylvester FWHT of 2^NB values (same butterfly as fwht()).
+#pragma unroll
+  for (int h = 1; h < (1 << NB); h <<= 1) {
+#pragma unroll
+    for (int q = 0; q < (1 << NB); ++q) {
+      if ((q & h) == 0) {
+        double a = v[q], b = v[q + h];
+        v[q] = a + b;
+        v[q + h] = a - b;
+      }
+    }
+  }
+}
+
+// One radix-2^NB pass over bits [b0, b0+NB) of a 2^LOGT tile in smem.
+template <int LOGT, int NB>
+__device__ __forceinline__ void fwht_pass(double* z, int b0) {
+  constexpr int T = 1 << LOGT;
+  constexpr int G = T >> NB;
+  for (int grp = threadIdx.x; grp < G; grp += blockDim.x) {
+    const int lo = grp & ((1 << b0) - 1);
+    const int base = lo | ((grp >> b0) << (b0 + NB));
+    double v[1 << NB];
+#pragma unroll
+    for (int q = 0; q < (1 << NB); ++q) v[q] = z[pidx(base + (q << b0))];
+    fwht_reg<NB>(v);
+#pragma unroll
+    for (int q = 0; q < (1 << NB); ++q) z[pidx(base + (q << b0))] = v[q];
+  }
+}
+
+template <int LOGT>
+__device__ __forceinline__ void fwht_tile(double* z) {
+  // passes of 3 bits from the top down (any bit order gives the transform)
+  int b0 = LOGT;
+#pragma unroll
+  for (int p = 0; p < (LOGT + 2) / 3; ++p) {
+    const int nb = (b0 >= 3) ? 3 : b0;
+    b0 -= nb;
+    if (nb == 3) fwht_pass<LOGT, 3>(z, b0);
+    else if (nb == 2) fwht_pass<LOGT, 2>(z, b0);
+    else fwht_pass<LOGT, 1>(z, b0);
+    __syncthreads();
+  }
+}
+
+template <typename TX>
+__device__ __forceinline__ double load_as_double(const TX* p) { return (double)__ldg(p); }
+
+constexpr int kSrhtThreads = 512;
+constexpr int kSrhtMaxLogT = 12;  // 4096-row tiles (32 KB of fp64)
+constexpr int kSrhtTargetCTAs = 148;
+
+template <typename TX, int LOGT>
+__global__ void __launch_bounds__(kSrhtThreads)
+srht_partials_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local,
+                     int64_t row0, int log2_block, const uint32_t* __restrict__ sign_bits,
+                     const int32_t* __restrict__ samples, int k, int tiles_per_cta,
+                     int64_t ntiles, double* __restrict__ partials,
+                     const sgs_status* st) {
+  if (status_stopped(st)) return;
+  constexpr int T = 1 << LOGT;
+  extern __shared__ double smem[];
+  double* z = smem;                       // pidx(T) entries
+  double* part = smem + pidx(T) + 8;      // k entries
+  const int col = blockIdx.y;
+  const int nparts = gridDim.x;
+  const TX* x = X + (int64_t)col * ldx;
+
+  for (int j = threadIdx.x; j < k; j += blockDim.x) part[j] = 0.0;
+
+  const int64_t t0 = (int64_t)blockIdx.x * tiles_per_cta;
+  const int64_t t1 = min(t0 + tiles_per_cta, ntiles);
+  const int64_t bmask = (int64_t(1) << log2_block) - 1;
+  for (int64_t t = t0; t < t1; ++t) {
+    const int64_t lr0 = t * T;            // first local row of the tile
+    const int64_t g0 = row0 + lr0;        // first global row
+    const int64_t blk = g0 >> log2_block;
+    const int64_t h = (g0 & bmask) >> LOGT;
+    __syncthreads();                      // previous tile's gather is done
+    for (int e = threadIdx.x; e < T; e += blockDim.x) {
+      const int64_t lr = lr0 + e;
+      double v = 0.0;
+      if (lr < n_local) {
+        v = load_as_double(x + lr);
+        const uint32_t word = __ldg(sign_bits + (lr >> 5));
+        if (((word >> (lr & 31)) & 1u) == 0u) v = -v;
+      }
+      z[pidx(e)] = v;
+    }
+    __syncthreads();
+    fwht_tile<LOGT>(z);
+    const int32_t* smp = samples + blk * (int64_t)k;
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+      const int32_t r = __ldg(smp + j);
+      const double v = z[pidx(r & (T - 1))];
+      const int64_t rh = (int64_t)(r >> LOGT);
+      part[j] += (__popcll(rh & h) & 1) ? -v : v;
+    }
+  }
+  __syncthreads();
+  double* out = partials + ((int64_t)col * nparts + blockIdx.x) * k;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) out[j] = part[j];
+}
+
+static void srht_geometry(int64_t n_local, int log2_block, int* logt, int64_t* ntiles,
+                          int* tpc, int* nparts) {
+  const int lt = log2_block < kSrhtMaxLogT ? log2_block : kSrhtMaxLogT;
+  const int64_t T = int64_t(1) << lt;
+  const int64_t nt = (n_local + T - 1) / T;
+  const int64_t per = (nt + kSrhtTargetCTAs - 1) / kSrhtTargetCTAs;
+  *logt = lt;
+  *ntiles = nt;
+  *tpc = (int)(per < 1 ? 1 : per);
+  *nparts = (int)((nt + *tpc - 1) / *tpc);
+}
+
+template <typename TX, int LOGT>
+static int launch_srht_t(const void* X, int64_t ldx, int ncols, int64_t n_local, int64_t row0,
+                         int log2_block, const uint32_t* sign_bits, const int32_t* samples,
+                         int k, double* partials, const sgs_status* st, cudaStream_t s,
+                         int tpc, int64_t ntiles, int nparts) {
+  constexpr int T = 1 << LOGT;
+  const size_t smem = (size_t)(T + T / 8 + 8 + k) * sizeof(double);
+  auto kern = srht_partials_kernel<TX, LOGT>;
+  if (smem > 48 * 1024) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  int threads = kSrhtThreads;
+  if (T / 8 < threads) threads = (T / 8 < 32) ? 32 : T / 8;
+  if (threads < 128 && k > 1024) threads = 128;
+  dim3 grid(nparts, ncols);
+  kern<<<grid, threads, smem, s>>>(static_cast<const TX*>(X), ldx, n_local, row0, log2_block,
+                                  sign_bits, samples, k, tpc, ntiles, partials, st);
+  return check_launch("srht_partials_kernel");
+}
+
+template <typename TX>
+static int launch_srht(int logt, const void* X, int64_t ldx, int ncols, int64_t n_local,
+                       int64_t row0, int log2_block, const uint32_t* sign_bits,
+                       const int32_t* samples, int k, double* partials, const sgs_status* st,
+                       cudaStream_t s, int tpc, int64_t ntiles, int nparts) {
+#define SGS_SRHT_CASE(L)                                                                   \
+  case L:                                                                                  \
+    return launch_srht_t<TX, L>(X, ldx, ncols, n_local, row0, log2_block, sign_bits,       \
+                                samples, k, partials, st, s, tpc, ntiles, nparts);
+  switch (logt) {
+    SGS_SRHT_CASE(0) SGS_SRHT_CASE(1) SGS_SRHT_CASE(2) SGS_SRHT_CASE(3) SGS_SRHT_CASE(4)
+    SGS_SRHT_CASE(5) SGS_SRHT_CASE(6) SGS_SRHT_CASE(7) SGS_SRHT_CASE(8) SGS_SRHT_CASE(9)
+    SGS_SRHT_CASE(10) SGS_SRHT_CASE(11) SGS_SRHT_CASE(12)
+    default:
+      set_error("srht: unsupported tile log %d", logt);
+      return SGS_EINVAL;
+  }
+#undef SGS_SRHT_CASE
+}
+
+// ---------------------------------------------------------------------------
+// Dense sketch: partials[c][p][j] = sum_{r in chunk p, ascending} ThetaT[r][j] * X[r][c]
+// with the chunking a pure function of n.  GEMV for one column, split-K GEMM
+// for several; identical per-output FMA chains make apply_block == apply.
+
+constexpr int kDenseMaxParts = 296;
+
+static int dense_nparts_host(int64_t n) {
+  int64_t p = (n + 31) / 32;
+  if (p > kDenseMaxParts) p = kDenseMaxParts;
+  if (p < 1) p = 1;
+  return (int)p;
+}
+
+__device__ __forceinline__ int64_t chunk_begin(int64_t n, int nparts, int p) {
+  return (n * p) / nparts;
+}
+
+template <typename TX, int QP>
+__global__ void __launch_bounds__(512)
+dense_gemv_kernel(const double* __restrict__ thetaT, int64_t ldt, int k,
+                  const TX* __restrict__ x, int64_t n, double* __restrict__ partials,
+                  const sgs_status* st) {
+  if (status_stopped(st)) return;
+  const int p = blockIdx.x, nparts = gridDim.x;
+  const int64_t r0 = chunk_begin(n, nparts, p), r1 = chunk_begin(n, nparts, p + 1);
+  const int kp = (k + 1) >> 1;  // column pairs (ldt even, zero padded)
+  double2 acc[QP];
+#pragma unroll
+  for (int q = 0; q < QP; ++q) acc[q] = make_double2(0.0, 0.0);
+  int64_t r = r0;
+  for (; r + 4 <= r1; r += 4) {
+    double xv[4];
+    double2 tv[4][QP];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      xv[u] = (double)__ldg(x + r + u);
+#pragma unroll
+      for (int q = 0; q < QP; ++q) {
+        const int jj = threadIdx.x + q * blockDim.x;
+        tv[u][q] = jj < kp ? __ldg(reinterpret_cast<const double2*>(thetaT + (r + u) * ldt) + jj)
+                           : make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+#pragma unroll
+      for (int q = 0; q < QP; ++q) {
+        acc[q].x = fma(tv[u][q].x, xv[u], acc[q].x);
+        acc[q].y = fma(tv[u][q].y, xv[u], acc[q].y);
+      }
+    }
+  }
+  for (; r < r1; ++r) {
+    const double xv = (double)__ldg(x + r);
+#pragma unroll
+    for (int q = 0; q < QP; ++q) {
+      const int jj = threadIdx.x + q * blockDim.x;
+      if (jj < kp) {
+        const double2 tv = __ldg(reinterpret_cast<const double2*>(thetaT + r * ldt) + jj);
+        acc[q].x = fma(tv.x, xv, acc[q].x);
+        acc[q].y = fma(tv.y, xv, acc[q].y);
+      }
+    }
+  }
+  double* out = partials + (int64_t)p * k;
+#pragma unroll
+  for (int q = 0; q < QP; ++q) {
+    const int jj = threadIdx.x + q * blockDim.x;
+    if (2 * jj < k) out[2 * jj] = acc[q].x;
+    if (2 * jj + 1 < k) out[2 * jj + 1] = acc[q].y;
+  }
+}
+
+// split-K GEMM tile: 64 sketch rows (j) x 32 columns (c), 16 data rows per stage.
+constexpr int kGBJ = 64, kGBC = 32, kGBR = 16;
+
+template <typename TX>
+__global__ void __launch_bounds__(256)
+dense_gemm_kernel(const double* __restrict__ thetaT, int64_t ldt, int k,
+                  const TX* __restrict__ X, int64_t ldx, int ncols, int64_t n,
+                  double* __restrict__ partials, const sgs_status* st) {
+  if (status_stopped(st)) return;
+  __shared__ double As[kGBR][kGBJ];
+  __shared__ double Bs[kGBR][kGBC + 1];
+  const int jt = blockIdx.x * kGBJ, ct = blockIdx.y * kGBC;
+  const int p = blockIdx.z, nparts = gridDim.z;
+  const int64_t r0 = chunk_begin(n, nparts, p), r1 = chunk_begin(n, nparts, p + 1);
+  const int tj = (threadIdx.x & 15) * 4;  // 4 sketch rows
+  const int tc = (threadIdx.x >> 4) * 2;  // 2 columns
+  double acc[4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) acc[a][0] = acc[a][1] = 0.0;
+  for (int64_t rs = r0; rs < r1; rs += kGBR) {
+    const int nrow = (int)min((int64_t)kGBR, r1 - rs);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kGBR * kGBJ; e += blockDim.x) {
+      const int rr = e / kGBJ, jj = e % kGBJ;
+      As[rr][jj] = (rr < nrow && jt + jj < k) ? __ldg(thetaT + (rs + rr) * ldt + jt + jj) : 0.0;
+    }
+    for (int e = threadIdx.x; e < kGBR * kGBC; e += blockDim.x) {
+      const int cc = e / kGBR, rr = e % kGBR;
+      Bs[rr][cc] = (rr < nrow && ct + cc < ncols)
+                       ? (double)__ldg(X + (int64_t)(ct + cc) * ldx + rs + rr) : 0.0;
+    }
+    __syncthreads();
+    for (int rr = 0; rr < nrow; ++rr) {  // ascending rows: same chain as the GEMV
+      double a[4], b[2];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) a[q] = As[rr][tj + q];
+      b[0] = Bs[rr][tc];
+      b[1] = Bs[rr][tc + 1];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        acc[q][0] = fma(a[q], b[0], acc[q][0]);
+        acc[q][1] = fma(a[q], b[1], acc[q][1]);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int j = jt + tj + q, c = ct + tc + u;
+      if (j < k && c < ncols) partials[((int64_t)c * nparts + p) * k + j] = acc[q][u];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <typename TY>
+__global__ void partials_reduce_kernel(const double* __restrict__ partials, int nparts, int k,
+                                       int ncols, double scale, TY* __restrict__ Y, int64_t ldy,
+                                       const sgs_status* st) {
+  if (status_stopped(st)) return;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)k * ncols) return;
+  const int c = (int)(idx / k), j = (int)(idx % k);
+  const double* p = partials + (int64_t)c * nparts * k + j;
+  double acc = 0.0;
+  for (int q = 0; q < nparts; ++q) acc += __ldg(p + (int64_t)q * k);
+  Y[(int64_t)c * ldy + j] = from_double<TY>(scale * acc);
+}
+
+// ---------------------------------------------------------------------------
+// Stand-alone FWHT (API parity with fwht(), sketch.py:90-109): tiles of up to
+// 4096 in shared memory, then radix-2 global passes over the remaining bits.
+template <int LOGT>
+__global__ void fwht_tile_kernel(double* X, int64_t ldx) {
+  constexpr int T = 1 << LOGT;
+  extern __shared__ double z[];
+  double* x = X + (int64_t)blockIdx.y * ldx + (int64_t)blockIdx.x * T;
+  for (int e = threadIdx.x; e < T; e += blockDim.x) z[pidx(e)] = x[e];
+  __syncthreads();
+  fwht_tile<LOGT>(z);
+  for (int e = threadIdx.x; e < T; e += blockDim.x) x[e] = z[pidx(e)];
+}
+
+__global__ void fwht_global_pass(double* X, int64_t ldx, int64_t s, int64_t h) {
+  double* x = X + (int64_t)blockIdx.y * ldx;
+  const int64_t half = s >> 1;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < half;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lo = t & (h - 1);
+    const int64_t i = ((t - lo) << 1) + lo;
+    const double a = x[i], b = x[i + h];
+    x[i] = a + b;
+    x[i + h] = a - b;
+  }
+}
+
+template <int LOGT>
+static int launch_fwht_tile(double* X, int64_t ldx, int64_t ntile, int ncols, cudaStream_t s) {
+  constexpr int T = 1 << LOGT;
+  const size_t smem = (size_t)(T + T / 8 + 8) * sizeof(double);
+  auto kern = fwht_tile_kernel<LOGT>;
+  int threads = T / 8 < 32 ? 32 : (T / 8 > 512 ? 512 : T / 8);
+  kern<<<dim3((unsigned)ntile, ncols), threads, smem, s>>>(X, ldx);
+  return check_launch("fwht_tile_kernel");
+}
+
+}  // namespace sgs
+
+using namespace sgs;
+
+extern "C" int sgs_srht_nparts(int64_t n_local, int log2_block) {
+  int lt, tpc, np;
+  int64_t nt;
+  if (n_local < 1 || log2_block < 0 || log2_block > 40) return 0;
+  srht_geometry(n_local, log2_block, &lt, &nt, &tpc, &np);
+  return np;
+}
+
+extern "C" int sgs_srht_partials(const void* X, int x_dtype, int64_t ldx, int ncols,
+                                 int64_t n_local, int64_t row0, int log2_block,
+                                 const uint32_t* sign_bits, const int32_t* samples, int k,
+                                 double* partials, const sgs_status* st, void* stream) {
+  SGS_REQUIRE(X && sign_bits && samples && partials, "srht: null pointer");
+  SGS_REQUIRE(n_local >= 1 && ncols >= 1 && k >= 1 && k <= 8192, "srht: bad sizes n=%lld k=%d",
+              (long long)n_local, k);
+  SGS_REQUIRE(log2_block >= 0 && log2_block <= 40, "srht: bad log2_block %d", log2_block);
+  SGS_REQUIRE(x_dtype == SGS_F32 || x_dtype == SGS_F64, "srht: bad dtype");
+  int lt, tpc, np;
+  int64_t nt;
+  srht_geometry(n_local, log2_block, &lt, &nt, &tpc, &np);
+  SGS_REQUIRE((row0 & ((int64_t(1) << lt) - 1)) == 0, "srht: row0 %lld not tile aligned",
+              (long long)row0);
+  cudaStream_t s = as_stream(stream);
+  if (x_dtype == SGS_F32)
+    return launch_srht<float>(lt, X, ldx, ncols, n_local, row0, log2_block, sign_bits, samples,
+                              k, partials, st, s, tpc, nt, np);
+  return launch_srht<double>(lt, X, ldx, ncols, n_local, row0, log2_block, sign_bits, samples,
+                             k, partials, st, s, tpc, nt, np);
+}
+
+extern "C" int sgs_dense_nparts(int64_t n) { return n < 1 ? 0 : dense_nparts_host(n); }
+
+template <typename TX>
+static int launch_dense(const double* thetaT, int64_t ldt, int k, const void* X, int64_t ldx,
+                        int ncols, int64_t n, double* partials, const sgs_status* st,
+                        cudaStream_t s) {
+  const int np = dense_nparts_host(n);
+  const TX* x = static_cast<const TX*>(X);
+  if (ncols == 1) {
+    const int kp = (k + 1) / 2;
+    int threads = ((kp + 31) / 32) * 32;
+    if (threads > 512) threads = 512;
+    const int qp = (kp + threads - 1) / threads;
+    if (qp <= 1)
+      dense_gemv_kernel<TX, 1><<<np, threads, 0, s>>>(thetaT, ldt, k, x, n, partials, st);
+    else if (qp <= 2)
+      dense_gemv_kernel<TX, 2><<<np, threads, 0, s>>>(thetaT, ldt, k, x, n, partials, st);
+    else if (qp <= 4)
+      dense_gemv_kernel<TX, 4><<<np, threads, 0, s>>>(thetaT, ldt, k, x, n, partials, st);
+    else if (qp <= 8)
+      dense_gemv_kernel<TX, 8><<<np, threads, 0, s>>>(thetaT, ldt, k, x, n, partials, st);
+    else {
+      set_error("dense sketch: k=%d too large", k);
+      return SGS_EINVAL;
+    }
+    return check_launch("dense_gemv_kernel");
+  }
+  dim3 grid((k + kGBJ - 1) / kGBJ, (ncols + kGBC - 1) / kGBC, np);
+  dense_gemm_kernel<TX><<<grid, 256, 0, s>>>(thetaT, ldt, k, x, ldx, ncols, n, partials, st);
+  return check_launch("dense_gemm_kernel");
+}
+
+extern "C" int sgs_dense_partials(const double* thetaT, int64_t ldt, int k, const void* X,
+                                  int x_dtype, int64_t ldx, int ncols, int64_t n,
+                                  double* partials, const sgs_status* st, void* stream) {
+  SGS_REQUIRE(thetaT && X && partials, "dense: null pointer");
+  SGS_REQUIRE(k >= 1 && n >= 1 && ncols >= 1, "dense: bad sizes");
+  SGS_REQUIRE(ldt >= k && (ldt % 2) == 0, "dense: ldt must be even and >= k");
+  SGS_REQUIRE(((uintptr_t)thetaT & 15) == 0, "dense: thetaT must be 16-byte aligned");
+  SGS_REQUIRE(x_dtype == SGS_F32 || x_dtype == SGS_F64, "dense: bad dtype");
+  cudaStream_t s = as_stream(stream);
+  if (x_dtype == SGS_F32) return launch_dense<float>(thetaT, ldt, k, X, ldx, ncols, n, partials, st, s);
+  return launch_dense<double>(thetaT, ldt, k, X, ldx, ncols, n, partials, st, s);
+}
+
+extern "C" int sgs_partials_reduce(const double* partials, int nparts, int k, int ncols,
+                                   double scale, void* Y, int y_dtype, int64_t ldy,
+                                   const sgs_status* st, void* stream) {
+  SGS_REQUIRE(partials && Y && nparts >= 1 && k >= 1 && ncols >= 1, "reduce: bad args");
+  SGS_REQUIRE(ldy >= k, "reduce: ldy < k");
+  cudaStream_t s = as_stream(stream);
+  const int64_t tot = (int64_t)k * ncols;
+  const int threads = 256;
+  const unsigned blocks = (unsigned)((tot + threads - 1) / threads);
+  if (y_dtype == SGS_F64)
+    partials_reduce_kernel<double><<<blocks, threads, 0, s>>>(partials, nparts, k, ncols, scale,
+                                                              static_cast<double*>(Y), ldy, st);
+  else if (y_dtype == SGS_F32)
+    partials_reduce_kernel<float><<<blocks, threads, 0, s>>>(partials, nparts, k, ncols, scale,
+                                                             static_cast<float*>(Y), ldy, st);
+  else {
+    set_error("reduce: bad dtype");
+    return SGS_EINVAL;
+  }
+  return check_launch("partials_reduce_kernel");
+}
+
+extern "C" int sgs_fwht(double* X, int64_t s_len, int ncols, int64_t ldx, void* stream) {
+  SGS_REQUIRE(X && s_len >= 1 && ncols >= 1 && ldx >= s_len, "fwht: bad args");
+  SGS_REQUIRE((s_len & (s_len - 1)) == 0, "fwht: length %lld is not a power of two",
+              (long long)s_len);
+  cudaStream_t s = as_stream(stream);
+  int L = 0;
+  while ((int64_t(1) << L) < s_len) ++L;
+  const int lt = L < kSrhtMaxLogT ? L : kSrhtMaxLogT;
+  const int64_t ntile = s_len >> lt;
+  int rc;
+  switch (lt) {
+    case 0: return SGS_OK;  // length-1 transform is the identity
+    case 1: rc = launch_fwht_tile<1>(X, ldx, ntile, ncols, s); break;
+    case 2: rc = launch_fwht_tile<2>(X, ldx, ntile, ncols, s); break;
+    case 3: rc = launch_fwht_tile<3>(X, ldx, ntile, ncols, s); break;
+    case 4: rc = launch_fwht_tile<4>(X, ldx, ntile, ncols, s); break;
+    case 5: rc = launch_fwht_tile<5>(X, ldx, ntile, ncols, s); break;
+    case 6: rc = launch_fwht_tile<6>(X, ldx, ntile, ncols, s); break;
+    case 7: rc = launch_fwht_tile<7>(X, ldx, ntile, ncols, s); break;
+    case 8: rc = launch_fwht_tile<8>(X, ldx, ntile, ncols, s); break;
+    case 9: rc = launch_fwht_tile<9>(X, ldx, ntile, ncols, s); break;
+    case 10: rc = launch_fwht_tile<10>(X, ldx, ntile, ncols, s); break;
+    case 11: rc = launch_fwht_tile<11>(X, ldx, ntile, ncols, s); break;
+    default: rc = launch_fwht_tile<12>(X, ldx, ntile, ncols, s); break;
+  }
+  if (rc) return rc;
+  for (int b = lt; b < L; ++b) {
+    const int64_t half = s_len >> 1;
+    int64_t blocks = (half + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    fwht_global_pass<<<dim3((unsigned)blocks, ncols), 256, 0, s>>>(X, ldx, s_len, int64_t(1) << b);
+    rc = check_launch("fwht_global_pass");
+    if (rc) return rc;
+  }
+  return SGS_OK;
+}

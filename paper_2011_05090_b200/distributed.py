@@ -1,0 +1,44 @@
+"""Row sharding of the RGS state across the GPUs of one node.
+
+The paper's distributed RGS (section 2.4, not implemented by the
+reference) partitions the tall dimension n into row blocks; the
+seeded sketch is applied blockwise with no communication, and each sketch of
+a column needs one global sum of a k-vector.  Here each rank owns a
+contiguous, tile-aligned row range (``workloads.shard_rows``), sketches its
+rows into per-CTA partials, sums them locally and all-reduces the k-vector
+over NCCL (NVLink/NVSwitch); the k-dimensional least-squares work is then
+replicated bit-identically on every rank, so no broadcast is needed.
+"""
+
+from __future__ import annotations
+
+import os
+
+import torch
+import torch.distributed as dist
+
+
+class TorchComm:
+    """All-reduce hook used by ``RgsState(comm=...)``: sum in place."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def allreduce_(self, t: torch.Tensor) -> None:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
+
+def init_from_env(backend: str = "nccl") -> TorchComm | None:
+    """Initialise the default process group from torchrun's environment
+    (RANK / WORLD_SIZE / LOCAL_RANK / MASTER_*); None when WORLD_SIZE <= 1."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world <= 1:
+        return None
+    if not dist.is_initialized():
+        if backend == "nccl":
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend=backend)
+    return TorchComm()

@@ -1,0 +1,500 @@
+"""Randomized Gram-Schmidt on the B200: ``RgsState`` / ``rgs_factorize``.
+
+Interface mirror of the reference's ``gram_schmidt.py`` (RgsState
+``:228-347``, rgs_factorize ``:350-375``, certificates ``:474-487``,
+BreakdownError ``:35-43``).  Per column the device runs, on torch's current
+stream and without host synchronisation:
+
+1. ``sgs_ls_step`` (solve): r = argmin ||S_{i-1} r - p_i|| (step 2),
+2. ``sgs_rgs_update``: q'_i = w_i - Q_{i-1} r in the coarse format (step 3),
+   normalising q'_{i-1} in the same pass in batch mode,
+3. the sketch partials of q'_i (step 4),
+4. ``sgs_ls_step`` (finalize): r_ii, breakdown guard, S, R, LS append
+   (steps 5-7).
+
+In ``rgs_factorize`` the sketches P = Theta W of all columns are computed up
+front in batched launches (bit-identical to per-column sketches), and the
+solve for column i+1 is fused into the finalize launch of column i, so a
+column costs three kernel launches.  Breakdown and rank deficiency are
+recorded on the device and raised at the next synchronisation with the
+reference's exception types and column numbers.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from enum import Enum
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call, stream_ptr
+from .precision import MIXED32_64, UNIFIED64, PrecisionPolicy
+from .sketch import SketchOperator, as_device_sketch
+
+__all__ = [
+    "GsVariant", "LsqSolver", "HOUSEHOLDER_QR", "QrFactors", "StabilityCertificate",
+    "BreakdownError", "RgsState", "rgs_factorize", "certificates", "loss_of_orthogonality",
+    "BREAKDOWN_FACTOR",
+]
+
+BREAKDOWN_FACTOR = 10.0
+
+
+class BreakdownError(RuntimeError):
+    """Vanishing projection residual at a given (1-based) column index."""
+
+    def __init__(self, column: int, r_ii: float, tol: float):
+        super().__init__(f"breakdown at column {column}: r_ii={r_ii:.3e} <= tol={tol:.3e}")
+        self.column = column
+        self.r_ii = r_ii
+        self.tol = tol
+
+
+class GsVariant(Enum):
+    CGS = "cgs"
+    MGS = "mgs"
+    CGS2 = "cgs2"
+    RGS = "rgs"
+
+
+@dataclass(frozen=True)
+class LsqSolver:
+    """Sketched least-squares solver selection (reference gram_schmidt.py:53-77).
+
+    The device implements the direct QR-based solver ("householder" in the
+    reference); the iterative alternatives are outside the B200 hot path."""
+
+    method: str = "householder"
+    iterations: int = 4
+
+    def __post_init__(self):
+        if self.method not in ("householder", "richardson", "smgs"):
+            raise ValueError(f"unknown least-squares method {self.method!r}")
+        if self.method == "richardson" and self.iterations < 1:
+            raise ValueError("richardson needs at least one iteration")
+
+
+HOUSEHOLDER_QR = LsqSolver("householder")
+
+
+@dataclass
+class QrFactors:
+    """Q (n x m), upper-triangular R (m x m), sketches S = Theta Q, P = Theta W.
+
+    numpy arrays by default; CUDA tensors when requested with ``device=True``."""
+
+    Q: object
+    R: object
+    S: object = None
+    P: object = None
+    S_phi: object = None
+    P_phi: object = None
+
+
+@dataclass
+class StabilityCertificate:
+    delta_m: float
+    delta_tilde_m: float
+    cond_S: float
+    omega: float | None = None
+    omega_bar: float | None = None
+    omega_bar_w: float | None = None
+    omega_bar_margin: float | None = None
+    omega_bar_w_margin: float | None = None
+    margin_precondition_ok: bool | None = None
+    omega_bar_halved: float | None = None
+
+    def passes_gate(self) -> bool:
+        return self.delta_m <= 0.1 and self.delta_tilde_m <= 0.1
+
+    def sigma_enclosure(self, eps: float, u_crs: float) -> tuple[float, float]:
+        lo = (1.0 + eps) ** -0.5 * (1.0 - self.delta_m - 0.1 * u_crs)
+        hi = (1.0 - eps) ** -0.5 * (1.0 + self.delta_m + 0.1 * u_crs)
+        return lo, hi
+
+
+def _round_up(x: int, a: int) -> int:
+    return (x + a - 1) // a * a
+
+
+class RgsState:
+    """Device-resident streaming state of the randomized factorizer.
+
+    ``push(w)`` runs one column and returns r_ii (it synchronises to do so, as
+    the reference returns a float).  ``Q``, ``R``, ``S``, ``P`` return host
+    copies trimmed to the committed columns; ``device_factors()`` returns the
+    CUDA tensors.  Device layout: Q is column-major (column j contiguous,
+    leading dimension a multiple of 32 rows), R column-major cap x cap fp64,
+    S/P column-major k x cap in the fine dtype.
+
+    ``comm`` (optional) row-shards the state: this rank holds rows
+    [row0, row0 + n_local) of W and Q, the sketch partials of the shard are
+    summed locally and combined with one all-reduce of the k-vector per
+    sketch; the k-dimensional work is then replicated bit-identically on all
+    ranks (no broadcast).
+    """
+
+    def __init__(self, theta, policy: PrecisionPolicy = MIXED32_64,
+                 solver: LsqSolver = HOUSEHOLDER_QR, phi=None, capacity: int = 16,
+                 breakdown_factor: float = BREAKDOWN_FACTOR, *, comm=None,
+                 row0: int = 0, n_local: int | None = None):
+        _lib.require_cuda()
+        if solver.method != "householder":
+            raise NotImplementedError("the device factorizer implements the direct "
+                                      "QR least-squares solver only (HOUSEHOLDER_QR)")
+        if phi is not None:
+            raise NotImplementedError("certification sketches (phi) are not on the "
+                                      "device hot path")
+        self.theta = as_device_sketch(theta)
+        self.policy = policy
+        self.solver = solver
+        self.phi = None
+        self.breakdown_factor = float(breakdown_factor)
+        self.comm = comm
+        self.n = self.theta.n
+        self.k = self.theta.k
+        self.row0 = int(row0)
+        self.n_local = self.n if n_local is None else int(n_local)
+        if comm is None and (self.row0 != 0 or self.n_local != self.n):
+            raise ValueError("row sharding needs a communicator")
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.cdt = _lib.torch_dtype(policy.coarse_dtype)
+        self.fdt = _lib.torch_dtype(policy.fine_dtype)
+        self.ccode = _lib.dtype_code(self.cdt)
+        self.fcode = _lib.dtype_code(self.fdt)
+        self.ldq = _round_up(self.n_local, 32)
+        self.m = 0
+        self.status = _lib.Status(self.device)
+        self.nparts = self.theta.nparts(self.n_local)
+        self._cap = 0
+        self._alloc(max(int(capacity), 2))
+        self._parts_s = torch.empty((self.nparts, self.k), dtype=torch.float64, device=self.device)
+        self._parts_p = torch.empty_like(self._parts_s)
+        if comm is not None:
+            self._kvec_s = torch.empty(self.k, dtype=torch.float64, device=self.device)
+            self._kvec_p = torch.empty_like(self._kvec_s)
+        self._theta_dev = self.theta.device_data(self.device)
+
+    # ---- storage ----------------------------------------------------------------
+    def _alloc(self, cap: int) -> None:
+        dev, k = self.device, self.k
+        old = None
+        if self._cap:
+            old = (self._Q, self._R, self._S, self._P, self._Qs, self._Rinv, self._cap)
+        self._Q = torch.zeros((cap, self.ldq), dtype=self.cdt, device=dev)
+        self._R = torch.zeros((cap, cap), dtype=torch.float64, device=dev)
+        self._S = torch.zeros((cap, k), dtype=self.fdt, device=dev)
+        self._P = torch.zeros((cap, k), dtype=self.fdt, device=dev)
+        self._Qs = torch.zeros((cap, k), dtype=self.fdt, device=dev)
+        self._Rinv = torch.zeros((cap, cap), dtype=self.fdt, device=dev)
+        self._scratch = torch.zeros(int(_lib.load().sgs_ls_scratch_elems(k, cap)),
+                                    dtype=torch.float64, device=dev)
+        self._rc = torch.zeros(cap, dtype=self.cdt, device=dev)
+        if old is not None:
+            Q, R, S, P, Qs, Rinv, oc = old
+            self._Q[:oc] = Q
+            self._R[:oc, :oc] = R
+            self._S[:oc] = S
+            self._P[:oc] = P
+            self._Qs[:oc] = Qs
+            self._Rinv[:oc, :oc] = Rinv
+        self._cap = cap
+
+    def _grow(self) -> None:
+        if self.m + 1 >= self._cap:
+            self._alloc(2 * self._cap)
+
+    # ---- kernels ---------------------------------------------------------------
+    def _ls(self, *, fin: int | None = None, s_parts=None, s_nparts=0, s_scale=1.0,
+            sol: int | None = None, p_parts=None, p_nparts=0, p_scale=1.0) -> None:
+        a = _lib.LsArgs()
+        a.k, a.cap, a.fine_dtype, a.coarse_dtype = self.k, self._cap, self.fcode, self.ccode
+        a.do_finalize = 1 if fin is not None else 0
+        a.col_fin = fin if fin is not None else 0
+        a.s_partials = s_parts
+        a.s_nparts = s_nparts
+        a.s_scale = s_scale
+        a.do_solve = 1 if sol is not None else 0
+        a.col_sol = sol if sol is not None else 0
+        a.p_partials = p_parts
+        a.p_nparts = p_nparts
+        a.p_scale = p_scale
+        a.bf_ucrs = self.breakdown_factor * self.policy.u_crs
+        a.S, a.P, a.R = self._S.data_ptr(), self._P.data_ptr(), self._R.data_ptr()
+        a.Qs, a.Rinv = self._Qs.data_ptr(), self._Rinv.data_ptr()
+        a.scratch, a.r_crs, a.st = self._scratch.data_ptr(), self._rc.data_ptr(), self.status.ptr
+        _lib.check(_lib.load().sgs_ls_step(ctypes_byref(a), stream_ptr()), "sgs_ls_step")
+
+    def _sketch_parts(self, x_ptr: int, x_code: int, ldx: int, out: torch.Tensor,
+                      kvec: torch.Tensor | None):
+        """Partials of one local column; sharded: reduce + all-reduce to a k-vector.
+        Returns (pointer, nparts, scale) for sgs_ls_step."""
+        self.theta.partials_into(x_ptr, x_code, ldx, 1, out, n_local=self.n_local,
+                                 row0=self.row0, status=self.status)
+        if self.comm is None:
+            return out.data_ptr(), self.nparts, self.theta.scale
+        call("sgs_partials_reduce", out.data_ptr(), self.nparts, self.k, 1, 1.0,
+             kvec.data_ptr(), _lib.SGS_F64, self.k, self.status.ptr, stream_ptr())
+        self.comm.allreduce_(kvec)
+        return kvec.data_ptr(), 1, self.theta.scale
+
+    def _update(self, i: int, w_ptr: int, w_code: int, normalize_prev: bool) -> None:
+        call("sgs_rgs_update", self._Q.data_ptr(), self.ccode, self.ldq, self.n_local, i,
+             w_ptr, w_code, self._rc.data_ptr(), 1 if normalize_prev else 0,
+             self._R.data_ptr(), self._cap, self.status.ptr, stream_ptr())
+
+    def _normalize(self, col: int, guarded: bool = True) -> None:
+        call("sgs_normalize_column", self._Q.data_ptr(), self.ccode, self.ldq, self.n_local,
+             col, self._R.data_ptr(), self._cap, self.status.ptr if guarded else None,
+             stream_ptr())
+
+    def _qcol_ptr(self, j: int) -> int:
+        return self._Q.data_ptr() + j * self.ldq * self._Q.element_size()
+
+    def _raise_status(self, st: dict) -> None:
+        code = st["code"]
+        if code in (_lib.ST_BREAKDOWN, _lib.ST_NONFINITE):
+            raise BreakdownError(st["column"], st["r_ii"], st["tol"])
+        if code == _lib.ST_RANK:
+            raise np.linalg.LinAlgError("sketched basis numerically rank deficient")
+
+    # ---- streaming API -----------------------------------------------------------
+    def _as_device_column(self, w) -> torch.Tensor:
+        if isinstance(w, torch.Tensor) and w.is_cuda:
+            t = w
+            if t.dtype not in (torch.float32, torch.float64):
+                t = t.to(torch.float64)
+        else:
+            t = torch.from_numpy(np.ascontiguousarray(np.asarray(w, dtype=np.float64)))
+            t = t.to(self.device)
+        if tuple(t.shape) != (self.n_local,):
+            raise ValueError("column length mismatch")
+        return t.contiguous()
+
+    def _push_async(self, w: torch.Tensor) -> None:
+        """Enqueue one column (column-at-a-time path, no host sync)."""
+        self._grow()
+        i = self.m
+        wc = _lib.dtype_code(w.dtype)
+        pp, pn, ps = self._sketch_parts(w.data_ptr(), wc, self.n_local, self._parts_p,
+                                        getattr(self, "_kvec_p", None))
+        if i == 0:
+            call("sgs_partials_reduce", pp, pn, self.k, 1, ps, self._P.data_ptr(), self.fcode,
+                 self.k, self.status.ptr, stream_ptr())
+            self._update(0, w.data_ptr(), wc, False)
+            self._ls(fin=0)
+        else:
+            self._ls(sol=i, p_parts=pp, p_nparts=pn, p_scale=ps)
+            self._update(i, w.data_ptr(), wc, False)
+            sp, sn, ss = self._sketch_parts(self._qcol_ptr(i), self.ccode, self.ldq,
+                                            self._parts_s, getattr(self, "_kvec_s", None))
+            self._ls(fin=i, s_parts=sp, s_nparts=sn, s_scale=ss)
+        self._normalize(i)
+        self.m += 1  # provisional; reconciled with the device count at sync
+
+    def _sync_status(self) -> dict:
+        st = self.status.read()
+        self.m = st["ncols"]
+        return st
+
+    def push(self, w) -> float:
+        """Run one iteration on the next column; returns the diagonal r_ii."""
+        st = self.status.read()
+        if st["code"]:
+            self.status.clear_code()
+        t = self._as_device_column(w)
+        self._push_async(t)
+        st = self._sync_status()
+        if st["code"]:
+            self.status.clear_code()
+            self._raise_status(st)
+        return st["r_ii"]
+
+    # ---- views -------------------------------------------------------------------
+    def device_factors(self) -> QrFactors:
+        m = self.m
+        return QrFactors(Q=self._Q[:m, :self.n_local].t(), R=self._R[:m, :m].t(),
+                         S=self._S[:m].t(), P=self._P[:m].t())
+
+    @property
+    def Q(self):
+        return self._Q[:self.m, :self.n_local].t().cpu().numpy()
+
+    @property
+    def R(self):
+        return self._R[:self.m, :self.m].t().cpu().numpy()
+
+    @property
+    def S(self):
+        return self._S[:self.m].t().cpu().numpy()
+
+    @property
+    def P(self):
+        return self._P[:self.m].t().cpu().numpy()
+
+    def factors(self, device: bool = False) -> QrFactors:
+        if device:
+            f = self.device_factors()
+            return QrFactors(Q=f.Q.clone(), R=f.R.clone(), S=f.S.clone(), P=f.P.clone())
+        return QrFactors(Q=self.Q, R=self.R, S=self.S, P=self.P)
+
+    # ---- batch path ----------------------------------------------------------------
+    def factorize_columns(self, Wcm: torch.Tensor, ldw: int, m: int) -> None:
+        """Factorise m columns of a device column-major W (column j at
+        offset j*ldw) with three launches per column; raises at the end on a
+        device-recorded breakdown / rank deficiency."""
+        if self.m != 0:
+            raise RuntimeError("factorize_columns needs a fresh state")
+        while self._cap < m + 1:
+            self._alloc(2 * self._cap)
+        wc = _lib.dtype_code(Wcm.dtype)
+        esz = Wcm.element_size()
+        base = Wcm.data_ptr()
+        k, sp = self.k, stream_ptr()
+        # P = Theta W, batched in column chunks (same kernel and parts as per column)
+        chunk = max(1, min(m, (256 << 20) // max(1, self.nparts * k * 8)))
+        parts = torch.empty((chunk, self.nparts, k), dtype=torch.float64, device=self.device)
+        if self.comm is not None:
+            kbuf = torch.empty((chunk, k), dtype=torch.float64, device=self.device)
+        for c0 in range(0, m, chunk):
+            nc = min(chunk, m - c0)
+            self.theta.partials_into(base + c0 * ldw * esz, wc, ldw, nc, parts,
+                                     n_local=self.n_local, row0=self.row0, status=self.status)
+            pdst = self._P.data_ptr() + c0 * k * self._P.element_size()
+            if self.comm is None:
+                call("sgs_partials_reduce", parts.data_ptr(), self.nparts, k, nc,
+                     self.theta.scale, pdst, self.fcode, k, self.status.ptr, sp)
+            else:
+                call("sgs_partials_reduce", parts.data_ptr(), self.nparts, k, nc, 1.0,
+                     kbuf.data_ptr(), _lib.SGS_F64, k, self.status.ptr, sp)
+                self.comm.allreduce_(kbuf[:nc])
+                call("sgs_partials_reduce", kbuf.data_ptr(), 1, k, nc, self.theta.scale,
+                     pdst, self.fcode, k, self.status.ptr, sp)
+        del parts
+        kvec = getattr(self, "_kvec_s", None)
+        for i in range(m):
+            self._update(i, base + i * ldw * esz, wc, i > 0)
+            sol = i + 1 if i + 1 < m else None
+            if i == 0:
+                self._ls(fin=0, sol=sol)
+            else:
+                spp, snp, ssc = self._sketch_parts(self._qcol_ptr(i), self.ccode, self.ldq,
+                                                   self._parts_s, kvec)
+                self._ls(fin=i, s_parts=spp, s_nparts=snp, s_scale=ssc, sol=sol)
+        self._normalize(m - 1)
+        st = self._sync_status()
+        if st["code"]:
+            self._raise_status(st)
+
+
+def ctypes_byref(a):
+    import ctypes
+    return ctypes.byref(a)
+
+
+def _device_columns(W, device) -> tuple[torch.Tensor, int]:
+    """Column-major device copy (or view) of an n x m W: returns (tensor whose
+    column j starts at j*ld, ld)."""
+    if isinstance(W, torch.Tensor) and W.is_cuda:
+        n, m = W.shape
+        if W.dtype not in (torch.float32, torch.float64):
+            W = W.to(torch.float64)
+        if W.stride(0) == 1 and W.stride(1) >= n and W.stride(1) % 4 == 0:
+            return W, W.stride(1)
+        Wt = torch.empty((m, _round_up(n, 4)), dtype=W.dtype, device=W.device)
+        Wt[:, :n] = W.t()
+        return Wt.t()[:n], Wt.stride(0)
+    Wn = np.asarray(W)
+    if Wn.dtype not in (np.float32, np.float64):
+        Wn = Wn.astype(np.float64)
+    n, m = Wn.shape
+    ld = _round_up(n, 4)
+    dt = _lib.torch_dtype(Wn.dtype)
+    Wt = torch.empty((m, ld), dtype=dt, device=device)
+    if Wn.flags.f_contiguous:
+        Wt[:, :n].copy_(torch.from_numpy(Wn.T))
+    else:
+        tmp = torch.from_numpy(np.ascontiguousarray(Wn)).to(device)
+        call("sgs_transpose", tmp.data_ptr(), m, Wt.data_ptr(), ld, n, m,
+             _lib.dtype_code(dt), stream_ptr())
+        del tmp
+    return Wt, ld
+
+
+def rgs_factorize(W, theta, policy: PrecisionPolicy = MIXED32_64,
+                  solver: LsqSolver = HOUSEHOLDER_QR, with_certificate: bool = True,
+                  phi=None, breakdown_factor: float = BREAKDOWN_FACTOR, *,
+                  device_factors: bool = False, comm=None, row0: int = 0):
+    """Randomized Gram-Schmidt QR of the columns of W on the GPU.
+
+    Returns (QrFactors, StabilityCertificate or None) like the reference
+    (gram_schmidt.py:350-375).  W may be an n x m numpy array, a CUDA tensor
+    (column-major views are used in place), or an iterable of columns
+    (streamed through ``RgsState.push``).  ``device_factors=True`` keeps the
+    factors on the GPU as CUDA tensors.  With ``comm`` W holds this rank's
+    rows [row0, row0 + n_local) of a row-sharded matrix.
+    """
+    theta = as_device_sketch(theta)
+    if isinstance(W, (np.ndarray, torch.Tensor)):
+        if W.ndim != 2:
+            raise ValueError("W must be a matrix")
+        n_loc, m = W.shape
+        n = theta.n if comm is not None else n_loc
+        if not (theta.k >= m and n >= m >= 1):
+            raise ValueError(f"need k >= m and n >= m >= 1, got "
+                             f"k={theta.k}, n={n}, m={m}")
+        if comm is None and n_loc != theta.n:
+            raise ValueError("column length mismatch")
+        state = RgsState(theta, policy, solver, phi=phi, capacity=m + 1,
+                         breakdown_factor=breakdown_factor, comm=comm, row0=row0,
+                         n_local=n_loc)
+        Wd, ld = _device_columns(W, state.device)
+        state.factorize_columns(Wd, ld, m)
+    else:
+        state = RgsState(theta, policy, solver, phi=phi, breakdown_factor=breakdown_factor)
+        for w in W:
+            state.push(w)
+    factors = state.factors(device=device_factors)
+    cert = certificates(factors) if with_certificate else None
+    return factors, cert
+
+
+def certificates(factors: QrFactors) -> StabilityCertificate:
+    """Delta_m, Delta~_m and cond(S) in binary64 (gram_schmidt.py:474-487)."""
+    if factors.S is None or factors.P is None:
+        raise ValueError("certificates need the sketches S and P (randomized factors)")
+    if isinstance(factors.S, torch.Tensor):
+        S = factors.S.to(torch.float64)
+        P = factors.P.to(torch.float64)
+        R = factors.R.to(torch.float64)
+        m = S.shape[1]
+        eye = torch.eye(m, dtype=torch.float64, device=S.device)
+        delta_m = float(torch.linalg.norm(eye - S.t() @ S))
+        delta_tilde = float(torch.linalg.norm(P - S @ R) / torch.linalg.norm(P))
+        sv = torch.linalg.svdvals(S)
+        cond_s = float(sv[0] / sv[-1]) if float(sv[-1]) > 0 else math.inf
+        return StabilityCertificate(delta_m, delta_tilde, cond_s)
+    S = np.asarray(factors.S, dtype=np.float64)
+    P = np.asarray(factors.P, dtype=np.float64)
+    R = np.asarray(factors.R)
+    m = S.shape[1]
+    delta_m = float(np.linalg.norm(np.eye(m) - S.T @ S))
+    delta_tilde = float(np.linalg.norm(P - S @ R) / np.linalg.norm(P))
+    sv = np.linalg.svd(S, compute_uv=False)
+    cond_s = float(sv[0] / sv[-1]) if sv[-1] > 0 else np.inf
+    return StabilityCertificate(delta_m=delta_m, delta_tilde_m=delta_tilde, cond_S=cond_s)
+
+
+def loss_of_orthogonality(Q) -> float:
+    """||I - Q^T Q||_F in binary64 (gram_schmidt.py:490-494)."""
+    if isinstance(Q, torch.Tensor):
+        Qd = Q.to(torch.float64)
+        m = Qd.shape[1]
+        return float(torch.linalg.norm(torch.eye(m, dtype=torch.float64, device=Qd.device)
+                                       - Qd.t() @ Qd))
+    Qn = np.asarray(Q, dtype=np.float64)
+    m = Qn.shape[1]
+    return float(np.linalg.norm(np.eye(m) - Qn.T @ Qn))

@@ -1,0 +1,365 @@
+"""Randomized GMRES on the B200 (reference ``krylov.py``: SparseMatrix
+``:28-83``, arnoldi ``:176-199``, gmres ``:229-319``).
+
+The Arnoldi step is the device RGS column step fed by a CSR SpMV kernel.
+The whole step - SpMV (with the 1/alpha scaling), sketch of w, sketched
+least-squares solve, projection update, sketch of q', finalize/append,
+normalisation and the progressive Givens rotation - is enqueued on one
+stream without host synchronisation; the host polls the device status block
+(convergence / lucky breakdown) every few steps and the kernels enqueued
+past a stop return immediately.  The final (k x k) triangular solve for y
+runs on the host, x = (||b|| / alpha) Q y on the device.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.linalg
+import scipy.sparse
+import torch
+
+from . import _lib
+from ._lib import call, stream_ptr
+from .gram_schmidt import (BREAKDOWN_FACTOR, HOUSEHOLDER_QR, GsVariant, LsqSolver, QrFactors,
+                           RgsState)
+from .precision import MIXED32_64, PrecisionPolicy
+
+__all__ = ["SparseMatrix", "arnoldi", "gmres", "gmres_restarted", "ArnoldiDecomposition",
+           "GmresResult", "RestartedResult"]
+
+_POLL = 8  # Arnoldi steps between status polls
+
+
+@dataclass
+class SparseMatrix:
+    """Square CSR matrix with explicit index arrays (krylov.py:28-83)."""
+
+    n: int
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+    symmetric_expansion_applied: bool = False
+
+    @classmethod
+    def from_coo(cls, n: int, rows, cols, vals, symmetric: bool = False) -> "SparseMatrix":
+        rows = np.asarray(rows, dtype=np.int64)
+        cols = np.asarray(cols, dtype=np.int64)
+        vals = np.asarray(vals, dtype=np.float64)
+        if not (rows.shape == cols.shape == vals.shape):
+            raise ValueError("coordinate arrays have mismatched lengths")
+        if rows.size and (rows.min() < 0 or rows.max() >= n or cols.min() < 0 or cols.max() >= n):
+            raise ValueError("coordinate index out of range")
+        if symmetric:
+            off = rows != cols
+            rows, cols, vals = (np.concatenate([rows, cols[off]]),
+                                np.concatenate([cols, rows[off]]),
+                                np.concatenate([vals, vals[off]]))
+        m = scipy.sparse.coo_matrix((vals, (rows, cols)), shape=(n, n)).tocsr()
+        m.sum_duplicates()
+        return cls(n=n, row_ptr=m.indptr.copy(), col_idx=m.indices.copy(),
+                   values=m.data.astype(np.float64), symmetric_expansion_applied=symmetric)
+
+    @classmethod
+    def from_scipy(cls, m) -> "SparseMatrix":
+        m = scipy.sparse.csr_matrix(m)
+        if m.shape[0] != m.shape[1]:
+            raise ValueError("matrix must be square")
+        m.sum_duplicates()
+        return cls(n=m.shape[0], row_ptr=m.indptr.copy(), col_idx=m.indices.copy(),
+                   values=m.data.astype(np.float64))
+
+    def to_scipy(self) -> scipy.sparse.csr_matrix:
+        return scipy.sparse.csr_matrix((self.values, self.col_idx, self.row_ptr),
+                                       shape=(self.n, self.n))
+
+    # ---- device ------------------------------------------------------------------
+    def device_arrays(self, device=None) -> tuple:
+        _lib.require_cuda()
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None \
+            else torch.device(device)
+        cache = self.__dict__.setdefault("_dev_cache", {})
+        d = cache.get(str(dev))
+        if d is None:
+            if int(self.row_ptr[-1]) >= 2**31:
+                raise ValueError("nnz exceeds int32 CSR indexing")
+            d = (torch.from_numpy(np.asarray(self.row_ptr, dtype=np.int32)).to(dev),
+                 torch.from_numpy(np.asarray(self.col_idx, dtype=np.int32)).to(dev),
+                 torch.from_numpy(np.asarray(self.values, dtype=np.float64)).to(dev))
+            cache[str(dev)] = d
+        return d
+
+    def spmv_into(self, x_ptr: int, x_code: int, y: torch.Tensor, alpha=None, status=None):
+        rp, ci, va = self.device_arrays(y.device)
+        call("sgs_csr_spmv", self.n, rp.data_ptr(), ci.data_ptr(), va.data_ptr(), x_ptr, x_code,
+             alpha.data_ptr() if alpha is not None else None, y.data_ptr(),
+             status.ptr if status is not None else None, stream_ptr())
+
+    def matvec(self, x):
+        """A @ x in binary64 (numpy in -> numpy out; CUDA tensor in -> CUDA out)."""
+        if isinstance(x, torch.Tensor) and x.is_cuda:
+            xd = x if x.dtype in (torch.float32, torch.float64) else x.to(torch.float64)
+            xd = xd.contiguous()
+            y = torch.empty(self.n, dtype=torch.float64, device=x.device)
+            self.spmv_into(xd.data_ptr(), _lib.dtype_code(xd.dtype), y)
+            return y
+        xn = np.asarray(x, dtype=np.float64)
+        _lib.require_cuda()
+        xd = torch.from_numpy(np.ascontiguousarray(xn)).cuda()
+        y = torch.empty(self.n, dtype=torch.float64, device=xd.device)
+        self.spmv_into(xd.data_ptr(), _lib.SGS_F64, y)
+        return y.cpu().numpy()
+
+    def __post_init__(self):
+        self.__dict__.setdefault("_dev_cache", {})
+
+
+@dataclass
+class ArnoldiDecomposition:
+    Q: np.ndarray
+    H: np.ndarray
+    R: np.ndarray
+    beta: float
+    breakdown: bool = False
+
+
+@dataclass
+class GmresResult:
+    x: object
+    residual_history: np.ndarray
+    final_residual: float
+    iterations: int
+    converged: bool
+    breakdown: bool
+    factors: QrFactors | None = None
+
+
+def _check_variant(variant, preconditioner=None, phi=None):
+    if variant is not GsVariant.RGS and getattr(variant, "value", None) != "rgs":
+        raise NotImplementedError("the device Krylov path implements the randomized "
+                                  "Gram-Schmidt variant (GsVariant.RGS)")
+    if preconditioner is not None:
+        raise NotImplementedError("preconditioned GMRES is outside the device hot path")
+    if phi is not None:
+        raise NotImplementedError("certification sketches (phi) are not on the device path")
+
+
+def _to_device_f64(b, n: int, device) -> torch.Tensor:
+    if isinstance(b, torch.Tensor) and b.is_cuda:
+        t = b.to(torch.float64).contiguous()
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(b, dtype=np.float64))).to(device)
+    if tuple(t.shape) != (n,):
+        raise ValueError("right-hand side length mismatch")
+    return t
+
+
+class _Workspace:
+    def __init__(self, n: int, device):
+        self.w = torch.empty(n, dtype=torch.float64, device=device)
+        self.v = torch.empty(n, dtype=torch.float64, device=device)
+        self.nrm = torch.zeros(4, dtype=torch.float64, device=device)
+        self.work = torch.empty(int(_lib.load().sgs_norm2_work_elems(n)), dtype=torch.float64,
+                                device=device)
+
+    def norm(self, x: torch.Tensor, out_slot: int = 0) -> None:
+        call("sgs_norm2", x.data_ptr(), _lib.dtype_code(x.dtype), x.numel(),
+             self.nrm[out_slot:].data_ptr(), self.work.data_ptr(), stream_ptr())
+
+
+def _operator_norm_estimate(A: SparseMatrix, ws: _Workspace, iters: int = 20) -> torch.Tensor:
+    """Device power iteration (krylov.py:213-226); returns a 1-element device
+    tensor (-1 when the reference would return 0.0)."""
+    n = A.n
+    sigma = torch.ones(1, dtype=torch.float64, device=ws.v.device)
+    call("sgs_cos_init", ws.v.data_ptr(), n, stream_ptr())
+    ws.norm(ws.v, 0)
+    call("sgs_scale", ws.v.data_ptr(), 1.0, ws.nrm.data_ptr(), 1, ws.v.data_ptr(), n, stream_ptr())
+    for _ in range(iters):
+        A.spmv_into(ws.v.data_ptr(), _lib.SGS_F64, ws.w)
+        ws.norm(ws.w, 1)
+        call("sgs_power_step", ws.w.data_ptr(), ws.nrm[1:].data_ptr(), ws.v.data_ptr(),
+             sigma.data_ptr(), n, stream_ptr())
+    return sigma
+
+
+class _ArnoldiEngine:
+    """Device Arnoldi driver over an RgsState (one stream, no per-step sync)."""
+
+    def __init__(self, A: SparseMatrix, theta, policy, solver, m: int,
+                 breakdown_factor: float = BREAKDOWN_FACTOR):
+        self.A = A
+        self.m = m
+        self.state = RgsState(theta, policy, solver, capacity=m + 2,
+                              breakdown_factor=breakdown_factor)
+        if self.state.n != A.n:
+            raise ValueError("sketch ambient dimension does not match the operator")
+        dev = self.state.device
+        self.ws = _Workspace(A.n, dev)
+        self.cs = torch.zeros(m + 1, dtype=torch.float64, device=dev)
+        self.sn = torch.zeros_like(self.cs)
+        self.g = torch.zeros(m + 2, dtype=torch.float64, device=dev)
+        self.T = torch.zeros((m + 1, m + 2), dtype=torch.float64, device=dev)  # T[i] = column i
+        self.hist = torch.zeros(m + 1, dtype=torch.float64, device=dev)
+
+    def step(self, i: int, alpha: torch.Tensor | None, tol: float | None) -> None:
+        st = self.state
+        A, ws = self.A, self.ws
+        # w = A q_i (/ alpha)
+        A.spmv_into(st._qcol_ptr(i), st.ccode, ws.w, alpha=alpha, status=st.status)
+        st._push_async(ws.w)
+        if tol is not None or alpha is not None:
+            call("sgs_givens_step", st._R.data_ptr(), st._cap, i, self.cs.data_ptr(),
+                 self.sn.data_ptr(), self.g.data_ptr(), self.T.data_ptr(), self.T.shape[1],
+                 self.hist.data_ptr(), -1.0 if tol is None else float(tol), st.status.ptr,
+                 stream_ptr())
+
+    def run(self, alpha, tol) -> dict:
+        """Steps 0..m-1 with periodic status polls; returns the final status."""
+        st = self.state
+        pending = []
+        for i in range(self.m):
+            self.step(i, alpha, tol)
+            if (i + 1) % _POLL == 0 and i + 1 < self.m:
+                hb = torch.empty(8, dtype=torch.int64, pin_memory=True)
+                hb.copy_(st.status.buf, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record()
+                pending.append((ev, hb))
+                if len(pending) >= 2:
+                    ev0, hb0 = pending.pop(0)
+                    ev0.synchronize()
+                    if int(hb0[0]) != 0:
+                        break
+        return st._sync_status()
+
+
+def arnoldi(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, theta=None,
+            policy: PrecisionPolicy = MIXED32_64, solver: LsqSolver = HOUSEHOLDER_QR,
+            phi=None) -> ArnoldiDecomposition:
+    """m-step RGS-Arnoldi (krylov.py:176-199); fewer columns on a lucky breakdown."""
+    _check_variant(variant, phi=phi)
+    if theta is None:
+        raise ValueError("the randomized variant needs a sketch operator")
+    eng = _ArnoldiEngine(A, theta, policy, solver, m)
+    st = eng.state
+    b_dev = _to_device_f64(b, A.n, st.device)
+    st._push_async(b_dev)
+    s0 = eng.run(alpha=None, tol=None)
+    breakdown = s0["code"] in (_lib.ST_BREAKDOWN, _lib.ST_NONFINITE)
+    if s0["code"] == _lib.ST_RANK:
+        raise np.linalg.LinAlgError("sketched basis numerically rank deficient")
+    if s0["code"] and s0["ncols"] == 0:
+        st._raise_status(s0)
+    R = st.R
+    return ArnoldiDecomposition(Q=st.Q, H=R[:, 1:].copy(), R=R, beta=float(R[0, 0]),
+                                breakdown=breakdown)
+
+
+def gmres(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, theta=None,
+          policy: PrecisionPolicy = MIXED32_64, solver: LsqSolver = HOUSEHOLDER_QR,
+          preconditioner=None, tol: float | None = None, phi=None) -> GmresResult:
+    """Single-cycle RGS-GMRES(m) with progressive Givens rotations (krylov.py:229-319)."""
+    _check_variant(variant, preconditioner, phi)
+    if theta is None:
+        raise ValueError("the randomized variant needs a sketch operator")
+    _lib.require_cuda()
+    device = torch.device("cuda", torch.cuda.current_device())
+    return_numpy = not (isinstance(b, torch.Tensor) and b.is_cuda)
+    b_dev = _to_device_f64(b, A.n, device)
+    ws0 = _Workspace(A.n, device)
+    ws0.norm(b_dev, 0)
+    b_norm = float(ws0.nrm[0])  # host sync: the zero-rhs branch needs it
+    if b_norm == 0.0:
+        x0 = np.zeros(A.n) if return_numpy else torch.zeros(A.n, dtype=torch.float64,
+                                                             device=device)
+        return GmresResult(x=x0, residual_history=np.zeros(0), final_residual=0.0,
+                           iterations=0, converged=True, breakdown=False)
+    eng = _ArnoldiEngine(A, theta, policy, solver, m)
+    st = eng.state
+    alpha = _operator_norm_estimate(A, eng.ws)
+    if float(alpha) <= 0.0:
+        raise np.linalg.LinAlgError("operator norm estimate is zero")
+    bn = torch.empty_like(b_dev)
+    call("sgs_cast_div", b_dev.data_ptr(), _lib.SGS_F64, bn.data_ptr(), _lib.SGS_F64,
+         ws0.nrm.data_ptr(), A.n, stream_ptr())
+    st._push_async(bn)
+    s1 = eng.run(alpha=alpha, tol=tol)
+    code = s1["code"]
+    if code == _lib.ST_RANK:
+        raise np.linalg.LinAlgError("sketched basis numerically rank deficient")
+    if code and s1["ncols"] == 0:
+        st._raise_status(s1)
+    breakdown = code in (_lib.ST_BREAKDOWN, _lib.ST_NONFINITE)
+    k = s1["iters"]
+    hist = eng.hist[:k].cpu().numpy()
+    x = torch.zeros(A.n, dtype=torch.float64, device=device)
+    if k > 0:
+        T = eng.T[:k, :k].t().cpu().numpy()
+        g = eng.g[:k].cpu().numpy()
+        y = scipy.linalg.solve_triangular(T, g, lower=False)
+        yd = torch.from_numpy(y).to(device)
+        z = torch.empty(A.n, dtype=torch.float64, device=device)
+        call("sgs_gemv_f64", st._Q.data_ptr(), st.ccode, st.ldq, A.n, k, yd.data_ptr(),
+             z.data_ptr(), stream_ptr())
+        call("sgs_scale", z.data_ptr(), b_norm, alpha.data_ptr(), 0, x.data_ptr(), A.n,
+             stream_ptr())
+    # true residual ||b - A x|| / ||b|| in binary64
+    ax = eng.ws.w
+    A.spmv_into(x.data_ptr(), _lib.SGS_F64, ax)
+    call("sgs_rsub", b_dev.data_ptr(), ax.data_ptr(), A.n, stream_ptr())
+    eng.ws.norm(ax, 2)
+    true_res = float(eng.ws.nrm[2]) / b_norm
+    converged = (true_res <= max(tol, 0.0)) if tol is not None else False
+    return GmresResult(x=x.cpu().numpy() if return_numpy else x,
+                       residual_history=np.asarray(hist), final_residual=true_res,
+                       iterations=k, converged=converged or breakdown, breakdown=breakdown,
+                       factors=st.factors())
+
+
+@dataclass
+class RestartedResult:
+    x: object
+    iterations: int
+    cycles: list
+    final_residual: float
+    converged: bool
+
+
+def gmres_restarted(A: SparseMatrix, b, theta, policy: PrecisionPolicy = MIXED32_64,
+                    restart: int = 300, max_iters: int = 3000, tol: float = 1e-8,
+                    solver: LsqSolver = HOUSEHOLDER_QR) -> RestartedResult:
+    """Restarted RGMRES(restart) for BASELINE config 3 (the reference is
+    single-cycle, krylov.py:236-241; the wrapper is shared verbatim with the
+    oracle): each cycle runs gmres(A, r, min(restart, max_iters - its), tol =
+    tol * ||b|| / ||r||), then x += dx and r = b - A x in binary64; stop at
+    ||r|| / ||b|| <= tol or its >= max_iters."""
+    _lib.require_cuda()
+    device = torch.device("cuda", torch.cuda.current_device())
+    return_numpy = not (isinstance(b, torch.Tensor) and b.is_cuda)
+    b_dev = _to_device_f64(b, A.n, device)
+    ws = _Workspace(A.n, device)
+    ws.norm(b_dev, 0)
+    b_norm = float(ws.nrm[0])
+    x = torch.zeros(A.n, dtype=torch.float64, device=device)
+    r = b_dev.clone()
+    its, cycles = 0, []
+    r_norm = b_norm
+    while True:
+        if b_norm == 0.0 or r_norm / b_norm <= tol or its >= max_iters:
+            break
+        res = gmres(A, r, m=min(restart, max_iters - its), theta=theta, policy=policy,
+                    solver=solver, tol=tol * b_norm / r_norm)
+        cycles.append(res.iterations)
+        its += res.iterations
+        x += res.x
+        A.spmv_into(x.data_ptr(), _lib.SGS_F64, r)
+        call("sgs_rsub", b_dev.data_ptr(), r.data_ptr(), A.n, stream_ptr())
+        ws.norm(r, 1)
+        r_norm = float(ws.nrm[1])
+        if res.iterations == 0:
+            break
+    rel = r_norm / b_norm if b_norm else 0.0
+    return RestartedResult(x=x.cpu().numpy() if return_numpy else x, iterations=its,
+                           cycles=cycles, final_residual=rel, converged=rel <= tol)

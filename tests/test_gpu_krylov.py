@@ -1,0 +1,117 @@
+"""GPU RGS-Arnoldi / RGS-GMRES vs the reference golden runs and the oracle."""
+
+import numpy as np
+import pytest
+import scipy.sparse.linalg
+import torch
+
+import paper_2011_05090_b200 as sg
+from conftest import golden
+from oracle import OracleSketch, csr_matvec, oracle_gmres, oracle_gmres_restarted
+from paper_2011_05090_b200.workloads import convdiff3d, rhs_gaussian
+
+pytestmark = pytest.mark.gpu
+
+
+def _A(g, p):
+    n = len(g[f"{p}_rp"]) - 1
+    return sg.SparseMatrix(n=n, row_ptr=g[f"{p}_rp"], col_idx=g[f"{p}_ci"], values=g[f"{p}_v"])
+
+
+def test_matvec_matches_scipy(cuda, rng):
+    S = scipy.sparse.random(50, 50, density=0.1, random_state=1, format="csr")
+    A = sg.SparseMatrix.from_scipy(S)
+    x = rng.standard_normal(50)
+    assert np.allclose(A.matvec(x), S @ x, atol=1e-14)
+
+
+def test_gmres_laplacian_matches_reference(cuda):
+    g = golden("krylov.npz")
+    A = _A(g, "lap")
+    th = sg.make_sketch(sg.SketchKind.PSRHT, 200, A.n, 0)
+    res = sg.gmres(A, g["lap_b"], m=150, theta=th, policy=sg.UNIFIED64, tol=1e-12)
+    assert res.final_residual < 1e-10
+    assert res.converged
+    assert abs(res.iterations - int(g["lap_its"])) <= max(1, 0.02 * int(g["lap_its"]))
+    xs = np.sin(np.arange(A.n) * 0.1)
+    assert np.linalg.norm(res.x - xs) / np.linalg.norm(xs) < 1e-8
+    assert np.linalg.norm(res.x - g["lap_x"]) / np.linalg.norm(g["lap_x"]) < 1e-8
+
+
+def test_arnoldi_identity_and_golden(cuda):
+    g = golden("krylov.npz")
+    B = _A(g, "rs")
+    th = sg.make_sketch(sg.SketchKind.PSRHT, 64, B.n, 0)
+    dec = sg.arnoldi(B, g["rs_b"], 15, theta=th, policy=sg.UNIFIED64)
+    assert dec.H.shape == (16, 15) and dec.beta > 0
+    AQ = np.column_stack([B.matvec(dec.Q[:, j]) for j in range(15)])
+    assert np.linalg.norm(AQ - dec.Q @ dec.H) / np.linalg.norm(AQ) < 1e-12
+    assert np.linalg.norm(dec.Q - g["rs_Q"]) / np.linalg.norm(g["rs_Q"]) < 1e-10
+    assert np.linalg.norm(dec.H - g["rs_H"]) / np.linalg.norm(g["rs_H"]) < 1e-10
+
+
+def test_gmres_matches_direct_solve(cuda, rng):
+    g = golden("krylov.npz")
+    B = _A(g, "rs")
+    b = rng.standard_normal(B.n)
+    th = sg.make_sketch(sg.SketchKind.PSRHT, 128, B.n, 1)
+    res = sg.gmres(B, b, m=100, theta=th, policy=sg.UNIFIED64, tol=1e-12)
+    x_ref = scipy.sparse.linalg.spsolve(B.to_scipy().tocsc(), b)
+    assert np.linalg.norm(res.x - x_ref) / np.linalg.norm(x_ref) < 1e-9
+    assert res.factors is not None
+
+
+def test_gmres_history_monotone_and_estimate(cuda, rng):
+    g = golden("krylov.npz")
+    A = _A(g, "l12")
+    b = rng.standard_normal(A.n)
+    th = sg.make_sketch(sg.SketchKind.PSRHT, 80, A.n, 0)
+    res = sg.gmres(A, b, m=60, theta=th, policy=sg.UNIFIED64)
+    h = res.residual_history
+    assert len(h) == 60 and np.all(np.diff(h) <= 1e-15)
+    assert abs(h[-1] - res.final_residual) <= 1e-8 + 0.1 * res.final_residual
+
+
+def test_gmres_mixed_plateau(cuda):
+    g = golden("krylov.npz")
+    A = _A(g, "l12")
+    th = sg.make_sketch(sg.SketchKind.PSRHT, 140, A.n, 0)
+    res = sg.gmres(A, g["l12_b"], m=120, theta=th, policy=sg.MIXED32_64)
+    assert res.final_residual < 1e-4
+    assert res.final_residual <= 10 * float(g["l12_res"])
+
+
+def test_gmres_zero_rhs(cuda):
+    g = golden("krylov.npz")
+    A = _A(g, "l12")
+    th = sg.make_sketch(sg.SketchKind.PSRHT, 20, A.n, 0)
+    res = sg.gmres(A, np.zeros(A.n), m=10, theta=th)
+    assert res.converged and np.all(res.x == 0.0)
+
+
+def test_convdiff_gmres_iterations_vs_reference(cuda):
+    g = golden("krylov.npz")
+    rp, ci, va = convdiff3d(16)
+    A = sg.SparseMatrix(n=16 ** 3, row_ptr=rp, col_idx=ci, values=va)
+    th = sg.make_sketch(sg.SketchKind.PSRHT, 200, A.n, 0)
+    res = sg.gmres(A, g["cd_b"], m=100, theta=th, policy=sg.UNIFIED64, tol=1e-8)
+    its = int(g["cd_its"])
+    assert abs(res.iterations - its) <= max(1, round(0.02 * its))
+    assert np.linalg.norm(res.x - g["cd_x"]) / np.linalg.norm(g["cd_x"]) < 1e-6
+
+
+@pytest.mark.parametrize("policy", ["f64", "mixed"])
+def test_restarted_convdiff_iterations_vs_oracle(cuda, policy):
+    N = 32
+    rp, ci, va = convdiff3d(N)
+    n = N ** 3
+    A = sg.SparseMatrix(n=n, row_ptr=rp, col_idx=ci, values=va)
+    b = rhs_gaussian(n, 0)
+    th = sg.make_sketch(sg.SketchKind.PSRHT, 300, n, 0)
+    pol = sg.UNIFIED64 if policy == "f64" else sg.MIXED32_64
+    ours = sg.gmres_restarted(A, b, th, pol, restart=60, max_iters=600, tol=1e-8)
+    mv = lambda x: csr_matvec(rp, ci, va, n, x)
+    ref = oracle_gmres_restarted(mv, n, b, OracleSketch("psrht", 300, n, 0), policy,
+                                 restart=60, max_iters=600, tol=1e-8)
+    assert abs(ours.iterations - ref["iterations"]) <= max(1, round(0.02 * ref["iterations"]))
+    assert ours.final_residual <= 1e-8 or ours.iterations >= 600

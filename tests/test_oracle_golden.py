@@ -1,0 +1,86 @@
+"""The CPU oracle reproduces the reference bit for bit on the golden vectors
+produced by running the reference itself (oracle/make_golden.py)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import (OracleSketch, csr_matvec, fwht_ref, oracle_arnoldi, oracle_certificates,
+                    oracle_gmres, oracle_rgs_factorize, psrht_setup)
+from oracle.ref_rgs import OracleBreakdown
+
+
+def test_fwht_kat_and_golden():
+    g = golden("fwht.npz")
+    assert np.array_equal(fwht_ref(g["kat_in"]), np.array([10.0, -2.0, -4.0, 0.0]))
+    assert np.array_equal(g["kat_out"], np.array([10.0, -2.0, -4.0, 0.0]))
+    for s in (1, 2, 8, 64, 1024, 4096, 16384):
+        assert np.array_equal(fwht_ref(g[f"x_{s}"]), g[f"y_{s}"]), s
+    assert np.array_equal(fwht_ref(g["X_mat"]), g["Y_mat"])
+
+
+def test_fwht_rejects_non_pow2():
+    with pytest.raises(ValueError):
+        fwht_ref(np.zeros(6))
+
+
+def test_psrht_construction_and_apply_match_reference():
+    g = golden("psrht.npz")
+    for (k, n, seed) in g["cases"]:
+        tag = f"{k}_{n}_{seed}"
+        s, signs, samples = psrht_setup(int(k), int(n), int(seed))
+        assert s == 1 << (int(n) - 1).bit_length()
+        assert np.array_equal(signs, g[f"signs_{tag}"])
+        assert np.array_equal(samples, g[f"samples_{tag}"])
+        op = OracleSketch("psrht", int(k), int(n), int(seed))
+        assert np.array_equal(op.apply(g[f"x_{tag}"]), g[f"y_{tag}"]), tag
+        assert np.array_equal(op.apply_block(g[f"X_{tag}"]), g[f"Y_{tag}"]), tag
+
+
+def test_rademacher_materialize_matches_reference():
+    g = golden("psrht.npz")
+    op = OracleSketch("rademacher", 20, 50, 5)
+    assert np.allclose(op.apply_block(np.eye(50)), g["rad_materialize_20_50_5"], atol=1e-15)
+
+
+@pytest.mark.parametrize("name", ["psrht_f64", "psrht_mixed", "rad_f64", "psrht_f32",
+                                  "psrht_mixed_wide", "c1shape_mixed"])
+def test_oracle_rgs_bit_identical_to_reference(name):
+    g = golden(f"rgs_{name}.npz")
+    n, m, k, seed = (int(v) for v in g["meta"])
+    op = OracleSketch(str(g["kind"]), k, n, seed)
+    out = oracle_rgs_factorize(g["W"], op, str(g["policy"]), float(g["bf"]))
+    for key in ("Q", "R", "S", "P"):
+        assert out[key].dtype == g[key].dtype
+        assert np.array_equal(out[key], g[key]), (name, key)
+    cert = oracle_certificates(out["S"], out["P"], out["R"])
+    assert np.allclose(cert, g["cert"], rtol=1e-12)
+
+
+def test_oracle_breakdown_column():
+    g = golden("rgs_breakdown.npz")
+    op = OracleSketch("psrht", 64, 200, 5)
+    with pytest.raises(OracleBreakdown) as e:
+        oracle_rgs_factorize(g["W"], op, "f64", 10.0)
+    assert e.value.column == int(g["column"]) == 5
+
+
+def test_oracle_krylov_matches_reference():
+    g = golden("krylov.npz")
+    n = len(g["lap_b"])
+    mv = lambda x: csr_matvec(g["lap_rp"], g["lap_ci"], g["lap_v"], n, x)
+    op = OracleSketch("psrht", 200, n, 0)
+    out = oracle_gmres(mv, n, g["lap_b"], 150, op, "f64", tol=1e-12)
+    assert out["iterations"] == int(g["lap_its"])
+    assert np.array_equal(out["x"], g["lap_x"])
+    assert np.array_equal(out["history"], g["lap_hist"])
+    nb = len(g["rs_b"])
+    mv2 = lambda x: csr_matvec(g["rs_rp"], g["rs_ci"], g["rs_v"], nb, x)
+    dec = oracle_arnoldi(mv2, nb, g["rs_b"], 15, OracleSketch("psrht", 64, nb, 0), "f64")
+    assert np.array_equal(dec["Q"], g["rs_Q"])
+    assert np.array_equal(dec["H"], g["rs_H"])
+    n12 = len(g["l12_b"])
+    mv3 = lambda x: csr_matvec(g["l12_rp"], g["l12_ci"], g["l12_v"], n12, x)
+    r12 = oracle_gmres(mv3, n12, g["l12_b"], 120, OracleSketch("psrht", 140, n12, 0), "mixed")
+    assert r12["iterations"] == int(g["l12_its"])
+    assert r12["final_residual"] == float(g["l12_res"])
