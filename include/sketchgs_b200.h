@@ -153,10 +153,13 @@ typedef struct sgs_ls_args {
   double bf_ucrs;        /* breakdown_factor * u_crs */
   void* S; void* P;      /* k x cap, fine, ld = k */
   double* R;             /* cap x cap, ld = cap */
-  void* Qs; void* Rinv;  /* k x cap and cap x cap, fine */
+  void* Qs; void* Rinv;  /* k x cap and cap x cap, fine: unnormalised orthogonal
+                            factor T of S and R_S^{-1} */
+  void* alpha;           /* cap, fine: column norms of T (Qs = T diag(1/alpha)) */
   double* scratch;       /* sgs_ls_scratch_elems(k, cap) doubles */
   void* r_crs;           /* cap, coarse */
   sgs_status* st;
+  long long* trace;      /* optional (NULL): clock64() at phase boundaries, CTA 0 */
 } sgs_ls_args;
 
 int64_t sgs_ls_scratch_elems(int k, int cap);

@@ -38,8 +38,8 @@ class LsArgs(ctypes.Structure):
         ("p_partials", c_void_p), ("p_nparts", c_int), ("p_scale", c_double),
         ("bf_ucrs", c_double),
         ("S", c_void_p), ("P", c_void_p), ("R", c_void_p),
-        ("Qs", c_void_p), ("Rinv", c_void_p), ("scratch", c_void_p),
-        ("r_crs", c_void_p), ("st", c_void_p),
+        ("Qs", c_void_p), ("Rinv", c_void_p), ("alpha", c_void_p), ("scratch", c_void_p),
+        ("r_crs", c_void_p), ("st", c_void_p), ("trace", c_void_p),
     ]
 
 

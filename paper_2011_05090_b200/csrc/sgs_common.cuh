@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdarg>
 #include <atomic>
+#include <utility>
 
 #include "../../include/sketchgs_b200.h"
 
@@ -73,6 +74,81 @@ __device__ __forceinline__ T block_sum(T v, T* red) {
   __syncthreads();
   T t = T(0);
   for (int w = 0; w < nw; ++w) t += red[w];  // same order in every thread
+  return t;
+}
+
+// ---- programmatic dependent launch (PDL) ---------------------------------------
+// Every hot-loop kernel is launched with programmatic stream serialisation: it
+// may be scheduled while its predecessor drains, waits here before touching
+// any predecessor output, and immediately lets its own successor launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_enter() {
+  pdl_wait();
+  pdl_trigger();
+}
+
+bool pdl_enabled();
+
+// cudaLaunchKernelEx wrapper: PDL attribute (when enabled) + optional cluster.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                             cudaStream_t s, int cluster, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (cluster > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = cluster;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+inline int check_ex(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    cudaGetLastError();
+    return SGS_ECUDA;
+  }
+  return check_launch(what);
+}
+
+// Canonical order for summing per-CTA partials (used by every consumer so
+// that the same vector reduced by different kernels gives the same bits):
+// eight interleaved ascending chains acc_g = sum_{p = g mod 8} x_p, then
+// sum_g acc_g in ascending g.
+constexpr int kCanonG = 8;
+__device__ __forceinline__ double canon_sum(const double* x, int64_t stride, int nparts) {
+  double acc[kCanonG];
+#pragma unroll
+  for (int g = 0; g < kCanonG; ++g) acc[g] = 0.0;
+  int p = 0;
+  for (; p + kCanonG <= nparts; p += kCanonG) {
+#pragma unroll
+    for (int g = 0; g < kCanonG; ++g) acc[g] += x[(int64_t)(p + g) * stride];
+  }
+#pragma unroll
+  for (int g = 0; g < kCanonG; ++g)
+    if (p + g < nparts) acc[g] += x[(int64_t)(p + g) * stride];
+  double t = 0.0;
+#pragma unroll
+  for (int g = 0; g < kCanonG; ++g) t += acc[g];
   return t;
 }
 

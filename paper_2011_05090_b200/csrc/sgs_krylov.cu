@@ -3,6 +3,7 @@
 // _operator_norm_estimate (krylov.py:213-226) and the progressive Givens
 // update (krylov.py:282-301) so the Arnoldi loop never waits on the host.
 
+#include <cstdlib>
 #include "sgs_common.cuh"
 
 namespace sgs {
@@ -16,6 +17,15 @@ void set_error(const char* fmt, ...) {
   va_start(ap, fmt);
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
+}
+
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SGS_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
 }
 
 int sm_count() {
@@ -34,6 +44,7 @@ __global__ void __launch_bounds__(256)
 csr_spmv_kernel(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                 const double* __restrict__ vals, const TX* __restrict__ x,
                 const double* __restrict__ alpha, double* __restrict__ y, const sgs_status* st) {
+  pdl_enter();
   if (status_stopped(st)) return;
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
@@ -127,6 +138,7 @@ __global__ void cos_init_kernel(double* v, int64_t n) {
 __global__ void givens_step_kernel(const double* __restrict__ R, int64_t ldr, int i,
                                    double* cs, double* sn, double* g, double* T, int64_t ldt,
                                    double* hist, double tol, sgs_status* st) {
+  pdl_enter();
   if (status_stopped(st)) return;
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const double beta = R[0];
@@ -207,12 +219,12 @@ extern "C" int sgs_csr_spmv(int64_t n, const int32_t* row_ptr, const int32_t* co
   cudaStream_t s = as_stream(stream);
   const unsigned blocks = (unsigned)((n + 255) / 256);
   if (x_dtype == SGS_F32)
-    csr_spmv_kernel<float><<<blocks, 256, 0, s>>>(n, row_ptr, col_idx, vals,
-                                                  static_cast<const float*>(x), alpha, y, st);
-  else
-    csr_spmv_kernel<double><<<blocks, 256, 0, s>>>(n, row_ptr, col_idx, vals,
-                                                   static_cast<const double*>(x), alpha, y, st);
-  return check_launch("csr_spmv_kernel");
+    return check_ex(launch_ex(csr_spmv_kernel<float>, dim3(blocks), dim3(256), 0, s, 1, n, row_ptr,
+                              col_idx, vals, static_cast<const float*>(x), alpha, y, st),
+                    "csr_spmv_kernel");
+  return check_ex(launch_ex(csr_spmv_kernel<double>, dim3(blocks), dim3(256), 0, s, 1, n, row_ptr,
+                            col_idx, vals, static_cast<const double*>(x), alpha, y, st),
+                  "csr_spmv_kernel");
 }
 
 extern "C" int64_t sgs_norm2_work_elems(int64_t n) { (void)n; return kNormBlocks; }
@@ -291,6 +303,6 @@ extern "C" int sgs_givens_step(const double* R, int64_t ldr, int i, double* cs, 
                                sgs_status* st, void* stream) {
   SGS_REQUIRE(R && cs && sn && g && T && hist && st && i >= 0 && ldr >= i + 2 && ldt >= i + 2,
               "givens: bad args");
-  givens_step_kernel<<<1, 32, 0, as_stream(stream)>>>(R, ldr, i, cs, sn, g, T, ldt, hist, tol, st);
-  return check_launch("givens_step_kernel");
+  return check_ex(launch_ex(givens_step_kernel, dim3(1), dim3(32), 0, as_stream(stream), 1, R, ldr,
+                            i, cs, sn, g, T, ldt, hist, tol, st), "givens_step_kernel");
 }

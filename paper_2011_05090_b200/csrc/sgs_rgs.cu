@@ -31,7 +31,9 @@ template <> struct VecT<double> { using type = double2; static constexpr int N =
 template <typename T>
 __device__ __forceinline__ void vload(const T* p, T* v) {
   using V = typename VecT<T>::type;
-  const V x = *reinterpret_cast<const V*>(p);
+  // streaming (evict-first) load: the 1 GB-per-column Q stream must not evict
+  // the small, reused k-dimensional state (S, P, T, R_S^{-1}) from L2
+  const V x = __ldcs(reinterpret_cast<const V*>(p));
   if constexpr (VecT<T>::N == 4) { v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; }
   else { v[0] = x.x; v[1] = x.y; }
 }
@@ -60,6 +62,7 @@ __global__ void __launch_bounds__(kUpdThreads)
 rgs_update_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* __restrict__ w,
                   const TQ* __restrict__ rc, int normalize_prev, const double* __restrict__ R,
                   int64_t ldr, const sgs_status* st) {
+  pdl_enter();
   if (status_stopped(st)) return;
   constexpr int V = VecT<TQ>::N;
   extern __shared__ unsigned char smem_raw[];
@@ -108,7 +111,7 @@ rgs_update_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
     }
     TQ out[V];
 #pragma unroll
-    for (int v = 0; v < V; ++v) out[v] = cvt<TQ>(w[row0 + v]) - acc[v];
+    for (int v = 0; v < V; ++v) out[v] = cvt<TQ>(__ldcs(w + row0 + v)) - acc[v];
     vstore(Q + (int64_t)i * ldq + row0, out);
   } else {
     const int nv = (int)(n - row0);
@@ -134,6 +137,7 @@ rgs_update_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
 template <typename TQ>
 __global__ void normalize_column_kernel(TQ* __restrict__ Q, int64_t n, const double* rjj_ptr,
                                         const sgs_status* st) {
+  pdl_enter();
   if (status_stopped(st)) return;
   const double rjj = *rjj_ptr;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
@@ -178,12 +182,25 @@ __global__ void transpose_kernel(const T* __restrict__ src, int64_t lds, T* __re
 }
 
 // ===========================================================================
-// Cluster least-squares step.
+// Cluster least-squares step (v3).
+//
+// Rows of every k-vector are split over the CTAs of one cluster (<= 16).  The
+// orthogonal factor of S is kept UNNORMALISED, T = Qs diag(alpha), with the
+// norms alpha in a device vector, so that everything the fused
+// finalize(i) + solve(i+1) launch needs crosses the cluster in two exchanges:
+//   #1  ||s'||^2, ||p_i||^2, T^T s', T^T p_{i+1}          (s' = Theta q'_i)
+//   #2  ||t||^2, t^T p_{i+1}                               (t = s - Qs Qs^T s)
+// (r_ii scales the first exchange afterwards: Qs^T s = (T^T s' / alpha) / r_ii).
+// A second Gram-Schmidt pass runs only when ||t||^2 < ||s||^2 / 2.  Each
+// column dot is computed by one fixed lane/shuffle pattern and summed over
+// the CTAs in rank order, whichever launch computes it, so streaming push and
+// the batched factorisation agree bit for bit.
 constexpr int kLsThreads = 512;
 constexpr int kLsWarps = kLsThreads / 32;
 constexpr int kLsMaxCluster = 16;
-constexpr int kLsChunk = 256;  // outputs per pass of the 2-D matvec helper
-constexpr int kLsRowsPerCta = 192;
+constexpr int kLsRowsPerCta = 96;
+constexpr int kLsChunk = 128;  // rows / outputs per pass of the 2-D helpers (4 per lane)
+constexpr int kLsCpw = 8;      // columns in flight per warp
 
 static int g_ls_max_cluster = 0;
 
@@ -201,59 +218,91 @@ static int ls_cluster_size_host(int k) {
   return cl;
 }
 
-struct LsCtx {
-  int rank, CL, ra, rb, nr, k, cap;
-};
-
-// GEMV-T over own rows: xpart[j] = sum_{rr<nr} M[j*ldm + rr] * v[rr], j < ncols.
-// Warp per column (4 in flight), lanes over rows, fixed shuffle tree.
-template <typename T>
-__device__ void ls_gemvT_rows(const T* __restrict__ M, int64_t ldm, int nr, int ncols,
-                              const T* v, T* __restrict__ xpart) {
+// Per-CTA partial dots of NV vectors with columns [j0, j1) of M over the
+// CTA's nr rows: o[j] = sum_rr M[j*ldm + rr] * v[rr].  Warp per column (8
+// columns in flight), lanes stride the rows, fixed xor-shuffle tree.
+template <typename T, int NV>
+__device__ __noinline__ void ls_coldot(const T* __restrict__ M, int64_t ldm, int nr, int j0,
+                                       int j1, const T* v0, const T* v1, T* __restrict__ o0,
+                                       T* __restrict__ o1) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int j0 = warp * 4; j0 < ncols; j0 += kLsWarps * 4) {
-    T acc[4] = {T(0), T(0), T(0), T(0)};
-    for (int rr = lane; rr < nr; rr += 32) {
-      const T vr = v[rr];
+  for (int rc = 0; rc < nr; rc += kLsChunk) {  // rows in chunks of 128 (4 per lane)
+    const int rn = min(kLsChunk, nr - rc);
+    T x0[4], x1[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (j0 + u < ncols) acc[u] = fma(M[(int64_t)(j0 + u) * ldm + rr], vr, acc[u]);
+    for (int q = 0; q < 4; ++q) {
+      const int rr = rc + lane + 32 * q;
+      x0[q] = (lane + 32 * q < rn) ? v0[rr] : T(0);
+      x1[q] = (NV > 1 && lane + 32 * q < rn) ? v1[rr] : T(0);
     }
+    for (int jb = j0 + warp * kLsCpw; jb < j1; jb += kLsWarps * kLsCpw) {
+      T mv[kLsCpw][4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const T s = warp_sum(acc[u]);
-      if (lane == 0 && j0 + u < ncols) xpart[j0 + u] = s;
+      for (int u = 0; u < kLsCpw; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          mv[u][q] = (jb + u < j1 && lane + 32 * q < rn)
+                         ? M[(int64_t)(jb + u) * ldm + rc + lane + 32 * q] : T(0);
+#pragma unroll
+      for (int u = 0; u < kLsCpw; ++u) {
+        T a0 = T(0), a1 = T(0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          a0 = fma(mv[u][q], x0[q], a0);
+          if (NV > 1) a1 = fma(mv[u][q], x1[q], a1);
+        }
+        a0 = warp_sum(a0);
+        if (NV > 1) a1 = warp_sum(a1);
+        if (lane == 0 && jb + u < j1) {
+          if (rc == 0) {
+            o0[jb + u] = a0;
+            if (NV > 1) o1[jb + u] = a1;
+          } else {  // rows beyond 128 per CTA (k > 2048): accumulate chunk sums in order
+            o0[jb + u] += a0;
+            if (NV > 1) o1[jb + u] += a1;
+          }
+        }
+      }
     }
+    if (rc + kLsChunk < nr) __syncwarp();
   }
 }
 
-// out[o - o0] = sum_{l in [lstart(o), l1)} M[l*ldm + o] * v[l] for o in [o0, o1),
-// lstart(o) = UPPER ? max(o, l0) : l0.  Warps split l (stride 16), lanes split o;
-// the per-warp partial sums are combined in fixed warp order.
+// out[o - o0] = sum_{l in [lbeg(o), l1)} M[l*ldm + o] * c[l], o in [o0, o1), with
+// lbeg(o) = UPPER ? o : 0.  Lanes own outputs (4 each), warps take 8 columns
+// at a time, warp partials combined in ascending warp order.
 template <typename T, bool UPPER>
-__device__ void ls_matvec(const T* __restrict__ M, int64_t ldm, int o0, int o1, int l0, int l1,
-                          const T* v, T* out, T* red) {
+__device__ __noinline__ void ls_matvec(const T* __restrict__ M, int64_t ldm, int o0, int o1,
+                                       int l1, const T* c, T* out, T* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int oc = o0; oc < o1; oc += kLsChunk) {
-    const int ocn = min(kLsChunk, o1 - oc);
-    T acc[kLsChunk / 32];
+    const int on = min(kLsChunk, o1 - oc);
+    const int lstart = UPPER ? oc : 0;
+    T acc[4] = {T(0), T(0), T(0), T(0)};
+    for (int lb = lstart + warp * kLsCpw; lb < l1; lb += kLsWarps * kLsCpw) {
+      T mv[kLsCpw][4];
 #pragma unroll
-    for (int q = 0; q < kLsChunk / 32; ++q) acc[q] = T(0);
-    for (int l = l0 + warp; l < l1; l += kLsWarps) {
-      const T vl = v[l];
-      const T* col = M + (int64_t)l * ldm;
+      for (int u = 0; u < kLsCpw; ++u) {
+        const int l = lb + u;
 #pragma unroll
-      for (int q = 0; q < kLsChunk / 32; ++q) {
-        const int ol = lane + 32 * q;
-        const int o = oc + ol;
-        if (ol < ocn && (!UPPER || l >= o)) acc[q] = fma(col[o], vl, acc[q]);
+        for (int q = 0; q < 4; ++q) {
+          const int ol = lane + 32 * q;
+          const bool ok = l < l1 && ol < on && (!UPPER || l >= oc + ol);
+          mv[u][q] = ok ? M[(int64_t)l * ldm + oc + ol] : T(0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kLsCpw; ++u) {
+        const T cl = (lb + u < l1) ? c[lb + u] : T(0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] = fma(mv[u][q], cl, acc[q]);
       }
     }
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < kLsChunk / 32; ++q) red[warp * kLsChunk + lane + 32 * q] = acc[q];
+    for (int q = 0; q < 4; ++q) red[warp * kLsChunk + lane + 32 * q] = acc[q];
     __syncthreads();
-    for (int ol = threadIdx.x; ol < ocn; ol += blockDim.x) {
+    for (int ol = threadIdx.x; ol < on; ol += blockDim.x) {
       T s = T(0);
       for (int w = 0; w < kLsWarps; ++w) s += red[w * kLsChunk + ol];
       out[oc - o0 + ol] = s;
@@ -262,35 +311,60 @@ __device__ void ls_matvec(const T* __restrict__ M, int64_t ldm, int o0, int o1, 
   __syncthreads();
 }
 
-// c[j] = sum_{q<CL} xpart[q*cap + j] (fixed order), read through L2.
+// c[j] = (sum_{q<CL} part[q*stride + j]) / div[j]  (ascending q), j in [j0, j1).
 template <typename T>
-__device__ void ls_gather(const T* xpart, int CL, int cap, int ncols, T* c) {
-  for (int j = threadIdx.x; j < ncols; j += blockDim.x) {
+__device__ __noinline__ void ls_gather(const T* part, int64_t stride, int CL, int j0, int j1,
+                                       const T* div, T* c) {
+  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+    T v[kLsMaxCluster];
+#pragma unroll
+    for (int q = 0; q < kLsMaxCluster; ++q) v[q] = q < CL ? __ldcg(part + (int64_t)q * stride + j) : T(0);
     T s = T(0);
-    for (int q = 0; q < CL; ++q) s += __ldcg(xpart + (int64_t)q * cap + j);
-    c[j] = s;
+#pragma unroll
+    for (int q = 0; q < kLsMaxCluster; ++q) if (q < CL) s += v[q];
+    c[j] = div ? s / __ldcg(div + j) : s;
+  }
+}
+
+// v[rr] = cast(scale * canon_sum(parts[:, ra+rr])) for the CTA's rows; the
+// eight canonical chains run in parallel thread groups.
+template <typename T>
+__device__ __noinline__ void ls_reduce_parts(const double* parts, int nparts, int k, int ra,
+                                             int nr, double scale, T* v, double* red) {
+  const int g = threadIdx.x >> 6, rl = threadIdx.x & 63;  // 8 groups x 64 rows
+  for (int r0 = 0; r0 < nr; r0 += 64) {
+    double acc = 0.0;
+    const int rr = r0 + rl;
+    if (rr < nr) {
+      const double* p = parts + ra + rr;
+#pragma unroll 4
+      for (int q = g; q < nparts; q += kCanonG) acc += __ldcg(p + (int64_t)q * k);
+    }
+    __syncthreads();
+    red[g * 64 + rl] = acc;
+    __syncthreads();
+    if (threadIdx.x < 64 && r0 + threadIdx.x < nr) {
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < kCanonG; ++q) t += red[q * 64 + threadIdx.x];
+      v[r0 + threadIdx.x] = from_double<T>(scale * t);
+    }
   }
   __syncthreads();
 }
 
+// Cluster sum of one scalar per CTA from slots[q*stride] (ascending q).
 template <typename T>
-__device__ T ls_cluster_sum(T local, T* slot, int rank, int CL, T* red, cg::cluster_group& cl) {
-  const T b = block_sum(local, red);
-  if (threadIdx.x == 0) slot[rank] = b;
-  cl.sync();
+__device__ __forceinline__ T ls_slot_sum(const T* slots, int64_t stride, int CL) {
   T s = T(0);
-  for (int q = 0; q < CL; ++q) s += __ldcg(slot + q);
+  for (int q = 0; q < CL; ++q) s += __ldcg(slots + (int64_t)q * stride);
   return s;
-}
-
-template <typename T>
-__device__ __forceinline__ T ld_fine(const void* p, int64_t idx) {
-  return static_cast<const T*>(p)[idx];
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   cg::cluster_group cl = cg::this_cluster();
+  pdl_enter();
   const int rank = (int)cl.block_rank();
   const int CL = (int)cl.num_blocks();
   const int k = a.k, cap = a.cap;
@@ -299,64 +373,92 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   const int nr = rb - ra;
   const int RM = (k + CL - 1) / CL;
 
-  // all CTAs read the status before anyone can write it (first write follows
-  // a cluster barrier), so every CTA takes the same branches.
+  // every CTA reads the status before any CTA can write it (the first write
+  // follows a cluster barrier), so all CTAs take identical branches.
   const int64_t code0 = *reinterpret_cast<volatile const int64_t*>(&a.st->code);
   double dmax = a.st->diag_max, dmin = a.st->diag_min;
   if (code0 != 0) return;
 
   extern __shared__ unsigned char smem_raw[];
-  T* vs = reinterpret_cast<T*>(smem_raw);  // RM   s (row slice)
+  T* vs = reinterpret_cast<T*>(smem_raw);  // RM   s' -> s (own rows)
   T* vt = vs + RM;                         // RM   t
   T* vp = vt + RM;                         // RM   p
-  T* tmp = vp + RM;                        // RM   matvec output
-  T* c1 = tmp + RM;                        // cap
-  T* c2 = c1 + cap;                        // cap
-  T* zc = c2 + cap;                        // cap
-  T* red = zc + cap;                       // kLsWarps * kLsChunk
+  T* tmp = vp + RM;                        // RM
+  T* c1 = tmp + RM;                        // cap  Qs^T s  (then coefficients)
+  T* zc = c1 + cap;                        // cap  Qs^T p
+  T* c2 = zc + cap;                        // cap
+  T* to = c2 + cap;                        // cap  TRMV outputs
+  T* red = to + cap;                       // kLsWarps * kLsChunk
+  double* dred = reinterpret_cast<double*>(red);
+  __shared__ T bc[8];
 
+  // scratch layout (T elements)
+  const int64_t sA = 2 * (int64_t)cap + 8;     // exchange #1 stride per CTA
   T* scr = reinterpret_cast<T*>(a.scratch);
-  T* X1 = scr;                                   // CL x cap
-  T* X2 = X1 + (int64_t)kLsMaxCluster * cap;     // CL x cap
-  T* XZ = X2 + (int64_t)kLsMaxCluster * cap;     // CL x cap
-  T* N0 = XZ + (int64_t)kLsMaxCluster * cap;     // 16: sum s'^2
-  T* N1 = N0 + kLsMaxCluster;                    // 16: sum p^2
-  T* N2 = N1 + kLsMaxCluster;                    // 16: sum t^2
+  T* XA = scr;                                  // 16 x sA
+  T* XB = XA + kLsMaxCluster * sA;              // 16 x 8  exchange #2
+  T* XR = XB + kLsMaxCluster * 8;               // 16 x sA reorthogonalisation
+  T* AL = static_cast<T*>(a.alpha);             // cap: column norms alpha_j of T
+  T* myA = XA + rank * sA;
+  T* myB = XB + rank * 8;
+  T* myR = XR + rank * sA;
 
   T* S = static_cast<T*>(a.S);
   T* P = static_cast<T*>(a.P);
-  T* Qs = static_cast<T*>(a.Qs);
+  T* Qs = static_cast<T*>(a.Qs);  // unnormalised T
   T* Rinv = static_cast<T*>(a.Rinv);
   double* R = a.R;
-  // output slice of [0, nq) for the TRMVs
-  auto oslice = [&](int nq, int& o0, int& o1) {
-    o0 = (int)(((int64_t)rank * nq) / CL);
-    o1 = (int)(((int64_t)(rank + 1) * nq) / CL);
+  const bool fused = a.do_finalize && a.do_solve;
+  long long* trc = (rank == 0 && threadIdx.x == 0) ? a.trace : nullptr;
+#define SGS_TR(ix) \
+  do {             \
+    if (trc) trc[ix] = clock64(); \
+  } while (0)
+  SGS_TR(0);
+  auto slice = [&](int n, int& o0, int& o1) {
+    o0 = (int)(((int64_t)rank * n) / CL);
+    o1 = (int)(((int64_t)(rank + 1) * n) / CL);
   };
+  T tp = T(0), alpha = T(0);
 
   if (a.do_finalize) {
     const int i = a.col_fin;
-    T lss = T(0), lpp = T(0);
-    for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
-      const int r = ra + rr;
-      T sp;
-      const T pv = P[(int64_t)i * k + r];
-      if (i == 0 || a.s_partials == nullptr) {
-        sp = pv;  // column 1: s'_1 = p_1 (gram_schmidt.py:307-310)
-      } else {
-        double acc = 0.0;
-        for (int q = 0; q < a.s_nparts; ++q) acc += a.s_partials[(int64_t)q * k + r];
-        sp = from_double<T>(a.s_scale * acc);
-      }
-      vs[rr] = sp;
-      lss = fma(sp, sp, lss);
-      lpp = fma(pv, pv, lpp);
+    const int nq = i;
+    if (i == 0) {
+      for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vs[rr] = P[ra + rr];  // s'_1 = p_1
+    } else {
+      ls_reduce_parts<T>(a.s_partials, a.s_nparts, k, ra, nr, a.s_scale, vs, dred);
     }
-    const T ss = ls_cluster_sum(lss, N0, rank, CL, red, cl);
-    // N1 slot written after the N0 barrier: reuse the same barrier pattern
-    const T pp = ls_cluster_sum(lpp, N1, rank, CL, red, cl);
-    const double r_ii = (double)sqrt(ss);
-    const double tol = a.bf_ucrs * (double)sqrt(pp);
+    if (fused)
+      for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vp[rr] = P[(int64_t)(i + 1) * k + ra + rr];
+    __syncthreads();
+    SGS_TR(1);
+    // ---- exchange #1 ---------------------------------------------------------
+    T l0 = T(0), l1 = T(0);
+    for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
+      const T pv = P[(int64_t)i * k + ra + rr];
+      l0 = fma(vs[rr], vs[rr], l0);
+      l1 = fma(pv, pv, l1);
+    }
+    l0 = block_sum(l0, red);
+    l1 = block_sum(l1, red);
+    if (threadIdx.x == 0) { myA[0] = l0; myA[1] = l1; }
+    if (nq > 0) {
+      if (fused) ls_coldot<T, 2>(Qs + ra, k, nr, 0, nq, vs, vp, myA + 8, myA + 8 + cap);
+      else ls_coldot<T, 1>(Qs + ra, k, nr, 0, nq, vs, nullptr, myA + 8, nullptr);
+    }
+    SGS_TR(2);
+    cl.sync();
+    SGS_TR(3);
+    if (threadIdx.x < 2) bc[threadIdx.x] = ls_slot_sum(XA + threadIdx.x, sA, CL);
+    if (nq > 0) {
+      ls_gather<T>(XA + 8, sA, CL, 0, nq, AL, c1);              // T^T s' / alpha
+      if (fused) ls_gather<T>(XA + 8 + cap, sA, CL, 0, nq, AL, zc);  // Qs^T p
+    }
+    __syncthreads();
+    SGS_TR(4);
+    const double r_ii = (double)sqrt(bc[0]);
+    const double tol = a.bf_ucrs * (double)sqrt(bc[1]);
     if (r_ii <= tol || !(r_ii == r_ii)) {
       if (rank == 0 && threadIdx.x == 0) {
         a.st->code = (r_ii <= tol) ? SGS_ST_BREAKDOWN : SGS_ST_NONFINITE;
@@ -368,48 +470,81 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     }
     const T rT = (T)r_ii;
     for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
-      const T s = vs[rr] / rT;
-      vs[rr] = s;
-      S[(int64_t)i * k + ra + rr] = s;
+      const T sv = vs[rr] / rT;
+      vs[rr] = sv;
+      S[(int64_t)i * k + ra + rr] = sv;
+    }
+    for (int j = threadIdx.x; j < nq; j += blockDim.x) {
+      const T cj = c1[j] / rT;             // (Qs^T s)_j
+      c1[j] = cj;
+      c2[j] = cj / __ldcg(AL + j);         // coefficient on the unnormalised column T_j
     }
     __syncthreads();
-    // ---- append s_i to the QR of S: two classical GS passes -----------------
-    const int nq = i;
     if (nq > 0) {
-      ls_gemvT_rows<T>(Qs + ra, k, nr, nq, vs, X1 + (int64_t)rank * cap);
-      cl.sync();
-      ls_gather<T>(X1, CL, cap, nq, c1);
-      ls_matvec<T, false>(Qs + ra, k, 0, nr, 0, nq, c1, tmp, red);
+      ls_matvec<T, false>(Qs + ra, k, 0, nr, nq, c2, tmp, red);
       for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vt[rr] = vs[rr] - tmp[rr];
-      __syncthreads();
-      ls_gemvT_rows<T>(Qs + ra, k, nr, nq, vt, X2 + (int64_t)rank * cap);
-      cl.sync();
-      ls_gather<T>(X2, CL, cap, nq, c2);
-      ls_matvec<T, false>(Qs + ra, k, 0, nr, 0, nq, c2, tmp, red);
-      for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vt[rr] = vt[rr] - tmp[rr];
-      __syncthreads();
     } else {
       for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vt[rr] = vs[rr];
-      __syncthreads();
     }
-    T ltt = T(0);
-    for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) ltt = fma(vt[rr], vt[rr], ltt);
-    const T tt = ls_cluster_sum(ltt, N2, rank, CL, red, cl);
-    const T alpha = sqrt(tt);
-    for (int rr = threadIdx.x; rr < nr; rr += blockDim.x)
-      Qs[(int64_t)i * k + ra + rr] = alpha > T(0) ? vt[rr] / alpha : T(0);
-    // Rinv[:i, i] = -Rinv[:i, :i] (c1 + c2) / alpha ; Rinv[i, i] = 1/alpha
-    if (nq > 0) {
-      for (int j = threadIdx.x; j < nq; j += blockDim.x) c1[j] = c1[j] + c2[j];
+    __syncthreads();
+    SGS_TR(5);
+    // ---- exchange #2: ||t||^2 and t^T p (dot with the stored column, coldot pattern)
+    for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) Qs[(int64_t)i * k + ra + rr] = vt[rr];
+    T lt = T(0);
+    for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) lt = fma(vt[rr], vt[rr], lt);
+    lt = block_sum(lt, red);  // its __syncthreads also publishes the T_i stores
+    if (threadIdx.x == 0) myB[0] = lt;
+    if (fused) ls_coldot<T, 1>(Qs + ra, k, nr, i, i + 1, vp, nullptr, myB + 1 - i, nullptr);
+    cl.sync();
+    SGS_TR(6);
+    if (threadIdx.x < 2) bc[2 + threadIdx.x] = ls_slot_sum(XB + threadIdx.x, 8, CL);
+    __syncthreads();
+    T tt = bc[2];
+    tp = bc[3];
+    const T ss = bc[0] / (rT * rT);
+    if (nq > 0 && tt < T(0.5) * ss) {
+      // cancellation: second classical Gram-Schmidt pass on t
+      ls_coldot<T, 1>(Qs + ra, k, nr, 0, nq, vt, nullptr, myR + 8, nullptr);
+      cl.sync();
+      ls_gather<T>(XR + 8, sA, CL, 0, nq, AL, c2);
       __syncthreads();
-      int o0, o1;
-      oslice(nq, o0, o1);
-      ls_matvec<T, true>(Rinv, cap, o0, o1, 0, nq, c1, tmp, red);
-      for (int o = o0 + threadIdx.x; o < o1; o += blockDim.x)
-        Rinv[(int64_t)i * cap + o] = alpha > T(0) ? -tmp[o - o0] / alpha : T(0);
+      for (int j = threadIdx.x; j < nq; j += blockDim.x) {
+        c1[j] = c1[j] + c2[j];
+        c2[j] = c2[j] / __ldcg(AL + j);
+      }
+      __syncthreads();
+      ls_matvec<T, false>(Qs + ra, k, 0, nr, nq, c2, tmp, red);
+      for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
+        const T t2 = vt[rr] - tmp[rr];
+        vt[rr] = t2;
+        Qs[(int64_t)i * k + ra + rr] = t2;
+      }
+      T l2 = T(0);
+      for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) l2 = fma(vt[rr], vt[rr], l2);
+      l2 = block_sum(l2, red);
+      if (threadIdx.x == 0) myR[0] = l2;
+      if (fused) ls_coldot<T, 1>(Qs + ra, k, nr, i, i + 1, vp, nullptr, myR + 1 - i, nullptr);
+      cl.sync();
+      if (threadIdx.x < 2) bc[4 + threadIdx.x] = ls_slot_sum(XR + threadIdx.x, sA, CL);
+      __syncthreads();
+      tt = bc[4];
+      tp = bc[5];
     }
-    if (rank == 0 && threadIdx.x == 0) {
+    SGS_TR(7);
+    alpha = sqrt(tt);
+    // R_S^{-1} column i on this CTA's slice of [0, i+1): -R_S^{-1}[:i,:i] c1 / alpha
+    int u0, u1;
+    slice(i + 1, u0, u1);
+    const int u1c = min(u1, nq);
+    if (u0 < u1c) {
+      ls_matvec<T, true>(Rinv, cap, u0, u1c, nq, c1, to, red);
+      for (int o = u0 + threadIdx.x; o < u1c; o += blockDim.x)
+        Rinv[(int64_t)i * cap + o] = alpha > T(0) ? -to[o - u0] / alpha : T(0);
+    }
+    if (threadIdx.x == 0 && u0 <= i && i < u1)
       Rinv[(int64_t)i * cap + i] = alpha > T(0) ? T(1) / alpha : T(0);
+    if (rank == 0 && threadIdx.x == 0) {
+      AL[i] = alpha;
       R[(int64_t)i * cap + i] = r_ii;
     }
     const double ad = (double)alpha;
@@ -421,81 +556,72 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
       a.st->ncols = i + 1;
       a.st->r_ii = r_ii;
     }
+    __syncthreads();
+    SGS_TR(8);
   }
 
   if (a.do_solve) {
-    const int col = a.col_sol;
-    const int nq = col;
-    if (a.do_finalize) cl.sync();  // Qs[:, i] and Rinv[:, i] visible cluster-wide
-    for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
-      const int r = ra + rr;
-      T pv;
+    const int c = a.col_sol;
+    const int nq = c;  // columns 0..c-1 of T
+    if (!fused) {
       if (a.p_partials != nullptr) {
-        double acc = 0.0;
-        for (int q = 0; q < a.p_nparts; ++q) acc += a.p_partials[(int64_t)q * k + r];
-        pv = from_double<T>(a.p_scale * acc);
-        P[(int64_t)col * k + r] = pv;
+        ls_reduce_parts<T>(a.p_partials, a.p_nparts, k, ra, nr, a.p_scale, vp, dred);
+        for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) P[(int64_t)c * k + ra + rr] = vp[rr];
       } else {
-        pv = P[(int64_t)col * k + r];
+        for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vp[rr] = P[(int64_t)c * k + ra + rr];
       }
-      vp[rr] = pv;
+      __syncthreads();
+    }
+    // rank check of the sketched basis (gram_schmidt.py:186-189)
+    if (dmin < 1e-8 * fmax(dmax, 1.0)) {
+      if (rank == 0 && threadIdx.x == 0) {
+        a.st->code = SGS_ST_RANK;
+        a.st->column = c + 1;
+      }
+      return;
+    }
+    if (fused) {
+      if (threadIdx.x == 0) zc[c - 1] = tp / alpha;  // = (T_{c-1}^T p) / alpha_{c-1}
+    } else {
+      ls_coldot<T, 1>(Qs + ra, k, nr, 0, nq, vp, nullptr, myA + 8 + cap, nullptr);
+      cl.sync();
+      ls_gather<T>(XA + 8 + cap, sA, CL, 0, nq, AL, zc);
     }
     __syncthreads();
-    if (nq > 0) {
-      // rank check of the sketched basis (gram_schmidt.py:186-189)
-      if (dmin < 1e-8 * fmax(dmax, 1.0)) {
-        if (rank == 0 && threadIdx.x == 0) {
-          a.st->code = SGS_ST_RANK;
-          a.st->column = col + 1;
-        }
-        return;
-      }
-      ls_gemvT_rows<T>(Qs + ra, k, nr, nq, vp, XZ + (int64_t)rank * cap);
-      cl.sync();
-      ls_gather<T>(XZ, CL, cap, nq, zc);
-      int o0, o1;
-      oslice(nq, o0, o1);
-      ls_matvec<T, true>(Rinv, cap, o0, o1, 0, nq, zc, tmp, red);
-      for (int o = o0 + threadIdx.x; o < o1; o += blockDim.x) {
-        const T r = tmp[o - o0];
-        R[(int64_t)col * cap + o] = (double)r;
-        if (a.coarse_dtype == SGS_F32) static_cast<float*>(a.r_crs)[o] = cvt<float>(r);
-        else static_cast<double*>(a.r_crs)[o] = (double)r;
-      }
+    SGS_TR(9);
+    int o0, o1;
+    slice(nq, o0, o1);
+    ls_matvec<T, true>(Rinv, cap, o0, o1, nq, zc, to, red);
+    for (int o = o0 + threadIdx.x; o < o1; o += blockDim.x) {
+      const T r = to[o - o0];
+      R[(int64_t)c * cap + o] = (double)r;
+      if (a.coarse_dtype == SGS_F32) static_cast<float*>(a.r_crs)[o] = cvt<float>(r);
+      else static_cast<double*>(a.r_crs)[o] = (double)r;
     }
+    SGS_TR(10);
   }
+#undef SGS_TR
 }
 
 static size_t ls_smem_bytes(int k, int cap, int CL, size_t esize) {
   const int RM = (k + CL - 1) / CL;
-  return (size_t)(4 * RM + 3 * cap + kLsWarps * kLsChunk + 8) * esize;
+  size_t n = (size_t)(4 * RM + 4 * cap + kLsWarps * kLsChunk + 8) * esize;
+  const size_t dmin = (size_t)(4 * RM + 4 * cap) * esize + 512 * sizeof(double) + 64;
+  return n > dmin ? n : dmin;
 }
 
 template <typename T>
 static int launch_ls(const sgs_ls_args* a, cudaStream_t s) {
   const int CL = ls_cluster_size_host(a->k);
   const size_t smem = ls_smem_bytes(a->k, a->cap, CL, sizeof(T));
+  if (smem > 227 * 1024) {
+    set_error("ls_step: k=%d cap=%d needs %zu bytes of shared memory", a->k, a->cap, smem);
+    return SGS_EINVAL;
+  }
   auto kern = ls_step_kernel<T>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (CL > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(CL, 1, 1);
-  cfg.blockDim = dim3(kLsThreads, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, *a);
-  if (e != cudaSuccess) {
-    set_error("ls_step_kernel launch (cluster %d, smem %zu): %s", CL, smem, cudaGetErrorString(e));
-    return SGS_ECUDA;
-  }
-  return check_launch("ls_step_kernel");
+  return check_ex(launch_ex(kern, dim3(CL), dim3(kLsThreads), smem, s, CL, *a), "ls_step_kernel");
 }
 
 }  // namespace sgs
@@ -515,15 +641,15 @@ extern "C" int sgs_rgs_update(void* Q, int q_dtype, int64_t ldq, int64_t n, int 
   const int64_t nthr = (n + V - 1) / V;
   const unsigned blocks = (unsigned)((nthr + kUpdThreads - 1) / kUpdThreads);
   const size_t smem = (size_t)(i > 0 ? i : 1) * (q_dtype == SGS_F32 ? 4 : 8);
+  cudaError_t err = cudaSuccess;
 #define SGS_UPD(TQ, TW)                                                                      \
   do {                                                                                       \
     auto kern = rgs_update_kernel<TQ, TW>;                                                   \
     if (smem > 48 * 1024)                                                                    \
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
-    kern<<<blocks, kUpdThreads, smem, s>>>(static_cast<TQ*>(Q), ldq, n, i,                   \
-                                           static_cast<const TW*>(w),                        \
-                                           static_cast<const TQ*>(r_crs), normalize_prev, R, \
-                                           ldr, st);                                         \
+    err = launch_ex(kern, dim3(blocks), dim3(kUpdThreads), smem, s, 1, static_cast<TQ*>(Q),   \
+                    ldq, n, i, static_cast<const TW*>(w), static_cast<const TQ*>(r_crs),     \
+                    normalize_prev, R, ldr, st);                                             \
   } while (0)
   if (q_dtype == SGS_F32 && w_dtype == SGS_F32) SGS_UPD(float, float);
   else if (q_dtype == SGS_F32 && w_dtype == SGS_F64) SGS_UPD(float, double);
@@ -534,7 +660,7 @@ extern "C" int sgs_rgs_update(void* Q, int q_dtype, int64_t ldq, int64_t n, int 
     return SGS_EINVAL;
   }
 #undef SGS_UPD
-  return check_launch("rgs_update_kernel");
+  return check_ex(err, "rgs_update_kernel");
 }
 
 extern "C" int sgs_normalize_column(void* Q, int q_dtype, int64_t ldq, int64_t n, int col,
@@ -546,12 +672,12 @@ extern "C" int sgs_normalize_column(void* Q, int q_dtype, int64_t ldq, int64_t n
   if (blocks > 4 * 148 * 4) blocks = 4 * 148 * 4;
   const double* rjj = R + (int64_t)col * ldr + col;
   if (q_dtype == SGS_F32)
-    normalize_column_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(
-        static_cast<float*>(Q) + (int64_t)col * ldq, n, rjj, st);
-  else
-    normalize_column_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(
-        static_cast<double*>(Q) + (int64_t)col * ldq, n, rjj, st);
-  return check_launch("normalize_column_kernel");
+    return check_ex(launch_ex(normalize_column_kernel<float>, dim3((unsigned)blocks), dim3(256), 0,
+                              s, 1, static_cast<float*>(Q) + (int64_t)col * ldq, n, rjj, st),
+                    "normalize_column_kernel");
+  return check_ex(launch_ex(normalize_column_kernel<double>, dim3((unsigned)blocks), dim3(256), 0,
+                            s, 1, static_cast<double*>(Q) + (int64_t)col * ldq, n, rjj, st),
+                  "normalize_column_kernel");
 }
 
 extern "C" int sgs_gemv_f64(const void* A, int a_dtype, int64_t lda, int64_t n, int ncols,
@@ -583,13 +709,14 @@ extern "C" int sgs_transpose(const void* src, int64_t lds, void* dst, int64_t ld
 
 extern "C" int64_t sgs_ls_scratch_elems(int k, int cap) {
   (void)k;
-  return 3 * (int64_t)kLsMaxCluster * cap + 4 * kLsMaxCluster;
+  const int64_t sA = 2 * (int64_t)cap + 8;
+  return 2 * kLsMaxCluster * sA + kLsMaxCluster * 8 + cap + 64;
 }
 
 extern "C" int sgs_ls_cluster_size(int k) { return ls_cluster_size_host(k); }
 
 extern "C" int sgs_ls_step(const sgs_ls_args* a, void* stream) {
-  SGS_REQUIRE(a && a->st && a->S && a->P && a->R && a->Qs && a->Rinv && a->scratch,
+  SGS_REQUIRE(a && a->st && a->S && a->P && a->R && a->Qs && a->Rinv && a->alpha && a->scratch,
               "ls_step: null pointer");
   SGS_REQUIRE(a->k >= 1 && a->cap >= 1 && a->cap <= 8192 && a->k <= 65536, "ls_step: bad sizes");
   SGS_REQUIRE(!a->do_finalize || (a->col_fin >= 0 && a->col_fin < a->cap), "ls_step: bad col_fin");

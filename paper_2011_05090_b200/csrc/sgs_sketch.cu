@@ -12,7 +12,10 @@
 // is written; a fixed-order reduction produces y.  Padding tiles are never
 // read.  Deterministic for a fixed (n_local, log2_block).
 
+#include <cooperative_groups.h>
 #include "sgs_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace sgs {
 
@@ -72,9 +75,14 @@ template <typename TX>
 __device__ __forceinline__ double load_as_double(const TX* p) { return (double)__ldg(p); }
 
 constexpr int kSrhtThreads = 512;
-constexpr int kSrhtMaxLogT = 12;  // 4096-row tiles (32 KB of fp64)
-constexpr int kSrhtTargetCTAs = 148;
+constexpr int kSrhtMaxLogT = 12;   // 4096-row tiles (32 KB of fp64)
+constexpr int kSrhtTargetCTAs = 296;
+constexpr int kSrhtCluster = 8;    // CTAs whose k-vector partials are combined through DSMEM
 
+// One CTA transforms `tiles_per_cta` consecutive tiles and accumulates the
+// signed sampled entries into a shared k-vector; the 8 CTAs of a cluster then
+// sum their k-vectors through distributed shared memory in rank order, each
+// CTA writing 1/8 of the group partial.  Output: one k-vector per cluster.
 template <typename TX, int LOGT>
 __global__ void __launch_bounds__(kSrhtThreads)
 srht_partials_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local,
@@ -82,13 +90,16 @@ srht_partials_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local,
                      const int32_t* __restrict__ samples, int k, int tiles_per_cta,
                      int64_t ntiles, double* __restrict__ partials,
                      const sgs_status* st) {
-  if (status_stopped(st)) return;
+  cg::cluster_group cl = cg::this_cluster();
+  pdl_enter();
+  if (status_stopped(st)) return;  // uniform across the cluster: nobody writes st here
   constexpr int T = 1 << LOGT;
   extern __shared__ double smem[];
   double* z = smem;                       // pidx(T) entries
   double* part = smem + pidx(T) + 8;      // k entries
+  int32_t* smp = reinterpret_cast<int32_t*>(part + k);  // k entries
   const int col = blockIdx.y;
-  const int nparts = gridDim.x;
+  const int ngroups = gridDim.x / kSrhtCluster;
   const TX* x = X + (int64_t)col * ldx;
 
   for (int j = threadIdx.x; j < k; j += blockDim.x) part[j] = 0.0;
@@ -96,12 +107,18 @@ srht_partials_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local,
   const int64_t t0 = (int64_t)blockIdx.x * tiles_per_cta;
   const int64_t t1 = min(t0 + tiles_per_cta, ntiles);
   const int64_t bmask = (int64_t(1) << log2_block) - 1;
+  int64_t cur_blk = -1;
   for (int64_t t = t0; t < t1; ++t) {
     const int64_t lr0 = t * T;            // first local row of the tile
     const int64_t g0 = row0 + lr0;        // first global row
     const int64_t blk = g0 >> log2_block;
     const int64_t h = (g0 & bmask) >> LOGT;
     __syncthreads();                      // previous tile's gather is done
+    if (blk != cur_blk) {
+      const int32_t* sb = samples + blk * (int64_t)k;
+      for (int j = threadIdx.x; j < k; j += blockDim.x) smp[j] = __ldg(sb + j);
+      cur_blk = blk;
+    }
     for (int e = threadIdx.x; e < T; e += blockDim.x) {
       const int64_t lr = lr0 + e;
       double v = 0.0;
@@ -114,21 +131,29 @@ srht_partials_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local,
     }
     __syncthreads();
     fwht_tile<LOGT>(z);
-    const int32_t* smp = samples + blk * (int64_t)k;
     for (int j = threadIdx.x; j < k; j += blockDim.x) {
-      const int32_t r = __ldg(smp + j);
+      const int32_t r = smp[j];
       const double v = z[pidx(r & (T - 1))];
       const int64_t rh = (int64_t)(r >> LOGT);
       part[j] += (__popcll(rh & h) & 1) ? -v : v;
     }
   }
-  __syncthreads();
-  double* out = partials + ((int64_t)col * nparts + blockIdx.x) * k;
-  for (int j = threadIdx.x; j < k; j += blockDim.x) out[j] = part[j];
+  cl.sync();  // all k-vectors of the cluster are final
+  const int rank = (int)cl.block_rank();
+  const int j0 = (int)(((int64_t)rank * k) / kSrhtCluster);
+  const int j1 = (int)(((int64_t)(rank + 1) * k) / kSrhtCluster);
+  double* out = partials + ((int64_t)col * ngroups + blockIdx.x / kSrhtCluster) * k;
+  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < kSrhtCluster; ++q) s += cl.map_shared_rank(part, q)[j];
+    out[j] = s;
+  }
+  cl.sync();  // keep shared memory alive until every CTA has read it
 }
 
 static void srht_geometry(int64_t n_local, int log2_block, int* logt, int64_t* ntiles,
-                          int* tpc, int* nparts) {
+                          int* tpc, int* nctas) {
   const int lt = log2_block < kSrhtMaxLogT ? log2_block : kSrhtMaxLogT;
   const int64_t T = int64_t(1) << lt;
   const int64_t nt = (n_local + T - 1) / T;
@@ -136,38 +161,41 @@ static void srht_geometry(int64_t n_local, int log2_block, int* logt, int64_t* n
   *logt = lt;
   *ntiles = nt;
   *tpc = (int)(per < 1 ? 1 : per);
-  *nparts = (int)((nt + *tpc - 1) / *tpc);
+  int64_t c = (nt + *tpc - 1) / *tpc;
+  c = (c + kSrhtCluster - 1) / kSrhtCluster * kSrhtCluster;
+  *nctas = (int)c;
 }
 
 template <typename TX, int LOGT>
 static int launch_srht_t(const void* X, int64_t ldx, int ncols, int64_t n_local, int64_t row0,
                          int log2_block, const uint32_t* sign_bits, const int32_t* samples,
                          int k, double* partials, const sgs_status* st, cudaStream_t s,
-                         int tpc, int64_t ntiles, int nparts) {
+                         int tpc, int64_t ntiles, int nctas) {
   constexpr int T = 1 << LOGT;
-  const size_t smem = (size_t)(T + T / 8 + 8 + k) * sizeof(double);
+  const size_t smem = (size_t)(T + T / 8 + 8 + k) * sizeof(double) + (size_t)k * sizeof(int32_t);
   auto kern = srht_partials_kernel<TX, LOGT>;
   if (smem > 48 * 1024) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
   int threads = kSrhtThreads;
-  if (T / 8 < threads) threads = (T / 8 < 32) ? 32 : T / 8;
-  if (threads < 128 && k > 1024) threads = 128;
-  dim3 grid(nparts, ncols);
-  kern<<<grid, threads, smem, s>>>(static_cast<const TX*>(X), ldx, n_local, row0, log2_block,
-                                  sign_bits, samples, k, tpc, ntiles, partials, st);
-  return check_launch("srht_partials_kernel");
+  if (T / 8 < threads) threads = (T / 8 < 64) ? 64 : T / 8;
+  if (threads < 256 && k > 1024) threads = 256;
+  dim3 grid(nctas, ncols);
+  return check_ex(launch_ex(kern, grid, dim3(threads), smem, s, kSrhtCluster,
+                            static_cast<const TX*>(X), ldx, n_local, row0, log2_block, sign_bits,
+                            samples, k, tpc, ntiles, partials, st),
+                  "srht_partials_kernel");
 }
 
 template <typename TX>
 static int launch_srht(int logt, const void* X, int64_t ldx, int ncols, int64_t n_local,
                        int64_t row0, int log2_block, const uint32_t* sign_bits,
                        const int32_t* samples, int k, double* partials, const sgs_status* st,
-                       cudaStream_t s, int tpc, int64_t ntiles, int nparts) {
+                       cudaStream_t s, int tpc, int64_t ntiles, int nctas) {
 #define SGS_SRHT_CASE(L)                                                                   \
   case L:                                                                                  \
     return launch_srht_t<TX, L>(X, ldx, ncols, n_local, row0, log2_block, sign_bits,       \
-                                samples, k, partials, st, s, tpc, ntiles, nparts);
+                                samples, k, partials, st, s, tpc, ntiles, nctas);
   switch (logt) {
     SGS_SRHT_CASE(0) SGS_SRHT_CASE(1) SGS_SRHT_CASE(2) SGS_SRHT_CASE(3) SGS_SRHT_CASE(4)
     SGS_SRHT_CASE(5) SGS_SRHT_CASE(6) SGS_SRHT_CASE(7) SGS_SRHT_CASE(8) SGS_SRHT_CASE(9)
@@ -202,6 +230,7 @@ __global__ void __launch_bounds__(512)
 dense_gemv_kernel(const double* __restrict__ thetaT, int64_t ldt, int k,
                   const TX* __restrict__ x, int64_t n, double* __restrict__ partials,
                   const sgs_status* st) {
+  pdl_enter();
   if (status_stopped(st)) return;
   const int p = blockIdx.x, nparts = gridDim.x;
   const int64_t r0 = chunk_begin(n, nparts, p), r1 = chunk_begin(n, nparts, p + 1);
@@ -261,6 +290,7 @@ __global__ void __launch_bounds__(256)
 dense_gemm_kernel(const double* __restrict__ thetaT, int64_t ldt, int k,
                   const TX* __restrict__ X, int64_t ldx, int ncols, int64_t n,
                   double* __restrict__ partials, const sgs_status* st) {
+  pdl_enter();
   if (status_stopped(st)) return;
   __shared__ double As[kGBR][kGBJ];
   __shared__ double Bs[kGBR][kGBC + 1];
@@ -313,13 +343,12 @@ template <typename TY>
 __global__ void partials_reduce_kernel(const double* __restrict__ partials, int nparts, int k,
                                        int ncols, double scale, TY* __restrict__ Y, int64_t ldy,
                                        const sgs_status* st) {
+  pdl_enter();
   if (status_stopped(st)) return;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)k * ncols) return;
   const int c = (int)(idx / k), j = (int)(idx % k);
-  const double* p = partials + (int64_t)c * nparts * k + j;
-  double acc = 0.0;
-  for (int q = 0; q < nparts; ++q) acc += __ldg(p + (int64_t)q * k);
+  const double acc = canon_sum(partials + (int64_t)c * nparts * k + j, k, nparts);
   Y[(int64_t)c * ldy + j] = from_double<TY>(scale * acc);
 }
 
@@ -365,11 +394,11 @@ static int launch_fwht_tile(double* X, int64_t ldx, int64_t ntile, int ncols, cu
 using namespace sgs;
 
 extern "C" int sgs_srht_nparts(int64_t n_local, int log2_block) {
-  int lt, tpc, np;
+  int lt, tpc, nc;
   int64_t nt;
   if (n_local < 1 || log2_block < 0 || log2_block > 40) return 0;
-  srht_geometry(n_local, log2_block, &lt, &nt, &tpc, &np);
-  return np;
+  srht_geometry(n_local, log2_block, &lt, &nt, &tpc, &nc);
+  return nc / kSrhtCluster;
 }
 
 extern "C" int sgs_srht_partials(const void* X, int x_dtype, int64_t ldx, int ncols,
@@ -383,7 +412,7 @@ extern "C" int sgs_srht_partials(const void* X, int x_dtype, int64_t ldx, int nc
   SGS_REQUIRE(x_dtype == SGS_F32 || x_dtype == SGS_F64, "srht: bad dtype");
   int lt, tpc, np;
   int64_t nt;
-  srht_geometry(n_local, log2_block, &lt, &nt, &tpc, &np);
+  srht_geometry(n_local, log2_block, &lt, &nt, &tpc, &np);  // np = CTAs
   SGS_REQUIRE((row0 & ((int64_t(1) << lt) - 1)) == 0, "srht: row0 %lld not tile aligned",
               (long long)row0);
   cudaStream_t s = as_stream(stream);
@@ -407,23 +436,24 @@ static int launch_dense(const double* thetaT, int64_t ldt, int k, const void* X,
     int threads = ((kp + 31) / 32) * 32;
     if (threads > 512) threads = 512;
     const int qp = (kp + threads - 1) / threads;
+    cudaError_t e;
     if (qp <= 1)
-      dense_gemv_kernel<TX, 1><<<np, threads, 0, s>>>(thetaT, ldt, k, x, n, partials, st);
+      e = launch_ex(dense_gemv_kernel<TX, 1>, dim3(np), dim3(threads), 0, s, 1, thetaT, ldt, k, x, n, partials, st);
     else if (qp <= 2)
-      dense_gemv_kernel<TX, 2><<<np, threads, 0, s>>>(thetaT, ldt, k, x, n, partials, st);
+      e = launch_ex(dense_gemv_kernel<TX, 2>, dim3(np), dim3(threads), 0, s, 1, thetaT, ldt, k, x, n, partials, st);
     else if (qp <= 4)
-      dense_gemv_kernel<TX, 4><<<np, threads, 0, s>>>(thetaT, ldt, k, x, n, partials, st);
+      e = launch_ex(dense_gemv_kernel<TX, 4>, dim3(np), dim3(threads), 0, s, 1, thetaT, ldt, k, x, n, partials, st);
     else if (qp <= 8)
-      dense_gemv_kernel<TX, 8><<<np, threads, 0, s>>>(thetaT, ldt, k, x, n, partials, st);
+      e = launch_ex(dense_gemv_kernel<TX, 8>, dim3(np), dim3(threads), 0, s, 1, thetaT, ldt, k, x, n, partials, st);
     else {
       set_error("dense sketch: k=%d too large", k);
       return SGS_EINVAL;
     }
-    return check_launch("dense_gemv_kernel");
+    return check_ex(e, "dense_gemv_kernel");
   }
   dim3 grid((k + kGBJ - 1) / kGBJ, (ncols + kGBC - 1) / kGBC, np);
-  dense_gemm_kernel<TX><<<grid, 256, 0, s>>>(thetaT, ldt, k, x, ldx, ncols, n, partials, st);
-  return check_launch("dense_gemm_kernel");
+  return check_ex(launch_ex(dense_gemm_kernel<TX>, grid, dim3(256), 0, s, 1, thetaT, ldt, k, x,
+                            ldx, ncols, n, partials, st), "dense_gemm_kernel");
 }
 
 extern "C" int sgs_dense_partials(const double* thetaT, int64_t ldt, int k, const void* X,
@@ -449,16 +479,15 @@ extern "C" int sgs_partials_reduce(const double* partials, int nparts, int k, in
   const int threads = 256;
   const unsigned blocks = (unsigned)((tot + threads - 1) / threads);
   if (y_dtype == SGS_F64)
-    partials_reduce_kernel<double><<<blocks, threads, 0, s>>>(partials, nparts, k, ncols, scale,
-                                                              static_cast<double*>(Y), ldy, st);
-  else if (y_dtype == SGS_F32)
-    partials_reduce_kernel<float><<<blocks, threads, 0, s>>>(partials, nparts, k, ncols, scale,
-                                                             static_cast<float*>(Y), ldy, st);
-  else {
-    set_error("reduce: bad dtype");
-    return SGS_EINVAL;
-  }
-  return check_launch("partials_reduce_kernel");
+    return check_ex(launch_ex(partials_reduce_kernel<double>, dim3(blocks), dim3(threads), 0, s,
+                              1, partials, nparts, k, ncols, scale, static_cast<double*>(Y), ldy,
+                              st), "partials_reduce_kernel");
+  if (y_dtype == SGS_F32)
+    return check_ex(launch_ex(partials_reduce_kernel<float>, dim3(blocks), dim3(threads), 0, s,
+                              1, partials, nparts, k, ncols, scale, static_cast<float*>(Y), ldy,
+                              st), "partials_reduce_kernel");
+  set_error("reduce: bad dtype");
+  return SGS_EINVAL;
 }
 
 extern "C" int sgs_fwht(double* X, int64_t s_len, int ncols, int64_t ldx, void* stream) {

@@ -183,24 +183,27 @@ class RgsState:
         dev, k = self.device, self.k
         old = None
         if self._cap:
-            old = (self._Q, self._R, self._S, self._P, self._Qs, self._Rinv, self._cap)
+            old = (self._Q, self._R, self._S, self._P, self._Qs, self._Rinv, self._alpha,
+                   self._cap)
         self._Q = torch.zeros((cap, self.ldq), dtype=self.cdt, device=dev)
         self._R = torch.zeros((cap, cap), dtype=torch.float64, device=dev)
         self._S = torch.zeros((cap, k), dtype=self.fdt, device=dev)
         self._P = torch.zeros((cap, k), dtype=self.fdt, device=dev)
         self._Qs = torch.zeros((cap, k), dtype=self.fdt, device=dev)
         self._Rinv = torch.zeros((cap, cap), dtype=self.fdt, device=dev)
+        self._alpha = torch.zeros(cap, dtype=self.fdt, device=dev)
         self._scratch = torch.zeros(int(_lib.load().sgs_ls_scratch_elems(k, cap)),
                                     dtype=torch.float64, device=dev)
         self._rc = torch.zeros(cap, dtype=self.cdt, device=dev)
         if old is not None:
-            Q, R, S, P, Qs, Rinv, oc = old
+            Q, R, S, P, Qs, Rinv, alpha, oc = old
             self._Q[:oc] = Q
             self._R[:oc, :oc] = R
             self._S[:oc] = S
             self._P[:oc] = P
             self._Qs[:oc] = Qs
             self._Rinv[:oc, :oc] = Rinv
+            self._alpha[:oc] = alpha
         self._cap = cap
 
     def _grow(self) -> None:
@@ -224,9 +227,18 @@ class RgsState:
         a.p_scale = p_scale
         a.bf_ucrs = self.breakdown_factor * self.policy.u_crs
         a.S, a.P, a.R = self._S.data_ptr(), self._P.data_ptr(), self._R.data_ptr()
-        a.Qs, a.Rinv = self._Qs.data_ptr(), self._Rinv.data_ptr()
+        a.Qs, a.Rinv, a.alpha = self._Qs.data_ptr(), self._Rinv.data_ptr(), self._alpha.data_ptr()
         a.scratch, a.r_crs, a.st = self._scratch.data_ptr(), self._rc.data_ptr(), self.status.ptr
+        a.trace = self._trace_ptr(fin if fin is not None else sol)
         _lib.check(_lib.load().sgs_ls_step(ctypes_byref(a), stream_ptr()), "sgs_ls_step")
+
+    _trace = None  # optional (cap, 16) int64 device tensor: per-column LS phase clocks
+
+    def _trace_ptr(self, col):
+        t = self._trace
+        if t is None or col is None or col >= t.shape[0]:
+            return None
+        return t.data_ptr() + col * t.shape[1] * 8
 
     def _sketch_parts(self, x_ptr: int, x_code: int, ldx: int, out: torch.Tensor,
                       kvec: torch.Tensor | None):
