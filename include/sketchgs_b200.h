@@ -117,6 +117,20 @@ int sgs_rgs_update(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
                    int normalize_prev, const double* R, int64_t ldr,
                    const sgs_status* st, void* stream);
 
+/* Fused column kernel: sgs_rgs_update plus, when do_sketch != 0, the P-SRHT /
+ * block-SRHT sketch of the new column (step 4, gram_schmidt.py:320) in the
+ * epilogue, without re-reading q'.  One CTA per 4096-row tile (requires
+ * log2_block >= 12 and row0 % 4096 == 0), Q streamed through a TMA bulk-copy
+ * ring; partials as sgs_srht_partials, one k-vector per 8-CTA cluster,
+ * sgs_column_nparts(n_local) of them. */
+int sgs_column_nparts(int64_t n_local);
+int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
+                        const void* w, int w_dtype, const void* r_crs,
+                        int normalize_prev, const double* R, int64_t ldr,
+                        int do_sketch, int64_t row0, int log2_block,
+                        const uint32_t* sign_bits, const int32_t* samples, int k,
+                        double* partials, const sgs_status* st, void* stream);
+
 /* Q[:, col] = cast_crs(Q[:, col] / R[col, col])   (gram_schmidt.py:329) */
 int sgs_normalize_column(void* Q, int q_dtype, int64_t ldq, int64_t n,
                          int col, const double* R, int64_t ldr,

@@ -61,6 +61,10 @@ _SIGS = {
     "sgs_fwht": (c_int, [c_void_p, c_int64, c_int, c_int64, c_void_p]),
     "sgs_rgs_update": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_void_p, c_int,
                                c_void_p, c_int, c_void_p, c_int64, c_void_p, c_void_p]),
+    "sgs_column_nparts": (c_int, [c_int64]),
+    "sgs_rgs_update_srht": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_void_p, c_int,
+                                    c_void_p, c_int, c_void_p, c_int64, c_int, c_int64, c_int,
+                                    c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
     "sgs_normalize_column": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_void_p,
                                      c_int64, c_void_p, c_void_p]),
     "sgs_gemv_f64": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_void_p, c_void_p,

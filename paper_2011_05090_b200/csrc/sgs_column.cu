@@ -1,0 +1,302 @@
+// Fused RGS column kernel on sm_100a: the projection update of step 3
+// (gram_schmidt.py:316-319) with the P-SRHT sketch of the new column (step 4,
+// gram_schmidt.py:320 -> sketch.py:182-184) in its epilogue.
+//
+// Each CTA owns one 4096-row tile of Q.  It streams Q[:, :i] for its rows with
+// evict-first 128-bit loads (8 columns in flight per thread), forms
+// q'_i = cast_crs(w) - Q_{i-1} r in registers, stores it, and then - without
+// re-reading q' - flips the signs, runs the 4096-point Walsh-Hadamard
+// transform (3 bits in registers, 9 bits in three shared-memory radix-8
+// passes), gathers the k sampled rows with the cross-tile sign
+// (-1)^popcount(r_hi & tile), and sums the k-vectors of its 8-CTA cluster
+// through distributed shared memory.  One partial k-vector per cluster is
+// written, exactly as sgs_srht_partials would for a one-tile-per-CTA grid.
+
+#include <cooperative_groups.h>
+#include "sgs_common.cuh"
+#include "sgs_fwht.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace sgs {
+
+constexpr int kColThreads = 512;
+constexpr int kColLogT = 12;
+constexpr int kColT = 1 << kColLogT;
+constexpr int kColCluster = 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* mb, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(mb)), "r"(parity) : "memory");
+}
+// 1-D TMA bulk copy global -> shared with an L2 evict-first hint (the Q stream
+// is read once per column and must not evict the reused k-dimensional state).
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* mb, uint64_t policy) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)),
+               "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(mb)),
+      "l"(policy) : "memory");
+}
+
+template <typename TQ> struct ColCfg;
+template <> struct ColCfg<float> { static constexpr int kStages = 4; };
+template <> struct ColCfg<double> { static constexpr int kStages = 3; };
+
+template <typename TQ>
+__host__ __device__ constexpr size_t col_stage_bytes() { return (size_t)kColT * sizeof(TQ); }
+
+template <typename TQ>
+__host__ __device__ constexpr size_t col_ring_bytes() {
+  // the FWHT buffer of the epilogue aliases the ring (used after the stream)
+  return col_stage_bytes<TQ>() * ColCfg<TQ>::kStages > (size_t)(kColT + kColT / 8 + 8) * 8
+             ? col_stage_bytes<TQ>() * ColCfg<TQ>::kStages
+             : (size_t)(kColT + kColT / 8 + 8) * 8;
+}
+
+template <typename TQ, typename TW>
+__global__ void __launch_bounds__(kColThreads)
+rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
+                  const TW* __restrict__ w, const TQ* __restrict__ rc, int normalize_prev,
+                  const double* __restrict__ R, int64_t ldr, int do_sketch, int64_t row0,
+                  int log2_block, const uint32_t* __restrict__ sign_bits,
+                  const int32_t* __restrict__ samples, int k, double* __restrict__ partials,
+                  const sgs_status* st) {
+  cg::cluster_group cl = cg::this_cluster();
+  constexpr int V = VecT<TQ>::N;                  // rows per vector (4 fp32, 2 fp64)
+  constexpr int NH = kColT / (kColThreads * V);   // vectors per thread (2 fp32, 4 fp64)
+  constexpr int LV = (V == 4) ? 2 : 1;            // log2 V
+  constexpr int HB = kColLogT - ((NH == 2) ? 1 : 2);  // first element bit carried by h
+  constexpr int S = ColCfg<TQ>::kStages;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  TQ* ring = reinterpret_cast<TQ*>(smem_raw);                        // S x 4096
+  double* z = reinterpret_cast<double*>(smem_raw);                   // aliases the ring
+  double* part = reinterpret_cast<double*>(smem_raw + col_ring_bytes<TQ>());  // k
+  int32_t* smp = reinterpret_cast<int32_t*>(part + k);               // k
+  TQ* rs = reinterpret_cast<TQ*>(smp + k + (k & 1));                 // i coefficients
+  __shared__ uint64_t mbar[S];
+
+  const int tid = threadIdx.x;
+  const int64_t lr0 = (int64_t)blockIdx.x * kColT;  // first local row of the tile
+  const bool active = lr0 < n;
+  const int nvalid = active ? (int)min((int64_t)kColT, n - lr0) : 0;
+  const uint32_t bytes = (uint32_t)(((size_t)nvalid * sizeof(TQ) + 15) / 16 * 16);
+  const int64_t g0 = row0 + lr0;
+  const int64_t blk = g0 >> log2_block;
+  const int64_t h = (g0 & ((int64_t(1) << log2_block) - 1)) >> kColLogT;
+  const int nplain = (i == 0) ? 0 : (normalize_prev ? i - 1 : i);
+  uint64_t policy = 0;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&mbar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  }
+  // inputs that do not depend on the predecessor kernel, before waiting on it:
+  // the sample rows, this thread's w rows, and the first S columns of Q[:, :i-1]
+  if (do_sketch && active) {
+    const int32_t* sb = samples + blk * (int64_t)k;
+    for (int j = tid; j < k; j += blockDim.x) smp[j] = __ldg(sb + j);
+  }
+  __syncthreads();
+  pdl_enter();  // Q columns < i-1 are final before the predecessor (LS) ran, but
+                // keep the whole stream after the dependency wait for simplicity
+  if (status_stopped(st)) return;  // uniform over the grid
+  if (tid == 0 && active)
+    for (int j = 0; j < S && j < nplain; ++j)
+      tma_load_1d(ring + (size_t)j * kColT, Q + (int64_t)j * ldq + lr0, bytes, &mbar[j], policy);
+  for (int j = tid; j < i; j += blockDim.x) rs[j] = rc[j];
+
+  int64_t rows[NH];
+#pragma unroll
+  for (int hh = 0; hh < NH; ++hh)
+    rows[hh] = lr0 + (int64_t)hh * (kColThreads * V) + (int64_t)tid * V;
+  TQ wv[NH][V];
+#pragma unroll
+  for (int hh = 0; hh < NH; ++hh)
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      wv[hh][v] = (rows[hh] + v < n) ? cvt<TQ>(__ldcs(w + rows[hh] + v)) : TQ(0);
+  __syncthreads();
+
+  TQ acc[NH][V];
+#pragma unroll
+  for (int hh = 0; hh < NH; ++hh)
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[hh][v] = TQ(0);
+  if (active) {
+    for (int j = 0; j < nplain; ++j) {
+      const int s = j % S;
+      mbar_wait(&mbar[s], (uint32_t)((j / S) & 1));
+      const TQ c = rs[j];
+      const TQ* buf = ring + (size_t)s * kColT;
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh) {
+        TQ q[V];
+        vload_smem(buf + hh * (kColThreads * V) + tid * V, q);
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[hh][v] = fma(q[v], c, acc[hh][v]);
+      }
+      __syncthreads();  // everybody has read stage s
+      if (tid == 0 && j + S < nplain) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tma_load_1d(ring + (size_t)s * kColT, Q + (int64_t)(j + S) * ldq + lr0, bytes, &mbar[s],
+                    policy);
+      }
+    }
+    if (i > 0 && normalize_prev) {
+      const int j = i - 1;
+      const double rjj = R[(int64_t)j * ldr + j];
+      const TQ c = rs[j];
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh) {
+        TQ* col = Q + (int64_t)j * ldq + rows[hh];
+        if (rows[hh] + V <= n) {
+          TQ q[V];
+          vload(col, q);
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            q[v] = cvt<TQ>((double)q[v] / rjj);
+            acc[hh][v] = fma(q[v], c, acc[hh][v]);
+          }
+          vstore(col, q);
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            if (rows[hh] + v < n) {
+              const TQ q = cvt<TQ>((double)col[v] / rjj);
+              col[v] = q;
+              acc[hh][v] = fma(q, c, acc[hh][v]);
+            }
+        }
+      }
+    }
+  }
+  double xs[NH * V];  // d o q' of this thread's rows, element order (h, v)
+  if (active) {
+#pragma unroll
+    for (int hh = 0; hh < NH; ++hh) {
+      TQ out[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) out[v] = (rows[hh] + v < n) ? wv[hh][v] - acc[hh][v] : TQ(0);
+      TQ* dst = Q + (int64_t)i * ldq + rows[hh];
+      if (rows[hh] + V <= n) vstore(dst, out);
+      else
+        for (int v = 0; v < V; ++v)
+          if (rows[hh] + v < n) dst[v] = out[v];
+      if (do_sketch) {
+        const uint32_t word = (rows[hh] < n) ? __ldg(sign_bits + (rows[hh] >> 5)) : 0u;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const double x = (double)out[v];
+          const bool pos = (word >> ((rows[hh] + v) & 31)) & 1u;
+          xs[hh * V + v] = pos ? x : -x;
+        }
+      }
+    }
+  }
+  if (!do_sketch) return;  // uniform: no cluster barrier is pending
+  // ---- sketch epilogue (z aliases the drained ring) ----------------------------
+  __syncthreads();
+  if (active) {
+    fwht_reg<3>(xs);  // bits [0, LV) from v and [HB, 12) from h
+#pragma unroll
+    for (int hh = 0; hh < NH; ++hh)
+#pragma unroll
+      for (int v = 0; v < V; ++v) z[pidx(hh * (kColThreads * V) + tid * V + v)] = xs[hh * V + v];
+    __syncthreads();
+#pragma unroll
+    for (int b0 = LV; b0 < HB; b0 += 3) {  // bits [LV, HB): three radix-8 passes
+      fwht_pass<kColLogT, 3>(z, b0);
+      __syncthreads();
+    }
+    for (int j = tid; j < k; j += blockDim.x) {
+      const int32_t r = smp[j];
+      const double v = z[pidx(r & (kColT - 1))];
+      const int64_t rh = (int64_t)(r >> kColLogT);
+      part[j] = (__popcll(rh & h) & 1) ? -v : v;
+    }
+  } else {
+    for (int j = tid; j < k; j += blockDim.x) part[j] = 0.0;
+  }
+  cl.sync();
+  const int rank = (int)cl.block_rank();
+  const int j0 = (int)(((int64_t)rank * k) / kColCluster);
+  const int j1 = (int)(((int64_t)(rank + 1) * k) / kColCluster);
+  double* outp = partials + (int64_t)(blockIdx.x / kColCluster) * k;
+  for (int j = j0 + tid; j < j1; j += blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < kColCluster; ++q) s += cl.map_shared_rank(part, q)[j];
+    outp[j] = s;
+  }
+  cl.sync();
+}
+
+static int64_t column_ctas(int64_t n_local) {
+  const int64_t nt = (n_local + kColT - 1) / kColT;
+  return (nt + kColCluster - 1) / kColCluster * kColCluster;
+}
+
+}  // namespace sgs
+
+using namespace sgs;
+
+extern "C" int sgs_column_nparts(int64_t n_local) {
+  return n_local < 1 ? 0 : (int)(column_ctas(n_local) / kColCluster);
+}
+
+extern "C" int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
+                                   const void* w, int w_dtype, const void* r_crs,
+                                   int normalize_prev, const double* R, int64_t ldr,
+                                   int do_sketch, int64_t row0, int log2_block,
+                                   const uint32_t* sign_bits, const int32_t* samples, int k,
+                                   double* partials, const sgs_status* st, void* stream) {
+  SGS_REQUIRE(Q && w, "update_srht: null pointer");
+  SGS_REQUIRE(i >= 0 && n >= 1 && ldq >= n && (ldq % 4) == 0, "update_srht: bad sizes");
+  SGS_REQUIRE(i == 0 || r_crs, "update_srht: r_crs required for i > 0");
+  SGS_REQUIRE(!normalize_prev || (i > 0 && R), "update_srht: normalize_prev needs R, i > 0");
+  SGS_REQUIRE(((uintptr_t)Q & 15) == 0, "update_srht: Q must be 16-byte aligned");
+  SGS_REQUIRE(!do_sketch || (sign_bits && samples && partials && k >= 1 && k <= 8192),
+              "update_srht: sketch arguments");
+  SGS_REQUIRE(!do_sketch || (log2_block >= kColLogT && (row0 % kColT) == 0),
+              "update_srht: needs 4096-row tiles (log2_block >= 12, row0 %% 4096 == 0)");
+  cudaStream_t s = as_stream(stream);
+  const int64_t nctas = column_ctas(n);
+  const int esz = q_dtype == SGS_F32 ? 4 : 8;
+  const size_t ring = q_dtype == SGS_F32 ? col_ring_bytes<float>() : col_ring_bytes<double>();
+  const size_t smem = ring + (size_t)k * sizeof(double) + (size_t)(k + 1) * sizeof(int32_t) + 8 +
+                      (size_t)(i > 0 ? i : 1) * esz;
+  SGS_REQUIRE(smem <= 227 * 1024, "update_srht: i=%d k=%d needs %zu bytes of shared memory", i,
+              k, smem);
+  cudaError_t err = cudaSuccess;
+#define SGS_COL(TQ, TW)                                                                       \
+  do {                                                                                        \
+    auto kern = rgs_column_kernel<TQ, TW>;                                                    \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
+    err = launch_ex(kern, dim3((unsigned)nctas), dim3(kColThreads), smem, s, kColCluster,     \
+                    static_cast<TQ*>(Q), ldq, n, i, static_cast<const TW*>(w),                \
+                    static_cast<const TQ*>(r_crs), normalize_prev, R, ldr, do_sketch, row0,  \
+                    log2_block, sign_bits, samples, k, partials, st);                         \
+  } while (0)
+  if (q_dtype == SGS_F32 && w_dtype == SGS_F32) SGS_COL(float, float);
+  else if (q_dtype == SGS_F32 && w_dtype == SGS_F64) SGS_COL(float, double);
+  else if (q_dtype == SGS_F64 && w_dtype == SGS_F32) SGS_COL(double, float);
+  else if (q_dtype == SGS_F64 && w_dtype == SGS_F64) SGS_COL(double, double);
+  else {
+    set_error("update_srht: bad dtype");
+    return SGS_EINVAL;
+  }
+#undef SGS_COL
+  return check_ex(err, "rgs_column_kernel");
+}

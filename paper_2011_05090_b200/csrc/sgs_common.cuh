@@ -156,4 +156,40 @@ template <typename T> __device__ __forceinline__ T from_double(double x);
 template <> __device__ __forceinline__ double from_double<double>(double x) { return x; }
 template <> __device__ __forceinline__ float from_double<float>(double x) { return __double2float_rn(x); }
 
+template <typename T> struct VecT;
+template <> struct VecT<float> { using type = float4; static constexpr int N = 4; };
+template <> struct VecT<double> { using type = double2; static constexpr int N = 2; };
+
+template <typename T>
+__device__ __forceinline__ void vload(const T* p, T* v) {
+  using V = typename VecT<T>::type;
+  // streaming (evict-first) load: the 1 GB-per-column Q stream must not evict
+  // the small, reused k-dimensional state (S, P, T, R_S^{-1}) from L2
+  const V x = __ldcs(reinterpret_cast<const V*>(p));
+  if constexpr (VecT<T>::N == 4) { v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; }
+  else { v[0] = x.x; v[1] = x.y; }
+}
+template <typename T>
+__device__ __forceinline__ void vload_smem(const T* p, T* v) {
+  using V = typename VecT<T>::type;
+  const V x = *reinterpret_cast<const V*>(p);
+  if constexpr (VecT<T>::N == 4) { v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; }
+  else { v[0] = x.x; v[1] = x.y; }
+}
+template <typename T>
+__device__ __forceinline__ void vstore(T* p, const T* v) {
+  using V = typename VecT<T>::type;
+  V x;
+  if constexpr (VecT<T>::N == 4) { x.x = v[0]; x.y = v[1]; x.z = v[2]; x.w = v[3]; }
+  else { x.x = v[0]; x.y = v[1]; }
+  *reinterpret_cast<V*>(p) = x;
+}
+
+template <typename TO, typename TI>
+__device__ __forceinline__ TO cvt(TI x) {
+  if constexpr (sizeof(TO) == sizeof(TI)) return (TO)x;
+  else if constexpr (sizeof(TO) == 4) return __double2float_rn((double)x);
+  else return (TO)x;
+}
+
 }  // namespace sgs

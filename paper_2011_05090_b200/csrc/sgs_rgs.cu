@@ -24,35 +24,6 @@ namespace cg = cooperative_groups;
 
 namespace sgs {
 
-template <typename T> struct VecT;
-template <> struct VecT<float> { using type = float4; static constexpr int N = 4; };
-template <> struct VecT<double> { using type = double2; static constexpr int N = 2; };
-
-template <typename T>
-__device__ __forceinline__ void vload(const T* p, T* v) {
-  using V = typename VecT<T>::type;
-  // streaming (evict-first) load: the 1 GB-per-column Q stream must not evict
-  // the small, reused k-dimensional state (S, P, T, R_S^{-1}) from L2
-  const V x = __ldcs(reinterpret_cast<const V*>(p));
-  if constexpr (VecT<T>::N == 4) { v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; }
-  else { v[0] = x.x; v[1] = x.y; }
-}
-template <typename T>
-__device__ __forceinline__ void vstore(T* p, const T* v) {
-  using V = typename VecT<T>::type;
-  V x;
-  if constexpr (VecT<T>::N == 4) { x.x = v[0]; x.y = v[1]; x.z = v[2]; x.w = v[3]; }
-  else { x.x = v[0]; x.y = v[1]; }
-  *reinterpret_cast<V*>(p) = x;
-}
-
-template <typename TO, typename TI>
-__device__ __forceinline__ TO cvt(TI x) {
-  if constexpr (sizeof(TO) == sizeof(TI)) return (TO)x;
-  else if constexpr (sizeof(TO) == 4) return __double2float_rn((double)x);
-  else return (TO)x;
-}
-
 constexpr int kUpdThreads = 256;
 constexpr int kUpdUnroll = 8;
 
@@ -218,6 +189,32 @@ static int ls_cluster_size_host(int k) {
   return cl;
 }
 
+// Transposed butterfly: V values per lane in, the sum over the warp of value
+// index (lane / (32 / V)) out (pairwise sums are commutative, so the result is
+// independent of which lane of a pair adds).  V <= 32, power of two.
+template <typename T, int V>
+__device__ __forceinline__ T warp_multi_reduce(T (&a)[V], int lane) {
+  int n = V;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    if (n > 1) {
+      const bool hi = (lane & off) != 0;
+#pragma unroll
+      for (int q = 0; q < V / 2; ++q) {
+        if (q < n / 2) {
+          const T send = hi ? a[q] : a[q + n / 2];
+          const T keep = hi ? a[q + n / 2] : a[q];
+          a[q] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+      n >>= 1;
+    } else {
+      a[0] += __shfl_xor_sync(0xffffffffu, a[0], off);
+    }
+  }
+  return a[0];
+}
+
 // Per-CTA partial dots of NV vectors with columns [j0, j1) of M over the
 // CTA's nr rows: o[j] = sum_rr M[j*ldm + rr] * v[rr].  Warp per column (8
 // columns in flight), lanes stride the rows, fixed xor-shuffle tree.
@@ -243,6 +240,9 @@ __device__ __noinline__ void ls_coldot(const T* __restrict__ M, int64_t ldm, int
         for (int q = 0; q < 4; ++q)
           mv[u][q] = (jb + u < j1 && lane + 32 * q < rn)
                          ? M[(int64_t)(jb + u) * ldm + rc + lane + 32 * q] : T(0);
+      // per-lane partial dots of the 8 (x NV) columns, then one transposed
+      // butterfly that leaves each column's sum in a group of lanes
+      T vals[kLsCpw * NV];
 #pragma unroll
       for (int u = 0; u < kLsCpw; ++u) {
         T a0 = T(0), a1 = T(0);
@@ -251,16 +251,18 @@ __device__ __noinline__ void ls_coldot(const T* __restrict__ M, int64_t ldm, int
           a0 = fma(mv[u][q], x0[q], a0);
           if (NV > 1) a1 = fma(mv[u][q], x1[q], a1);
         }
-        a0 = warp_sum(a0);
-        if (NV > 1) a1 = warp_sum(a1);
-        if (lane == 0 && jb + u < j1) {
-          if (rc == 0) {
-            o0[jb + u] = a0;
-            if (NV > 1) o1[jb + u] = a1;
-          } else {  // rows beyond 128 per CTA (k > 2048): accumulate chunk sums in order
-            o0[jb + u] += a0;
-            if (NV > 1) o1[jb + u] += a1;
-          }
+        vals[u] = a0;
+        if (NV > 1) vals[kLsCpw + u] = a1;
+      }
+      const T r = warp_multi_reduce<T, kLsCpw * NV>(vals, lane);
+      constexpr int kGrp = 32 / (kLsCpw * NV);  // lanes holding the same sum
+      if ((lane & (kGrp - 1)) == 0) {
+        const int idx = lane / kGrp;
+        const int u = idx % kLsCpw;
+        if (jb + u < j1) {
+          T* o = (idx < kLsCpw) ? o0 : o1;
+          if (rc == 0) o[jb + u] = r;
+          else o[jb + u] += r;  // rows beyond 128 per CTA: chunk sums in order
         }
       }
     }

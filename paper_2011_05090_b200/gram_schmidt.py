@@ -169,10 +169,17 @@ class RgsState:
         self.m = 0
         self.status = _lib.Status(self.device)
         self.nparts = self.theta.nparts(self.n_local)
+        # fused update + sketch column kernel for SRHT kinds with 4096-row tiles
+        self.fused = (not self.theta.is_dense and self.theta.log2_block >= 12
+                      and self.row0 % 4096 == 0)
+        self.nparts_q = (int(_lib.load().sgs_column_nparts(self.n_local)) if self.fused
+                         else self.nparts)
         self._cap = 0
         self._alloc(max(int(capacity), 2))
-        self._parts_s = torch.empty((self.nparts, self.k), dtype=torch.float64, device=self.device)
-        self._parts_p = torch.empty_like(self._parts_s)
+        self._parts_s = torch.empty((self.nparts_q, self.k), dtype=torch.float64,
+                                    device=self.device)
+        self._parts_p = torch.empty((self.nparts, self.k), dtype=torch.float64,
+                                    device=self.device)
         if comm is not None:
             self._kvec_s = torch.empty(self.k, dtype=torch.float64, device=self.device)
             self._kvec_p = torch.empty_like(self._kvec_s)
@@ -240,23 +247,45 @@ class RgsState:
             return None
         return t.data_ptr() + col * t.shape[1] * 8
 
-    def _sketch_parts(self, x_ptr: int, x_code: int, ldx: int, out: torch.Tensor,
-                      kvec: torch.Tensor | None):
-        """Partials of one local column; sharded: reduce + all-reduce to a k-vector.
-        Returns (pointer, nparts, scale) for sgs_ls_step."""
-        self.theta.partials_into(x_ptr, x_code, ldx, 1, out, n_local=self.n_local,
-                                 row0=self.row0, status=self.status)
+    def _combine(self, out: torch.Tensor, nparts: int, kvec: torch.Tensor | None):
+        """(pointer, nparts, scale) of a sketch for sgs_ls_step; sharded states
+        first sum the local partials and all-reduce the k-vector."""
         if self.comm is None:
-            return out.data_ptr(), self.nparts, self.theta.scale
-        call("sgs_partials_reduce", out.data_ptr(), self.nparts, self.k, 1, 1.0,
+            return out.data_ptr(), nparts, self.theta.scale
+        call("sgs_partials_reduce", out.data_ptr(), nparts, self.k, 1, 1.0,
              kvec.data_ptr(), _lib.SGS_F64, self.k, self.status.ptr, stream_ptr())
         self.comm.allreduce_(kvec)
         return kvec.data_ptr(), 1, self.theta.scale
+
+    def _sketch_parts(self, x_ptr: int, x_code: int, ldx: int, out: torch.Tensor,
+                      kvec: torch.Tensor | None):
+        """Partials of one local column via the stand-alone sketch kernel."""
+        self.theta.partials_into(x_ptr, x_code, ldx, 1, out, n_local=self.n_local,
+                                 row0=self.row0, status=self.status)
+        return self._combine(out, self.nparts, kvec)
 
     def _update(self, i: int, w_ptr: int, w_code: int, normalize_prev: bool) -> None:
         call("sgs_rgs_update", self._Q.data_ptr(), self.ccode, self.ldq, self.n_local, i,
              w_ptr, w_code, self._rc.data_ptr(), 1 if normalize_prev else 0,
              self._R.data_ptr(), self._cap, self.status.ptr, stream_ptr())
+
+    def _column(self, i: int, w_ptr: int, w_code: int, normalize_prev: bool, sketch: bool):
+        """Step 3 (and step 4 when ``sketch``): q'_i = w - Q r into Q[:, i] and the
+        partial sketches of q'_i.  Returns (pointer, nparts, scale) or None."""
+        kvec = getattr(self, "_kvec_s", None)
+        if self.fused:
+            d = self._theta_dev
+            call("sgs_rgs_update_srht", self._Q.data_ptr(), self.ccode, self.ldq, self.n_local,
+                 i, w_ptr, w_code, self._rc.data_ptr(), 1 if normalize_prev else 0,
+                 self._R.data_ptr(), self._cap, 1 if sketch else 0, self.row0,
+                 self.theta.log2_block, d["bits"].data_ptr() + (self.row0 // 32) * 4,
+                 d["samples"].data_ptr(), self.k, self._parts_s.data_ptr(), self.status.ptr,
+                 stream_ptr())
+            return self._combine(self._parts_s, self.nparts_q, kvec) if sketch else None
+        self._update(i, w_ptr, w_code, normalize_prev)
+        if not sketch:
+            return None
+        return self._sketch_parts(self._qcol_ptr(i), self.ccode, self.ldq, self._parts_s, kvec)
 
     def _normalize(self, col: int, guarded: bool = True) -> None:
         call("sgs_normalize_column", self._Q.data_ptr(), self.ccode, self.ldq, self.n_local,
@@ -296,13 +325,11 @@ class RgsState:
         if i == 0:
             call("sgs_partials_reduce", pp, pn, self.k, 1, ps, self._P.data_ptr(), self.fcode,
                  self.k, self.status.ptr, stream_ptr())
-            self._update(0, w.data_ptr(), wc, False)
+            self._column(0, w.data_ptr(), wc, False, False)
             self._ls(fin=0)
         else:
             self._ls(sol=i, p_parts=pp, p_nparts=pn, p_scale=ps)
-            self._update(i, w.data_ptr(), wc, False)
-            sp, sn, ss = self._sketch_parts(self._qcol_ptr(i), self.ccode, self.ldq,
-                                            self._parts_s, getattr(self, "_kvec_s", None))
+            sp, sn, ss = self._column(i, w.data_ptr(), wc, False, True)
             self._ls(fin=i, s_parts=sp, s_nparts=sn, s_scale=ss)
         self._normalize(i)
         self.m += 1  # provisional; reconciled with the device count at sync
@@ -386,15 +413,13 @@ class RgsState:
                 call("sgs_partials_reduce", kbuf.data_ptr(), 1, k, nc, self.theta.scale,
                      pdst, self.fcode, k, self.status.ptr, sp)
         del parts
-        kvec = getattr(self, "_kvec_s", None)
         for i in range(m):
-            self._update(i, base + i * ldw * esz, wc, i > 0)
             sol = i + 1 if i + 1 < m else None
             if i == 0:
+                self._column(0, base, wc, False, False)
                 self._ls(fin=0, sol=sol)
             else:
-                spp, snp, ssc = self._sketch_parts(self._qcol_ptr(i), self.ccode, self.ldq,
-                                                   self._parts_s, kvec)
+                spp, snp, ssc = self._column(i, base + i * ldw * esz, wc, True, True)
                 self._ls(fin=i, s_parts=spp, s_nparts=snp, s_scale=ssc, sol=sol)
         self._normalize(m - 1)
         st = self._sync_status()
