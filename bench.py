@@ -184,6 +184,23 @@ def run_qr(args, cfg_name):
         st.factorize_columns(Wt, ldw, m)
         return st
 
+    # the timed steps replay one CUDA graph of the whole factorisation (every
+    # kernel re-runs; the graph only removes host launch overhead)
+    gstate = sg.RgsState(th, pol, capacity=m + 1, breakdown_factor=bf, comm=comm, row0=row0,
+                         n_local=n_loc)
+    graph = None
+    graph_launches = 0
+    if not args.no_graph and comm is None:
+        lcg = _lib.launch_count()
+        graph = gstate.capture_factorization(Wt, ldw, m)
+        graph_launches = _lib.launch_count() - lcg
+
+    def timed_step():
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
+
     def barrier():
         torch.cuda.synchronize()
         if comm:
@@ -192,18 +209,23 @@ def run_qr(args, cfg_name):
 
     # state allocation is part of a step (RgsState buffers), sync at the end is too
     for _ in range(args.warmup):
-        step()
+        timed_step()
     barrier()
+    if graph is not None:
+        gstate.finish()
     lc0 = _lib.launch_count()
     clocks = Clocks(local)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
-        step()
+        timed_step()
     e1.record()
     barrier()
     clk = clocks.stop()
     launches = _lib.launch_count() - lc0
+    if graph is not None:
+        gstate.finish()  # raises if the replayed factorisation recorded a breakdown
+        launches = graph_launches * args.steps
     ms = e0.elapsed_time(e1) / args.steps
     if comm:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -347,6 +369,7 @@ def main():
     ap.add_argument("--cpu-cols", type=int, default=24)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args, args.config if args.config != "c3" else "c1")

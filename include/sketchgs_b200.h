@@ -174,6 +174,7 @@ typedef struct sgs_ls_args {
   void* r_crs;           /* cap, coarse */
   sgs_status* st;
   long long* trace;      /* optional (NULL): clock64() at phase boundaries, CTA 0 */
+  int cache_cols;        /* set by the library: columns of T cached in shared memory */
 } sgs_ls_args;
 
 int64_t sgs_ls_scratch_elems(int k, int cap);

@@ -39,7 +39,7 @@ class LsArgs(ctypes.Structure):
         ("bf_ucrs", c_double),
         ("S", c_void_p), ("P", c_void_p), ("R", c_void_p),
         ("Qs", c_void_p), ("Rinv", c_void_p), ("alpha", c_void_p), ("scratch", c_void_p),
-        ("r_crs", c_void_p), ("st", c_void_p), ("trace", c_void_p),
+        ("r_crs", c_void_p), ("st", c_void_p), ("trace", c_void_p), ("cache_cols", c_int),
     ]
 
 

@@ -218,10 +218,26 @@ __device__ __forceinline__ T warp_multi_reduce(T (&a)[V], int lane) {
 // Per-CTA partial dots of NV vectors with columns [j0, j1) of M over the
 // CTA's nr rows: o[j] = sum_rr M[j*ldm + rr] * v[rr].  Warp per column (8
 // columns in flight), lanes stride the rows, fixed xor-shuffle tree.
+// Column j of the CTA's row slice of T: rows cached in shared memory for
+// j < ncache (prefetched while the predecessor kernel ran), global otherwise.
+template <typename T>
+struct ColSrc {
+  const T* sq;   // smem cache, column j at sq + j*ldc
+  int ldc;
+  int ncache;
+  const T* g;    // global T + ra, column j at g + j*ldg
+  int64_t ldg;
+  __device__ __forceinline__ const T* col(int j) const {
+    return j < ncache ? sq + (int64_t)j * ldc : g + (int64_t)j * ldg;
+  }
+};
+
+// Per-CTA partial dots of NV vectors with columns [j0, j1) over the CTA's nr
+// rows: o[j] = sum_rr M(rr, j) * v[rr].  Warp per column (8 columns in
+// flight), lanes stride the rows, one transposed butterfly for the 8 sums.
 template <typename T, int NV>
-__device__ __noinline__ void ls_coldot(const T* __restrict__ M, int64_t ldm, int nr, int j0,
-                                       int j1, const T* v0, const T* v1, T* __restrict__ o0,
-                                       T* __restrict__ o1) {
+__device__ __noinline__ void ls_coldot(ColSrc<T> M, int nr, int j0, int j1, const T* v0,
+                                       const T* v1, T* __restrict__ o0, T* __restrict__ o1) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int rc = 0; rc < nr; rc += kLsChunk) {  // rows in chunks of 128 (4 per lane)
     const int rn = min(kLsChunk, nr - rc);
@@ -235,11 +251,12 @@ __device__ __noinline__ void ls_coldot(const T* __restrict__ M, int64_t ldm, int
     for (int jb = j0 + warp * kLsCpw; jb < j1; jb += kLsWarps * kLsCpw) {
       T mv[kLsCpw][4];
 #pragma unroll
-      for (int u = 0; u < kLsCpw; ++u)
+      for (int u = 0; u < kLsCpw; ++u) {
+        const T* cp = M.col(min(jb + u, j1 - 1)) + rc + lane;
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          mv[u][q] = (jb + u < j1 && lane + 32 * q < rn)
-                         ? M[(int64_t)(jb + u) * ldm + rc + lane + 32 * q] : T(0);
+          mv[u][q] = (jb + u < j1 && lane + 32 * q < rn) ? cp[32 * q] : T(0);
+      }
       // per-lane partial dots of the 8 (x NV) columns, then one transposed
       // butterfly that leaves each column's sum in a group of lanes
       T vals[kLsCpw * NV];
@@ -270,13 +287,80 @@ __device__ __noinline__ void ls_coldot(const T* __restrict__ M, int64_t ldm, int
   }
 }
 
-// out[o - o0] = sum_{l in [lbeg(o), l1)} M[l*ldm + o] * c[l], o in [o0, o1), with
-// lbeg(o) = UPPER ? o : 0.  Lanes own outputs (4 each), warps take 8 columns
-// at a time, warp partials combined in ascending warp order.
+// out[rr] = sum_{l < l1} M(rr, l) * c[l] for the CTA's rows rr < nr (lanes own
+// rows, warps take 8 columns at a time, warp partials combined in order).
+template <typename T>
+__device__ __noinline__ void ls_rows_gemv(ColSrc<T> M, int nr, int l1, const T* c, T* out,
+                                          T* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int oc = 0; oc < nr; oc += kLsChunk) {
+    const int on = min(kLsChunk, nr - oc);
+    T acc[4] = {T(0), T(0), T(0), T(0)};
+    for (int lb = warp * kLsCpw; lb < l1; lb += kLsWarps * kLsCpw) {
+      T mv[kLsCpw][4];
+#pragma unroll
+      for (int u = 0; u < kLsCpw; ++u) {
+        const int l = lb + u;
+        const T* cp = M.col(min(l, l1 - 1)) + oc + lane;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          mv[u][q] = (l < l1 && lane + 32 * q < on) ? cp[32 * q] : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < kLsCpw; ++u) {
+        const T cl = (lb + u < l1) ? c[lb + u] : T(0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] = fma(mv[u][q], cl, acc[q]);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) red[warp * kLsChunk + lane + 32 * q] = acc[q];
+    __syncthreads();
+    for (int ol = threadIdx.x; ol < on; ol += blockDim.x) {
+      T s = T(0);
+      for (int w = 0; w < kLsWarps; ++w) s += red[w * kLsChunk + ol];
+      out[oc + ol] = s;
+    }
+  }
+  __syncthreads();
+}
+
+// Upper-triangular row slice: out[o - o0] = sum_{l=o}^{l1-1} M[l*ldm + o] * c[l]
+// for o in [o0, o1).  Lanes own outputs (1 or 4 each), warps take columns
+// (16 or 8 at a time), warp partials combined in ascending warp order.
 template <typename T, bool UPPER>
 __device__ __noinline__ void ls_matvec(const T* __restrict__ M, int64_t ldm, int o0, int o1,
                                        int l1, const T* c, T* out, T* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (o1 - o0 <= 32) {
+    // narrow slice: one output per lane, 16 columns in flight per warp
+    constexpr int kC = 16;
+    const int on = o1 - o0;
+    const int lstart = UPPER ? o0 : 0;
+    T acc = T(0);
+    for (int lb = lstart + warp * kC; lb < l1; lb += kLsWarps * kC) {
+      T mv[kC];
+#pragma unroll
+      for (int u = 0; u < kC; ++u) {
+        const int l = lb + u;
+        const bool ok = l < l1 && lane < on && (!UPPER || l >= o0 + lane);
+        mv[u] = ok ? M[(int64_t)l * ldm + o0 + lane] : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < kC; ++u) acc = fma(mv[u], (lb + u < l1) ? c[lb + u] : T(0), acc);
+    }
+    __syncthreads();
+    red[warp * 32 + lane] = acc;
+    __syncthreads();
+    if (threadIdx.x < on) {
+      T s = T(0);
+      for (int w = 0; w < kLsWarps; ++w) s += red[w * 32 + threadIdx.x];
+      out[threadIdx.x] = s;
+    }
+    __syncthreads();
+    return;
+  }
   for (int oc = o0; oc < o1; oc += kLsChunk) {
     const int on = min(kLsChunk, o1 - oc);
     const int lstart = UPPER ? oc : 0;
@@ -363,10 +447,31 @@ __device__ __forceinline__ T ls_slot_sum(const T* slots, int64_t stride, int CL)
   return s;
 }
 
+// Shared-memory carve-up of ls_step_kernel (16-byte aligned sub-arrays).
+__host__ __device__ constexpr size_t ls_align16(size_t x) { return (x + 15) / 16 * 16; }
+template <typename T>
+struct LsSmem {
+  T *vs, *vt, *vp, *tmp, *c1, *zc, *c2, *yv, *to, *red, *sq;
+  size_t bytes;  // fixed part (before the cache)
+  __host__ __device__ LsSmem(unsigned char* base, int RM, int cap) {
+    size_t off = 0;
+    auto take = [&](size_t n) {
+      T* p = reinterpret_cast<T*>(base + off);
+      off += ls_align16(n * sizeof(T));
+      return p;
+    };
+    vs = take(RM); vt = take(RM); vp = take(RM); tmp = take(RM);
+    c1 = take(cap); zc = take(cap); c2 = take(cap); yv = take(cap); to = take(cap);
+    const size_t nred = (size_t)kLsWarps * kLsChunk;
+    red = take(nred * sizeof(T) >= 512 * sizeof(double) ? nred : 512 * sizeof(double) / sizeof(T));
+    sq = reinterpret_cast<T*>(base + off);
+    bytes = off;
+  }
+};
+
 template <typename T>
 __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   cg::cluster_group cl = cg::this_cluster();
-  pdl_enter();
   const int rank = (int)cl.block_rank();
   const int CL = (int)cl.num_blocks();
   const int k = a.k, cap = a.cap;
@@ -374,55 +479,88 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   const int rb = (int)(((int64_t)(rank + 1) * k) / CL);
   const int nr = rb - ra;
   const int RM = (k + CL - 1) / CL;
+  const bool fused = a.do_finalize && a.do_solve;
 
-  // every CTA reads the status before any CTA can write it (the first write
-  // follows a cluster barrier), so all CTAs take identical branches.
-  const int64_t code0 = *reinterpret_cast<volatile const int64_t*>(&a.st->code);
-  double dmax = a.st->diag_max, dmin = a.st->diag_min;
-  if (code0 != 0) return;
-
-  extern __shared__ unsigned char smem_raw[];
-  T* vs = reinterpret_cast<T*>(smem_raw);  // RM   s' -> s (own rows)
-  T* vt = vs + RM;                         // RM   t
-  T* vp = vt + RM;                         // RM   p
-  T* tmp = vp + RM;                        // RM
-  T* c1 = tmp + RM;                        // cap  Qs^T s  (then coefficients)
-  T* zc = c1 + cap;                        // cap  Qs^T p
-  T* c2 = zc + cap;                        // cap
-  T* to = c2 + cap;                        // cap  TRMV outputs
-  T* red = to + cap;                       // kLsWarps * kLsChunk
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  LsSmem<T> L(smem_raw, RM, cap);
+  T* vs = L.vs;    // RM   s' -> s (own rows)
+  T* vt = L.vt;    // RM   t
+  T* vp = L.vp;    // RM   p
+  T* tmp = L.tmp;  // RM
+  T* c1 = L.c1;    // cap  Qs^T s
+  T* zc = L.zc;    // cap  Qs^T p
+  T* c2 = L.c2;    // cap
+  T* yv = L.yv;    // cap  R_S^{-1}[:, :c-1] z (own slice)
+  T* to = L.to;    // cap  TRMV outputs
+  T* red = L.red;  // kLsWarps * kLsChunk, 16-byte aligned (also used as doubles)
+  T* sq = L.sq;    // cache: own rows of T, RM per column
   double* dred = reinterpret_cast<double*>(red);
   __shared__ T bc[8];
 
-  // scratch layout (T elements)
-  const int64_t sA = 2 * (int64_t)cap + 8;     // exchange #1 stride per CTA
+  const int64_t sA = 2 * (int64_t)cap + 8;     // exchange stride per CTA
   T* scr = reinterpret_cast<T*>(a.scratch);
   T* XA = scr;                                  // 16 x sA
-  T* XB = XA + kLsMaxCluster * sA;              // 16 x 8  exchange #2
-  T* XR = XB + kLsMaxCluster * 8;               // 16 x sA reorthogonalisation
-  T* AL = static_cast<T*>(a.alpha);             // cap: column norms alpha_j of T
+  T* XB = XA + kLsMaxCluster * sA;              // 16 x 8
+  T* XR = XB + kLsMaxCluster * 8;               // 16 x sA
+  T* AL = static_cast<T*>(a.alpha);             // cap: column norms of T
   T* myA = XA + rank * sA;
   T* myB = XB + rank * 8;
   T* myR = XR + rank * sA;
-
   T* S = static_cast<T*>(a.S);
   T* P = static_cast<T*>(a.P);
-  T* Qs = static_cast<T*>(a.Qs);  // unnormalised T
+  T* Tm = static_cast<T*>(a.Qs);  // unnormalised T
   T* Rinv = static_cast<T*>(a.Rinv);
   double* R = a.R;
-  const bool fused = a.do_finalize && a.do_solve;
   long long* trc = (rank == 0 && threadIdx.x == 0) ? a.trace : nullptr;
 #define SGS_TR(ix) \
   do {             \
     if (trc) trc[ix] = clock64(); \
   } while (0)
-  SGS_TR(0);
   auto slice = [&](int n, int& o0, int& o1) {
     o0 = (int)(((int64_t)rank * n) / CL);
     o1 = (int)(((int64_t)(rank + 1) * n) / CL);
   };
-  T tp = T(0), alpha = T(0);
 
+  // ---- before the dependency wait -------------------------------------------------
+  // Everything the LS state (T, R_S^{-1}, alpha, P, status) provides was written
+  // by earlier launches that completed before the predecessor started; only the
+  // sketch partials of q'_i come from the predecessor.  So the cache of this
+  // CTA's rows of T and, in the fused QR path, the whole solve except the last
+  // column's term run while the predecessor column kernel is still streaming Q.
+  SGS_TR(0);
+  const int64_t code0 = *reinterpret_cast<volatile const int64_t*>(&a.st->code);
+  double dmax = a.st->diag_max, dmin = a.st->diag_min;
+  const int ncols_t = a.do_finalize ? a.col_fin : a.col_sol;  // columns of T in use
+  const int ncache = min(ncols_t, a.cache_cols);
+  for (int e = threadIdx.x; e < ncache * nr; e += blockDim.x) {
+    const int j = e / nr, rr = e - j * nr;
+    sq[(int64_t)j * RM + rr] = Tm[(int64_t)j * k + ra + rr];
+  }
+  __syncthreads();
+  const ColSrc<T> TS{sq, RM, ncache, Tm + ra, (int64_t)k};
+  int s0 = 0, s1 = 0;  // output slice of the solve: [0, c) for c = col_sol
+  if (a.do_solve) slice(a.col_sol, s0, s1);
+  if (fused && code0 == 0) {
+    const int i = a.col_fin;  // solve for c = i + 1 uses T[:, :i] now, T[:, i] later
+    for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vp[rr] = P[(int64_t)(i + 1) * k + ra + rr];
+    __syncthreads();
+    if (i > 0) {
+      ls_coldot<T, 1>(TS, nr, 0, i, vp, nullptr, myA + 8 + cap, nullptr);
+      cl.sync();
+      ls_gather<T>(XA + 8 + cap, sA, CL, 0, i, AL, zc);
+      __syncthreads();
+      ls_matvec<T, true>(Rinv, cap, s0, s1, i, zc, yv, red);  // y = R_S^{-1}[:, :i] z[:i]
+    } else {
+      for (int o = s0 + threadIdx.x; o < s1; o += blockDim.x) yv[o - s0] = T(0);
+      __syncthreads();
+    }
+  }
+  SGS_TR(1);
+  pdl_enter();
+  SGS_TR(2);
+  if (code0 != 0) return;  // uniform: nobody writes st before a cluster barrier
+
+  T tp = T(0), alpha = T(0);
   if (a.do_finalize) {
     const int i = a.col_fin;
     const int nq = i;
@@ -431,11 +569,9 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     } else {
       ls_reduce_parts<T>(a.s_partials, a.s_nparts, k, ra, nr, a.s_scale, vs, dred);
     }
-    if (fused)
-      for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vp[rr] = P[(int64_t)(i + 1) * k + ra + rr];
     __syncthreads();
-    SGS_TR(1);
-    // ---- exchange #1 ---------------------------------------------------------
+    SGS_TR(3);
+    // ---- exchange #1: ||s'||^2, ||p_i||^2, T^T s' --------------------------------
     T l0 = T(0), l1 = T(0);
     for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
       const T pv = P[(int64_t)i * k + ra + rr];
@@ -445,20 +581,12 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     l0 = block_sum(l0, red);
     l1 = block_sum(l1, red);
     if (threadIdx.x == 0) { myA[0] = l0; myA[1] = l1; }
-    if (nq > 0) {
-      if (fused) ls_coldot<T, 2>(Qs + ra, k, nr, 0, nq, vs, vp, myA + 8, myA + 8 + cap);
-      else ls_coldot<T, 1>(Qs + ra, k, nr, 0, nq, vs, nullptr, myA + 8, nullptr);
-    }
-    SGS_TR(2);
+    if (nq > 0) ls_coldot<T, 1>(TS, nr, 0, nq, vs, nullptr, myA + 8, nullptr);
     cl.sync();
-    SGS_TR(3);
-    if (threadIdx.x < 2) bc[threadIdx.x] = ls_slot_sum(XA + threadIdx.x, sA, CL);
-    if (nq > 0) {
-      ls_gather<T>(XA + 8, sA, CL, 0, nq, AL, c1);              // T^T s' / alpha
-      if (fused) ls_gather<T>(XA + 8 + cap, sA, CL, 0, nq, AL, zc);  // Qs^T p
-    }
-    __syncthreads();
     SGS_TR(4);
+    if (threadIdx.x < 2) bc[threadIdx.x] = ls_slot_sum(XA + threadIdx.x, sA, CL);
+    if (nq > 0) ls_gather<T>(XA + 8, sA, CL, 0, nq, AL, c1);  // T^T s' / alpha
+    __syncthreads();
     const double r_ii = (double)sqrt(bc[0]);
     const double tol = a.bf_ucrs * (double)sqrt(bc[1]);
     if (r_ii <= tol || !(r_ii == r_ii)) {
@@ -477,26 +605,27 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
       S[(int64_t)i * k + ra + rr] = sv;
     }
     for (int j = threadIdx.x; j < nq; j += blockDim.x) {
-      const T cj = c1[j] / rT;             // (Qs^T s)_j
+      const T cj = c1[j] / rT;       // (Qs^T s)_j
       c1[j] = cj;
-      c2[j] = cj / __ldcg(AL + j);         // coefficient on the unnormalised column T_j
+      c2[j] = cj / __ldcg(AL + j);   // coefficient on the unnormalised column T_j
     }
     __syncthreads();
     if (nq > 0) {
-      ls_matvec<T, false>(Qs + ra, k, 0, nr, nq, c2, tmp, red);
+      ls_rows_gemv<T>(TS, nr, nq, c2, tmp, red);
       for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vt[rr] = vs[rr] - tmp[rr];
     } else {
       for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vt[rr] = vs[rr];
     }
     __syncthreads();
     SGS_TR(5);
-    // ---- exchange #2: ||t||^2 and t^T p (dot with the stored column, coldot pattern)
-    for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) Qs[(int64_t)i * k + ra + rr] = vt[rr];
+    // ---- exchange #2: ||t||^2 and t^T p (dot with the stored column) ------------------
+    for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) Tm[(int64_t)i * k + ra + rr] = vt[rr];
     T lt = T(0);
     for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) lt = fma(vt[rr], vt[rr], lt);
-    lt = block_sum(lt, red);  // its __syncthreads also publishes the T_i stores
+    lt = block_sum(lt, red);  // its __syncthreads also publishes the T_i stores in the CTA
     if (threadIdx.x == 0) myB[0] = lt;
-    if (fused) ls_coldot<T, 1>(Qs + ra, k, nr, i, i + 1, vp, nullptr, myB + 1 - i, nullptr);
+    const ColSrc<T> TG{sq, RM, 0, Tm + ra, (int64_t)k};
+    if (fused) ls_coldot<T, 1>(TG, nr, i, i + 1, vp, nullptr, myB + 1 - i, nullptr);
     cl.sync();
     SGS_TR(6);
     if (threadIdx.x < 2) bc[2 + threadIdx.x] = ls_slot_sum(XB + threadIdx.x, 8, CL);
@@ -506,7 +635,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     const T ss = bc[0] / (rT * rT);
     if (nq > 0 && tt < T(0.5) * ss) {
       // cancellation: second classical Gram-Schmidt pass on t
-      ls_coldot<T, 1>(Qs + ra, k, nr, 0, nq, vt, nullptr, myR + 8, nullptr);
+      ls_coldot<T, 1>(TS, nr, 0, nq, vt, nullptr, myR + 8, nullptr);
       cl.sync();
       ls_gather<T>(XR + 8, sA, CL, 0, nq, AL, c2);
       __syncthreads();
@@ -515,17 +644,17 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
         c2[j] = c2[j] / __ldcg(AL + j);
       }
       __syncthreads();
-      ls_matvec<T, false>(Qs + ra, k, 0, nr, nq, c2, tmp, red);
+      ls_rows_gemv<T>(TS, nr, nq, c2, tmp, red);
       for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
         const T t2 = vt[rr] - tmp[rr];
         vt[rr] = t2;
-        Qs[(int64_t)i * k + ra + rr] = t2;
+        Tm[(int64_t)i * k + ra + rr] = t2;
       }
       T l2 = T(0);
       for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) l2 = fma(vt[rr], vt[rr], l2);
       l2 = block_sum(l2, red);
       if (threadIdx.x == 0) myR[0] = l2;
-      if (fused) ls_coldot<T, 1>(Qs + ra, k, nr, i, i + 1, vp, nullptr, myR + 1 - i, nullptr);
+      if (fused) ls_coldot<T, 1>(TG, nr, i, i + 1, vp, nullptr, myR + 1 - i, nullptr);
       cl.sync();
       if (threadIdx.x < 2) bc[4 + threadIdx.x] = ls_slot_sum(XR + threadIdx.x, sA, CL);
       __syncthreads();
@@ -563,17 +692,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   }
 
   if (a.do_solve) {
-    const int c = a.col_sol;
-    const int nq = c;  // columns 0..c-1 of T
-    if (!fused) {
-      if (a.p_partials != nullptr) {
-        ls_reduce_parts<T>(a.p_partials, a.p_nparts, k, ra, nr, a.p_scale, vp, dred);
-        for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) P[(int64_t)c * k + ra + rr] = vp[rr];
-      } else {
-        for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vp[rr] = P[(int64_t)c * k + ra + rr];
-      }
-      __syncthreads();
-    }
+    const int c = a.col_sol;  // r = R_S^{-1}[:c,:c] z, z = Qs[:, :c]^T p
     // rank check of the sketched basis (gram_schmidt.py:186-189)
     if (dmin < 1e-8 * fmax(dmax, 1.0)) {
       if (rank == 0 && threadIdx.x == 0) {
@@ -582,20 +701,28 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
       }
       return;
     }
+    T zl;  // z[c-1]
     if (fused) {
-      if (threadIdx.x == 0) zc[c - 1] = tp / alpha;  // = (T_{c-1}^T p) / alpha_{c-1}
+      zl = tp / alpha;  // (T_{c-1}^T p) / alpha_{c-1}; y was formed before the wait
     } else {
-      ls_coldot<T, 1>(Qs + ra, k, nr, 0, nq, vp, nullptr, myA + 8 + cap, nullptr);
+      if (a.p_partials != nullptr) {
+        ls_reduce_parts<T>(a.p_partials, a.p_nparts, k, ra, nr, a.p_scale, vp, dred);
+        for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) P[(int64_t)c * k + ra + rr] = vp[rr];
+      } else {
+        for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vp[rr] = P[(int64_t)c * k + ra + rr];
+      }
+      __syncthreads();
+      ls_coldot<T, 1>(TS, nr, 0, c, vp, nullptr, myA + 8 + cap, nullptr);
       cl.sync();
-      ls_gather<T>(XA + 8 + cap, sA, CL, 0, nq, AL, zc);
+      ls_gather<T>(XA + 8 + cap, sA, CL, 0, c, AL, zc);
+      __syncthreads();
+      ls_matvec<T, true>(Rinv, cap, s0, s1, c - 1, zc, yv, red);
+      zl = zc[c - 1];
     }
-    __syncthreads();
     SGS_TR(9);
-    int o0, o1;
-    slice(nq, o0, o1);
-    ls_matvec<T, true>(Rinv, cap, o0, o1, nq, zc, to, red);
-    for (int o = o0 + threadIdx.x; o < o1; o += blockDim.x) {
-      const T r = to[o - o0];
+    // r_o = y_o + R_S^{-1}[o, c-1] z[c-1]  (same two-term form on every path)
+    for (int o = s0 + threadIdx.x; o < s1; o += blockDim.x) {
+      const T r = fma(Rinv[(int64_t)(c - 1) * cap + o], zl, yv[o - s0]);
       R[(int64_t)c * cap + o] = (double)r;
       if (a.coarse_dtype == SGS_F32) static_cast<float*>(a.r_crs)[o] = cvt<float>(r);
       else static_cast<double*>(a.r_crs)[o] = (double)r;
@@ -605,25 +732,34 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
 #undef SGS_TR
 }
 
-static size_t ls_smem_bytes(int k, int cap, int CL, size_t esize) {
+template <typename T>
+static size_t ls_smem_fixed(int k, int cap, int CL) {
   const int RM = (k + CL - 1) / CL;
-  size_t n = (size_t)(4 * RM + 4 * cap + kLsWarps * kLsChunk + 8) * esize;
-  const size_t dmin = (size_t)(4 * RM + 4 * cap) * esize + 512 * sizeof(double) + 64;
-  return n > dmin ? n : dmin;
+  return LsSmem<T>(nullptr, RM, cap).bytes;
 }
+constexpr size_t kLsSmemMax = 227 * 1024;
 
 template <typename T>
 static int launch_ls(const sgs_ls_args* a, cudaStream_t s) {
   const int CL = ls_cluster_size_host(a->k);
-  const size_t smem = ls_smem_bytes(a->k, a->cap, CL, sizeof(T));
-  if (smem > 227 * 1024) {
-    set_error("ls_step: k=%d cap=%d needs %zu bytes of shared memory", a->k, a->cap, smem);
+  const size_t fixed = ls_smem_fixed<T>(a->k, a->cap, CL);
+  if (fixed > kLsSmemMax) {
+    set_error("ls_step: k=%d cap=%d needs %zu bytes of shared memory", a->k, a->cap, fixed);
     return SGS_EINVAL;
   }
+  // cache as many columns of this CTA's rows of T as fit
+  const int RM = (a->k + CL - 1) / CL;
+  const int ncols_t = a->do_finalize ? a->col_fin : a->col_sol;
+  int cache = (int)((kLsSmemMax - fixed) / ((size_t)RM * sizeof(T)));
+  if (cache > ncols_t) cache = ncols_t;
+  if (cache < 0) cache = 0;
+  const size_t smem = fixed + (size_t)cache * RM * sizeof(T);
+  sgs_ls_args aa = *a;
+  aa.cache_cols = cache;
   auto kern = ls_step_kernel<T>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (CL > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  return check_ex(launch_ex(kern, dim3(CL), dim3(kLsThreads), smem, s, CL, *a), "ls_step_kernel");
+  return check_ex(launch_ex(kern, dim3(CL), dim3(kLsThreads), smem, s, CL, aa), "ls_step_kernel");
 }
 
 }  // namespace sgs
@@ -709,10 +845,26 @@ extern "C" int sgs_transpose(const void* src, int64_t lds, void* dst, int64_t ld
   return check_launch("transpose_kernel");
 }
 
+namespace sgs {
+int launch_ls_grid(const sgs_ls_args* a, cudaStream_t s);
+int64_t ls_grid_scratch_elems(int cap);
+int ls_grid_size(int k);
+static int ls_mode() {  // 0 = single cluster (default), 1 = grid-wide (SGS_LS_MODE=grid)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SGS_LS_MODE");
+    v = (e && e[0] == 'g') ? 1 : 0;
+  }
+  return v;
+}
+}  // namespace sgs
+
 extern "C" int64_t sgs_ls_scratch_elems(int k, int cap) {
   (void)k;
   const int64_t sA = 2 * (int64_t)cap + 8;
-  return 2 * kLsMaxCluster * sA + kLsMaxCluster * 8 + cap + 64;
+  const int64_t cl = 2 * kLsMaxCluster * sA + kLsMaxCluster * 8 + cap + 64;
+  const int64_t gr = ls_grid_scratch_elems(cap);
+  return cl > gr ? cl : gr;
 }
 
 extern "C" int sgs_ls_cluster_size(int k) { return ls_cluster_size_host(k); }
@@ -728,6 +880,7 @@ extern "C" int sgs_ls_step(const sgs_ls_args* a, void* stream) {
   SGS_REQUIRE(!(a->do_finalize && a->do_solve) || a->col_sol == a->col_fin + 1,
               "ls_step: fused solve must target the next column");
   cudaStream_t s = as_stream(stream);
+  if (ls_mode() == 1) return launch_ls_grid(a, s);
   if (a->fine_dtype == SGS_F64) return launch_ls<double>(a, s);
   if (a->fine_dtype == SGS_F32) return launch_ls<float>(a, s);
   set_error("ls_step: bad fine dtype");

@@ -381,14 +381,17 @@ class RgsState:
         return QrFactors(Q=self.Q, R=self.R, S=self.S, P=self.P)
 
     # ---- batch path ----------------------------------------------------------------
-    def factorize_columns(self, Wcm: torch.Tensor, ldw: int, m: int) -> None:
-        """Factorise m columns of a device column-major W (column j at
-        offset j*ldw) with three launches per column; raises at the end on a
-        device-recorded breakdown / rank deficiency."""
-        if self.m != 0:
-            raise RuntimeError("factorize_columns needs a fresh state")
-        while self._cap < m + 1:
+    def _reserve(self, ncols: int) -> None:
+        while self._cap < ncols:
             self._alloc(2 * self._cap)
+
+    def _enqueue_factorization(self, Wcm: torch.Tensor, ldw: int, m: int) -> None:
+        """Enqueue a complete factorisation of m columns of a device
+        column-major W (column j at offset j*ldw) on the current stream: status
+        reset, batched P = Theta W, then per column the fused column kernel and
+        one LS launch (finalize i + solve i+1).  No host synchronisation, so the
+        sequence can be captured in a CUDA graph."""
+        self.status.reset()
         wc = _lib.dtype_code(Wcm.dtype)
         esz = Wcm.element_size()
         base = Wcm.data_ptr()
@@ -412,7 +415,6 @@ class RgsState:
                 self.comm.allreduce_(kbuf[:nc])
                 call("sgs_partials_reduce", kbuf.data_ptr(), 1, k, nc, self.theta.scale,
                      pdst, self.fcode, k, self.status.ptr, sp)
-        del parts
         for i in range(m):
             sol = i + 1 if i + 1 < m else None
             if i == 0:
@@ -422,9 +424,37 @@ class RgsState:
                 spp, snp, ssc = self._column(i, base + i * ldw * esz, wc, True, True)
                 self._ls(fin=i, s_parts=spp, s_nparts=snp, s_scale=ssc, sol=sol)
         self._normalize(m - 1)
+        self._keep = parts  # keep the chunk buffer alive for graph replays
+
+    def factorize_columns(self, Wcm: torch.Tensor, ldw: int, m: int) -> None:
+        """Factorise m columns of a device column-major W with two launches per
+        column; raises at the end on a device-recorded breakdown / rank
+        deficiency (reference exception types and column numbers)."""
+        if self.m != 0:
+            raise RuntimeError("factorize_columns needs a fresh state")
+        self._reserve(m + 1)
+        self._enqueue_factorization(Wcm, ldw, m)
+        self.finish()
+
+    def finish(self) -> None:
+        """Synchronise with the device status and raise what it recorded."""
         st = self._sync_status()
         if st["code"]:
             self._raise_status(st)
+
+    def capture_factorization(self, Wcm: torch.Tensor, ldw: int, m: int):
+        """Capture the whole factorisation in a CUDA graph; ``graph.replay()``
+        re-runs every kernel (status reset included) and ``finish()`` reads the
+        outcome.  Used for repeated factorisations of same-shaped inputs."""
+        self._reserve(m + 1)
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                self._enqueue_factorization(Wcm, ldw, m)
+        torch.cuda.current_stream().wait_stream(side)
+        return g
 
 
 def ctypes_byref(a):

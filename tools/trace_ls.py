@@ -16,18 +16,25 @@ for rep in range(2):
     st._trace = torch.zeros((m + 1, 16), dtype=torch.int64, device="cuda")
     st.factorize_columns(W, W.shape[1], m)
 tr = st._trace[:m].cpu().numpy().astype(np.float64)
-names = {1: "reduce_parts", 2: "exch1_local", 3: "clsync1", 4: "gather1", 5: "s_matvec",
-         6: "exch2", 7: "reorth", 8: "rinv_col", 9: "solve_prep", 10: "trmv_store"}
+import os as _os
+if not _os.environ.get("SGS_LS_MODE", "cluster").startswith("g"):
+    names = {1: "prewait(cache,z,y)", 2: "wait", 3: "reduce_parts", 4: "exch1", 5: "gather+s+matvec",
+             6: "exch2", 7: "reorth", 8: "rinv_col", 9: "solve_prep", 10: "store"}
+else:
+    names = {1: "reduce_parts", 2: "coldot+B1", 3: "reduce_scatter+B2", 4: "gather+t", 5: "B3",
+             6: "reorth+rinv_col", 7: "solve_prep", 8: "trmv_store"}
+LAST = max(names)
 out = {}
-for dec, rows in enumerate(np.array_split(tr[1:], 5)):
+for dec, rows in enumerate(np.array_split(tr[1:-1], 5)):
     d = {}
-    for ix in range(1, 11):
+    for ix in range(1, LAST + 1):
         prev = ix - 1
         while prev > 0 and np.all(rows[:, prev] == 0):
             prev -= 1
         ok = (rows[:, ix] > 0) & (rows[:, prev] > 0)
         if ok.any():
             d[names[ix]] = round(float(np.mean(rows[ok, ix] - rows[ok, prev])) / 1.965e3, 2)
-    d["total_us"] = round(float(np.mean(rows[:, 10] - rows[:, 0])) / 1.965e3, 2)
+    d["total_us"] = round(float(np.mean(rows[:, LAST] - rows[:, 0])) / 1.965e3, 2)
+    d["post_wait_us"] = round(float(np.mean(rows[:, LAST] - rows[:, 2])) / 1.965e3, 2)
     out[f"quintile{dec}"] = d
 print(json.dumps(out, indent=1))
