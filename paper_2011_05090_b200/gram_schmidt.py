@@ -442,6 +442,81 @@ class RgsState:
         if st["code"]:
             self._raise_status(st)
 
+    def factorize_host_pipelined(self, Wh: np.ndarray, m: int, chunk: int = 32) -> QrFactors:
+        """End-to-end factorisation of a pinned, column-major host W (n x m,
+        Fortran order): W streams to the GPU in column chunks on one copy
+        stream while the compute stream sketches each chunk as it lands and
+        starts the column loop; finished Q columns stream back to a pinned host
+        buffer on a second copy stream.  Returns host factors (Q is a view of
+        pinned memory)."""
+        if self.m != 0:
+            raise RuntimeError("factorize_host_pipelined needs a fresh state")
+        n, k = self.n_local, self.k
+        self._reserve(m + 1)
+        dt = _lib.torch_dtype(Wh.dtype)
+        Wt = torch.from_numpy(Wh.T)  # (m, n) view of the pinned buffer
+        Wd = torch.empty((m, n), dtype=dt, device=self.device)
+        comp = torch.cuda.current_stream()
+        h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+        h2d.wait_stream(comp)
+        nchunks = (m + chunk - 1) // chunk
+        landed = []
+        with torch.cuda.stream(h2d):
+            for c in range(nchunks):
+                c0, c1 = c * chunk, min(m, (c + 1) * chunk)
+                Wd[c0:c1].copy_(Wt[c0:c1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(h2d)
+                landed.append(ev)
+        Qh, Qarr = _pinned_buffer((m, n), self.cdt)
+        wc, esz, base = _lib.dtype_code(dt), Wd.element_size(), Wd.data_ptr()
+        parts = torch.empty((chunk, self.nparts, k), dtype=torch.float64, device=self.device)
+        self.status.reset()
+
+        def sketch_chunk(c):
+            comp.wait_event(landed[c])
+            c0, c1 = c * chunk, min(m, (c + 1) * chunk)
+            self.theta.partials_into(base + c0 * n * esz, wc, n, c1 - c0, parts,
+                                     n_local=n, row0=self.row0, status=self.status)
+            call("sgs_partials_reduce", parts.data_ptr(), self.nparts, k, c1 - c0,
+                 self.theta.scale, self._P.data_ptr() + c0 * k * self._P.element_size(),
+                 self.fcode, k, self.status.ptr, stream_ptr())
+
+        def ship(c0, c1):
+            ev = torch.cuda.Event()
+            ev.record(comp)
+            d2h.wait_event(ev)
+            with torch.cuda.stream(d2h):
+                Qh[c0:c1].copy_(self._Q[c0:c1, :n], non_blocking=True)
+
+        sketch_chunk(0)
+        shipped = 0
+        for i in range(m):
+            nxt = i + 1
+            if nxt < m and nxt % chunk == 0:
+                sketch_chunk(nxt // chunk)
+            sol = nxt if nxt < m else None
+            if i == 0:
+                self._column(0, base, wc, False, False)
+                self._ls(fin=0, sol=sol)
+            else:
+                spp, snp, ssc = self._column(i, base + i * n * esz, wc, True, True)
+                self._ls(fin=i, s_parts=spp, s_nparts=snp, s_scale=ssc, sol=sol)
+                # columns < i are final once the column kernel i has normalised i-1
+                if i - shipped >= chunk:
+                    ship(shipped, shipped + chunk)
+                    shipped += chunk
+        self._normalize(m - 1)
+        if shipped < m:
+            ship(shipped, m)
+        comp.wait_stream(d2h)
+        st = self._sync_status()
+        if st["code"]:
+            self._raise_status(st)
+        Rh = self._R[:m, :m].t().cpu().numpy()
+        return QrFactors(Q=Qarr.T, R=Rh, S=self._S[:m].t().cpu().numpy(),
+                         P=self._P[:m].t().cpu().numpy())
+
     def capture_factorization(self, Wcm: torch.Tensor, ldw: int, m: int):
         """Capture the whole factorisation in a CUDA graph; ``graph.replay()``
         re-runs every kernel (status reset included) and ``finish()`` reads the
@@ -455,6 +530,34 @@ class RgsState:
                 self._enqueue_factorization(Wcm, ldw, m)
         torch.cuda.current_stream().wait_stream(side)
         return g
+
+
+_PINNED_POOL: list = []
+
+
+def _pinned_buffer(shape, dtype):
+    """Pinned host buffer (tensor, numpy view) for returned factors.  A buffer
+    whose numpy view is no longer referenced by a previous result is reused;
+    page-locking gigabytes on every call would dominate the end-to-end time."""
+    import sys
+    for ent in _PINNED_POOL:
+        t, arr = ent
+        # references: the pool tuple, the loop variable, getrefcount's argument
+        if tuple(t.shape) == tuple(shape) and t.dtype == dtype and sys.getrefcount(arr) <= 3:
+            return ent
+    t = torch.empty(shape, dtype=dtype, pin_memory=True)
+    ent = (t, t.numpy())
+    _PINNED_POOL.append(ent)
+    if len(_PINNED_POOL) > 4:
+        _PINNED_POOL.pop(0)
+    return ent
+
+
+def _is_pinned(a: np.ndarray) -> bool:
+    try:
+        return torch.from_numpy(a.T if a.flags.f_contiguous else a).is_pinned()
+    except Exception:
+        return False
 
 
 def ctypes_byref(a):
@@ -518,6 +621,12 @@ def rgs_factorize(W, theta, policy: PrecisionPolicy = MIXED32_64,
         state = RgsState(theta, policy, solver, phi=phi, capacity=m + 1,
                          breakdown_factor=breakdown_factor, comm=comm, row0=row0,
                          n_local=n_loc)
+        if (isinstance(W, np.ndarray) and not device_factors and comm is None
+                and W.dtype in (np.float32, np.float64) and W.flags.f_contiguous
+                and _is_pinned(W)):
+            factors = state.factorize_host_pipelined(W, m)
+            cert = certificates(factors) if with_certificate else None
+            return factors, cert
         Wd, ld = _device_columns(W, state.device)
         state.factorize_columns(Wd, ld, m)
     else:

@@ -190,3 +190,18 @@ def test_device_factors_and_certificates(cuda):
     assert np.array_equal(f.Q.cpu().numpy(), fh.Q)
     assert cert.delta_m == pytest.approx(certh.delta_m, rel=1e-10, abs=1e-15)
     assert cert.passes_gate()
+
+
+def test_pinned_host_pipeline_matches_device_path(cuda):
+    # the end-to-end path (chunked H2D / compute / D2H overlap) gives the same bits
+    n, m, k = 200_000, 80, 300
+    W = make_w(n, m, 1e-8, 21, dtype=np.float32)
+    pin = torch.empty((m, n), dtype=torch.float32, pin_memory=True)
+    pin.copy_(torch.from_numpy(np.ascontiguousarray(W.T)))
+    Wh = pin.numpy().T
+    assert Wh.flags.f_contiguous
+    th = sg.make_sketch(sg.SketchKind.PSRHT, k, n, 21)
+    a, _ = sg.rgs_factorize(Wh, th, sg.MIXED32_64, breakdown_factor=0.0)
+    b, _ = sg.rgs_factorize(W, th, sg.MIXED32_64, breakdown_factor=0.0)
+    for key in ("Q", "R", "S", "P"):
+        assert np.array_equal(getattr(a, key), getattr(b, key)), key
