@@ -262,8 +262,18 @@ def run_qr(args, cfg_name):
         tot_ms = sum(a.elapsed_time(b) for _, a, b in evs)
         tot_b = sum(update_alg_bytes(n_loc, i, bq, bw) for i, _, _ in evs)
         ach = tot_b / (tot_ms / 1e3) / 1e9
+        traffic, traffic_note = None, None
+        try:
+            with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+                tj = json.load(fh)
+            if tj.get("config") == cfg_name:
+                traffic = tj["dram_bytes"]
+                traffic_note = (f"ncu --set full, column {tj['column']}: {tj['dram_bytes']:.4g} B "
+                                f"DRAM vs {tj['alg_bytes']:.4g} B algorithmic ({tj['source']})")
+        except Exception:
+            pass
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": None, "kernel": "rgs_column_kernel (update + SRHT epilogue)" if cfg["kind"] != "gaussian" else "rgs_update_kernel",
+                "frac": round(ach / peak, 4), "traffic": traffic, "traffic_note": traffic_note, "kernel": "rgs_column_kernel (update + SRHT epilogue)" if cfg["kind"] != "gaussian" else "rgs_update_kernel",
                 "peak_source": peak_kind,
                 "share_of_step": round(tot_ms / ms, 4),
                 "launches": len(evs), "avg_launch_us": round(1e3 * tot_ms / len(evs), 2)}

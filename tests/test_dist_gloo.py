@@ -1,0 +1,101 @@
+"""Row-sharded RGS on two CPU ranks (gloo): the host logic of the multi-GPU
+path.  Each rank owns a tile-aligned row range (workloads.shard_rows), runs
+the n-dimensional steps on its rows, and gets every sketch as the all-reduce
+of its local (zero-padded) sketch; the k-dimensional least squares is
+replicated.  The result must equal the unsharded oracle: this is the
+structure RgsState(comm=...) runs on the GPUs with NCCL."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import OracleSketch, oracle_rgs_factorize
+from oracle.ref_rgs import householder_lsq
+from paper_2011_05090_b200.distributed import TorchComm
+from paper_2011_05090_b200.workloads import make_w, shard_rows
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _sharded_rgs(W, op, comm, row0, n_loc):
+    """RGS with sharded rows (fp64): local update, all-reduced sketches."""
+    n, m = W.shape
+    k = op.k
+
+    def sketch(local):
+        full = np.zeros(n)
+        full[row0:row0 + n_loc] = local
+        t = torch.from_numpy(op.apply(full))  # linear: sum of per-rank sketches
+        comm.allreduce_(t)
+        return t.numpy()
+
+    ls = householder_lsq(k, np.float64)
+    Q = np.zeros((n_loc, m))
+    R = np.zeros((m, m))
+    S = np.zeros((k, m))
+    for i in range(m):
+        w = W[row0:row0 + n_loc, i]
+        p = sketch(w)
+        if i == 0:
+            qp, sp, r = w.copy(), p.copy(), np.zeros(0)
+        else:
+            r = ls.solve(p)
+            qp = w - Q[:, :i] @ r
+            sp = sketch(qp)
+        rii = float(np.sqrt(np.sum(sp * sp)))
+        S[:, i] = sp / rii
+        Q[:, i] = qp / rii
+        R[:i, i] = r
+        R[i, i] = rii
+        ls.add(S[:, i])
+    return Q, R, S
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = TorchComm()
+    # 1. the all-reduce hook
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    comm.allreduce_(t)
+    assert float(t) == sum(range(1, world + 1))
+    # 2. sharded RGS on a tile-aligned row partition
+    n, m, k = 3 * 4096 + 123, 12, 64
+    W = make_w(n, m, 1e-4, 2)
+    op = OracleSketch("psrht", k, n, 2)
+    row0, n_loc = shard_rows(n, world, rank, 4096)
+    Q, R, S = _sharded_rgs(W, op, comm, row0, n_loc)
+    out[rank] = (row0, n_loc, Q, R, S)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_sharded_rgs_matches_unsharded():
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
+    n, m, k = 3 * 4096 + 123, 12, 64
+    W = make_w(n, m, 1e-4, 2)
+    ref = oracle_rgs_factorize(W, OracleSketch("psrht", k, n, 2), "f64")
+    Q = np.concatenate([out[r][2] for r in range(world)], axis=0)
+    assert [out[r][0] for r in range(world)] == [0, 8192]
+    for r in range(world):  # replicated k-dimensional state is identical
+        assert np.array_equal(out[r][3], out[0][3])
+        assert np.array_equal(out[r][4], out[0][4])
+    rel = lambda a, b: np.linalg.norm(a - b) / np.linalg.norm(b)
+    assert rel(Q, ref["Q"]) < 1e-12
+    assert rel(out[0][3], ref["R"]) < 1e-12
+    assert rel(out[0][4], ref["S"]) < 1e-12
