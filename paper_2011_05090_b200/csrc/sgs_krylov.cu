@@ -132,42 +132,60 @@ __global__ void cos_init_kernel(double* v, int64_t n) {
     v[r] = cos((double)r + 1.0);
 }
 
-// One progressive Givens step. Sequential over the previous rotations (O(i)
-// single-thread work); products and sums are not contracted so the rotation
-// arithmetic matches numpy's scalar expressions.
-__global__ void givens_step_kernel(const double* __restrict__ R, int64_t ldr, int i,
-                                   double* cs, double* sn, double* g, double* T, int64_t ldt,
-                                   double* hist, double tol, sgs_status* st) {
+// One progressive Givens step (krylov.py:282-301).  The O(i) rotation chain
+// is sequential; the Hessenberg column and the rotations are staged in shared
+// memory by the whole block so the single-thread chain only touches shared
+// memory.  Products and sums are not contracted so the arithmetic matches
+// numpy's scalar expressions.
+constexpr int kGivMax = 4096;
+__global__ void __launch_bounds__(256)
+givens_step_kernel(const double* __restrict__ R, int64_t ldr, int i, double* cs, double* sn,
+                   double* g, double* T, int64_t ldt, double* hist, double tol, sgs_status* st) {
   pdl_enter();
   if (status_stopped(st)) return;
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const double beta = R[0];
-  if (i == 0) g[0] = beta;
-  double* h = T + (int64_t)i * ldt;
+  extern __shared__ double gsm[];
+  double* h = gsm;            // i + 2
+  double* c_s = gsm + i + 2;  // i
+  double* s_s = c_s + i;      // i
   const double* rc = R + (int64_t)(i + 1) * ldr;
-  for (int j = 0; j < i + 2; ++j) h[j] = rc[j];
-  for (int j = 0; j < i; ++j) {
-    const double t = __dadd_rn(__dmul_rn(cs[j], h[j]), __dmul_rn(sn[j], h[j + 1]));
-    h[j + 1] = __dadd_rn(__dmul_rn(-sn[j], h[j]), __dmul_rn(cs[j], h[j + 1]));
-    h[j] = t;
+  for (int j = threadIdx.x; j < i + 2; j += blockDim.x) h[j] = rc[j];
+  for (int j = threadIdx.x; j < i; j += blockDim.x) {
+    c_s[j] = cs[j];
+    s_s[j] = sn[j];
   }
-  const double r = hypot(h[i], h[i + 1]);
-  double c, s;
-  if (r == 0.0) { c = 1.0; s = 0.0; }
-  else { c = h[i] / r; s = h[i + 1] / r; }
-  cs[i] = c;
-  sn[i] = s;
-  h[i] = r;
-  h[i + 1] = 0.0;
-  g[i + 1] = __dmul_rn(-s, g[i]);
-  g[i] = __dmul_rn(c, g[i]);
-  const double est = fabs(g[i + 1]) / beta;
-  hist[i] = est;
-  st->iters = i + 1;
-  if (tol >= 0.0 && est <= tol) {
-    st->code = SGS_ST_CONVERGED;
-    st->column = i + 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double beta = R[0];
+    if (i == 0) g[0] = beta;
+    double carry = h[0];
+    for (int j = 0; j < i; ++j) {
+      const double c = c_s[j], s = s_s[j], hn = h[j + 1];
+      h[j] = __dadd_rn(__dmul_rn(c, carry), __dmul_rn(s, hn));
+      carry = __dadd_rn(__dmul_rn(-s, carry), __dmul_rn(c, hn));
+    }
+    h[i] = carry;
+    const double r = hypot(h[i], h[i + 1]);
+    double c, s;
+    if (r == 0.0) { c = 1.0; s = 0.0; }
+    else { c = h[i] / r; s = h[i + 1] / r; }
+    cs[i] = c;
+    sn[i] = s;
+    h[i] = r;
+    h[i + 1] = 0.0;
+    const double gi = g[i];
+    g[i + 1] = __dmul_rn(-s, gi);
+    g[i] = __dmul_rn(c, gi);
+    const double est = fabs(g[i + 1]) / beta;
+    hist[i] = est;
+    st->iters = i + 1;
+    if (tol >= 0.0 && est <= tol) {
+      st->code = SGS_ST_CONVERGED;
+      st->column = i + 1;
+    }
   }
+  __syncthreads();
+  double* Tc = T + (int64_t)i * ldt;
+  for (int j = threadIdx.x; j < i + 2; j += blockDim.x) Tc[j] = h[j];
 }
 
 __global__ void status_init_kernel(sgs_status* st) {
@@ -303,6 +321,10 @@ extern "C" int sgs_givens_step(const double* R, int64_t ldr, int i, double* cs, 
                                sgs_status* st, void* stream) {
   SGS_REQUIRE(R && cs && sn && g && T && hist && st && i >= 0 && ldr >= i + 2 && ldt >= i + 2,
               "givens: bad args");
-  return check_ex(launch_ex(givens_step_kernel, dim3(1), dim3(32), 0, as_stream(stream), 1, R, ldr,
-                            i, cs, sn, g, T, ldt, hist, tol, st), "givens_step_kernel");
+  SGS_REQUIRE(i + 2 <= kGivMax, "givens: restart length %d too large", i + 2);
+  const size_t smem = (size_t)(3 * i + 2) * sizeof(double);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(givens_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return check_ex(launch_ex(givens_step_kernel, dim3(1), dim3(256), smem, as_stream(stream), 1, R,
+                            ldr, i, cs, sn, g, T, ldt, hist, tol, st), "givens_step_kernel");
 }

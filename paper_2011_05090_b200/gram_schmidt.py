@@ -94,6 +94,31 @@ class QrFactors:
     P_phi: object = None
 
 
+class LazyFactors:
+    """QrFactors view of a device state whose host copies are made on first
+    access (the Krylov drivers return factors like the reference, but most
+    callers never read them; copying an n x m basis back per cycle would
+    dominate the solve)."""
+
+    def __init__(self, state: "RgsState", m: int, device: bool = False):
+        self._state, self._m, self._device = state, m, device
+        self._cache = {}
+        self.S_phi = self.P_phi = None
+
+    def _get(self, name):
+        if name not in self._cache:
+            st, m = self._state, self._m
+            t = {"Q": lambda: st._Q[:m, :st.n_local].t(), "R": lambda: st._R[:m, :m].t(),
+                 "S": lambda: st._S[:m].t(), "P": lambda: st._P[:m].t()}[name]()
+            self._cache[name] = t.clone() if self._device else t.cpu().numpy()
+        return self._cache[name]
+
+    Q = property(lambda self: self._get("Q"))
+    R = property(lambda self: self._get("R"))
+    S = property(lambda self: self._get("S"))
+    P = property(lambda self: self._get("P"))
+
+
 @dataclass
 class StabilityCertificate:
     delta_m: float

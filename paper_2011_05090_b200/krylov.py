@@ -22,8 +22,8 @@ import torch
 
 from . import _lib
 from ._lib import call, stream_ptr
-from .gram_schmidt import (BREAKDOWN_FACTOR, HOUSEHOLDER_QR, GsVariant, LsqSolver, QrFactors,
-                           RgsState)
+from .gram_schmidt import (BREAKDOWN_FACTOR, HOUSEHOLDER_QR, GsVariant, LazyFactors, LsqSolver,
+                           QrFactors, RgsState)
 from .precision import MIXED32_64, PrecisionPolicy
 
 __all__ = ["SparseMatrix", "arnoldi", "gmres", "gmres_restarted", "ArnoldiDecomposition",
@@ -185,7 +185,13 @@ def _operator_norm_estimate(A: SparseMatrix, ws: _Workspace, iters: int = 20) ->
 
 
 class _ArnoldiEngine:
-    """Device Arnoldi driver over an RgsState (one stream, no per-step sync)."""
+    """Device Arnoldi driver over an RgsState (one stream, no per-step sync).
+
+    With an SRHT sketch on 4096-row tiles a step is five launches: the fused
+    SpMV (x = q'_i / r_ii formed on the fly, 1/alpha, SRHT of w in the
+    epilogue), the LS solve, the fused column kernel (which normalises q'_i in
+    place and sketches q'_{i+1}), the LS finalize and the Givens update.
+    Otherwise the generic path (separate SpMV, sketch and normalisation)."""
 
     def __init__(self, A: SparseMatrix, theta, policy, solver, m: int,
                  breakdown_factor: float = BREAKDOWN_FACTOR):
@@ -193,22 +199,56 @@ class _ArnoldiEngine:
         self.m = m
         self.state = RgsState(theta, policy, solver, capacity=m + 2,
                               breakdown_factor=breakdown_factor)
-        if self.state.n != A.n:
+        st = self.state
+        if st.n != A.n:
             raise ValueError("sketch ambient dimension does not match the operator")
-        dev = self.state.device
+        self.fused = st.fused
+        dev = st.device
         self.ws = _Workspace(A.n, dev)
         self.cs = torch.zeros(m + 1, dtype=torch.float64, device=dev)
         self.sn = torch.zeros_like(self.cs)
         self.g = torch.zeros(m + 2, dtype=torch.float64, device=dev)
         self.T = torch.zeros((m + 1, m + 2), dtype=torch.float64, device=dev)  # T[i] = column i
         self.hist = torch.zeros(m + 1, dtype=torch.float64, device=dev)
+        if self.fused:
+            self.parts_w = torch.empty((st.nparts_q, st.k), dtype=torch.float64, device=dev)
+
+    def start(self, b_dev: torch.Tensor, b_norm_ptr) -> None:
+        """Push b (divided by ||b|| when b_norm_ptr is given) as column 0."""
+        st, n = self.state, self.A.n
+        bn = self.ws.v
+        call("sgs_cast_div", b_dev.data_ptr(), _lib.SGS_F64, bn.data_ptr(), _lib.SGS_F64,
+             b_norm_ptr, n, stream_ptr())
+        if not self.fused:
+            st._push_async(bn)
+            return
+        pp, pn, ps = st._sketch_parts(bn.data_ptr(), _lib.SGS_F64, n, st._parts_p, None)
+        call("sgs_partials_reduce", pp, pn, st.k, 1, ps, st._P.data_ptr(), st.fcode, st.k,
+             st.status.ptr, stream_ptr())
+        st._column(0, bn.data_ptr(), _lib.SGS_F64, False, False)
+        st._ls(fin=0)
+        st.m = 1
 
     def step(self, i: int, alpha: torch.Tensor | None, tol: float | None) -> None:
         st = self.state
         A, ws = self.A, self.ws
-        # w = A q_i (/ alpha)
-        A.spmv_into(st._qcol_ptr(i), st.ccode, ws.w, alpha=alpha, status=st.status)
-        st._push_async(ws.w)
+        if self.fused:
+            rp, ci, va = A.device_arrays(ws.w.device)
+            d = st._theta_dev
+            rii = st._R.data_ptr() + (i * st._cap + i) * 8
+            call("sgs_csr_spmv_srht", A.n, rp.data_ptr(), ci.data_ptr(), va.data_ptr(),
+                 st._qcol_ptr(i), st.ccode, rii, alpha.data_ptr() if alpha is not None else None,
+                 ws.w.data_ptr(), 1, 0, st.theta.log2_block, d["bits"].data_ptr(),
+                 d["samples"].data_ptr(), st.k, self.parts_w.data_ptr(), st.status.ptr,
+                 stream_ptr())
+            st._ls(sol=i + 1, p_parts=self.parts_w.data_ptr(), p_nparts=st.nparts_q,
+                   p_scale=st.theta.scale)
+            sp, sn, ss = st._column(i + 1, ws.w.data_ptr(), _lib.SGS_F64, True, True)
+            st._ls(fin=i + 1, s_parts=sp, s_nparts=sn, s_scale=ss)
+            st.m = i + 2
+        else:
+            A.spmv_into(st._qcol_ptr(i), st.ccode, ws.w, alpha=alpha, status=st.status)
+            st._push_async(ws.w)
         if tol is not None or alpha is not None:
             call("sgs_givens_step", st._R.data_ptr(), st._cap, i, self.cs.data_ptr(),
                  self.sn.data_ptr(), self.g.data_ptr(), self.T.data_ptr(), self.T.shape[1],
@@ -232,7 +272,13 @@ class _ArnoldiEngine:
                     ev0.synchronize()
                     if int(hb0[0]) != 0:
                         break
-        return st._sync_status()
+        out = st._sync_status()
+        # fused path: the newest committed column is still q'/r_ii unless the
+        # stop was a breakdown (then the column kernel already normalised it)
+        if self.fused and out["ncols"] > 0 and out["code"] not in (_lib.ST_BREAKDOWN,
+                                                                   _lib.ST_NONFINITE):
+            st._normalize(out["ncols"] - 1, guarded=False)
+        return out
 
 
 def arnoldi(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, theta=None,
@@ -245,7 +291,7 @@ def arnoldi(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, thet
     eng = _ArnoldiEngine(A, theta, policy, solver, m)
     st = eng.state
     b_dev = _to_device_f64(b, A.n, st.device)
-    st._push_async(b_dev)
+    eng.start(b_dev, None)
     s0 = eng.run(alpha=None, tol=None)
     breakdown = s0["code"] in (_lib.ST_BREAKDOWN, _lib.ST_NONFINITE)
     if s0["code"] == _lib.ST_RANK:
@@ -281,10 +327,7 @@ def gmres(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, theta=
     alpha = _operator_norm_estimate(A, eng.ws)
     if float(alpha) <= 0.0:
         raise np.linalg.LinAlgError("operator norm estimate is zero")
-    bn = torch.empty_like(b_dev)
-    call("sgs_cast_div", b_dev.data_ptr(), _lib.SGS_F64, bn.data_ptr(), _lib.SGS_F64,
-         ws0.nrm.data_ptr(), A.n, stream_ptr())
-    st._push_async(bn)
+    eng.start(b_dev, ws0.nrm.data_ptr())
     s1 = eng.run(alpha=alpha, tol=tol)
     code = s1["code"]
     if code == _lib.ST_RANK:
@@ -315,7 +358,7 @@ def gmres(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, theta=
     return GmresResult(x=x.cpu().numpy() if return_numpy else x,
                        residual_history=np.asarray(hist), final_residual=true_res,
                        iterations=k, converged=converged or breakdown, breakdown=breakdown,
-                       factors=st.factors())
+                       factors=LazyFactors(st, st.m, device=not return_numpy))
 
 
 @dataclass
