@@ -178,16 +178,17 @@ def run_qr(args, cfg_name):
     th.device_data(dev)
     torch.cuda.synchronize()
 
-    def step():
-        st = sg.RgsState(th, pol, capacity=m + 1, breakdown_factor=bf, comm=comm, row0=row0,
+    # one device state for every step (W and Q of c2 are 67 GB each)
+    gstate = sg.RgsState(th, pol, capacity=m + 1, breakdown_factor=bf, comm=comm, row0=row0,
                          n_local=n_loc)
-        st.factorize_columns(Wt, ldw, m)
-        return st
+
+    def step():
+        gstate.m = 0
+        gstate.factorize_columns(Wt, ldw, m)
+        return gstate
 
     # the timed steps replay one CUDA graph of the whole factorisation (every
     # kernel re-runs; the graph only removes host launch overhead)
-    gstate = sg.RgsState(th, pol, capacity=m + 1, breakdown_factor=bf, comm=comm, row0=row0,
-                         n_local=n_loc)
     graph = None
     graph_launches = 0
     if not args.no_graph and comm is None:
@@ -281,6 +282,8 @@ def run_qr(args, cfg_name):
     # ---- e2e through the public API (pinned host W -> factors on the host)
     e2e = None
     if world == 1 and not args.no_e2e:
+        del graph, gstate
+        torch.cuda.empty_cache()
         pin = torch.empty((m, n), dtype=wdt, pin_memory=True)
         pin.copy_(Wt[:, :n])
         Wh = pin.numpy().T  # (n, m) Fortran-ordered numpy view of pinned memory
