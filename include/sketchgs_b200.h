@@ -131,6 +131,15 @@ int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
                         const uint32_t* sign_bits, const int32_t* samples, int k,
                         double* partials, const sgs_status* st, void* stream);
 
+/* Fused column kernel for dense sketches: sgs_rgs_update over the row chunks
+ * of sgs_dense_partials, q' kept in shared memory, then (do_sketch != 0) the
+ * Theta^T GEMV of the chunk - bit-identical partials to sgs_dense_partials. */
+int sgs_rgs_update_dense(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
+                         const void* w, int w_dtype, const void* r_crs,
+                         int normalize_prev, const double* R, int64_t ldr,
+                         int do_sketch, const double* thetaT, int64_t ldt, int k,
+                         double* partials, const sgs_status* st, void* stream);
+
 /* Q[:, col] = cast_crs(Q[:, col] / R[col, col])   (gram_schmidt.py:329) */
 int sgs_normalize_column(void* Q, int q_dtype, int64_t ldq, int64_t n,
                          int col, const double* R, int64_t ldr,

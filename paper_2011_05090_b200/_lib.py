@@ -65,6 +65,9 @@ _SIGS = {
     "sgs_rgs_update_srht": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_void_p, c_int,
                                     c_void_p, c_int, c_void_p, c_int64, c_int, c_int64, c_int,
                                     c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
+    "sgs_rgs_update_dense": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_void_p, c_int,
+                                     c_void_p, c_int, c_void_p, c_int64, c_int, c_void_p,
+                                     c_int64, c_int, c_void_p, c_void_p, c_void_p]),
     "sgs_normalize_column": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_void_p,
                                      c_int64, c_void_p, c_void_p]),
     "sgs_gemv_f64": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_void_p, c_void_p,

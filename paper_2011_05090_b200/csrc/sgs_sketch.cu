@@ -187,12 +187,13 @@ dense_gemv_kernel(const double* __restrict__ thetaT, int64_t ldt, int k,
   double2 acc[QP];
 #pragma unroll
   for (int q = 0; q < QP; ++q) acc[q] = make_double2(0.0, 0.0);
+  constexpr int U = (QP <= 2) ? 8 : 4;  // rows in flight per thread
   int64_t r = r0;
-  for (; r + 4 <= r1; r += 4) {
-    double xv[4];
-    double2 tv[4][QP];
+  for (; r + U <= r1; r += U) {
+    double xv[U];
+    double2 tv[U][QP];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       xv[u] = (double)__ldg(x + r + u);
 #pragma unroll
       for (int q = 0; q < QP; ++q) {
@@ -202,7 +203,7 @@ dense_gemv_kernel(const double* __restrict__ thetaT, int64_t ldt, int k,
       }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
 #pragma unroll
       for (int q = 0; q < QP; ++q) {
         acc[q].x = fma(tv[u][q].x, xv[u], acc[q].x);
@@ -231,8 +232,11 @@ dense_gemv_kernel(const double* __restrict__ thetaT, int64_t ldt, int k,
   }
 }
 
-// split-K GEMM tile: 64 sketch rows (j) x 32 columns (c), 16 data rows per stage.
-constexpr int kGBJ = 64, kGBC = 32, kGBR = 16;
+// split-K GEMM tile: 128 sketch rows (j) x 64 columns (c), 8 data rows per stage,
+// 256 threads each owning 8 (j) x 4 (c) outputs; per output the chain is the
+// ascending-row FMA of dense_gemv_kernel, so P = Theta W is bit-identical to
+// per-column sketches.
+constexpr int kGBJ = 128, kGBC = 64, kGBR = 8;
 
 template <typename TX>
 __global__ void __launch_bounds__(256)
@@ -241,48 +245,59 @@ dense_gemm_kernel(const double* __restrict__ thetaT, int64_t ldt, int k,
                   double* __restrict__ partials, const sgs_status* st) {
   pdl_enter();
   if (status_stopped(st)) return;
-  __shared__ double As[kGBR][kGBJ];
-  __shared__ double Bs[kGBR][kGBC + 1];
+  __shared__ __align__(16) double As[2][kGBR][kGBJ];
+  __shared__ __align__(16) double Bs[2][kGBR][kGBC];
   const int jt = blockIdx.x * kGBJ, ct = blockIdx.y * kGBC;
   const int p = blockIdx.z, nparts = gridDim.z;
   const int64_t r0 = chunk_begin(n, nparts, p), r1 = chunk_begin(n, nparts, p + 1);
-  const int tj = (threadIdx.x & 15) * 4;  // 4 sketch rows
-  const int tc = (threadIdx.x >> 4) * 2;  // 2 columns
-  double acc[4][2];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads
+  // thread outputs: j = jt + tx*4 + {0..3} and jt + 64 + tx*4 + {0..3};
+  //                 c = ct + ty*2 + {0,1} and ct + 32 + ty*2 + {0,1}
+  double acc[8][4];
 #pragma unroll
-  for (int a = 0; a < 4; ++a) acc[a][0] = acc[a][1] = 0.0;
-  for (int64_t rs = r0; rs < r1; rs += kGBR) {
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  auto load_stage = [&](int buf, int64_t rs) {
     const int nrow = (int)min((int64_t)kGBR, r1 - rs);
-    __syncthreads();
     for (int e = threadIdx.x; e < kGBR * kGBJ; e += blockDim.x) {
       const int rr = e / kGBJ, jj = e % kGBJ;
-      As[rr][jj] = (rr < nrow && jt + jj < k) ? __ldg(thetaT + (rs + rr) * ldt + jt + jj) : 0.0;
+      As[buf][rr][jj] = (rr < nrow && jt + jj < k) ? __ldg(thetaT + (rs + rr) * ldt + jt + jj) : 0.0;
     }
     for (int e = threadIdx.x; e < kGBR * kGBC; e += blockDim.x) {
       const int cc = e / kGBR, rr = e % kGBR;
-      Bs[rr][cc] = (rr < nrow && ct + cc < ncols)
-                       ? (double)__ldg(X + (int64_t)(ct + cc) * ldx + rs + rr) : 0.0;
+      Bs[buf][rr][cc] = (rr < nrow && ct + cc < ncols)
+                            ? (double)__ldg(X + (int64_t)(ct + cc) * ldx + rs + rr) : 0.0;
+    }
+  };
+  int buf = 0;
+  if (r0 < r1) load_stage(0, r0);
+  __syncthreads();
+  for (int64_t rs = r0; rs < r1; rs += kGBR) {
+    const int nrow = (int)min((int64_t)kGBR, r1 - rs);
+    if (rs + kGBR < r1) load_stage(buf ^ 1, rs + kGBR);
+    for (int rr = 0; rr < nrow; ++rr) {  // ascending rows: the GEMV's chain
+      const double4 a0 = *reinterpret_cast<const double4*>(&As[buf][rr][tx * 4]);
+      const double4 a1 = *reinterpret_cast<const double4*>(&As[buf][rr][64 + tx * 4]);
+      const double2 b0 = *reinterpret_cast<const double2*>(&Bs[buf][rr][ty * 2]);
+      const double2 b1 = *reinterpret_cast<const double2*>(&Bs[buf][rr][32 + ty * 2]);
+      const double av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const double bv[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
     }
     __syncthreads();
-    for (int rr = 0; rr < nrow; ++rr) {  // ascending rows: same chain as the GEMV
-      double a[4], b[2];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) a[q] = As[rr][tj + q];
-      b[0] = Bs[rr][tc];
-      b[1] = Bs[rr][tc + 1];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        acc[q][0] = fma(a[q], b[0], acc[q][0]);
-        acc[q][1] = fma(a[q], b[1], acc[q][1]);
-      }
-    }
+    buf ^= 1;
   }
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int a = 0; a < 8; ++a) {
+    const int j = jt + (a < 4 ? tx * 4 + a : 64 + tx * 4 + a - 4);
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int j = jt + tj + q, c = ct + tc + u;
-      if (j < k && c < ncols) partials[((int64_t)c * nparts + p) * k + j] = acc[q][u];
+    for (int b = 0; b < 4; ++b) {
+      const int c = ct + (b < 2 ? ty * 2 + b : 32 + ty * 2 + b - 2);
+      if (j < k && c < ncols) partials[((int64_t)c * nparts + p) * k + j] = acc[a][b];
     }
   }
 }
@@ -336,6 +351,164 @@ static int launch_fwht_tile(double* X, int64_t ldx, int64_t ntile, int ncols, cu
   int threads = T / 8 < 32 ? 32 : (T / 8 > 512 ? 512 : T / 8);
   kern<<<dim3((unsigned)ntile, ncols), threads, smem, s>>>(X, ldx);
   return check_launch("fwht_tile_kernel");
+}
+
+
+// ---------------------------------------------------------------------------
+// Fused column kernel for dense sketches (Gaussian / Rademacher, BASELINE
+// config 0): step 3 of push for the CTA's row chunk (the chunks of the dense
+// sketch, chunk_begin), q' kept in shared memory, then step 4 as the GEMV of
+// Theta^T[chunk, :] with q' - the same ascending-row FMA chain as
+// dense_gemv_kernel, so the sketch is bit-identical to the stand-alone one.
+template <typename TQ, typename TW, int QP>
+__global__ void __launch_bounds__(512)
+dense_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* __restrict__ w,
+                    const TQ* __restrict__ rc, int normalize_prev, const double* __restrict__ R,
+                    int64_t ldr, int do_sketch, const double* __restrict__ thetaT, int64_t ldt,
+                    int k, double* __restrict__ partials, const sgs_status* st) {
+  pdl_enter();
+  if (status_stopped(st)) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TQ* rs = reinterpret_cast<TQ*>(smem_raw);                       // i coefficients
+  double* xq = reinterpret_cast<double*>(smem_raw + ((size_t)(i > 0 ? i : 1) * sizeof(TQ) + 15) / 16 * 16);
+  const int p = blockIdx.x, nparts = gridDim.x;
+  const int64_t r0 = chunk_begin(n, nparts, p), r1 = chunk_begin(n, nparts, p + 1);
+  for (int j = threadIdx.x; j < i; j += blockDim.x) rs[j] = rc[j];
+  __syncthreads();
+  const int nplain = (i == 0) ? 0 : (normalize_prev ? i - 1 : i);
+  // rows of the chunk in passes of 2 x blockDim, each a single sweep over the columns
+  constexpr int RPT = 2;
+  for (int64_t base = r0; base < r1; base += (int64_t)RPT * blockDim.x) {
+  int64_t rr[RPT];
+  bool ok[RPT];
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    rr[u] = base + threadIdx.x + (int64_t)u * blockDim.x;
+    ok[u] = rr[u] < r1;
+  }
+  TQ acc[RPT];
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) acc[u] = TQ(0);
+  if (ok[0]) {
+    int j = 0;
+    for (; j + 8 <= nplain; j += 8) {
+      TQ q[8][RPT];
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+#pragma unroll
+        for (int u = 0; u < RPT; ++u)
+          q[c][u] = ok[u] ? __ldcs(Q + (int64_t)(j + c) * ldq + rr[u]) : TQ(0);
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) acc[u] = fma(q[c][u], rs[j + c], acc[u]);
+    }
+    for (; j < nplain; ++j)
+#pragma unroll
+      for (int u = 0; u < RPT; ++u)
+        if (ok[u]) acc[u] = fma(__ldcs(Q + (int64_t)j * ldq + rr[u]), rs[j], acc[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    if (!ok[u]) continue;
+    const int64_t r = rr[u];
+    if (i > 0 && normalize_prev) {
+      const int jj = i - 1;
+      TQ* cp = Q + (int64_t)jj * ldq + r;
+      const TQ qn = cvt<TQ>((double)*cp / R[(int64_t)jj * ldr + jj]);
+      *cp = qn;
+      acc[u] = fma(qn, rs[jj], acc[u]);
+    }
+    const TQ out = cvt<TQ>(__ldcs(w + r)) - acc[u];
+    Q[(int64_t)i * ldq + r] = out;
+    xq[r - r0] = (double)out;
+  }
+  }  // row passes
+  if (!do_sketch) return;
+  __syncthreads();
+  const int kp = (k + 1) >> 1;
+  double2 acc2[QP];
+#pragma unroll
+  for (int q = 0; q < QP; ++q) acc2[q] = make_double2(0.0, 0.0);
+  int64_t r = r0;
+  constexpr int U = (QP <= 2) ? 8 : 4;
+  for (; r + U <= r1; r += U) {
+    double2 tv[U][QP];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int q = 0; q < QP; ++q) {
+        const int jj = threadIdx.x + q * blockDim.x;
+        tv[u][q] = jj < kp ? __ldcs(reinterpret_cast<const double2*>(thetaT + (r + u) * ldt) + jj)
+                           : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double xv = xq[r + u - r0];
+#pragma unroll
+      for (int q = 0; q < QP; ++q) {
+        acc2[q].x = fma(tv[u][q].x, xv, acc2[q].x);
+        acc2[q].y = fma(tv[u][q].y, xv, acc2[q].y);
+      }
+    }
+  }
+  for (; r < r1; ++r) {
+    const double xv = xq[r - r0];
+#pragma unroll
+    for (int q = 0; q < QP; ++q) {
+      const int jj = threadIdx.x + q * blockDim.x;
+      if (jj < kp) {
+        const double2 tv = __ldcs(reinterpret_cast<const double2*>(thetaT + r * ldt) + jj);
+        acc2[q].x = fma(tv.x, xv, acc2[q].x);
+        acc2[q].y = fma(tv.y, xv, acc2[q].y);
+      }
+    }
+  }
+  double* outp = partials + (int64_t)p * k;
+#pragma unroll
+  for (int q = 0; q < QP; ++q) {
+    const int jj = threadIdx.x + q * blockDim.x;
+    if (2 * jj < k) outp[2 * jj] = acc2[q].x;
+    if (2 * jj + 1 < k) outp[2 * jj + 1] = acc2[q].y;
+  }
+}
+
+template <typename TQ, typename TW>
+static int launch_dense_column(void* Q, int64_t ldq, int64_t n, int i, const void* w,
+                               const void* r_crs, int normalize_prev, const double* R,
+                               int64_t ldr, int do_sketch, const double* thetaT, int64_t ldt,
+                               int k, double* partials, const sgs_status* st, cudaStream_t s) {
+  const int np = dense_nparts_host(n);
+  const int kp = (k + 1) / 2;
+  int threads = ((kp + 31) / 32) * 32;
+  if (threads < 256) threads = 256;
+  if (threads > 512) threads = 512;
+  const int qp = (kp + threads - 1) / threads;
+  const int64_t maxchunk = (n + np - 1) / np + 1;
+  if ((size_t)maxchunk * 8 > 160 * 1024) {
+    set_error("dense column: row chunk %lld too large for shared memory", (long long)maxchunk);
+    return SGS_EINVAL;
+  }
+  const size_t smem = ((size_t)(i > 0 ? i : 1) * sizeof(TQ) + 15) / 16 * 16 + (size_t)maxchunk * 8;
+  cudaError_t e;
+#define SGS_DC(QPV)                                                                             \
+  do {                                                                                          \
+    auto kern = dense_column_kernel<TQ, TW, QPV>;                                               \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
+    e = launch_ex(kern, dim3(np), dim3(threads), smem, s, 1, static_cast<TQ*>(Q), ldq, n, i,    \
+                  static_cast<const TW*>(w), static_cast<const TQ*>(r_crs), normalize_prev, R,  \
+                  ldr, do_sketch, thetaT, ldt, k, partials, st);                                \
+  } while (0)
+  if (qp <= 1) SGS_DC(1);
+  else if (qp <= 2) SGS_DC(2);
+  else if (qp <= 4) SGS_DC(4);
+  else if (qp <= 8) SGS_DC(8);
+  else {
+    set_error("dense column: k=%d too large", k);
+    return SGS_EINVAL;
+  }
+#undef SGS_DC
+  return check_ex(e, "dense_column_kernel");
 }
 
 }  // namespace sgs
@@ -474,4 +647,26 @@ extern "C" int sgs_fwht(double* X, int64_t s_len, int ncols, int64_t ldx, void* 
     if (rc) return rc;
   }
   return SGS_OK;
+}
+
+extern "C" int sgs_rgs_update_dense(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
+                                    const void* w, int w_dtype, const void* r_crs,
+                                    int normalize_prev, const double* R, int64_t ldr,
+                                    int do_sketch, const double* thetaT, int64_t ldt, int k,
+                                    double* partials, const sgs_status* st, void* stream) {
+  SGS_REQUIRE(Q && w && (i == 0 || r_crs) && n >= 1 && i >= 0, "update_dense: bad args");
+  SGS_REQUIRE(!normalize_prev || (i > 0 && R), "update_dense: normalize_prev needs R");
+  SGS_REQUIRE(!do_sketch || (thetaT && partials && ldt >= k && (ldt % 2) == 0 &&
+                             ((uintptr_t)thetaT & 15) == 0), "update_dense: sketch args");
+  cudaStream_t s = as_stream(stream);
+#define SGS_DCL(TQ, TW)                                                                        \
+  return launch_dense_column<TQ, TW>(Q, ldq, n, i, w, r_crs, normalize_prev, R, ldr, do_sketch, \
+                                     thetaT, ldt, k, partials, st, s)
+  if (q_dtype == SGS_F32 && w_dtype == SGS_F32) SGS_DCL(float, float);
+  if (q_dtype == SGS_F32 && w_dtype == SGS_F64) SGS_DCL(float, double);
+  if (q_dtype == SGS_F64 && w_dtype == SGS_F32) SGS_DCL(double, float);
+  if (q_dtype == SGS_F64 && w_dtype == SGS_F64) SGS_DCL(double, double);
+#undef SGS_DCL
+  set_error("update_dense: bad dtype");
+  return SGS_EINVAL;
 }

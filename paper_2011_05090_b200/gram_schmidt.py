@@ -307,6 +307,14 @@ class RgsState:
                  d["samples"].data_ptr(), self.k, self._parts_s.data_ptr(), self.status.ptr,
                  stream_ptr())
             return self._combine(self._parts_s, self.nparts_q, kvec) if sketch else None
+        if self.theta.is_dense:
+            d = self._theta_dev
+            call("sgs_rgs_update_dense", self._Q.data_ptr(), self.ccode, self.ldq, self.n_local,
+                 i, w_ptr, w_code, self._rc.data_ptr(), 1 if normalize_prev else 0,
+                 self._R.data_ptr(), self._cap, 1 if sketch else 0,
+                 d["thetaT"].data_ptr() + self.row0 * d["ldt"] * 8, d["ldt"], self.k,
+                 self._parts_s.data_ptr(), self.status.ptr, stream_ptr())
+            return self._combine(self._parts_s, self.nparts, kvec) if sketch else None
         self._update(i, w_ptr, w_code, normalize_prev)
         if not sketch:
             return None
