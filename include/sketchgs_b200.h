@@ -65,6 +65,9 @@ typedef struct sgs_status {
 
 /* ---- library ------------------------------------------------------------ */
 int sgs_abi_version(void);
+/* debug: %globaltimer stamps per column (8 x u64 each) into buf; NULL disables */
+void sgs_debug_timeline(void* buf);
+void sgs_debug_timeline_col(int64_t col);
 const char* sgs_last_error(void);
 /* number of kernels this library has launched (process-wide counter) */
 uint64_t sgs_launch_count(void);
@@ -184,6 +187,7 @@ typedef struct sgs_ls_args {
   sgs_status* st;
   long long* trace;      /* optional (NULL): clock64() at phase boundaries, CTA 0 */
   int cache_cols;        /* set by the library: columns of T cached in shared memory */
+  unsigned long long* timeline;  /* set by the library (debug timeline) */
 } sgs_ls_args;
 
 int64_t sgs_ls_scratch_elems(int k, int cap);
@@ -193,9 +197,11 @@ int sgs_ls_step(const sgs_ls_args* a, void* stream);
 /* ---- Krylov ---------------------------------------------------------------
  * SparseMatrix.matvec (krylov.py:81-83) fused with the 1/alpha scaling of
  * gmres (krylov.py:276): y = (A x) / alpha[0] (alpha == NULL: no scaling).
- * x is fp64 or a coarse column of Q. CSR with int32 indices, fp64 values. */
+ * x is fp64 or a coarse column of Q; xdiv != NULL forms x = cast(q / xdiv[0])
+ * on the fly (the basis column before its deferred normalisation).  CSR with
+ * int32 indices, fp64 values. */
 int sgs_csr_spmv(int64_t n, const int32_t* row_ptr, const int32_t* col_idx,
-                 const double* vals, const void* x, int x_dtype,
+                 const double* vals, const void* x, int x_dtype, const double* xdiv,
                  const double* alpha, double* y, const sgs_status* st,
                  void* stream);
 

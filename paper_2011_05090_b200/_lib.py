@@ -40,12 +40,15 @@ class LsArgs(ctypes.Structure):
         ("S", c_void_p), ("P", c_void_p), ("R", c_void_p),
         ("Qs", c_void_p), ("Rinv", c_void_p), ("alpha", c_void_p), ("scratch", c_void_p),
         ("r_crs", c_void_p), ("st", c_void_p), ("trace", c_void_p), ("cache_cols", c_int),
+        ("timeline", c_void_p),
     ]
 
 
 # name -> (restype, argtypes)
 _SIGS = {
     "sgs_abi_version": (c_int, []),
+    "sgs_debug_timeline": (None, [c_void_p]),
+    "sgs_debug_timeline_col": (None, [c_int64]),
     "sgs_last_error": (ctypes.c_char_p, []),
     "sgs_launch_count": (c_uint64, []),
     "sgs_device_sm_count": (c_int, [c_int]),
@@ -76,7 +79,7 @@ _SIGS = {
     "sgs_ls_cluster_size": (c_int, [c_int]),
     "sgs_ls_step": (c_int, [POINTER(LsArgs), c_void_p]),
     "sgs_csr_spmv": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p,
-                             c_void_p, c_void_p, c_void_p]),
+                             c_void_p, c_void_p, c_void_p, c_void_p]),
     "sgs_csr_spmv_srht": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p,
                                   c_void_p, c_void_p, c_int, c_int64, c_int, c_void_p, c_void_p,
                                   c_int, c_void_p, c_void_p, c_void_p]),

@@ -72,8 +72,9 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
                   const double* __restrict__ R, int64_t ldr, int do_sketch, int64_t row0,
                   int log2_block, const uint32_t* __restrict__ sign_bits,
                   const int32_t* __restrict__ samples, int k, double* __restrict__ partials,
-                  const sgs_status* st) {
+                  const sgs_status* st, unsigned long long* tl) {
   cg::cluster_group cl = cg::this_cluster();
+  if (tl && threadIdx.x == 0) atomicMin(tl + (int64_t)i * 16 + 0, gtimer());
   constexpr int V = VecT<TQ>::N;                  // rows per vector (4 fp32, 2 fp64)
   constexpr int NH = kColT / (kColThreads * V);   // vectors per thread (2 fp32, 4 fp64)
   constexpr int LV = (V == 4) ? 2 : 1;            // log2 V
@@ -109,14 +110,14 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
     for (int j = tid; j < k; j += blockDim.x) smp[j] = __ldg(sb + j);
   }
   __syncthreads();
-  pdl_enter();  // Q columns < i-1 are final before the predecessor (LS) ran, but
-                // keep the whole stream after the dependency wait for simplicity
-  if (status_stopped(st)) return;  // uniform over the grid
+  // Columns 0..i-2 of Q were finalised by the column kernel before the
+  // predecessor (the LS launch, which waited on it before letting this grid
+  // start), and w is an input: the ring prologue and the w rows are issued
+  // before the dependency wait, so the stream is already in flight when the
+  // coefficients r arrive.
   if (tid == 0 && active)
     for (int j = 0; j < S && j < nplain; ++j)
       tma_load_1d(ring + (size_t)j * kColT, Q + (int64_t)j * ldq + lr0, bytes, &mbar[j], policy);
-  for (int j = tid; j < i; j += blockDim.x) rs[j] = rc[j];
-
   int64_t rows[NH];
 #pragma unroll
   for (int hh = 0; hh < NH; ++hh)
@@ -127,6 +128,15 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
 #pragma unroll
     for (int v = 0; v < V; ++v)
       wv[hh][v] = (rows[hh] + v < n) ? cvt<TQ>(__ldcs(w + rows[hh] + v)) : TQ(0);
+  pdl_enter();
+  if (tl && threadIdx.x == 0) atomicMin(tl + (int64_t)i * 16 + 1, gtimer());
+  if (status_stopped(st)) {  // uniform over the grid; drain the prologue before leaving
+    if (tid == 0 && active)
+      for (int j = 0; j < S && j < nplain; ++j) mbar_wait(&mbar[j], 0u);
+    __syncthreads();
+    return;
+  }
+  for (int j = tid; j < i; j += blockDim.x) rs[j] = rc[j];
   __syncthreads();
 
   TQ acc[NH][V];
@@ -241,6 +251,7 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
     outp[j] = s;
   }
   cl.sync();
+  if (tl && threadIdx.x == 0) atomicMax(tl + (int64_t)i * 16 + 2, gtimer());
 }
 
 static int64_t column_ctas(int64_t n_local) {
@@ -287,7 +298,7 @@ extern "C" int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n,
     err = launch_ex(kern, dim3((unsigned)nctas), dim3(kColThreads), smem, s, kColCluster,     \
                     static_cast<TQ*>(Q), ldq, n, i, static_cast<const TW*>(w),                \
                     static_cast<const TQ*>(r_crs), normalize_prev, R, ldr, do_sketch, row0,  \
-                    log2_block, sign_bits, samples, k, partials, st);                         \
+                    log2_block, sign_bits, samples, k, partials, st, debug_timeline());       \
   } while (0)
   if (q_dtype == SGS_F32 && w_dtype == SGS_F32) SGS_COL(float, float);
   else if (q_dtype == SGS_F32 && w_dtype == SGS_F64) SGS_COL(float, double);
@@ -311,6 +322,8 @@ extern "C" int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n,
 // CSR streams coalesce; the tile then goes through the shared-memory FWHT.
 namespace sgs {
 
+constexpr int kSpmvBuf = 4096;  // products per 512-row chunk held in shared memory
+
 template <typename TX>
 __global__ void __launch_bounds__(kColThreads)
 csr_spmv_srht_kernel(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
@@ -318,12 +331,13 @@ csr_spmv_srht_kernel(int64_t n, const int32_t* __restrict__ rp, const int32_t* _
                      const double* __restrict__ xdiv, const double* __restrict__ alpha,
                      double* __restrict__ y, int do_sketch, int64_t row0, int log2_block,
                      const uint32_t* __restrict__ sign_bits, const int32_t* __restrict__ samples,
-                     int k, double* __restrict__ partials, const sgs_status* st) {
+                     int k, double* __restrict__ partials, const sgs_status* st,
+                     unsigned long long* tl) {
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* z = reinterpret_cast<double*>(smem_raw);  // pidx(4096) + 8
-  double* part = z + pidx(kColT) + 8;               // k
-  int32_t* smp = reinterpret_cast<int32_t*>(part + k);
+  double* part = z + pidx(kColT) + 8;               // max(k, kSpmvBuf)
+  int32_t* smp = reinterpret_cast<int32_t*>(part + (k > kSpmvBuf ? k : kSpmvBuf));
   const int tid = threadIdx.x;
   const int64_t lr0 = (int64_t)blockIdx.x * kColT;
   const bool active = lr0 < n;
@@ -335,28 +349,48 @@ csr_spmv_srht_kernel(int64_t n, const int32_t* __restrict__ rp, const int32_t* _
     for (int j = tid; j < k; j += blockDim.x) smp[j] = __ldg(sb + j);
   }
   pdl_enter();
+  if (tl && threadIdx.x == 0) atomicMin(tl + 9, gtimer());
   if (status_stopped(st)) return;  // uniform (nobody writes st here)
   const double dv = xdiv ? *xdiv : 1.0;
   const double al = alpha ? *alpha : 1.0;
+  auto xval = [&](int32_t c) -> double {
+    const TX xr = x[c];
+    return xdiv ? (double)cvt<TX>((double)xr / dv) : (double)xr;
+  };
   if (active) {
-#pragma unroll 2
-    for (int q = 0; q < kColT / kColThreads; ++q) {
-      const int e = q * kColThreads + tid;
-      const int64_t r = lr0 + e;
+    // CSR-stream: the tile's rows in chunks of 512 rows; the chunk's nonzeros
+    // are swept by all threads (coalesced vals / col_idx) into shared-memory
+    // products, then each thread sums its row in CSR order.  Chunks whose
+    // nonzeros exceed the product buffer fall back to thread-per-row.
+    double* prod = part;  // reuse: k + extra doubles sized by the host (kSpmvBuf)
+    for (int c0 = 0; c0 < kColT; c0 += kColThreads) {
+      const int64_t ra = lr0 + c0;
+      const int64_t rbnd = min(ra + kColThreads, n);
+      const int e = c0 + tid;
+      const int64_t r = ra + tid;
       double v = 0.0;
-      if (r < n) {
-        const int b = __ldg(rp + r), eidx = __ldg(rp + r + 1);
-        double acc = 0.0;
-        for (int p = b; p < eidx; ++p) {
-          const TX xr = x[__ldg(ci + p)];
-          const double xv = xdiv ? (double)cvt<TX>((double)xr / dv) : (double)xr;
-          acc = fma(__ldg(vals + p), xv, acc);
+      if (ra < n) {
+        const int64_t e0 = __ldg(rp + ra), e1 = __ldg(rp + rbnd);
+        const bool stream = (e1 - e0) <= kSpmvBuf;
+        __syncthreads();  // previous chunk's products consumed
+        if (stream) {
+          for (int64_t q = e0 + tid; q < e1; q += kColThreads)
+            prod[q - e0] = __ldg(vals + q) * xval(__ldg(ci + q));
         }
-        const double yv = alpha ? acc / al : acc;
-        y[r] = yv;
-        if (do_sketch) {
-          const uint32_t word = __ldg(sign_bits + (r >> 5));
-          v = ((word >> (r & 31)) & 1u) ? yv : -yv;
+        __syncthreads();
+        if (r < n) {
+          const int b = __ldg(rp + r), eidx = __ldg(rp + r + 1);
+          double acc = 0.0;
+          if (stream)
+            for (int q = b; q < eidx; ++q) acc += prod[q - e0];
+          else
+            for (int q = b; q < eidx; ++q) acc += __ldg(vals + q) * xval(__ldg(ci + q));
+          const double yv = alpha ? acc / al : acc;
+          y[r] = yv;
+          if (do_sketch) {
+            const uint32_t word = __ldg(sign_bits + (r >> 5));
+            v = ((word >> (r & 31)) & 1u) ? yv : -yv;
+          }
         }
       }
       if (do_sketch) z[pidx(e)] = v;
@@ -387,9 +421,14 @@ csr_spmv_srht_kernel(int64_t n, const int32_t* __restrict__ rp, const int32_t* _
     outp[j] = s;
   }
   cl.sync();
+  if (tl && threadIdx.x == 0) atomicMax(tl + 10, gtimer());
 }
 
 }  // namespace sgs
+
+// debug timeline row used by the next SpMV launch (set by sgs_debug_timeline_col)
+static int64_t g_timeline_col = 0;
+extern "C" void sgs_debug_timeline_col(int64_t col) { g_timeline_col = col; }
 
 extern "C" int sgs_csr_spmv_srht(int64_t n, const int32_t* row_ptr, const int32_t* col_idx,
                                  const double* vals, const void* x, int x_dtype,
@@ -404,20 +443,22 @@ extern "C" int sgs_csr_spmv_srht(int64_t n, const int32_t* row_ptr, const int32_
               "spmv_srht: needs 4096-row tiles");
   cudaStream_t s = as_stream(stream);
   const int64_t nctas = column_ctas(n);
-  const size_t smem = (size_t)(pidx(kColT) + 8 + k) * sizeof(double) + (size_t)k * sizeof(int32_t);
+  const size_t smem = (size_t)(pidx(kColT) + 8 + (k > kSpmvBuf ? k : kSpmvBuf)) * sizeof(double) +
+                      (size_t)k * sizeof(int32_t);
+  unsigned long long* tlr = debug_timeline() ? debug_timeline() + g_timeline_col * 16 : nullptr;
   cudaError_t err;
   if (x_dtype == SGS_F32) {
     auto kern = csr_spmv_srht_kernel<float>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     err = launch_ex(kern, dim3((unsigned)nctas), dim3(kColThreads), smem, s, kColCluster, n,
                     row_ptr, col_idx, vals, static_cast<const float*>(x), xdiv, alpha, y,
-                    do_sketch, row0, log2_block, sign_bits, samples, k, partials, st);
+                    do_sketch, row0, log2_block, sign_bits, samples, k, partials, st, tlr);
   } else {
     auto kern = csr_spmv_srht_kernel<double>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     err = launch_ex(kern, dim3((unsigned)nctas), dim3(kColThreads), smem, s, kColCluster, n,
                     row_ptr, col_idx, vals, static_cast<const double*>(x), xdiv, alpha, y,
-                    do_sketch, row0, log2_block, sign_bits, samples, k, partials, st);
+                    do_sketch, row0, log2_block, sign_bits, samples, k, partials, st, tlr);
   }
   return check_ex(err, "csr_spmv_srht_kernel");
 }

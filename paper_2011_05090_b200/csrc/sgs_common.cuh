@@ -92,6 +92,15 @@ __device__ __forceinline__ void pdl_enter() {
 
 bool pdl_enabled();
 
+// Optional debug timeline (sgs_debug_timeline): per column 8 x u64 of
+// %globaltimer stamps, written by the column and LS kernels when non-null.
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+unsigned long long* debug_timeline();
+
 // cudaLaunchKernelEx wrapper: PDL attribute (when enabled) + optional cluster.
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,

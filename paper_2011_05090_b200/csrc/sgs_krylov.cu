@@ -19,6 +19,9 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 
+static unsigned long long* g_timeline = nullptr;
+unsigned long long* debug_timeline() { return g_timeline; }
+
 bool pdl_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -39,18 +42,33 @@ int sm_count() {
   return cached;
 }
 
+// y = (A x) / alpha with, when xdiv != NULL, x = cast(q / xdiv[0]) formed on the
+// fly from a not yet normalised basis column (the rounding the next column
+// kernel applies when it normalises q in place).  Thread per row.
 template <typename TX>
 __global__ void __launch_bounds__(256)
 csr_spmv_kernel(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                 const double* __restrict__ vals, const TX* __restrict__ x,
-                const double* __restrict__ alpha, double* __restrict__ y, const sgs_status* st) {
+                const double* __restrict__ xdiv, const double* __restrict__ alpha,
+                double* __restrict__ y, const sgs_status* st) {
   pdl_enter();
   if (status_stopped(st)) return;
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const int b = __ldg(rp + r), e = __ldg(rp + r + 1);
   double acc = 0.0;
-  for (int q = b; q < e; ++q) acc = fma(__ldg(vals + q), (double)__ldg(x + __ldg(ci + q)), acc);
+  if (xdiv) {
+    const double dv = __ldg(xdiv);
+    for (int q = b; q < e; ++q) {
+      const TX xr = __ldg(x + __ldg(ci + q));
+      TX xn;
+      if constexpr (sizeof(TX) == 4) xn = __double2float_rn((double)xr / dv);
+      else xn = (TX)((double)xr / dv);
+      acc = fma(__ldg(vals + q), (double)xn, acc);
+    }
+  } else {
+    for (int q = b; q < e; ++q) acc = fma(__ldg(vals + q), (double)__ldg(x + __ldg(ci + q)), acc);
+  }
   y[r] = alpha ? acc / __ldg(alpha) : acc;
 }
 
@@ -140,7 +158,8 @@ __global__ void cos_init_kernel(double* v, int64_t n) {
 constexpr int kGivMax = 4096;
 __global__ void __launch_bounds__(256)
 givens_step_kernel(const double* __restrict__ R, int64_t ldr, int i, double* cs, double* sn,
-                   double* g, double* T, int64_t ldt, double* hist, double tol, sgs_status* st) {
+                   double* g, double* T, int64_t ldt, double* hist, double tol, sgs_status* st,
+                   unsigned long long* tl) {
   pdl_enter();
   if (status_stopped(st)) return;
   extern __shared__ double gsm[];
@@ -186,6 +205,7 @@ givens_step_kernel(const double* __restrict__ R, int64_t ldr, int i, double* cs,
   __syncthreads();
   double* Tc = T + (int64_t)i * ldt;
   for (int j = threadIdx.x; j < i + 2; j += blockDim.x) Tc[j] = h[j];
+  if (tl && threadIdx.x == 0) tl[(int64_t)(i + 1) * 16 + 11] = gtimer();
 }
 
 __global__ void status_init_kernel(sgs_status* st) {
@@ -212,6 +232,10 @@ static unsigned grid_for(int64_t n, int threads = 256) {
 using namespace sgs;
 
 extern "C" int sgs_abi_version(void) { return SGS_ABI_VERSION; }
+/* debug: per-column kernel timeline (8 x u64 per column), NULL disables */
+extern "C" void sgs_debug_timeline(void* buf) {
+  g_timeline = static_cast<unsigned long long*>(buf);
+}
 extern "C" const char* sgs_last_error(void) { return g_err; }
 extern "C" uint64_t sgs_launch_count(void) { return g_launches.load(); }
 
@@ -231,17 +255,17 @@ extern "C" int sgs_status_init(sgs_status* st, void* stream) {
 }
 
 extern "C" int sgs_csr_spmv(int64_t n, const int32_t* row_ptr, const int32_t* col_idx,
-                            const double* vals, const void* x, int x_dtype, const double* alpha,
-                            double* y, const sgs_status* st, void* stream) {
+                            const double* vals, const void* x, int x_dtype, const double* xdiv,
+                            const double* alpha, double* y, const sgs_status* st, void* stream) {
   SGS_REQUIRE(n >= 1 && row_ptr && col_idx && vals && x && y, "spmv: bad args");
   cudaStream_t s = as_stream(stream);
   const unsigned blocks = (unsigned)((n + 255) / 256);
   if (x_dtype == SGS_F32)
     return check_ex(launch_ex(csr_spmv_kernel<float>, dim3(blocks), dim3(256), 0, s, 1, n, row_ptr,
-                              col_idx, vals, static_cast<const float*>(x), alpha, y, st),
+                              col_idx, vals, static_cast<const float*>(x), xdiv, alpha, y, st),
                     "csr_spmv_kernel");
   return check_ex(launch_ex(csr_spmv_kernel<double>, dim3(blocks), dim3(256), 0, s, 1, n, row_ptr,
-                            col_idx, vals, static_cast<const double*>(x), alpha, y, st),
+                            col_idx, vals, static_cast<const double*>(x), xdiv, alpha, y, st),
                   "csr_spmv_kernel");
 }
 
@@ -326,5 +350,6 @@ extern "C" int sgs_givens_step(const double* R, int64_t ldr, int i, double* cs, 
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(givens_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   return check_ex(launch_ex(givens_step_kernel, dim3(1), dim3(256), smem, as_stream(stream), 1, R,
-                            ldr, i, cs, sn, g, T, ldt, hist, tol, st), "givens_step_kernel");
+                            ldr, i, cs, sn, g, T, ldt, hist, tol, st, debug_timeline()),
+                  "givens_step_kernel");
 }

@@ -556,7 +556,10 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     }
   }
   SGS_TR(1);
+  unsigned long long* tl = a.timeline;
+  if (tl && rank == 0 && threadIdx.x == 0) tl[3] = gtimer();
   pdl_enter();
+  if (tl && rank == 0 && threadIdx.x == 0) tl[4] = gtimer();
   SGS_TR(2);
   if (code0 != 0) return;  // uniform: nobody writes st before a cluster barrier
 
@@ -729,6 +732,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     }
     SGS_TR(10);
   }
+  if (tl && rank == 0 && threadIdx.x == 0) tl[5] = gtimer();
 #undef SGS_TR
 }
 
@@ -749,13 +753,18 @@ static int launch_ls(const sgs_ls_args* a, cudaStream_t s) {
   }
   // cache as many columns of this CTA's rows of T as fit
   const int RM = (a->k + CL - 1) / CL;
-  const int ncols_t = a->do_finalize ? a->col_fin : a->col_sol;
+  const int ncols_t = a->do_finalize ? a->col_fin : 0;  // solve-only: read T once, no cache
   int cache = (int)((kLsSmemMax - fixed) / ((size_t)RM * sizeof(T)));
   if (cache > ncols_t) cache = ncols_t;
   if (cache < 0) cache = 0;
   const size_t smem = fixed + (size_t)cache * RM * sizeof(T);
   sgs_ls_args aa = *a;
   aa.cache_cols = cache;
+  {
+    unsigned long long* tlb = debug_timeline();
+    const int col = a->do_finalize ? a->col_fin : a->col_sol;
+    aa.timeline = tlb ? tlb + (int64_t)col * 16 + (a->do_finalize ? 0 : 3) : nullptr;
+  }
   auto kern = ls_step_kernel<T>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (CL > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

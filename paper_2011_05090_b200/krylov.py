@@ -90,10 +90,11 @@ class SparseMatrix:
             cache[str(dev)] = d
         return d
 
-    def spmv_into(self, x_ptr: int, x_code: int, y: torch.Tensor, alpha=None, status=None):
+    def spmv_into(self, x_ptr: int, x_code: int, y: torch.Tensor, alpha=None, status=None,
+                  xdiv_ptr=None):
         rp, ci, va = self.device_arrays(y.device)
         call("sgs_csr_spmv", self.n, rp.data_ptr(), ci.data_ptr(), va.data_ptr(), x_ptr, x_code,
-             alpha.data_ptr() if alpha is not None else None, y.data_ptr(),
+             xdiv_ptr, alpha.data_ptr() if alpha is not None else None, y.data_ptr(),
              status.ptr if status is not None else None, stream_ptr())
 
     def matvec(self, x):
@@ -210,8 +211,6 @@ class _ArnoldiEngine:
         self.g = torch.zeros(m + 2, dtype=torch.float64, device=dev)
         self.T = torch.zeros((m + 1, m + 2), dtype=torch.float64, device=dev)  # T[i] = column i
         self.hist = torch.zeros(m + 1, dtype=torch.float64, device=dev)
-        if self.fused:
-            self.parts_w = torch.empty((st.nparts_q, st.k), dtype=torch.float64, device=dev)
 
     def start(self, b_dev: torch.Tensor, b_norm_ptr) -> None:
         """Push b (divided by ||b|| when b_norm_ptr is given) as column 0."""
@@ -233,16 +232,11 @@ class _ArnoldiEngine:
         st = self.state
         A, ws = self.A, self.ws
         if self.fused:
-            rp, ci, va = A.device_arrays(ws.w.device)
-            d = st._theta_dev
             rii = st._R.data_ptr() + (i * st._cap + i) * 8
-            call("sgs_csr_spmv_srht", A.n, rp.data_ptr(), ci.data_ptr(), va.data_ptr(),
-                 st._qcol_ptr(i), st.ccode, rii, alpha.data_ptr() if alpha is not None else None,
-                 ws.w.data_ptr(), 1, 0, st.theta.log2_block, d["bits"].data_ptr(),
-                 d["samples"].data_ptr(), st.k, self.parts_w.data_ptr(), st.status.ptr,
-                 stream_ptr())
-            st._ls(sol=i + 1, p_parts=self.parts_w.data_ptr(), p_nparts=st.nparts_q,
-                   p_scale=st.theta.scale)
+            A.spmv_into(st._qcol_ptr(i), st.ccode, ws.w, alpha=alpha, status=st.status,
+                        xdiv_ptr=rii)
+            pp, pn, ps = st._sketch_parts(ws.w.data_ptr(), _lib.SGS_F64, A.n, st._parts_p, None)
+            st._ls(sol=i + 1, p_parts=pp, p_nparts=pn, p_scale=ps)
             sp, sn, ss = st._column(i + 1, ws.w.data_ptr(), _lib.SGS_F64, True, True)
             st._ls(fin=i + 1, s_parts=sp, s_nparts=sn, s_scale=ss)
             st.m = i + 2

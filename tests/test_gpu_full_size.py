@@ -1,0 +1,62 @@
+"""BASELINE-size checks on the GPU, through size-independent properties and
+the oracle-pinned RGMRES iteration counts (tests/golden/c3_oracle_128.json,
+produced by oracle/run_c3_oracle.py)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2011_05090_b200 as sg
+from conftest import GOLDEN
+from paper_2011_05090_b200.workloads import CONFIGS, convdiff3d, make_w_device, rhs_gaussian
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("policy", ["f64", "mixed"])
+def test_c3_rgmres_iterations_match_oracle(cuda, policy):
+    ref = json.load(open(os.path.join(GOLDEN, "c3_oracle_128.json")))[policy]
+    cfg = CONFIGS["c3"]
+    N = cfg["grid"]
+    rp, ci, va = convdiff3d(N, (cfg["beta"],) * 3)
+    A = sg.SparseMatrix(n=N ** 3, row_ptr=rp, col_idx=ci, values=va)
+    b = torch.from_numpy(rhs_gaussian(A.n, 0)).cuda()
+    th = sg.make_sketch(sg.SketchKind.PSRHT, cfg["k"], A.n, 0)
+    res = sg.gmres_restarted(A, b, th, sg.policy_from_name(policy), cfg["restart"],
+                             cfg["max_iters"], cfg["tol"])
+    its = ref["iterations"]
+    assert abs(res.iterations - its) <= round(0.02 * its), (res.iterations, its)
+    assert res.final_residual <= cfg["tol"]
+    assert res.cycles[0] == ref["cycles"][0]
+
+
+def test_c1_size_factorization_properties(cuda):
+    # c1 shape (n = 1e6, k = 1500 P-SRHT, mixed, breakdown_factor 0) with m = 96
+    n, m, k = 1_000_000, 96, 1500
+    W = make_w_device(n, m, 1e-10, 0, torch.float32, "cuda")
+    th = sg.make_sketch(sg.SketchKind.PSRHT, k, n, 0)
+    st = sg.RgsState(th, sg.MIXED32_64, capacity=m + 1, breakdown_factor=0.0)
+    st.factorize_columns(W, W.shape[1], m)
+    f = st.device_factors()
+    Q64, R = f.Q.double(), f.R
+    Wm = W[:, :n].t().double()
+    # S = Theta Q and P = Theta W for the computed factors (fine-dtype sketches)
+    cols = [0, 1, m // 2, m - 1]
+    SQ = th.apply_block(f.Q[:, cols])
+    assert float(torch.linalg.norm(SQ - f.S[:, cols]) / torch.linalg.norm(f.S[:, cols])) < 1e-6
+    PW = th.apply_block(Wm[:, cols])
+    assert float(torch.linalg.norm(PW - f.P[:, cols]) / torch.linalg.norm(f.P[:, cols])) < 1e-12
+    # W = Q R to the coarse roundoff, S nearly orthonormal, R upper triangular
+    rel = float(torch.linalg.norm(Wm - Q64 @ R) / torch.linalg.norm(Wm))
+    assert rel < 1e-5
+    eye = torch.eye(m, dtype=torch.float64, device="cuda")
+    assert float(torch.linalg.norm(eye - f.S.t() @ f.S, 2)) < 0.5
+    assert float(torch.linalg.norm(torch.tril(R, -1))) == 0.0
+    # bit-identical rerun of the whole factorisation
+    st2 = sg.RgsState(th, sg.MIXED32_64, capacity=m + 1, breakdown_factor=0.0)
+    st2.factorize_columns(W, W.shape[1], m)
+    g = st2.device_factors()
+    assert torch.equal(f.Q, g.Q) and torch.equal(f.R, g.R) and torch.equal(f.S, g.S)
