@@ -25,7 +25,7 @@ __device__ __forceinline__ double load_as_double(const TX* p) { return (double)_
 
 constexpr int kSrhtThreads = 512;
 constexpr int kSrhtMaxLogT = 12;   // 4096-row tiles (32 KB of fp64)
-constexpr int kSrhtTargetCTAs = 296;
+constexpr int kSrhtTargetCTAs = 1024;  // one tile per CTA up to 1024 tiles (4M rows)
 constexpr int kSrhtCluster = 8;    // CTAs whose k-vector partials are combined through DSMEM
 
 // One CTA transforms `tiles_per_cta` consecutive tiles and accumulates the
