@@ -205,3 +205,28 @@ def test_pinned_host_pipeline_matches_device_path(cuda):
     b, _ = sg.rgs_factorize(W, th, sg.MIXED32_64, breakdown_factor=0.0)
     for key in ("Q", "R", "S", "P"):
         assert np.array_equal(getattr(a, key), getattr(b, key)), key
+
+
+@pytest.mark.parametrize("kind,k,n,pol,blog", [
+    ("psrht", 300, 20_000, "f32", None),          # UNIFIED32 through the fused column kernel
+    ("block_srht", 3000, 4 * 16384, "mixed", 14),  # c4-like: k = 3000 (> 128 rows per LS CTA)
+    ("block_srht", 2000, 8 * 8192, "f64", 13),     # c2-like block structure
+])
+def test_rgs_larger_k_and_policies_vs_oracle(cuda, kind, k, n, pol, blog):
+    m = 40
+    W = make_w(n, m, 1e-6, 5, dtype=np.float32 if pol != "f64" else np.float64)
+    kw = {"block_log2": blog} if blog else {}
+    th = sg.make_sketch(sg.SketchKind(kind), k, n, 5, **kw)
+    f, _ = sg.rgs_factorize(W, th, POL[pol], breakdown_factor=0.0)
+    ref = oracle_rgs_factorize(W, OracleSketch(kind, k, n, 5, **kw), pol, 0.0)
+    ours = factor_metrics(W, f.Q, f.R, f.S)
+    theirs = factor_metrics(W, ref["Q"], ref["R"], ref["S"])
+    for key in ours:
+        assert _within_10x(ours[key], theirs[key]), (key, ours[key], theirs[key])
+    if pol == "f64":
+        assert rel_diff(f.Q, ref["Q"]) <= 1e-10 and rel_diff(f.R, ref["R"]) <= 1e-10
+    # streaming == batch holds on these paths too
+    st = sg.RgsState(th, POL[pol], breakdown_factor=0.0)
+    for j in range(8):
+        st.push(W[:, j])
+    assert np.array_equal(st.R, f.R[:8, :8])
