@@ -245,7 +245,9 @@ class RgsState:
     # ---- kernels ---------------------------------------------------------------
     def _ls(self, *, fin: int | None = None, s_parts=None, s_nparts=0, s_scale=1.0,
             sol: int | None = None, p_parts=None, p_nparts=0, p_scale=1.0) -> None:
-        a = _lib.LsArgs()
+        a = self.__dict__.get("_ls_args")
+        if a is None:
+            a = self._ls_args = _lib.LsArgs()  # reused: the library copies it at launch
         a.k, a.cap, a.fine_dtype, a.coarse_dtype = self.k, self._cap, self.fcode, self.ccode
         a.do_finalize = 1 if fin is not None else 0
         a.col_fin = fin if fin is not None else 0
@@ -523,7 +525,7 @@ class RgsState:
                 Qh[c0:c1].copy_(self._Q[c0:c1, :n], non_blocking=True)
 
         sketch_chunk(0)
-        shipped = 0
+        shipped, ship_chunk = 0, 8
         for i in range(m):
             nxt = i + 1
             if nxt < m and nxt % chunk == 0:
@@ -536,9 +538,9 @@ class RgsState:
                 spp, snp, ssc = self._column(i, base + i * n * esz, wc, True, True)
                 self._ls(fin=i, s_parts=spp, s_nparts=snp, s_scale=ssc, sol=sol)
                 # columns < i are final once the column kernel i has normalised i-1
-                if i - shipped >= chunk:
-                    ship(shipped, shipped + chunk)
-                    shipped += chunk
+                if i - shipped >= ship_chunk:
+                    ship(shipped, shipped + ship_chunk)
+                    shipped += ship_chunk
         self._normalize(m - 1)
         if shipped < m:
             ship(shipped, m)

@@ -51,3 +51,24 @@ def test_pure_host_queries_without_gpu():
     assert lib.sgs_dense_nparts(100_000) == 296
     assert 1 <= lib.sgs_ls_cluster_size(1500) <= 16
     assert lib.sgs_ls_scratch_elems(1500, 501) > 0
+
+
+def test_error_convention_without_gpu():
+    # argument validation happens before any CUDA call: negative code + message
+    from paper_2011_05090_b200 import _lib
+    lib = _lib.load()
+    rc = lib.sgs_srht_partials(None, 1, 10, 1, 10, 0, 4, None, None, 4, None, None, None)
+    assert rc == -1
+    assert b"null pointer" in lib.sgs_last_error()
+    rc = lib.sgs_fwht(None, 6, 1, 6, None)
+    assert rc == -1
+    rc = lib.sgs_rgs_update(None, 0, 8, 8, 0, None, 0, None, 0, None, 8, None, None)
+    assert rc == -1 and b"update" in lib.sgs_last_error()
+    a = _lib.LsArgs()
+    assert lib.sgs_ls_step(ctypes_byref(a), None) == -1
+    assert b"ls_step" in lib.sgs_last_error()
+
+
+def ctypes_byref(x):
+    import ctypes
+    return ctypes.byref(x)
