@@ -104,6 +104,12 @@ int sgs_partials_reduce(const double* partials, int nparts, int k, int ncols,
                         double scale, void* Y, int y_dtype, int64_t ldy,
                         const sgs_status* st, void* stream);
 
+/* as sgs_partials_reduce, then divided by den[0]: the certification sketch
+ * S_phi[:, i] = (Phi q'_i) / r_ii of gram_schmidt.py:333-335 */
+int sgs_partials_reduce_div(const double* partials, int nparts, int k, int ncols,
+                            double scale, const double* den, void* Y, int y_dtype,
+                            int64_t ldy, const sgs_status* st, void* stream);
+
 /* Unnormalised Sylvester FWHT along axis 0 of a power-of-two length vector,
  * batched over columns (sketch.py:90-109). */
 int sgs_fwht(double* X, int64_t s, int ncols, int64_t ldx, void* stream);

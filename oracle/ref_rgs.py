@@ -81,8 +81,9 @@ class OracleRgs:
     """Streaming RGS state (gram_schmidt.py:228-347) with preallocated storage."""
 
     def __init__(self, theta, policy: str = "mixed", breakdown_factor: float = 10.0,
-                 capacity: int = 16):
+                 capacity: int = 16, phi=None):
         self.theta = theta
+        self.phi = phi
         self.crs, self.fine, self.u_crs = POLICIES[policy]
         self.bf = float(breakdown_factor)
         n, k = theta.n, theta.k
@@ -92,6 +93,9 @@ class OracleRgs:
         self._S = np.zeros((k, capacity), dtype=self.fine)
         self._P = np.zeros((k, capacity), dtype=self.fine)
         self.ls = householder_lsq(k, self.fine)
+        if phi is not None:
+            self._S_phi = np.zeros((phi.k, capacity), dtype=self.fine)
+            self._P_phi = np.zeros((phi.k, capacity), dtype=self.fine)
 
     def _ensure(self):
         cap = self._Q.shape[1]
@@ -99,6 +103,8 @@ class OracleRgs:
             return
         grow = lambda a: np.concatenate([a, np.zeros((a.shape[0], cap), a.dtype)], axis=1)
         self._Q, self._S, self._P = grow(self._Q), grow(self._S), grow(self._P)
+        if self.phi is not None:
+            self._S_phi, self._P_phi = grow(self._S_phi), grow(self._P_phi)
         R = np.zeros((2 * cap, 2 * cap))
         R[:cap, :cap] = self._R
         self._R = R
@@ -110,6 +116,8 @@ class OracleRgs:
         fine = np.dtype(self.fine)
         w64 = np.asarray(w, dtype=np.float64)
         p = self.theta.apply(w64).astype(fine)                      # step 1
+        if self.phi is not None:                                    # gram_schmidt.py:304-305
+            self._P_phi[:, i] = self.phi.apply(w64).astype(fine)
         if i == 0:
             r = np.zeros(0, dtype=fine)
             qp = w64.astype(self.crs)
@@ -127,6 +135,8 @@ class OracleRgs:
         self._P[:, i] = p
         self._R[:i, i] = r.astype(np.float64)
         self._R[i, i] = r_ii
+        if self.phi is not None:                                    # gram_schmidt.py:333-335
+            self._S_phi[:, i] = (self.phi.apply(qp.astype(np.float64)) / r_ii).astype(fine)
         self.ls.add(self._S[:, i])
         self.m += 1
         return r_ii
@@ -148,16 +158,21 @@ class OracleRgs:
         return self._P[:, :self.m]
 
 
-def oracle_rgs_factorize(W, theta, policy: str = "mixed", breakdown_factor: float = 10.0):
-    """Returns dict Q, R, S, P (gram_schmidt.py:350-375)."""
+def oracle_rgs_factorize(W, theta, policy: str = "mixed", breakdown_factor: float = 10.0,
+                         phi=None):
+    """Returns dict Q, R, S, P (+ S_phi, P_phi) (gram_schmidt.py:350-375)."""
     W = np.asarray(W)
     n, m = W.shape
     if not (theta.k >= m and n >= m >= 1):
         raise ValueError("need k >= m and n >= m >= 1")
-    st = OracleRgs(theta, policy, breakdown_factor, capacity=16)
+    st = OracleRgs(theta, policy, breakdown_factor, capacity=16, phi=phi)
     for j in range(m):
         st.push(W[:, j])
-    return {"Q": st.Q.copy(), "R": st.R.copy(), "S": st.S.copy(), "P": st.P.copy()}
+    out = {"Q": st.Q.copy(), "R": st.R.copy(), "S": st.S.copy(), "P": st.P.copy()}
+    if phi is not None:
+        out["S_phi"] = st._S_phi[:, :st.m].copy()
+        out["P_phi"] = st._P_phi[:, :st.m].copy()
+    return out
 
 
 def oracle_certificates(S, P, R):

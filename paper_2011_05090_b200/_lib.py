@@ -61,6 +61,8 @@ _SIGS = {
                                    c_int64, c_void_p, c_void_p, c_void_p]),
     "sgs_partials_reduce": (c_int, [c_void_p, c_int, c_int, c_int, c_double, c_void_p, c_int,
                                     c_int64, c_void_p, c_void_p]),
+    "sgs_partials_reduce_div": (c_int, [c_void_p, c_int, c_int, c_int, c_double, c_void_p,
+                                        c_void_p, c_int, c_int64, c_void_p, c_void_p]),
     "sgs_fwht": (c_int, [c_void_p, c_int64, c_int, c_int64, c_void_p]),
     "sgs_rgs_update": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_void_p, c_int,
                                c_void_p, c_int, c_void_p, c_int64, c_void_p, c_void_p]),

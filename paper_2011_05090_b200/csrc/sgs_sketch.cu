@@ -305,15 +305,16 @@ dense_gemm_kernel(const double* __restrict__ thetaT, int64_t ldt, int k,
 // ---------------------------------------------------------------------------
 template <typename TY>
 __global__ void partials_reduce_kernel(const double* __restrict__ partials, int nparts, int k,
-                                       int ncols, double scale, TY* __restrict__ Y, int64_t ldy,
-                                       const sgs_status* st) {
+                                       int ncols, double scale, const double* __restrict__ den,
+                                       TY* __restrict__ Y, int64_t ldy, const sgs_status* st) {
   pdl_enter();
   if (status_stopped(st)) return;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)k * ncols) return;
   const int c = (int)(idx / k), j = (int)(idx % k);
   const double acc = canon_sum(partials + (int64_t)c * nparts * k + j, k, nparts);
-  Y[(int64_t)c * ldy + j] = from_double<TY>(scale * acc);
+  const double y = scale * acc;
+  Y[(int64_t)c * ldy + j] = from_double<TY>(den ? y / *den : y);
 }
 
 // ---------------------------------------------------------------------------
@@ -591,9 +592,27 @@ extern "C" int sgs_dense_partials(const double* thetaT, int64_t ldt, int k, cons
   return launch_dense<double>(thetaT, ldt, k, X, ldx, ncols, n, partials, st, s);
 }
 
+static int partials_reduce_impl(const double* partials, int nparts, int k, int ncols,
+                                double scale, const double* den, void* Y, int y_dtype,
+                                int64_t ldy, const sgs_status* st, void* stream);
+
 extern "C" int sgs_partials_reduce(const double* partials, int nparts, int k, int ncols,
                                    double scale, void* Y, int y_dtype, int64_t ldy,
                                    const sgs_status* st, void* stream) {
+  return partials_reduce_impl(partials, nparts, k, ncols, scale, nullptr, Y, y_dtype, ldy, st,
+                              stream);
+}
+
+extern "C" int sgs_partials_reduce_div(const double* partials, int nparts, int k, int ncols,
+                                       double scale, const double* den, void* Y, int y_dtype,
+                                       int64_t ldy, const sgs_status* st, void* stream) {
+  return partials_reduce_impl(partials, nparts, k, ncols, scale, den, Y, y_dtype, ldy, st,
+                              stream);
+}
+
+static int partials_reduce_impl(const double* partials, int nparts, int k, int ncols,
+                                double scale, const double* den, void* Y, int y_dtype,
+                                int64_t ldy, const sgs_status* st, void* stream) {
   SGS_REQUIRE(partials && Y && nparts >= 1 && k >= 1 && ncols >= 1, "reduce: bad args");
   SGS_REQUIRE(ldy >= k, "reduce: ldy < k");
   cudaStream_t s = as_stream(stream);
@@ -602,12 +621,12 @@ extern "C" int sgs_partials_reduce(const double* partials, int nparts, int k, in
   const unsigned blocks = (unsigned)((tot + threads - 1) / threads);
   if (y_dtype == SGS_F64)
     return check_ex(launch_ex(partials_reduce_kernel<double>, dim3(blocks), dim3(threads), 0, s,
-                              1, partials, nparts, k, ncols, scale, static_cast<double*>(Y), ldy,
-                              st), "partials_reduce_kernel");
+                              1, partials, nparts, k, ncols, scale, den, static_cast<double*>(Y),
+                              ldy, st), "partials_reduce_kernel");
   if (y_dtype == SGS_F32)
     return check_ex(launch_ex(partials_reduce_kernel<float>, dim3(blocks), dim3(threads), 0, s,
-                              1, partials, nparts, k, ncols, scale, static_cast<float*>(Y), ldy,
-                              st), "partials_reduce_kernel");
+                              1, partials, nparts, k, ncols, scale, den, static_cast<float*>(Y),
+                              ldy, st), "partials_reduce_kernel");
   set_error("reduce: bad dtype");
   return SGS_EINVAL;
 }

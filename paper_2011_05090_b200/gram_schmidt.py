@@ -103,13 +103,13 @@ class LazyFactors:
     def __init__(self, state: "RgsState", m: int, device: bool = False):
         self._state, self._m, self._device = state, m, device
         self._cache = {}
-        self.S_phi = self.P_phi = None
 
     def _get(self, name):
         if name not in self._cache:
             st, m = self._state, self._m
             t = {"Q": lambda: st._Q[:m, :st.n_local].t(), "R": lambda: st._R[:m, :m].t(),
-                 "S": lambda: st._S[:m].t(), "P": lambda: st._P[:m].t()}[name]()
+                 "S": lambda: st._S[:m].t(), "P": lambda: st._P[:m].t(),
+                 "S_phi": lambda: st._S_phi[:m].t(), "P_phi": lambda: st._P_phi[:m].t()}[name]()
             self._cache[name] = t.clone() if self._device else t.cpu().numpy()
         return self._cache[name]
 
@@ -117,6 +117,8 @@ class LazyFactors:
     R = property(lambda self: self._get("R"))
     S = property(lambda self: self._get("S"))
     P = property(lambda self: self._get("P"))
+    S_phi = property(lambda self: self._get("S_phi") if self._state.phi is not None else None)
+    P_phi = property(lambda self: self._get("P_phi") if self._state.phi is not None else None)
 
 
 @dataclass
@@ -170,13 +172,12 @@ class RgsState:
         if solver.method != "householder":
             raise NotImplementedError("the device factorizer implements the direct "
                                       "QR least-squares solver only (HOUSEHOLDER_QR)")
-        if phi is not None:
-            raise NotImplementedError("certification sketches (phi) are not on the "
-                                      "device hot path")
         self.theta = as_device_sketch(theta)
+        self.phi = as_device_sketch(phi) if phi is not None else None
+        if self.phi is not None and self.phi.n != self.theta.n:
+            raise ValueError("certification sketch has mismatched ambient dimension")
         self.policy = policy
         self.solver = solver
-        self.phi = None
         self.breakdown_factor = float(breakdown_factor)
         self.comm = comm
         self.n = self.theta.n
@@ -209,6 +210,13 @@ class RgsState:
             self._kvec_s = torch.empty(self.k, dtype=torch.float64, device=self.device)
             self._kvec_p = torch.empty_like(self._kvec_s)
         self._theta_dev = self.theta.device_data(self.device)
+        if self.phi is not None:  # certification sketches (gram_schmidt.py:304-305, 333-335)
+            self.phi.device_data(self.device)
+            self.nparts_phi = self.phi.nparts(self.n_local)
+            self._parts_phi = torch.empty((self.nparts_phi, self.phi.k), dtype=torch.float64,
+                                          device=self.device)
+            if comm is not None:
+                self._kvec_phi = torch.empty(self.phi.k, dtype=torch.float64, device=self.device)
 
     # ---- storage ----------------------------------------------------------------
     def _alloc(self, cap: int) -> None:
@@ -224,6 +232,14 @@ class RgsState:
         self._Qs = torch.zeros((cap, k), dtype=self.fdt, device=dev)
         self._Rinv = torch.zeros((cap, cap), dtype=self.fdt, device=dev)
         self._alpha = torch.zeros(cap, dtype=self.fdt, device=dev)
+        if self.phi is not None:
+            kp = self.phi.k
+            old_phi = (self._S_phi, self._P_phi) if self._cap else None
+            self._S_phi = torch.zeros((cap, kp), dtype=self.fdt, device=dev)
+            self._P_phi = torch.zeros((cap, kp), dtype=self.fdt, device=dev)
+            if old_phi is not None:
+                self._S_phi[:self._cap] = old_phi[0]
+                self._P_phi[:self._cap] = old_phi[1]
         self._scratch = torch.zeros(int(_lib.load().sgs_ls_scratch_elems(k, cap)),
                                     dtype=torch.float64, device=dev)
         self._rc = torch.zeros(cap, dtype=self.cdt, device=dev)
@@ -322,6 +338,44 @@ class RgsState:
             return None
         return self._sketch_parts(self._qcol_ptr(i), self.ccode, self.ldq, self._parts_s, kvec)
 
+    # ---- certification sketches ------------------------------------------------------
+    def _phi_parts(self, x_ptr: int, x_code: int, ldx: int, ncols: int = 1):
+        """Partials of Phi x over the local rows (summed across ranks when sharded)."""
+        ph = self.phi
+        self.phi.partials_into(x_ptr, x_code, ldx, ncols, self._parts_phi, n_local=self.n_local,
+                               row0=self.row0, status=self.status)
+        if self.comm is None:
+            return self._parts_phi.data_ptr(), self.nparts_phi
+        call("sgs_partials_reduce", self._parts_phi.data_ptr(), self.nparts_phi, ph.k, 1, 1.0,
+             self._kvec_phi.data_ptr(), _lib.SGS_F64, ph.k, self.status.ptr, stream_ptr())
+        self.comm.allreduce_(self._kvec_phi)
+        return self._kvec_phi.data_ptr(), 1
+
+    def _phi_w(self, i: int, w_ptr: int, w_code: int, ldw: int) -> None:
+        """P_phi[:, i] = Phi w_i (gram_schmidt.py:304-305)."""
+        if self.phi is None:
+            return
+        pp, pn = self._phi_parts(w_ptr, w_code, ldw)
+        call("sgs_partials_reduce", pp, pn, self.phi.k, 1, self.phi.scale,
+             self._P_phi.data_ptr() + i * self.phi.k * self._P_phi.element_size(), self.fcode,
+             self.phi.k, self.status.ptr, stream_ptr())
+
+    def _phi_q_parts(self, i: int):
+        """Partials of Phi q'_i while Q[:, i] still holds the unnormalised q'."""
+        if self.phi is None:
+            return None
+        return self._phi_parts(self._qcol_ptr(i), self.ccode, self.ldq)
+
+    def _phi_q_finish(self, i: int, parts) -> None:
+        """S_phi[:, i] = (Phi q'_i) / r_ii (gram_schmidt.py:333-335)."""
+        if self.phi is None:
+            return
+        pp, pn = parts
+        call("sgs_partials_reduce_div", pp, pn, self.phi.k, 1, self.phi.scale,
+             self._R.data_ptr() + (i * self._cap + i) * 8,
+             self._S_phi.data_ptr() + i * self.phi.k * self._S_phi.element_size(), self.fcode,
+             self.phi.k, self.status.ptr, stream_ptr())
+
     def _normalize(self, col: int, guarded: bool = True) -> None:
         call("sgs_normalize_column", self._Q.data_ptr(), self.ccode, self.ldq, self.n_local,
              col, self._R.data_ptr(), self._cap, self.status.ptr if guarded else None,
@@ -357,15 +411,19 @@ class RgsState:
         wc = _lib.dtype_code(w.dtype)
         pp, pn, ps = self._sketch_parts(w.data_ptr(), wc, self.n_local, self._parts_p,
                                         getattr(self, "_kvec_p", None))
+        self._phi_w(i, w.data_ptr(), wc, self.n_local)
         if i == 0:
             call("sgs_partials_reduce", pp, pn, self.k, 1, ps, self._P.data_ptr(), self.fcode,
                  self.k, self.status.ptr, stream_ptr())
             self._column(0, w.data_ptr(), wc, False, False)
+            phq = self._phi_q_parts(0)
             self._ls(fin=0)
         else:
             self._ls(sol=i, p_parts=pp, p_nparts=pn, p_scale=ps)
             sp, sn, ss = self._column(i, w.data_ptr(), wc, False, True)
+            phq = self._phi_q_parts(i)
             self._ls(fin=i, s_parts=sp, s_nparts=sn, s_scale=ss)
+        self._phi_q_finish(i, phq)
         self._normalize(i)
         self.m += 1  # provisional; reconciled with the device count at sync
 
@@ -390,8 +448,11 @@ class RgsState:
     # ---- views -------------------------------------------------------------------
     def device_factors(self) -> QrFactors:
         m = self.m
-        return QrFactors(Q=self._Q[:m, :self.n_local].t(), R=self._R[:m, :m].t(),
-                         S=self._S[:m].t(), P=self._P[:m].t())
+        f = QrFactors(Q=self._Q[:m, :self.n_local].t(), R=self._R[:m, :m].t(),
+                      S=self._S[:m].t(), P=self._P[:m].t())
+        if self.phi is not None:
+            f.S_phi, f.P_phi = self._S_phi[:m].t(), self._P_phi[:m].t()
+        return f
 
     @property
     def Q(self):
@@ -412,8 +473,15 @@ class RgsState:
     def factors(self, device: bool = False) -> QrFactors:
         if device:
             f = self.device_factors()
-            return QrFactors(Q=f.Q.clone(), R=f.R.clone(), S=f.S.clone(), P=f.P.clone())
-        return QrFactors(Q=self.Q, R=self.R, S=self.S, P=self.P)
+            out = QrFactors(Q=f.Q.clone(), R=f.R.clone(), S=f.S.clone(), P=f.P.clone())
+            if self.phi is not None:
+                out.S_phi, out.P_phi = f.S_phi.clone(), f.P_phi.clone()
+            return out
+        out = QrFactors(Q=self.Q, R=self.R, S=self.S, P=self.P)
+        if self.phi is not None:
+            out.S_phi = self._S_phi[:self.m].t().cpu().numpy()
+            out.P_phi = self._P_phi[:self.m].t().cpu().numpy()
+        return out
 
     # ---- batch path ----------------------------------------------------------------
     def _reserve(self, ncols: int) -> None:
@@ -450,14 +518,20 @@ class RgsState:
                 self.comm.allreduce_(kbuf[:nc])
                 call("sgs_partials_reduce", kbuf.data_ptr(), 1, k, nc, self.theta.scale,
                      pdst, self.fcode, k, self.status.ptr, sp)
+        if self.phi is not None:  # P_phi = Phi W, column by column
+            for j in range(m):
+                self._phi_w(j, base + j * ldw * esz, wc, ldw)
         for i in range(m):
             sol = i + 1 if i + 1 < m else None
             if i == 0:
                 self._column(0, base, wc, False, False)
+                phq = self._phi_q_parts(0)
                 self._ls(fin=0, sol=sol)
             else:
                 spp, snp, ssc = self._column(i, base + i * ldw * esz, wc, True, True)
+                phq = self._phi_q_parts(i)
                 self._ls(fin=i, s_parts=spp, s_nparts=snp, s_scale=ssc, sol=sol)
+            self._phi_q_finish(i, phq)
         self._normalize(m - 1)
         self._keep = parts  # keep the chunk buffer alive for graph replays
 
@@ -656,7 +730,7 @@ def rgs_factorize(W, theta, policy: PrecisionPolicy = MIXED32_64,
         state = RgsState(theta, policy, solver, phi=phi, capacity=m + 1,
                          breakdown_factor=breakdown_factor, comm=comm, row0=row0,
                          n_local=n_loc)
-        if (isinstance(W, np.ndarray) and not device_factors and comm is None
+        if (isinstance(W, np.ndarray) and not device_factors and comm is None and phi is None
                 and W.dtype in (np.float32, np.float64) and W.flags.f_contiguous
                 and _is_pinned(W)):
             factors = state.factorize_host_pipelined(W, m)

@@ -136,14 +136,12 @@ class GmresResult:
     factors: QrFactors | None = None
 
 
-def _check_variant(variant, preconditioner=None, phi=None):
+def _check_variant(variant, preconditioner=None):
     if variant is not GsVariant.RGS and getattr(variant, "value", None) != "rgs":
         raise NotImplementedError("the device Krylov path implements the randomized "
                                   "Gram-Schmidt variant (GsVariant.RGS)")
     if preconditioner is not None:
         raise NotImplementedError("preconditioned GMRES is outside the device hot path")
-    if phi is not None:
-        raise NotImplementedError("certification sketches (phi) are not on the device path")
 
 
 def _to_device_f64(b, n: int, device) -> torch.Tensor:
@@ -195,10 +193,10 @@ class _ArnoldiEngine:
     Otherwise the generic path (separate SpMV, sketch and normalisation)."""
 
     def __init__(self, A: SparseMatrix, theta, policy, solver, m: int,
-                 breakdown_factor: float = BREAKDOWN_FACTOR):
+                 breakdown_factor: float = BREAKDOWN_FACTOR, phi=None):
         self.A = A
         self.m = m
-        self.state = RgsState(theta, policy, solver, capacity=m + 2,
+        self.state = RgsState(theta, policy, solver, phi=phi, capacity=m + 2,
                               breakdown_factor=breakdown_factor)
         st = self.state
         if st.n != A.n:
@@ -224,8 +222,11 @@ class _ArnoldiEngine:
         pp, pn, ps = st._sketch_parts(bn.data_ptr(), _lib.SGS_F64, n, st._parts_p, None)
         call("sgs_partials_reduce", pp, pn, st.k, 1, ps, st._P.data_ptr(), st.fcode, st.k,
              st.status.ptr, stream_ptr())
+        st._phi_w(0, bn.data_ptr(), _lib.SGS_F64, n)
         st._column(0, bn.data_ptr(), _lib.SGS_F64, False, False)
+        phq = st._phi_q_parts(0)
         st._ls(fin=0)
+        st._phi_q_finish(0, phq)
         st.m = 1
 
     def step(self, i: int, alpha: torch.Tensor | None, tol: float | None) -> None:
@@ -236,9 +237,12 @@ class _ArnoldiEngine:
             A.spmv_into(st._qcol_ptr(i), st.ccode, ws.w, alpha=alpha, status=st.status,
                         xdiv_ptr=rii)
             pp, pn, ps = st._sketch_parts(ws.w.data_ptr(), _lib.SGS_F64, A.n, st._parts_p, None)
+            st._phi_w(i + 1, ws.w.data_ptr(), _lib.SGS_F64, A.n)
             st._ls(sol=i + 1, p_parts=pp, p_nparts=pn, p_scale=ps)
             sp, sn, ss = st._column(i + 1, ws.w.data_ptr(), _lib.SGS_F64, True, True)
+            phq = st._phi_q_parts(i + 1)
             st._ls(fin=i + 1, s_parts=sp, s_nparts=sn, s_scale=ss)
+            st._phi_q_finish(i + 1, phq)
             st.m = i + 2
         else:
             A.spmv_into(st._qcol_ptr(i), st.ccode, ws.w, alpha=alpha, status=st.status)
@@ -279,10 +283,10 @@ def arnoldi(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, thet
             policy: PrecisionPolicy = MIXED32_64, solver: LsqSolver = HOUSEHOLDER_QR,
             phi=None) -> ArnoldiDecomposition:
     """m-step RGS-Arnoldi (krylov.py:176-199); fewer columns on a lucky breakdown."""
-    _check_variant(variant, phi=phi)
+    _check_variant(variant)
     if theta is None:
         raise ValueError("the randomized variant needs a sketch operator")
-    eng = _ArnoldiEngine(A, theta, policy, solver, m)
+    eng = _ArnoldiEngine(A, theta, policy, solver, m, phi=phi)
     st = eng.state
     b_dev = _to_device_f64(b, A.n, st.device)
     eng.start(b_dev, None)
@@ -301,7 +305,7 @@ def gmres(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, theta=
           policy: PrecisionPolicy = MIXED32_64, solver: LsqSolver = HOUSEHOLDER_QR,
           preconditioner=None, tol: float | None = None, phi=None) -> GmresResult:
     """Single-cycle RGS-GMRES(m) with progressive Givens rotations (krylov.py:229-319)."""
-    _check_variant(variant, preconditioner, phi)
+    _check_variant(variant, preconditioner)
     if theta is None:
         raise ValueError("the randomized variant needs a sketch operator")
     _lib.require_cuda()
@@ -316,7 +320,7 @@ def gmres(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, theta=
                                                              device=device)
         return GmresResult(x=x0, residual_history=np.zeros(0), final_residual=0.0,
                            iterations=0, converged=True, breakdown=False)
-    eng = _ArnoldiEngine(A, theta, policy, solver, m)
+    eng = _ArnoldiEngine(A, theta, policy, solver, m, phi=phi)
     st = eng.state
     alpha = _operator_norm_estimate(A, eng.ws)
     if float(alpha) <= 0.0:

@@ -230,3 +230,26 @@ def test_rgs_larger_k_and_policies_vs_oracle(cuda, kind, k, n, pol, blog):
     for j in range(8):
         st.push(W[:, j])
     assert np.array_equal(st.R, f.R[:8, :8])
+
+
+@pytest.mark.parametrize("phikind,n", [("rademacher", 3000), ("psrht", 20000)])
+def test_certification_sketches_phi(cuda, phikind, n):
+    # S_phi = Phi q'_i / r_ii and P_phi = Phi w_i (gram_schmidt.py:304-305, 333-335)
+    m, k, kphi = 20, 120, 60
+    W = make_w(n, m, 1e-4, 8)
+    th = sg.make_sketch(sg.SketchKind.PSRHT, k, n, 8)
+    phi = sg.make_sketch(sg.SketchKind(phikind), kphi, n, 99)
+    f, _ = sg.rgs_factorize(W, th, sg.UNIFIED64, phi=phi)
+    ref = oracle_rgs_factorize(W, OracleSketch("psrht", k, n, 8), "f64",
+                               phi=OracleSketch(phikind, kphi, n, 99))
+    assert f.S_phi.shape == (kphi, m) and f.P_phi.shape == (kphi, m)
+    assert rel_diff(f.P_phi, ref["P_phi"]) <= 1e-13
+    assert rel_diff(f.S_phi, ref["S_phi"]) <= 1e-10
+    # streaming carries them too
+    st = sg.RgsState(th, sg.UNIFIED64, phi=phi)
+    for j in range(m):
+        st.push(W[:, j])
+    g = st.factors()
+    assert np.array_equal(g.S_phi, f.S_phi) and np.array_equal(g.P_phi, f.P_phi)
+    with pytest.raises(ValueError):
+        sg.RgsState(th, sg.UNIFIED64, phi=sg.make_sketch(sg.SketchKind.PSRHT, 10, n + 1, 0))
