@@ -194,6 +194,7 @@ typedef struct sgs_ls_args {
   long long* trace;      /* optional (NULL): clock64() at phase boundaries, CTA 0 */
   int cache_cols;        /* set by the library: columns of T cached in shared memory */
   unsigned long long* timeline;  /* set by the library (debug timeline) */
+  void* xbar;            /* set by the library: cross-cluster barrier words in scratch */
 } sgs_ls_args;
 
 int64_t sgs_ls_scratch_elems(int k, int cap);
