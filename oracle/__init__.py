@@ -21,6 +21,6 @@ order, so with single-threaded BLAS it reproduces the reference bit for bit
 
 from .ref_sketch import OracleSketch, fwht_ref, psrht_setup
 from .ref_rgs import OracleRgs, householder_lsq, oracle_certificates, oracle_rgs_factorize
-from .ref_krylov import (csr_matvec, oracle_arnoldi, oracle_gmres, oracle_gmres_restarted,
+from .ref_krylov import (OracleIlu0, csr_matvec, oracle_arnoldi, oracle_gmres, oracle_gmres_restarted,
                          power_norm_estimate)
 from .metrics import factor_metrics, rel_diff

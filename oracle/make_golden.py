@@ -28,9 +28,53 @@ def _problem(rng, n, m, cond):
     return (U * sv) @ V.T
 
 
-def main():
+def ilu_fixtures(sg):
+    """ILU(0) factors, M^{-1} v and a preconditioned GMRES (krylov.py:86-151, :229-319)."""
+    d = {}
+    mats = {"lap6": sg.generate_laplacian_2d(6), "rs60": sg.generate_random_sparse(60, 4, seed=3),
+            "rs300": sg.generate_random_sparse(300, 8, seed=2, diag_shift=0.1),
+            "lap40": sg.generate_laplacian_2d(40)}
+    for name, A in mats.items():
+        pre = sg.ilu0(A)
+        v = np.random.default_rng(A.n).standard_normal(A.n)
+        full = (pre.L - sg.krylov.scipy.sparse.eye(A.n, format="csr") + pre.U).tocsr()
+        full.sort_indices()
+        d.update({f"{name}_rp": A.row_ptr, f"{name}_ci": A.col_idx, f"{name}_v": A.values,
+                  f"{name}_Lrp": pre.L.indptr, f"{name}_Lci": pre.L.indices,
+                  f"{name}_Lv": pre.L.data, f"{name}_Urp": pre.U.indptr,
+                  f"{name}_Uci": pre.U.indices, f"{name}_Uv": pre.U.data,
+                  f"{name}_sv": v, f"{name}_solve": pre.solve(v)})
+    A = mats["lap40"]
+    b = np.random.default_rng(0).standard_normal(A.n)
+    th = sg.make_sketch(sg.SketchKind.PSRHT, 200, A.n, seed=0)
+    res = sg.gmres(A, b, m=60, theta=th, policy=sg.UNIFIED64, preconditioner=sg.ilu0(A),
+                   tol=1e-12)
+    d.update({"pg_b": b, "pg_x": res.x, "pg_its": res.iterations, "pg_res": res.final_residual,
+              "pg_hist": res.residual_history})
+    B = mats["rs300"]
+    bb = np.random.default_rng(1).standard_normal(300)
+    th2 = sg.make_sketch(sg.SketchKind.PSRHT, 200, 300, seed=0)
+    r2 = sg.gmres(B, bb, m=40, theta=th2, policy=sg.MIXED32_64, preconditioner=sg.ilu0(B))
+    d.update({"pr_b": bb, "pr_x": r2.x, "pr_its": r2.iterations, "pr_res": r2.final_residual,
+              "pr_hist": r2.residual_history})
+    # ZeroDivisionError / ValueError messages
+    Z = sg.SparseMatrix.from_coo(3, [0, 0, 1, 1, 2], [0, 1, 0, 1, 2], [1.0, 1.0, 1.0, 1.0, 1.0])
+    try:
+        sg.ilu0(Z)
+        d["zero_pivot_msg"] = np.array("")
+    except ZeroDivisionError as e:
+        d["zero_pivot_msg"] = np.array(str(e))
+    np.savez_compressed(os.path.join(OUT, "ilu.npz"), **d)
+
+
+def main(only=None):
     sys.path.insert(0, REF)
     import sketchgs as sg
+    if only == "ilu":
+        os.makedirs(OUT, exist_ok=True)
+        ilu_fixtures(sg)
+        print("ilu fixtures written to", os.path.abspath(OUT))
+        return
     sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
     from paper_2011_05090_b200.workloads import make_w, convdiff3d, rhs_gaussian
     os.makedirs(OUT, exist_ok=True)
@@ -139,8 +183,9 @@ def main():
     d.update({"cd_b": b3, "cd_x": r3.x, "cd_its": r3.iterations, "cd_res": r3.final_residual,
               "cd_hist": r3.residual_history})
     np.savez_compressed(os.path.join(OUT, "krylov.npz"), **d)
+    ilu_fixtures(sg)
     print("golden fixtures written to", os.path.abspath(OUT))
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1] if len(sys.argv) > 1 else None)

@@ -2,7 +2,7 @@
 
 Restates reference krylov.py: SparseMatrix.matvec (:81-83, scipy CSR),
 _operator_norm_estimate (:213-226), arnoldi (:176-199), gmres (:229-319,
-unpreconditioned), and the restart wrapper BASELINE config 3 needs
+with the ILU(0) right preconditioner of :86-151), and the restart wrapper BASELINE config 3 needs
 (identical definition to paper_2011_05090_b200.gmres_restarted).
 """
 
@@ -18,6 +18,60 @@ from .ref_rgs import OracleBreakdown, OracleRgs
 def csr_matvec(row_ptr, col_idx, values, n, x):
     A = scipy.sparse.csr_matrix((values, col_idx, row_ptr), shape=(n, n))
     return A @ np.asarray(x, dtype=np.float64)
+
+
+class OracleIlu0:
+    """ILU(0) factors (krylov.py:86-151): F holds L (strict lower, unit
+    diagonal implied) and U (upper incl. diagonal) on A's pattern."""
+
+    def __init__(self, row_ptr, col_idx, values, n, pivot_tol=1e-30):
+        self.n = n
+        indptr = np.asarray(row_ptr, dtype=np.int64)
+        indices = np.asarray(col_idx, dtype=np.int64)
+        data = np.asarray(values, dtype=np.float64).copy()
+        # krylov.py:114-124: {col: pos} per row (last one wins), structural check
+        diag = np.full(n, -1, dtype=np.int64)
+        maps = []
+        for i in range(n):
+            cm = {}
+            for p in range(indptr[i], indptr[i + 1]):
+                cm[int(indices[p])] = p
+            maps.append(cm)
+            diag[i] = cm.get(i, -1)
+        if np.any(diag < 0):
+            raise ValueError(f"structural zero diagonal at row {int(np.argmin(diag))}")
+        # krylov.py:125-145: row-oriented IKJ elimination in storage order
+        for i in range(1, n):
+            lo, hi = int(indptr[i]), int(indptr[i + 1])
+            for p in range(lo, hi):
+                k = int(indices[p])
+                if k >= i:
+                    break
+                pivot = data[diag[k]]
+                if abs(pivot) < pivot_tol:
+                    raise ZeroDivisionError(f"ILU(0) pivot too small at row {k}")
+                lik = data[p] / pivot
+                data[p] = lik
+                cmk = maps[k]
+                for q in range(p + 1, hi):
+                    pos = cmk.get(int(indices[q]))
+                    if pos is not None:
+                        data[q] -= lik * data[pos]
+            if abs(data[diag[i]]) < pivot_tol:
+                raise ZeroDivisionError(f"ILU(0) pivot too small at row {i}")
+        self.F = data
+        full = scipy.sparse.csr_matrix((data, indices.copy(), indptr.copy()), shape=(n, n))
+        # krylov.py:146-151
+        self.L = (scipy.sparse.tril(full, k=-1, format="csr")
+                  + scipy.sparse.eye(n, format="csr")).tocsr()
+        self.U = scipy.sparse.triu(full, k=0, format="csr")
+
+    def solve(self, v):
+        """M^{-1} v = U^{-1} L^{-1} v with scipy's triangular solves (krylov.py:95-99)."""
+        import scipy.sparse.linalg as spla
+        v = np.asarray(v, dtype=np.float64)
+        y = spla.spsolve_triangular(self.L, v, lower=True, unit_diagonal=True)
+        return spla.spsolve_triangular(self.U, y, lower=False)
 
 
 def power_norm_estimate(matvec, n: int, iters: int = 20) -> float:
@@ -50,8 +104,14 @@ def oracle_arnoldi(matvec, n, b, m, theta, policy="mixed"):
             "breakdown": broke}
 
 
-def oracle_gmres(matvec, n, b, m, theta, policy="mixed", tol=None):
+def oracle_gmres(matvec, n, b, m, theta, policy="mixed", tol=None, precond=None):
+    """krylov.py:229-319; `precond` is an OracleIlu0 (right preconditioning:
+    the Arnoldi operator is A M^{-1}, x = M^{-1} x_tilde, residual on A)."""
     b = np.asarray(b, dtype=np.float64)
+    a_matvec = matvec
+    if precond is not None:
+        def matvec(v):  # noqa: F811 - effective operator A M^{-1}
+            return a_matvec(precond.solve(v))
     b_norm = float(np.linalg.norm(b))
     if b_norm == 0.0:
         return {"x": np.zeros(n), "history": np.zeros(0), "final_residual": 0.0,
@@ -99,7 +159,9 @@ def oracle_gmres(matvec, n, b, m, theta, policy="mixed", tol=None):
     else:
         y = scipy.linalg.solve_triangular(T[:k, :k], g[:k], lower=False)
         x = (b_norm / alpha) * (st.Q[:, :k].astype(np.float64) @ y)
-    res = float(np.linalg.norm(b - matvec(x)) / b_norm)
+        if precond is not None:
+            x = precond.solve(x)
+    res = float(np.linalg.norm(b - a_matvec(x)) / b_norm)
     conv = (res <= max(tol, 0.0)) if tol is not None else False
     return {"x": x, "history": np.asarray(hist), "final_residual": res, "iterations": k,
             "converged": conv or broke, "breakdown": broke, "R": st.R.copy(),

@@ -14,8 +14,8 @@ from .sketch import SketchKind, SketchOperator, as_device_sketch, block_seed, fw
 from .gram_schmidt import (BREAKDOWN_FACTOR, HOUSEHOLDER_QR, BreakdownError, GsVariant,
                            LsqSolver, QrFactors, RgsState, StabilityCertificate, certificates,
                            loss_of_orthogonality, rgs_factorize)
-from .krylov import (ArnoldiDecomposition, GmresResult, RestartedResult, SparseMatrix, arnoldi,
-                     gmres, gmres_restarted)
+from .krylov import (ArnoldiDecomposition, GmresResult, Ilu0Preconditioner, RestartedResult,
+                     SparseMatrix, arnoldi, gmres, gmres_restarted, ilu0)
 
 __version__ = "0.1.0"
 
@@ -25,5 +25,6 @@ __all__ = [
     "make_sketch", "BREAKDOWN_FACTOR", "HOUSEHOLDER_QR", "BreakdownError", "GsVariant",
     "LsqSolver", "QrFactors", "RgsState", "StabilityCertificate", "certificates",
     "loss_of_orthogonality", "rgs_factorize", "ArnoldiDecomposition", "GmresResult",
-    "RestartedResult", "SparseMatrix", "arnoldi", "gmres", "gmres_restarted",
+    "RestartedResult", "SparseMatrix", "Ilu0Preconditioner", "ilu0", "arnoldi", "gmres",
+    "gmres_restarted",
 ]

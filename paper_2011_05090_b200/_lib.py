@@ -96,6 +96,11 @@ _SIGS = {
                                 c_void_p, c_int64, c_void_p, c_double, c_void_p, c_void_p]),
     "sgs_transpose": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int,
                               c_void_p]),
+    "sgs_ilu0_factor": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                c_void_p, c_void_p, c_void_p, c_double, c_void_p]),
+    "sgs_ilu0_solve": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
+                               c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                               c_void_p]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -265,9 +265,9 @@ __global__ void __launch_bounds__(kLgThreads, 1) ls_grid_kernel(sgs_ls_args a) {
     __syncthreads();
     const double r_ii = (double)sqrt(fe[0]);
     const double tol = a.bf_ucrs * (double)sqrt(fe[1]);
-    if (r_ii <= tol || !(r_ii == r_ii)) {
+    if (r_ii <= tol) {  // NaN compares false and propagates, as in numpy
       if (g == 0 && threadIdx.x == 0) {
-        a.st->code = (r_ii <= tol) ? SGS_ST_BREAKDOWN : SGS_ST_NONFINITE;
+        a.st->code = SGS_ST_BREAKDOWN;
         a.st->column = i + 1;
         a.st->r_ii = r_ii;
         a.st->tol = tol;

@@ -635,9 +635,9 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     __syncthreads();
     const double r_ii = (double)sqrt(bc[0]);
     const double tol = a.bf_ucrs * (double)sqrt(bc[1]);
-    if (r_ii <= tol || !(r_ii == r_ii)) {
+    if (r_ii <= tol) {  // NaN compares false and propagates, as in numpy (gram_schmidt.py:325)
       if (rank == 0 && threadIdx.x == 0) {
-        a.st->code = (r_ii <= tol) ? SGS_ST_BREAKDOWN : SGS_ST_NONFINITE;
+        a.st->code = SGS_ST_BREAKDOWN;
         a.st->column = i + 1;
         a.st->r_ii = r_ii;
         a.st->tol = tol;

@@ -26,8 +26,8 @@ from .gram_schmidt import (BREAKDOWN_FACTOR, HOUSEHOLDER_QR, GsVariant, LazyFact
                            QrFactors, RgsState)
 from .precision import MIXED32_64, PrecisionPolicy
 
-__all__ = ["SparseMatrix", "arnoldi", "gmres", "gmres_restarted", "ArnoldiDecomposition",
-           "GmresResult", "RestartedResult"]
+__all__ = ["SparseMatrix", "Ilu0Preconditioner", "ilu0", "arnoldi", "gmres", "gmres_restarted",
+           "ArnoldiDecomposition", "GmresResult", "RestartedResult"]
 
 _POLL = 8  # Arnoldi steps between status polls
 
@@ -116,6 +116,132 @@ class SparseMatrix:
         self.__dict__.setdefault("_dev_cache", {})
 
 
+class Ilu0Preconditioner:
+    """Zero-fill incomplete LU factors on A's pattern (krylov.py:86-100).
+
+    The factors live on the device as one CSR array F (strict lower part = L
+    with an implied unit diagonal, the rest = U); ``solve(v)`` applies
+    M^{-1} v = U^{-1} (L^{-1} v) with the two sync-free sweep kernels of
+    ``sgs_ilu0_solve``.  ``L`` and ``U`` are the reference's scipy CSR
+    matrices, copied from the device on first use.  Built by ``ilu0(A)``, or
+    from host factors ``Ilu0Preconditioner(L, U)`` as the reference's
+    dataclass is.  One preconditioner runs one solve at a time (its flag
+    array and control block are shared by its launches)."""
+
+    def __init__(self, L=None, U=None, *, _device=None):
+        if _device is not None:
+            (self.n, self._rp, self._ci, self._F, self._diag) = _device
+            self._L = self._U = None
+        else:
+            if L is None or U is None:
+                raise TypeError("Ilu0Preconditioner needs L and U")
+            _lib.require_cuda()
+            L = scipy.sparse.csr_matrix(L)
+            U = scipy.sparse.csr_matrix(U)
+            n = L.shape[0]
+            full = (scipy.sparse.tril(L, k=-1, format="csr") + U).tocsr()
+            full.sum_duplicates()
+            full.sort_indices()
+            dev = torch.device("cuda", torch.cuda.current_device())
+            self.n = n
+            self._rp = torch.from_numpy(full.indptr.astype(np.int32)).to(dev)
+            self._ci = torch.from_numpy(full.indices.astype(np.int32)).to(dev)
+            self._F = torch.from_numpy(full.data.astype(np.float64)).to(dev)
+            d = full.diagonal()
+            if np.any(d == 0.0):
+                raise np.linalg.LinAlgError("A is singular: zero entry on diagonal.")
+            pos = np.full(n, -1, dtype=np.int32)
+            rows = np.repeat(np.arange(n), np.diff(full.indptr))
+            on = full.indices == rows
+            pos[rows[on]] = np.nonzero(on)[0]
+            self._diag = torch.from_numpy(pos).to(dev)
+            self._L, self._U = L, U
+        dev = self._F.device
+        self._flags = torch.zeros(max(self.n, 1), dtype=torch.int32, device=dev)
+        self._ctl = torch.zeros(2, dtype=torch.int64, device=dev)
+        self._tmp = torch.empty(max(self.n, 1), dtype=torch.float64, device=dev)
+
+    # ---- host views (reference dataclass fields) ----------------------------------
+    def _host_full(self):
+        return scipy.sparse.csr_matrix((self._F.cpu().numpy(), self._ci.cpu().numpy(),
+                                        self._rp.cpu().numpy()), shape=(self.n, self.n))
+
+    @property
+    def L(self) -> scipy.sparse.csr_matrix:
+        if self._L is None:
+            full = self._host_full()
+            self._L = (scipy.sparse.tril(full, k=-1, format="csr")
+                       + scipy.sparse.eye(self.n, format="csr")).tocsr()
+        return self._L
+
+    @property
+    def U(self) -> scipy.sparse.csr_matrix:
+        if self._U is None:
+            self._U = scipy.sparse.triu(self._host_full(), k=0, format="csr")
+        return self._U
+
+    # ---- device solve ---------------------------------------------------------
+    def solve_into(self, x_ptr: int, x_code: int, out: torch.Tensor, xdiv_ptr=None,
+                   status=None) -> None:
+        """out = M^{-1} x on the current stream (x binary32/64 at x_ptr; with
+        xdiv_ptr the input is cast(x / *xdiv) first, as SparseMatrix.spmv_into)."""
+        call("sgs_ilu0_solve", self.n, self._rp.data_ptr(), self._ci.data_ptr(),
+             self._F.data_ptr(), self._diag.data_ptr(), x_ptr, x_code, xdiv_ptr,
+             self._tmp.data_ptr(), out.data_ptr(), self._flags.data_ptr(), self._ctl.data_ptr(),
+             status.ptr if status is not None else None, stream_ptr())
+
+    def solve(self, v):
+        """M^{-1} v in binary64 (numpy in -> numpy out; CUDA tensor in -> CUDA out)."""
+        on_dev = isinstance(v, torch.Tensor) and v.is_cuda
+        if on_dev:
+            vd = v if v.dtype in (torch.float32, torch.float64) else v.to(torch.float64)
+            vd = vd.contiguous()
+        else:
+            vd = torch.from_numpy(np.ascontiguousarray(np.asarray(v, dtype=np.float64))).to(
+                self._F.device)
+        if tuple(vd.shape) != (self.n,):
+            raise ValueError("vector length mismatch")
+        out = torch.empty(self.n, dtype=torch.float64, device=self._F.device)
+        self.solve_into(vd.data_ptr(), _lib.dtype_code(vd.dtype), out)
+        return out if on_dev else out.cpu().numpy()
+
+
+def ilu0(A: SparseMatrix, pivot_tol: float = 1e-30) -> Ilu0Preconditioner:
+    """ILU(0) on the device (krylov.py:103-151): the reference's row-oriented
+    IKJ elimination, bit-identical (one thread per row, rows released in
+    dependency order).  Raises ValueError on a structural zero diagonal and
+    ZeroDivisionError on a pivot below pivot_tol, naming the same row."""
+    rp, ci, va = A.device_arrays()
+    n = A.n
+    dev = va.device
+    F = torch.empty_like(va)
+    diag = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    flags = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+    ctl = torch.zeros(2, dtype=torch.int64, device=dev)
+    aux = torch.empty(2, dtype=torch.int64, device=dev)
+    call("sgs_ilu0_factor", n, rp.data_ptr(), ci.data_ptr(), va.data_ptr(), F.data_ptr(),
+         diag.data_ptr(), flags.data_ptr(), ctl.data_ptr(), aux.data_ptr(), float(pivot_tol),
+         stream_ptr())
+    if n:
+        a = aux.cpu().numpy().view(np.uint64)
+        if int(a[0]) != n:
+            raise ValueError(f"structural zero diagonal at row {int(a[0])}")
+        if int(a[1]) != 2**64 - 1:
+            key = int(a[1])
+            raise ZeroDivisionError(f"ILU(0) pivot too small at row {key >> 1 if key & 1 else 0}")
+    pre = Ilu0Preconditioner(_device=(n, rp, ci, F, diag))
+    pre._flags, pre._ctl = flags, ctl  # the factor launch advanced this control block
+    return pre
+
+
+def _as_preconditioner(pre):
+    if pre is None or isinstance(pre, Ilu0Preconditioner):
+        return pre
+    if hasattr(pre, "L") and hasattr(pre, "U"):  # the reference's Ilu0Preconditioner
+        return Ilu0Preconditioner(pre.L, pre.U)
+    raise TypeError("preconditioner must be an Ilu0Preconditioner (or carry L and U factors)")
+
+
 @dataclass
 class ArnoldiDecomposition:
     Q: np.ndarray
@@ -136,12 +262,10 @@ class GmresResult:
     factors: QrFactors | None = None
 
 
-def _check_variant(variant, preconditioner=None):
+def _check_variant(variant):
     if variant is not GsVariant.RGS and getattr(variant, "value", None) != "rgs":
         raise NotImplementedError("the device Krylov path implements the randomized "
                                   "Gram-Schmidt variant (GsVariant.RGS)")
-    if preconditioner is not None:
-        raise NotImplementedError("preconditioned GMRES is outside the device hot path")
 
 
 def _to_device_f64(b, n: int, device) -> torch.Tensor:
@@ -158,6 +282,7 @@ class _Workspace:
     def __init__(self, n: int, device):
         self.w = torch.empty(n, dtype=torch.float64, device=device)
         self.v = torch.empty(n, dtype=torch.float64, device=device)
+        self.z = None  # M^{-1} x when preconditioned
         self.nrm = torch.zeros(4, dtype=torch.float64, device=device)
         self.work = torch.empty(int(_lib.load().sgs_norm2_work_elems(n)), dtype=torch.float64,
                                 device=device)
@@ -167,16 +292,30 @@ class _Workspace:
              self.nrm[out_slot:].data_ptr(), self.work.data_ptr(), stream_ptr())
 
 
-def _operator_norm_estimate(A: SparseMatrix, ws: _Workspace, iters: int = 20) -> torch.Tensor:
-    """Device power iteration (krylov.py:213-226); returns a 1-element device
-    tensor (-1 when the reference would return 0.0)."""
+def _eff_matvec_into(A: SparseMatrix, M, ws: _Workspace, x_ptr: int, x_code: int,
+                     out: torch.Tensor, alpha=None, status=None, xdiv_ptr=None) -> None:
+    """out = A M^{-1} x (/ alpha): the right-preconditioned operator of
+    krylov.py:251-255 (M = None: plain A)."""
+    if M is None:
+        A.spmv_into(x_ptr, x_code, out, alpha=alpha, status=status, xdiv_ptr=xdiv_ptr)
+        return
+    if ws.z is None:
+        ws.z = torch.empty(A.n, dtype=torch.float64, device=out.device)
+    M.solve_into(x_ptr, x_code, ws.z, xdiv_ptr=xdiv_ptr, status=status)
+    A.spmv_into(ws.z.data_ptr(), _lib.SGS_F64, out, alpha=alpha, status=status)
+
+
+def _operator_norm_estimate(A: SparseMatrix, ws: _Workspace, iters: int = 20,
+                            M=None) -> torch.Tensor:
+    """Device power iteration (krylov.py:213-226) on A M^{-1}; returns a
+    1-element device tensor (-1 when the reference would return 0.0)."""
     n = A.n
     sigma = torch.ones(1, dtype=torch.float64, device=ws.v.device)
     call("sgs_cos_init", ws.v.data_ptr(), n, stream_ptr())
     ws.norm(ws.v, 0)
     call("sgs_scale", ws.v.data_ptr(), 1.0, ws.nrm.data_ptr(), 1, ws.v.data_ptr(), n, stream_ptr())
     for _ in range(iters):
-        A.spmv_into(ws.v.data_ptr(), _lib.SGS_F64, ws.w)
+        _eff_matvec_into(A, M, ws, ws.v.data_ptr(), _lib.SGS_F64, ws.w)
         ws.norm(ws.w, 1)
         call("sgs_power_step", ws.w.data_ptr(), ws.nrm[1:].data_ptr(), ws.v.data_ptr(),
              sigma.data_ptr(), n, stream_ptr())
@@ -193,8 +332,9 @@ class _ArnoldiEngine:
     Otherwise the generic path (separate SpMV, sketch and normalisation)."""
 
     def __init__(self, A: SparseMatrix, theta, policy, solver, m: int,
-                 breakdown_factor: float = BREAKDOWN_FACTOR, phi=None):
+                 breakdown_factor: float = BREAKDOWN_FACTOR, phi=None, M=None):
         self.A = A
+        self.M = M
         self.m = m
         self.state = RgsState(theta, policy, solver, phi=phi, capacity=m + 2,
                               breakdown_factor=breakdown_factor)
@@ -234,8 +374,8 @@ class _ArnoldiEngine:
         A, ws = self.A, self.ws
         if self.fused:
             rii = st._R.data_ptr() + (i * st._cap + i) * 8
-            A.spmv_into(st._qcol_ptr(i), st.ccode, ws.w, alpha=alpha, status=st.status,
-                        xdiv_ptr=rii)
+            _eff_matvec_into(A, self.M, ws, st._qcol_ptr(i), st.ccode, ws.w, alpha=alpha,
+                             status=st.status, xdiv_ptr=rii)
             pp, pn, ps = st._sketch_parts(ws.w.data_ptr(), _lib.SGS_F64, A.n, st._parts_p, None)
             st._phi_w(i + 1, ws.w.data_ptr(), _lib.SGS_F64, A.n)
             st._ls(sol=i + 1, p_parts=pp, p_nparts=pn, p_scale=ps)
@@ -245,7 +385,8 @@ class _ArnoldiEngine:
             st._phi_q_finish(i + 1, phq)
             st.m = i + 2
         else:
-            A.spmv_into(st._qcol_ptr(i), st.ccode, ws.w, alpha=alpha, status=st.status)
+            _eff_matvec_into(A, self.M, ws, st._qcol_ptr(i), st.ccode, ws.w, alpha=alpha,
+                             status=st.status)
             st._push_async(ws.w)
         if tol is not None or alpha is not None:
             call("sgs_givens_step", st._R.data_ptr(), st._cap, i, self.cs.data_ptr(),
@@ -304,8 +445,10 @@ def arnoldi(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, thet
 def gmres(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, theta=None,
           policy: PrecisionPolicy = MIXED32_64, solver: LsqSolver = HOUSEHOLDER_QR,
           preconditioner=None, tol: float | None = None, phi=None) -> GmresResult:
-    """Single-cycle RGS-GMRES(m) with progressive Givens rotations (krylov.py:229-319)."""
-    _check_variant(variant, preconditioner)
+    """Single-cycle RGS-GMRES(m) with progressive Givens rotations (krylov.py:229-319),
+    right-preconditioned by an ILU(0) ``preconditioner`` when given."""
+    _check_variant(variant)
+    M = _as_preconditioner(preconditioner)
     if theta is None:
         raise ValueError("the randomized variant needs a sketch operator")
     _lib.require_cuda()
@@ -320,9 +463,9 @@ def gmres(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, theta=
                                                              device=device)
         return GmresResult(x=x0, residual_history=np.zeros(0), final_residual=0.0,
                            iterations=0, converged=True, breakdown=False)
-    eng = _ArnoldiEngine(A, theta, policy, solver, m, phi=phi)
+    eng = _ArnoldiEngine(A, theta, policy, solver, m, phi=phi, M=M)
     st = eng.state
-    alpha = _operator_norm_estimate(A, eng.ws)
+    alpha = _operator_norm_estimate(A, eng.ws, M=M)
     if float(alpha) <= 0.0:
         raise np.linalg.LinAlgError("operator norm estimate is zero")
     eng.start(b_dev, ws0.nrm.data_ptr())
@@ -346,6 +489,9 @@ def gmres(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, theta=
              z.data_ptr(), stream_ptr())
         call("sgs_scale", z.data_ptr(), b_norm, alpha.data_ptr(), 0, x.data_ptr(), A.n,
              stream_ptr())
+        if M is not None:  # x = M^{-1} x_tilde (krylov.py:309-310)
+            M.solve_into(x.data_ptr(), _lib.SGS_F64, z)
+            x = z
     # true residual ||b - A x|| / ||b|| in binary64
     ax = eng.ws.w
     A.spmv_into(x.data_ptr(), _lib.SGS_F64, ax)
@@ -370,7 +516,7 @@ class RestartedResult:
 
 def gmres_restarted(A: SparseMatrix, b, theta, policy: PrecisionPolicy = MIXED32_64,
                     restart: int = 300, max_iters: int = 3000, tol: float = 1e-8,
-                    solver: LsqSolver = HOUSEHOLDER_QR) -> RestartedResult:
+                    solver: LsqSolver = HOUSEHOLDER_QR, preconditioner=None) -> RestartedResult:
     """Restarted RGMRES(restart) for BASELINE config 3 (the reference is
     single-cycle, krylov.py:236-241; the wrapper is shared verbatim with the
     oracle): each cycle runs gmres(A, r, min(restart, max_iters - its), tol =
@@ -387,11 +533,12 @@ def gmres_restarted(A: SparseMatrix, b, theta, policy: PrecisionPolicy = MIXED32
     r = b_dev.clone()
     its, cycles = 0, []
     r_norm = b_norm
+    M = _as_preconditioner(preconditioner)
     while True:
         if b_norm == 0.0 or r_norm / b_norm <= tol or its >= max_iters:
             break
         res = gmres(A, r, m=min(restart, max_iters - its), theta=theta, policy=policy,
-                    solver=solver, tol=tol * b_norm / r_norm)
+                    solver=solver, tol=tol * b_norm / r_norm, preconditioner=M)
         cycles.append(res.iterations)
         its += res.iterations
         x += res.x

@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 from conftest import golden
-from oracle import (OracleSketch, csr_matvec, fwht_ref, oracle_arnoldi, oracle_certificates,
+from oracle import (OracleIlu0, OracleSketch, csr_matvec, fwht_ref, oracle_arnoldi, oracle_certificates,
                     oracle_gmres, oracle_rgs_factorize, psrht_setup)
 from oracle.ref_rgs import OracleBreakdown
 
@@ -84,3 +84,50 @@ def test_oracle_krylov_matches_reference():
     r12 = oracle_gmres(mv3, n12, g["l12_b"], 120, OracleSketch("psrht", 140, n12, 0), "mixed")
     assert r12["iterations"] == int(g["l12_its"])
     assert r12["final_residual"] == float(g["l12_res"])
+
+
+ILU_MATS = ("lap6", "rs60", "rs300", "lap40")
+
+
+@pytest.mark.parametrize("name", ILU_MATS)
+def test_oracle_ilu0_bit_identical_to_reference(name):
+    g = golden("ilu.npz")
+    n = len(g[f"{name}_sv"])
+    pre = OracleIlu0(g[f"{name}_rp"], g[f"{name}_ci"], g[f"{name}_v"], n)
+    for f in ("L", "U"):
+        M = getattr(pre, f)
+        assert np.array_equal(M.indptr, g[f"{name}_{f}rp"])
+        assert np.array_equal(M.indices, g[f"{name}_{f}ci"])
+        assert np.array_equal(M.data, g[f"{name}_{f}v"])
+    assert np.array_equal(pre.solve(g[f"{name}_sv"]), g[f"{name}_solve"])
+
+
+def test_oracle_ilu0_errors_match_reference():
+    import scipy.sparse
+    g = golden("ilu.npz")
+    Z = scipy.sparse.csr_matrix(np.array([[1.0, 1, 0], [1, 1, 0], [0, 0, 1]]))
+    with pytest.raises(ZeroDivisionError) as e:
+        OracleIlu0(Z.indptr, Z.indices, Z.data, 3)
+    assert str(e.value) == str(g["zero_pivot_msg"])
+    S = scipy.sparse.csr_matrix(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    with pytest.raises(ValueError, match="structural zero diagonal at row 0"):
+        OracleIlu0(S.indptr, S.indices, S.data, 2)
+
+
+def test_oracle_preconditioned_gmres_matches_reference():
+    g = golden("ilu.npz")
+    n = len(g["lap40_sv"])
+    mv = lambda x: csr_matvec(g["lap40_rp"], g["lap40_ci"], g["lap40_v"], n, x)
+    pre = OracleIlu0(g["lap40_rp"], g["lap40_ci"], g["lap40_v"], n)
+    out = oracle_gmres(mv, n, g["pg_b"], 60, OracleSketch("psrht", 200, n, 0), "f64",
+                       tol=1e-12, precond=pre)
+    assert out["iterations"] == int(g["pg_its"])
+    assert np.array_equal(out["history"], g["pg_hist"])
+    assert np.array_equal(out["x"], g["pg_x"])
+    assert out["final_residual"] == float(g["pg_res"])
+    mv2 = lambda x: csr_matvec(g["rs300_rp"], g["rs300_ci"], g["rs300_v"], 300, x)
+    pre2 = OracleIlu0(g["rs300_rp"], g["rs300_ci"], g["rs300_v"], 300)
+    out2 = oracle_gmres(mv2, 300, g["pr_b"], 40, OracleSketch("psrht", 200, 300, 0), "mixed",
+                        precond=pre2)
+    assert out2["iterations"] == int(g["pr_its"])
+    assert np.array_equal(out2["x"], g["pr_x"])
