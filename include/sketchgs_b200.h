@@ -260,17 +260,26 @@ int sgs_transpose(const void* src, int64_t lds, void* dst, int64_t ldd,
                   int64_t rows, int64_t cols, int dtype, void* stream);
 
 /* ---- ILU(0) right preconditioning (krylov.py:86-151) ----------------------
- * Sync-free row kernels: rows are claimed in order through a ticket counter
- * and wait on per-row readiness flags, so no level analysis is needed.
- * `ctl` (sgs_ilu_ctl, zeroed once by the caller) and `flags` (n uint32,
- * zeroed once) are owned by one factorization and reused by its solves;
- * each launch advances ctl->epoch itself, so launches need no host
- * bookkeeping and can be captured in a CUDA graph. */
+ * Level-scheduled, sync-free row kernels: sgs_ilu0_analyse gives every row
+ * its dependency level in the lower and the upper triangle and sorts the
+ * rows by level; the factorization and the sweeps hand rows out in that
+ * order through a ticket counter and wait on their dependencies row by row
+ * (no per-level launches).  `ctl` (zeroed once by the caller) is owned by one
+ * preconditioner and reused by its launches, which advance it themselves, so
+ * they need no host bookkeeping and can be captured in a CUDA graph. */
 typedef struct sgs_ilu_ctl {
   uint64_t ticket;   /* next row block to hand out */
   uint32_t done;     /* finished blocks of the running launch */
-  uint32_t epoch;    /* launches completed; flags[i] == epoch+1 means row i ready */
+  uint32_t epoch;    /* launches completed (factor flags: row i ready when == epoch+1) */
 } sgs_ilu_ctl;
+
+/* int32 elements of the `work` buffer sgs_ilu0_analyse needs. */
+int64_t sgs_ilu0_analysis_work_elems(int64_t n);
+
+/* perm_lower / perm_upper (n int32 each) = rows ordered by level in the
+ * lower (j < i) / upper (j > i) dependency graph of the pattern (rp, ci). */
+int sgs_ilu0_analyse(int64_t n, const int32_t* rp, const int32_t* ci, int32_t* perm_lower,
+                     int32_t* perm_upper, int32_t* work, sgs_ilu_ctl* ctl, void* stream);
 
 /* ILU(0) of the CSR matrix (rp, ci, vals) into F (nnz doubles, same pattern):
  * row-oriented IKJ elimination (krylov.py:103-151), bit-identical to the
@@ -278,19 +287,25 @@ typedef struct sgs_ilu_ctl {
  * structural zero diagonal (n if none; reference raises ValueError), aux[1] =
  * 2*i (+1) for the first row i at which the reference raises
  * ZeroDivisionError: +1 = row i's own pivot, +0 = row 0's pivot used by row i
- * (UINT64_MAX if none).  diag_pos: n int32 out. */
+ * (UINT64_MAX if none).  diag_pos: n int32 out; flags: n uint32, zeroed once. */
 int sgs_ilu0_factor(int64_t n, const int32_t* rp, const int32_t* ci, const double* vals,
-                    double* F, int32_t* diag_pos, uint32_t* flags, sgs_ilu_ctl* ctl,
-                    uint64_t* aux, double pivot_tol, void* stream);
+                    double* F, int32_t* diag_pos, const int32_t* perm_lower, uint32_t* flags,
+                    sgs_ilu_ctl* ctl, uint64_t* aux, double pivot_tol, void* stream);
+
+/* Arms a sweep buffer (fills it with the "not yet written" sentinel).  The
+ * `tmp` of sgs_ilu0_solve must be armed once before its first solve; each
+ * solve leaves it armed again. */
+int sgs_ilu0_pending_fill(double* v, int64_t n, void* stream);
 
 /* out = U^{-1} L^{-1} x (Ilu0Preconditioner.solve, krylov.py:95-99): forward
  * sweep with the unit lower part of F into tmp, then backward sweep with the
  * upper part into out.  x is binary32 or binary64; when xdiv is non-null the
  * input is cast(x / *xdiv) to x's dtype first (the normalised Arnoldi vector,
- * as sgs_csr_spmv).  Returns at once when st->code is set. */
+ * as sgs_csr_spmv).  x, tmp and out must be distinct.  Returns at once when
+ * st->code is set. */
 int sgs_ilu0_solve(int64_t n, const int32_t* rp, const int32_t* ci, const double* F,
-                   const int32_t* diag_pos, const void* x, int x_dtype, const double* xdiv,
-                   double* tmp, double* out, uint32_t* flags, sgs_ilu_ctl* ctl,
+                   const int32_t* perm_lower, const int32_t* perm_upper, const void* x,
+                   int x_dtype, const double* xdiv, double* tmp, double* out, sgs_ilu_ctl* ctl,
                    const sgs_status* st, void* stream);
 
 #ifdef __cplusplus

@@ -96,10 +96,14 @@ _SIGS = {
                                 c_void_p, c_int64, c_void_p, c_double, c_void_p, c_void_p]),
     "sgs_transpose": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int,
                               c_void_p]),
+    "sgs_ilu0_analysis_work_elems": (c_int64, [c_int64]),
+    "sgs_ilu0_analyse": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                 c_void_p, c_void_p]),
     "sgs_ilu0_factor": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                c_void_p, c_void_p, c_void_p, c_double, c_void_p]),
-    "sgs_ilu0_solve": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
-                               c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_void_p]),
+    "sgs_ilu0_pending_fill": (c_int, [c_void_p, c_int64, c_void_p]),
+    "sgs_ilu0_solve": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                               c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                c_void_p]),
 }
 

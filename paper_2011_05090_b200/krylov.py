@@ -120,17 +120,18 @@ class Ilu0Preconditioner:
     """Zero-fill incomplete LU factors on A's pattern (krylov.py:86-100).
 
     The factors live on the device as one CSR array F (strict lower part = L
-    with an implied unit diagonal, the rest = U); ``solve(v)`` applies
-    M^{-1} v = U^{-1} (L^{-1} v) with the two sync-free sweep kernels of
-    ``sgs_ilu0_solve``.  ``L`` and ``U`` are the reference's scipy CSR
-    matrices, copied from the device on first use.  Built by ``ilu0(A)``, or
-    from host factors ``Ilu0Preconditioner(L, U)`` as the reference's
-    dataclass is.  One preconditioner runs one solve at a time (its flag
-    array and control block are shared by its launches)."""
+    with an implied unit diagonal, the rest = U), with the two level orders of
+    ``sgs_ilu0_analyse``; ``solve(v)`` applies M^{-1} v = U^{-1} (L^{-1} v)
+    with the two sync-free sweep kernels of ``sgs_ilu0_solve``.  ``L`` and
+    ``U`` are the reference's scipy CSR matrices, copied from the device on
+    first use.  Built by ``ilu0(A)``, or from host factors
+    ``Ilu0Preconditioner(L, U)`` as the reference's dataclass is.  One
+    preconditioner runs one solve at a time (its control block and sweep
+    buffer are shared by its launches)."""
 
     def __init__(self, L=None, U=None, *, _device=None):
         if _device is not None:
-            (self.n, self._rp, self._ci, self._F, self._diag) = _device
+            (self.n, self._rp, self._ci, self._F, self._perm_l, self._perm_u, self._ctl) = _device
             self._L = self._U = None
         else:
             if L is None or U is None:
@@ -142,24 +143,18 @@ class Ilu0Preconditioner:
             full = (scipy.sparse.tril(L, k=-1, format="csr") + U).tocsr()
             full.sum_duplicates()
             full.sort_indices()
+            if np.any(full.diagonal() == 0.0):
+                raise np.linalg.LinAlgError("A is singular: zero entry on diagonal.")
             dev = torch.device("cuda", torch.cuda.current_device())
             self.n = n
             self._rp = torch.from_numpy(full.indptr.astype(np.int32)).to(dev)
             self._ci = torch.from_numpy(full.indices.astype(np.int32)).to(dev)
             self._F = torch.from_numpy(full.data.astype(np.float64)).to(dev)
-            d = full.diagonal()
-            if np.any(d == 0.0):
-                raise np.linalg.LinAlgError("A is singular: zero entry on diagonal.")
-            pos = np.full(n, -1, dtype=np.int32)
-            rows = np.repeat(np.arange(n), np.diff(full.indptr))
-            on = full.indices == rows
-            pos[rows[on]] = np.nonzero(on)[0]
-            self._diag = torch.from_numpy(pos).to(dev)
+            self._ctl = torch.zeros(2, dtype=torch.int64, device=dev)
+            self._perm_l, self._perm_u = _ilu_analyse(n, self._rp, self._ci, self._ctl)
             self._L, self._U = L, U
-        dev = self._F.device
-        self._flags = torch.zeros(max(self.n, 1), dtype=torch.int32, device=dev)
-        self._ctl = torch.zeros(2, dtype=torch.int64, device=dev)
-        self._tmp = torch.empty(max(self.n, 1), dtype=torch.float64, device=dev)
+        self._tmp = torch.empty(max(self.n, 1), dtype=torch.float64, device=self._F.device)
+        call("sgs_ilu0_pending_fill", self._tmp.data_ptr(), self.n, stream_ptr())
 
     # ---- host views (reference dataclass fields) ----------------------------------
     def _host_full(self):
@@ -183,11 +178,12 @@ class Ilu0Preconditioner:
     # ---- device solve ---------------------------------------------------------
     def solve_into(self, x_ptr: int, x_code: int, out: torch.Tensor, xdiv_ptr=None,
                    status=None) -> None:
-        """out = M^{-1} x on the current stream (x binary32/64 at x_ptr; with
-        xdiv_ptr the input is cast(x / *xdiv) first, as SparseMatrix.spmv_into)."""
+        """out = M^{-1} x on the current stream (x binary32/64 at x_ptr, distinct
+        from out; with xdiv_ptr the input is cast(x / *xdiv) first, as
+        SparseMatrix.spmv_into)."""
         call("sgs_ilu0_solve", self.n, self._rp.data_ptr(), self._ci.data_ptr(),
-             self._F.data_ptr(), self._diag.data_ptr(), x_ptr, x_code, xdiv_ptr,
-             self._tmp.data_ptr(), out.data_ptr(), self._flags.data_ptr(), self._ctl.data_ptr(),
+             self._F.data_ptr(), self._perm_l.data_ptr(), self._perm_u.data_ptr(), x_ptr, x_code,
+             xdiv_ptr, self._tmp.data_ptr(), out.data_ptr(), self._ctl.data_ptr(),
              status.ptr if status is not None else None, stream_ptr())
 
     def solve(self, v):
@@ -206,22 +202,34 @@ class Ilu0Preconditioner:
         return out if on_dev else out.cpu().numpy()
 
 
+def _ilu_analyse(n, rp, ci, ctl):
+    dev = rp.device
+    perm_l = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    perm_u = torch.empty_like(perm_l)
+    work = torch.empty(int(_lib.load().sgs_ilu0_analysis_work_elems(n)), dtype=torch.int32,
+                       device=dev)
+    call("sgs_ilu0_analyse", n, rp.data_ptr(), ci.data_ptr(), perm_l.data_ptr(),
+         perm_u.data_ptr(), work.data_ptr(), ctl.data_ptr(), stream_ptr())
+    return perm_l, perm_u
+
+
 def ilu0(A: SparseMatrix, pivot_tol: float = 1e-30) -> Ilu0Preconditioner:
     """ILU(0) on the device (krylov.py:103-151): the reference's row-oriented
     IKJ elimination, bit-identical (one thread per row, rows released in
-    dependency order).  Raises ValueError on a structural zero diagonal and
+    level order).  Raises ValueError on a structural zero diagonal and
     ZeroDivisionError on a pivot below pivot_tol, naming the same row."""
     rp, ci, va = A.device_arrays()
     n = A.n
     dev = va.device
+    ctl = torch.zeros(2, dtype=torch.int64, device=dev)
+    perm_l, perm_u = _ilu_analyse(n, rp, ci, ctl)
     F = torch.empty_like(va)
     diag = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     flags = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
-    ctl = torch.zeros(2, dtype=torch.int64, device=dev)
     aux = torch.empty(2, dtype=torch.int64, device=dev)
     call("sgs_ilu0_factor", n, rp.data_ptr(), ci.data_ptr(), va.data_ptr(), F.data_ptr(),
-         diag.data_ptr(), flags.data_ptr(), ctl.data_ptr(), aux.data_ptr(), float(pivot_tol),
-         stream_ptr())
+         diag.data_ptr(), perm_l.data_ptr(), flags.data_ptr(), ctl.data_ptr(), aux.data_ptr(),
+         float(pivot_tol), stream_ptr())
     if n:
         a = aux.cpu().numpy().view(np.uint64)
         if int(a[0]) != n:
@@ -229,9 +237,7 @@ def ilu0(A: SparseMatrix, pivot_tol: float = 1e-30) -> Ilu0Preconditioner:
         if int(a[1]) != 2**64 - 1:
             key = int(a[1])
             raise ZeroDivisionError(f"ILU(0) pivot too small at row {key >> 1 if key & 1 else 0}")
-    pre = Ilu0Preconditioner(_device=(n, rp, ci, F, diag))
-    pre._flags, pre._ctl = flags, ctl  # the factor launch advanced this control block
-    return pre
+    return Ilu0Preconditioner(_device=(n, rp, ci, F, perm_l, perm_u, ctl))
 
 
 def _as_preconditioner(pre):
