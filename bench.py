@@ -159,10 +159,12 @@ def run_qr(args, cfg_name):
     from paper_2011_05090_b200.distributed import init_from_env
     from paper_2011_05090_b200.workloads import CONFIGS, make_w_device, shard_rows
 
-    comm = init_from_env("nccl")
+    # SGS_DIST_BACKEND=gloo runs several ranks on one GPU: a functional check of
+    # the sharded path only, never a timing
+    comm = init_from_env(os.environ.get("SGS_DIST_BACKEND", "nccl"))
     rank = comm.rank if comm else 0
     world = comm.world if comm else 1
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     cfg = CONFIGS[cfg_name]
@@ -170,6 +172,12 @@ def run_qr(args, cfg_name):
     pol = sg.policy_from_name(cfg["policy"])
     bf = cfg["breakdown_factor"]
     kw = {"block_log2": cfg["block_log2"]} if "block_log2" in cfg else {}
+    # N > 1: c1 is weak-scaled (n = N x 1e6 rows, ~1e6 per GPU, one P-SRHT over
+    # next_pow2(n)); the fixed-n configs (c0, c2) are strong-scaled row shards.
+    weak = world > 1 and args.scaling == "weak" and cfg["kind"] == "psrht"
+    n_per_gpu = n
+    if weak:
+        n = n_per_gpu * world
     th = sg.make_sketch(sg.SketchKind(cfg["kind"]), k, n, 0, **kw)
     row0, n_loc = (0, n) if world == 1 else shard_rows(n, world, rank, th.row_align())
     wdt = torch.float32 if pol.coarse_dtype == np.float32 else torch.float64
@@ -232,7 +240,10 @@ def run_qr(args, cfg_name):
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t)
-    value = m / (ms / 1e3)
+    # weak: every rank factorises its ~1e6-row share of each column, so the
+    # work unit is a c1-sized column shard (world of them per column)
+    units = m * world if weak else m
+    value = units / (ms / 1e3)
     bq = 4 if pol.coarse_dtype == np.float32 else 8
     bw = bq
     alg = qr_alg_bytes(n, m, bq, bw, k, cfg["kind"] == "gaussian")
@@ -241,7 +252,7 @@ def run_qr(args, cfg_name):
     # ---- roofline of the dominant kernel (sgs_rgs_update), CUDA events per launch
     peak, peak_kind = _peaks()
     roof = None
-    if rank == 0:
+    if True:  # every rank: the step holds collectives; rank 0 reports
         import paper_2011_05090_b200.gram_schmidt as gsm
         evs = []
         orig = gsm.RgsState._column
@@ -285,25 +296,36 @@ def run_qr(args, cfg_name):
 
     # ---- e2e through the public API (pinned host W -> factors on the host)
     e2e = None
-    if world == 1 and not args.no_e2e:
+    if not args.no_e2e:
         del graph, gstate
         torch.cuda.empty_cache()
-        pin = torch.empty((m, n), dtype=wdt, pin_memory=True)
-        pin.copy_(Wt[:, :n])
-        Wh = pin.numpy().T  # (n, m) Fortran-ordered numpy view of pinned memory
+        pin = torch.empty((m, n_loc), dtype=wdt, pin_memory=True)
+        pin.copy_(Wt[:, :n_loc])
+        Wh = pin.numpy().T  # (n_loc, m) Fortran-ordered numpy view of pinned memory
+        kw_sh = {"comm": comm, "row0": row0} if comm else {}
+
+        def e2e_call():
+            return sg.rgs_factorize(Wh, th, pol, with_certificate=False, breakdown_factor=bf,
+                                    **kw_sh)
+
         for _ in range(2):  # allocates the pinned output buffers once
-            f, _ = sg.rgs_factorize(Wh, th, pol, with_certificate=False, breakdown_factor=bf)
-        torch.cuda.synchronize()
+            f, _ = e2e_call()
+        barrier()
         t0 = time.perf_counter()
         ne = max(1, min(args.steps, 3))
         for _ in range(ne):
-            f, _ = sg.rgs_factorize(Wh, th, pol, with_certificate=False, breakdown_factor=bf)
+            f, _ = e2e_call()
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) / ne
+        if comm:
+            t = torch.tensor([dt], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            dt = float(t)
         fb = np.dtype(pol.fine_dtype).itemsize
-        e2e = {"value": m / dt, "unit": "columns/s", "h2d_bytes_per_step": n * m * bq,
-               "d2h_bytes_per_step": n * m * bq + m * m * 8 + 2 * k * m * fb,
-               "ms_per_step": 1e3 * dt}
+        e2e = {"value": units / dt, "unit": "columns/s", "h2d_bytes_per_step": n * m * bq,
+               "d2h_bytes_per_step": n * m * bq + world * (m * m * 8 + 2 * k * m * fb),
+               "ms_per_step": 1e3 * dt,
+               "path": "rgs_factorize(pinned host W shard) -> host Q, R, S, P"}
         del pin, Wh, f
 
     cpu = None
@@ -318,16 +340,19 @@ def run_qr(args, cfg_name):
         print(json.dumps({
             "metric": "RGS-QR columns/s", "value": value, "unit": "columns/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong",
+            "higher_is_better": True, "scaling": "weak" if weak else "strong",
             "vs_baseline": None,
             "dtype": "f32 (Q, update) / f64 (sketch, LS)" if cfg["policy"] == "mixed" else "f64",
             "data": "synthetic (W = G diag(sigma) V^T generated on device, seeded)",
-            "config": {"workload": cfg_name, "n": n, "m": m, "k": k, "sketch": cfg["kind"],
-                       "policy": cfg["policy"], "breakdown_factor": bf,
+            "config": {"workload": cfg_name + ("-weak" if weak else ""), "n": n, "m": m, "k": k,
+                       "sketch": cfg["kind"], "policy": cfg["policy"], "breakdown_factor": bf,
                        "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+                       **({"weak": f"n = {world} x {n_per_gpu} rows (~{n_per_gpu} per GPU); "
+                                   f"value counts column shards: {world} per column"}
+                          if weak else {}),
                        "l2": "inputs larger than L2 (W, Q >> 126 MB)"},
             "hbm_gbs_whole_step": round(hbm_gbs, 1),
-            "hbm_frac_whole_step": round(hbm_gbs / peak, 4),
+            "hbm_frac_whole_step": round(hbm_gbs / (peak * world), 4),
             "alg_bytes_per_step": alg,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk,
@@ -382,6 +407,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c1")
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
+                    help="N > 1 on c1: weak (1e6 rows per GPU, default) or strong (n = 1e6 split)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-cols", type=int, default=24)
     ap.add_argument("--no-cpu", action="store_true")

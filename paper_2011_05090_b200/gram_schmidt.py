@@ -500,7 +500,10 @@ class RgsState:
         base = Wcm.data_ptr()
         k, sp = self.k, stream_ptr()
         # P = Theta W, batched in column chunks (same kernel and parts as per column)
-        chunk = max(1, min(m, (256 << 20) // max(1, self.nparts * k * 8)))
+        # the chunk size sets the all-reduce message size, so a sharded state
+        # sizes it from the global row count (identical on every rank)
+        np_size = self.nparts if self.comm is None else max(self.nparts, self.theta.nparts(self.n))
+        chunk = max(1, min(m, (256 << 20) // max(1, np_size * k * 8)))
         parts = torch.empty((chunk, self.nparts, k), dtype=torch.float64, device=self.device)
         if self.comm is not None:
             kbuf = torch.empty((chunk, k), dtype=torch.float64, device=self.device)
@@ -582,14 +585,24 @@ class RgsState:
         parts = torch.empty((chunk, self.nparts, k), dtype=torch.float64, device=self.device)
         self.status.reset()
 
+        kbuf = (torch.empty((chunk, k), dtype=torch.float64, device=self.device)
+                if self.comm is not None else None)
+
         def sketch_chunk(c):
             comp.wait_event(landed[c])
             c0, c1 = c * chunk, min(m, (c + 1) * chunk)
             self.theta.partials_into(base + c0 * n * esz, wc, n, c1 - c0, parts,
                                      n_local=n, row0=self.row0, status=self.status)
-            call("sgs_partials_reduce", parts.data_ptr(), self.nparts, k, c1 - c0,
-                 self.theta.scale, self._P.data_ptr() + c0 * k * self._P.element_size(),
-                 self.fcode, k, self.status.ptr, stream_ptr())
+            pdst = self._P.data_ptr() + c0 * k * self._P.element_size()
+            if self.comm is None:
+                call("sgs_partials_reduce", parts.data_ptr(), self.nparts, k, c1 - c0,
+                     self.theta.scale, pdst, self.fcode, k, self.status.ptr, stream_ptr())
+            else:  # same order as _enqueue_factorization: local sum, all-reduce, scale
+                call("sgs_partials_reduce", parts.data_ptr(), self.nparts, k, c1 - c0, 1.0,
+                     kbuf.data_ptr(), _lib.SGS_F64, k, self.status.ptr, stream_ptr())
+                self.comm.allreduce_(kbuf[:c1 - c0])
+                call("sgs_partials_reduce", kbuf.data_ptr(), 1, k, c1 - c0, self.theta.scale,
+                     pdst, self.fcode, k, self.status.ptr, stream_ptr())
 
         def ship(c0, c1):
             ev = torch.cuda.Event()
@@ -730,7 +743,7 @@ def rgs_factorize(W, theta, policy: PrecisionPolicy = MIXED32_64,
         state = RgsState(theta, policy, solver, phi=phi, capacity=m + 1,
                          breakdown_factor=breakdown_factor, comm=comm, row0=row0,
                          n_local=n_loc)
-        if (isinstance(W, np.ndarray) and not device_factors and comm is None and phi is None
+        if (isinstance(W, np.ndarray) and not device_factors and phi is None
                 and W.dtype in (np.float32, np.float64) and W.flags.f_contiguous
                 and _is_pinned(W)):
             factors = state.factorize_host_pipelined(W, m)

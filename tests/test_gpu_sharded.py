@@ -47,6 +47,14 @@ def _worker(rank, world, port, case, out):
     W = make_w(c["n"], c["m"], 1e-6, 4, dtype=dt)[row0:row0 + n_loc]
     f, _ = sg.rgs_factorize(np.asfortranarray(W), th, sg.policy_from_name(c["pol"]),
                             breakdown_factor=0.0, comm=comm, row0=row0, with_certificate=False)
+    # the pinned host shard takes the overlapped H2D/compute/D2H pipeline, which
+    # all-reduces P chunk by chunk: same kernels and order, so the same bits
+    pin = torch.empty((c["m"], n_loc), dtype=torch.from_numpy(W[:1]).dtype, pin_memory=True)
+    pin.copy_(torch.from_numpy(np.ascontiguousarray(W.T)))
+    fp, _ = sg.rgs_factorize(pin.numpy().T, th, sg.policy_from_name(c["pol"]),
+                             breakdown_factor=0.0, comm=comm, row0=row0, with_certificate=False)
+    for a, b in ((f.Q, fp.Q), (f.R, fp.R), (f.S, fp.S), (f.P, fp.P)):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
     out[rank] = (row0, n_loc, f.Q, f.R, f.S, f.P)
     dist.barrier()
     dist.destroy_process_group()
