@@ -283,6 +283,8 @@ class RgsState:
         _lib.check(_lib.load().sgs_ls_step(ctypes_byref(a), stream_ptr()), "sgs_ls_step")
 
     _trace = None  # optional (cap, 16) int64 device tensor: per-column LS phase clocks
+    _e2e_late = (192, 64)  # pipelined path: (column from which chunks grow, late chunk cap)
+    _e2e_ship = 8          # pipelined path: Q columns per D2H copy
 
     def _trace_ptr(self, col):
         t = self._trace
@@ -554,7 +556,7 @@ class RgsState:
         if st["code"]:
             self._raise_status(st)
 
-    def factorize_host_pipelined(self, Wh: np.ndarray, m: int, chunk: int = 32) -> QrFactors:
+    def factorize_host_pipelined(self, Wh: np.ndarray, m: int, chunk: int = 8) -> QrFactors:
         """End-to-end factorisation of a pinned, column-major host W (n x m,
         Fortran order): W streams to the GPU in column chunks on one copy
         stream while the compute stream sketches each chunk as it lands and
@@ -571,26 +573,41 @@ class RgsState:
         comp = torch.cuda.current_stream()
         h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
         h2d.wait_stream(comp)
-        nchunks = (m + chunk - 1) // chunk
+        # graduated chunks (2, 4, 8, ... up to `chunk` columns) so the column
+        # loop starts after a few MB have landed instead of a full chunk
+        # Early columns outrun PCIe (~50 GB/s) and need fine arrival steps; past
+        # `late` the GPU is the bottleneck and larger chunks mean fewer
+        # cross-stream waits in the kernel chain.
+        late, late_chunk = self._e2e_late
+        bounds, c0, sz = [0], 0, 2
+        while c0 < m:
+            c0 = min(m, c0 + min(sz, chunk if c0 < late else late_chunk))
+            bounds.append(c0)
+            sz *= 2
+        nchunks = len(bounds) - 1
+        chunk_of = np.zeros(m + 1, dtype=np.int64)
+        for c in range(nchunks):
+            chunk_of[bounds[c]:bounds[c + 1]] = c
         landed = []
         with torch.cuda.stream(h2d):
             for c in range(nchunks):
-                c0, c1 = c * chunk, min(m, (c + 1) * chunk)
+                c0, c1 = bounds[c], bounds[c + 1]
                 Wd[c0:c1].copy_(Wt[c0:c1], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(h2d)
                 landed.append(ev)
         Qh, Qarr = _pinned_buffer((m, n), self.cdt)
         wc, esz, base = _lib.dtype_code(dt), Wd.element_size(), Wd.data_ptr()
-        parts = torch.empty((chunk, self.nparts, k), dtype=torch.float64, device=self.device)
+        pmax = max(chunk, self._e2e_late[1])
+        parts = torch.empty((pmax, self.nparts, k), dtype=torch.float64, device=self.device)
         self.status.reset()
 
-        kbuf = (torch.empty((chunk, k), dtype=torch.float64, device=self.device)
+        kbuf = (torch.empty((pmax, k), dtype=torch.float64, device=self.device)
                 if self.comm is not None else None)
 
         def sketch_chunk(c):
             comp.wait_event(landed[c])
-            c0, c1 = c * chunk, min(m, (c + 1) * chunk)
+            c0, c1 = bounds[c], bounds[c + 1]
             self.theta.partials_into(base + c0 * n * esz, wc, n, c1 - c0, parts,
                                      n_local=n, row0=self.row0, status=self.status)
             pdst = self._P.data_ptr() + c0 * k * self._P.element_size()
@@ -612,11 +629,11 @@ class RgsState:
                 Qh[c0:c1].copy_(self._Q[c0:c1, :n], non_blocking=True)
 
         sketch_chunk(0)
-        shipped, ship_chunk = 0, 8
+        shipped, ship_chunk = 0, self._e2e_ship
         for i in range(m):
             nxt = i + 1
-            if nxt < m and nxt % chunk == 0:
-                sketch_chunk(nxt // chunk)
+            if nxt < m and bounds[chunk_of[nxt]] == nxt:
+                sketch_chunk(int(chunk_of[nxt]))
             sol = nxt if nxt < m else None
             if i == 0:
                 self._column(0, base, wc, False, False)
@@ -629,15 +646,25 @@ class RgsState:
                     ship(shipped, shipped + ship_chunk)
                     shipped += ship_chunk
         self._normalize(m - 1)
-        if shipped < m:
-            ship(shipped, m)
+        # the tail: last Q columns and R, S, P into pinned buffers on the copy
+        # stream (pageable .cpu() copies of R/S/P cost ~3.5 ms at c1)
+        Rh, Rarr = _pinned_buffer((m, m), torch.float64)
+        Sh, Sarr = _pinned_buffer((m, k), self.fdt)
+        Ph, Parr = _pinned_buffer((m, k), self.fdt)
+        ev = torch.cuda.Event()
+        ev.record(comp)
+        d2h.wait_event(ev)
+        with torch.cuda.stream(d2h):
+            if shipped < m:
+                Qh[shipped:m].copy_(self._Q[shipped:m, :n], non_blocking=True)
+            Rh.copy_(self._R[:m, :m], non_blocking=True)
+            Sh.copy_(self._S[:m], non_blocking=True)
+            Ph.copy_(self._P[:m], non_blocking=True)
         comp.wait_stream(d2h)
         st = self._sync_status()
         if st["code"]:
             self._raise_status(st)
-        Rh = self._R[:m, :m].t().cpu().numpy()
-        return QrFactors(Q=Qarr.T, R=Rh, S=self._S[:m].t().cpu().numpy(),
-                         P=self._P[:m].t().cpu().numpy())
+        return QrFactors(Q=Qarr.T, R=Rarr.T, S=Sarr.T, P=Parr.T)
 
     def capture_factorization(self, Wcm: torch.Tensor, ldw: int, m: int):
         """Capture the whole factorisation in a CUDA graph; ``graph.replay()``
@@ -670,7 +697,7 @@ def _pinned_buffer(shape, dtype):
     t = torch.empty(shape, dtype=dtype, pin_memory=True)
     ent = (t, t.numpy())
     _PINNED_POOL.append(ent)
-    if len(_PINNED_POOL) > 4:
+    if len(_PINNED_POOL) > 12:  # Q, R, S, P of three live results
         _PINNED_POOL.pop(0)
     return ent
 
