@@ -195,6 +195,12 @@ typedef struct sgs_ls_args {
   int cache_cols;        /* set by the library: columns of T cached in shared memory */
   unsigned long long* timeline;  /* set by the library (debug timeline) */
   void* xbar;            /* set by the library: cross-cluster barrier words in scratch */
+  int* t_pend;           /* optional (NULL: off): column of T whose formation is deferred, -1 none */
+  void* t_coef;          /* cap, fine: its projection coefficients (with t_pend).  A finalize
+                            that sees no cancellation (||t||^2 >= ||s||^2/2 by Pythagoras)
+                            publishes r without forming t = s - T c; the next launch forms
+                            T[:, t_pend] before its dependency wait, overlapping the column
+                            kernel.  Bit-identical T; alpha from the Pythagorean norm. */
 } sgs_ls_args;
 
 int64_t sgs_ls_scratch_elems(int k, int cap);

@@ -573,14 +573,36 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   SGS_TR(0);
   const int64_t code0 = *reinterpret_cast<volatile const int64_t*>(&a.st->code);
   double dmax = a.st->diag_max, dmin = a.st->diag_min;
+  // The previous finalize may have deferred its T column: form it now, while
+  // the predecessor kernel streams (same arithmetic as the explicit path:
+  // t = s - T[:, :pend] c2, rows of this CTA, from the shared-memory cache).
+  // Idempotent, so a launch that stops early and leaves t_pend set only makes
+  // the next one redo it.
+  const int pend = a.t_pend ? *reinterpret_cast<volatile const int*>(a.t_pend) : -1;
   const int ncols_t = a.do_finalize ? a.col_fin : a.col_sol;  // columns of T in use
   const int ncache = min(ncols_t, a.cache_cols);
   for (int e = threadIdx.x; e < ncache * nr; e += blockDim.x) {
     const int j = e / nr, rr = e - j * nr;
-    sq[(int64_t)j * RM + rr] = Tm[(int64_t)j * k + ra + rr];
+    if (j != pend) sq[(int64_t)j * RM + rr] = Tm[(int64_t)j * k + ra + rr];
+  }
+  const ColSrc<T> TS{sq, RM, ncache, Tm + ra, (int64_t)k};
+  if (pend >= 0 && code0 == 0) {
+    const T* coef = static_cast<const T*>(a.t_coef);  // [c1 (cap) | s' (k)] of column pend
+    for (int j = threadIdx.x; j < pend; j += blockDim.x) {
+      const T cj = __ldcg(coef + j);
+      c1[j] = cj;                       // kept for a solve-only launch (identity below)
+      c2[j] = cj / __ldcg(AL + j);      // as the explicit path: coefficient on T_j
+    }
+    for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vt[rr] = S[(int64_t)pend * k + ra + rr];
+    __syncthreads();
+    if (pend > 0) ls_rows_gemv<T>(TS, nr, pend, c2, tmp, red);  // columns < pend only
+    for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
+      const T tv = pend > 0 ? vt[rr] - tmp[rr] : vt[rr];
+      Tm[(int64_t)pend * k + ra + rr] = tv;
+      if (pend < ncache) sq[(int64_t)pend * RM + rr] = tv;
+    }
   }
   __syncthreads();
-  const ColSrc<T> TS{sq, RM, ncache, Tm + ra, (int64_t)k};
   int s0 = 0, s1 = 0;  // output slice of the solve: [0, c) for c = col_sol
   if (a.do_solve) slice(a.col_sol, s0, s1);
   if (fused && code0 == 0) {
@@ -618,19 +640,22 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     __syncthreads();
     SGS_TR(3);
     // ---- exchange #1: ||s'||^2, ||p_i||^2, T^T s' --------------------------------
-    T l0 = T(0), l1 = T(0);
+    const bool defer = a.t_pend != nullptr;
+    T l0 = T(0), l1 = T(0), l2 = T(0);
     for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
       const T pv = P[(int64_t)i * k + ra + rr];
       l0 = fma(vs[rr], vs[rr], l0);
       l1 = fma(pv, pv, l1);
+      if (defer && fused) l2 = fma(vs[rr], vp[rr], l2);  // s'^T p_{i+1}
     }
     l0 = block_sum(l0, red);
     l1 = block_sum(l1, red);
-    if (threadIdx.x == 0) { myA[0] = l0; myA[1] = l1; }
+    if (defer && fused) l2 = block_sum(l2, red);
+    if (threadIdx.x == 0) { myA[0] = l0; myA[1] = l1; myA[2] = l2; }
     if (nq > 0) ls_coldot<T, 1>(TS, nr, 0, nq, vs, nullptr, myA + 8, nullptr);
     xsync();
     SGS_TR(4);
-    if (threadIdx.x < 2) bc[threadIdx.x] = ls_slot_sum(XA + threadIdx.x, sA, CL);
+    if (threadIdx.x < 3) bc[threadIdx.x] = ls_slot_sum(XA + threadIdx.x, sA, CL);
     if (nq > 0) ls_gather<T>(XA + 8, sA, CL, 0, nq, AL, c1);  // T^T s' / alpha
     __syncthreads();
     const double r_ii = (double)sqrt(bc[0]);
@@ -645,7 +670,9 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
       return;
     }
     const T rT = (T)r_ii;
+    T* sprime = defer ? static_cast<T*>(a.t_coef) + cap : nullptr;
     for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
+      if (sprime) sprime[ra + rr] = vs[rr];  // s', for a solve-only launch's identity
       const T sv = vs[rr] / rT;
       vs[rr] = sv;
       S[(int64_t)i * k + ra + rr] = sv;
@@ -656,6 +683,37 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
       c2[j] = cj / __ldcg(AL + j);   // coefficient on the unnormalised column T_j
     }
     __syncthreads();
+    // Fast path: Q_s = T diag(1/alpha) is orthonormal, so ||t||^2 = ||s||^2 -
+    // sum_j c1_j^2 and t^T p = s^T p - sum_j c1_j zc_j (zc = Q_s^T p from before
+    // the wait).  Every CTA evaluates them from identical gathered values in
+    // the same order, so the branch is uniform across the cluster.  Without
+    // cancellation the estimate is accurate to a few ulps and r is published
+    // without forming t; with it (the reorthogonalisation case) the explicit
+    // path below runs.
+    bool explicit_t = true;
+    T tt = T(0);
+    if (defer) {
+      T acc_c = T(0), acc_p = T(0);
+      for (int j = threadIdx.x; j < nq; j += blockDim.x) {
+        acc_c = fma(c1[j], c1[j], acc_c);
+        if (fused) acc_p = fma(c1[j], zc[j], acc_p);
+      }
+      acc_c = block_sum(acc_c, red);
+      if (fused) acc_p = block_sum(acc_p, red);
+      const T ss0 = bc[0] / (rT * rT);
+      const T tt_est = ss0 - acc_c;
+      if (nq == 0 || tt_est >= T(0.5) * ss0) {
+        explicit_t = false;
+        tt = tt_est;
+        if (fused) tp = bc[2] / rT - acc_p;
+        if (rank == 0) {
+          T* coef = static_cast<T*>(a.t_coef);
+          for (int j = threadIdx.x; j < nq; j += blockDim.x) coef[j] = c1[j];
+          if (threadIdx.x == 0) *a.t_pend = i;
+        }
+      }
+    }
+    if (explicit_t) {
     if (nq > 0) {
       ls_rows_gemv<T>(TS, nr, nq, c2, tmp, red);
       for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vt[rr] = vs[rr] - tmp[rr];
@@ -676,7 +734,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     SGS_TR(6);
     if (threadIdx.x < 2) bc[2 + threadIdx.x] = ls_slot_sum(XB + threadIdx.x, 8, CL);
     __syncthreads();
-    T tt = bc[2];
+    tt = bc[2];
     tp = bc[3];
     const T ss = bc[0] / (rT * rT);
     if (nq > 0 && tt < T(0.5) * ss) {
@@ -707,6 +765,8 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
       tt = bc[4];
       tp = bc[5];
     }
+    if (defer && rank == 0 && threadIdx.x == 0) *a.t_pend = -1;  // T[:, i] stored
+    }  // explicit_t
     SGS_TR(7);
     alpha = sqrt(tt);
     // R_S^{-1} column i on this CTA's slice of [0, i+1): -R_S^{-1}[:i,:i] c1 / alpha
@@ -758,12 +818,34 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
         for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vp[rr] = P[(int64_t)c * k + ra + rr];
       }
       __syncthreads();
+      // Newest column deferred by its finalize: z from the same identity and
+      // arithmetic as the fused launch (t^T p = s'^T p / r_ii - sum_j c1_j zc_j),
+      // so streaming push and batch factorisation stay bit-identical.
+      const bool idz = a.t_pend != nullptr && pend >= 0 && pend == c - 1;
+      if (idz) {
+        const T* sprime = static_cast<const T*>(a.t_coef) + cap;
+        T l2 = T(0);
+        for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) l2 = fma(__ldcg(sprime + ra + rr), vp[rr], l2);
+        l2 = block_sum(l2, red);
+        if (threadIdx.x == 0) myA[2] = l2;
+      }
       ls_coldot<T, 1>(TS, nr, 0, c, vp, nullptr, myA + 8 + cap, nullptr);
       xsync();
+      // every CTA has read t_pend (pre-wait) and formed its rows of it
+      if (!a.do_finalize && pend >= 0 && rank == 0 && threadIdx.x == 0) *a.t_pend = -1;
       ls_gather<T>(XA + 8 + cap, sA, CL, 0, c, AL, zc);
+      if (idz && threadIdx.x == 0) bc[2] = ls_slot_sum(XA + 2, sA, CL);
       __syncthreads();
       ls_matvec<T, true>(Rinv, cap, s0, s1, c - 1, zc, yv, red);
-      zl = zc[c - 1];
+      if (idz) {
+        T acc_p = T(0);
+        for (int j = threadIdx.x; j < c - 1; j += blockDim.x) acc_p = fma(c1[j], zc[j], acc_p);
+        acc_p = block_sum(acc_p, red);
+        const T rTn = (T)R[(int64_t)(c - 1) * cap + (c - 1)];
+        zl = (bc[2] / rTn - acc_p) / __ldcg(AL + (c - 1));
+      } else {
+        zl = zc[c - 1];
+      }
     }
     SGS_TR(9);
     // r_o = y_o + R_S^{-1}[o, c-1] z[c-1]  (same two-term form on every path)

@@ -22,6 +22,8 @@ reference's exception types and column numbers.
 
 from __future__ import annotations
 
+import os
+
 import math
 from dataclasses import dataclass
 from enum import Enum
@@ -242,6 +244,15 @@ class RgsState:
                 self._P_phi[:self._cap] = old_phi[1]
         self._scratch = torch.zeros(int(_lib.load().sgs_ls_scratch_elems(k, cap)),
                                     dtype=torch.float64, device=dev)
+        # deferred formation of the newest T column (sgs_ls_args.t_pend / t_coef)
+        old_coef = self.__dict__.get("_tcoef")
+        self._tcoef = torch.zeros(cap + k, dtype=self.fdt, device=dev)  # [c1 (cap) | s' (k)]
+        if old_coef is not None:
+            oc_ = old_coef.shape[0] - k
+            self._tcoef[:oc_] = old_coef[:oc_]
+            self._tcoef[cap:] = old_coef[oc_:]
+        if "_tpend" not in self.__dict__:
+            self._tpend = torch.full((1,), -1, dtype=torch.int32, device=dev)
         self._rc = torch.zeros(cap, dtype=self.cdt, device=dev)
         if old is not None:
             Q, R, S, P, Qs, Rinv, alpha, oc = old
@@ -280,6 +291,10 @@ class RgsState:
         a.Qs, a.Rinv, a.alpha = self._Qs.data_ptr(), self._Rinv.data_ptr(), self._alpha.data_ptr()
         a.scratch, a.r_crs, a.st = self._scratch.data_ptr(), self._rc.data_ptr(), self.status.ptr
         a.trace = self._trace_ptr(fin if fin is not None else sol)
+        if _LS_DEFER:
+            a.t_pend, a.t_coef = self._tpend.data_ptr(), self._tcoef.data_ptr()
+        else:
+            a.t_pend = a.t_coef = None
         _lib.check(_lib.load().sgs_ls_step(ctypes_byref(a), stream_ptr()), "sgs_ls_step")
 
     _trace = None  # optional (cap, 16) int64 device tensor: per-column LS phase clocks
@@ -682,6 +697,10 @@ class RgsState:
 
 
 _PINNED_POOL: list = []
+
+
+# SGS_LS_DEFER=0 forms every T column inside its own finalize (A/B switch)
+_LS_DEFER = os.environ.get("SGS_LS_DEFER", "1") != "0"
 
 
 def _pinned_buffer(shape, dtype):
