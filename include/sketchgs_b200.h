@@ -194,7 +194,6 @@ typedef struct sgs_ls_args {
   long long* trace;      /* optional (NULL): clock64() at phase boundaries, CTA 0 */
   int cache_cols;        /* set by the library: columns of T cached in shared memory */
   unsigned long long* timeline;  /* set by the library (debug timeline) */
-  void* xbar;            /* set by the library: cross-cluster barrier words in scratch */
   int* t_pend;           /* optional (NULL: off): column of T whose formation is deferred, -1 none */
   void* t_coef;          /* cap, fine: its projection coefficients (with t_pend).  A finalize
                             that sees no cancellation (||t||^2 >= ||s||^2/2 by Pythagoras)

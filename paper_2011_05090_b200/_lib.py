@@ -40,7 +40,7 @@ class LsArgs(ctypes.Structure):
         ("S", c_void_p), ("P", c_void_p), ("R", c_void_p),
         ("Qs", c_void_p), ("Rinv", c_void_p), ("alpha", c_void_p), ("scratch", c_void_p),
         ("r_crs", c_void_p), ("st", c_void_p), ("trace", c_void_p), ("cache_cols", c_int),
-        ("timeline", c_void_p), ("xbar", c_void_p), ("t_pend", c_void_p), ("t_coef", c_void_p),
+        ("timeline", c_void_p), ("t_pend", c_void_p), ("t_coef", c_void_p),
     ]
 
 

@@ -169,8 +169,6 @@ __global__ void transpose_kernel(const T* __restrict__ src, int64_t lds, T* __re
 constexpr int kLsThreads = 512;
 constexpr int kLsWarps = kLsThreads / 32;
 constexpr int kLsMaxCluster = 16;
-constexpr int kLsMaxGroups = 4;                      // clusters per LS launch
-constexpr int kLsMaxCTAs = kLsMaxCluster * kLsMaxGroups;
 constexpr int kLsRowsPerCta = 96;
 constexpr int kLsChunk = 128;  // rows / outputs per pass of the 2-D helpers (4 per lane)
 constexpr int kLsCpw = 8;      // columns in flight per warp
@@ -220,39 +218,6 @@ __device__ __forceinline__ T warp_multi_reduce(T (&a)[V], int lane) {
 // Per-CTA partial dots of NV vectors with columns [j0, j1) of M over the
 // CTA's nr rows: o[j] = sum_rr M[j*ldm + rr] * v[rr].  Warp per column (8
 // columns in flight), lanes stride the rows, fixed xor-shuffle tree.
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Barrier over the G clusters of one LS launch: a cluster barrier, then the
-// clusters' rank-0 threads meet on a counter in global memory (fences are
-// cumulative, so the cluster's writes published by the first barrier become
-// visible GPU-wide), then a second cluster barrier releases the CTAs.  The
-// generation is read by every CTA at kernel start; it can only change after
-// every cluster - hence every CTA - has arrived once.
-__device__ __forceinline__ void ls_cluster_group_sync(cg::cluster_group& cl, unsigned* bar, int G,
-                                                      unsigned& gen) {
-  cl.sync();
-  if (G > 1) {
-    if (cl.block_rank() == 0 && threadIdx.x == 0) {
-      __threadfence();
-      const unsigned arrived = atomicAdd(bar, 1u);
-      if (arrived == (unsigned)G - 1) {
-        bar[0] = 0u;
-        __threadfence();
-        atomicExch(bar + 1, gen + 1u);
-      } else {
-        while (ld_acquire_u32(bar + 1) == gen) __nanosleep(32);
-      }
-      __threadfence();
-    }
-    gen += 1u;
-    cl.sync();
-  }
-}
-
 // Column j of the CTA's row slice of T: rows cached in shared memory for
 // j < ncache (prefetched while the predecessor kernel ran), global otherwise.
 template <typename T>
@@ -436,16 +401,14 @@ __device__ __noinline__ void ls_matvec(const T* __restrict__ M, int64_t ldm, int
 template <typename T>
 __device__ __noinline__ void ls_gather(const T* part, int64_t stride, int CL, int j0, int j1,
                                        const T* div, T* c) {
-  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+  for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {  // CL <= 16: all loads in flight
+    T v[kLsMaxCluster];
+#pragma unroll
+    for (int q = 0; q < kLsMaxCluster; ++q)
+      v[q] = q < CL ? __ldcg(part + (int64_t)q * stride + j) : T(0);
     T s = T(0);
-    for (int q0 = 0; q0 < CL; q0 += kLsMaxCluster) {  // 16 loads in flight, ascending order
-      T v[kLsMaxCluster];
 #pragma unroll
-      for (int q = 0; q < kLsMaxCluster; ++q)
-        v[q] = q0 + q < CL ? __ldcg(part + (int64_t)(q0 + q) * stride + j) : T(0);
-#pragma unroll
-      for (int q = 0; q < kLsMaxCluster; ++q) if (q0 + q < CL) s += v[q];
-    }
+    for (int q = 0; q < kLsMaxCluster; ++q) if (q < CL) s += v[q];
     c[j] = div ? s / __ldcg(div + j) : s;
   }
 }
@@ -510,13 +473,9 @@ struct LsSmem {
 template <typename T>
 __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   cg::cluster_group cl = cg::this_cluster();
-  // G clusters of CL CTAs; rows and output slices are split over all NT CTAs
-  const int rank = (int)blockIdx.x;
-  const int CL = (int)gridDim.x;  // total CTAs (NT) - every partition below uses it
-  const int G = CL / (int)cl.num_blocks();
-  unsigned* xbar = reinterpret_cast<unsigned*>(a.xbar);
-  unsigned xgen = (G > 1) ? ld_acquire_u32(xbar + 1) : 0u;
-  auto xsync = [&]() { ls_cluster_group_sync(cl, xbar, G, xgen); };
+  const int rank = (int)cl.block_rank();
+  const int CL = (int)cl.num_blocks();
+#define xsync() cl.sync()
   const int k = a.k, cap = a.cap;
   const int ra = (int)(((int64_t)rank * k) / CL);
   const int rb = (int)(((int64_t)(rank + 1) * k) / CL);
@@ -542,9 +501,9 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
 
   const int64_t sA = 2 * (int64_t)cap + 8;     // exchange stride per CTA
   T* scr = reinterpret_cast<T*>(a.scratch);
-  T* XA = scr;                                  // NT x sA
-  T* XB = XA + kLsMaxCTAs * sA;                 // NT x 8
-  T* XR = XB + kLsMaxCTAs * 8;                  // NT x sA
+  T* XA = scr;                                  // CL x sA
+  T* XB = XA + kLsMaxCluster * sA;              // CL x 8
+  T* XR = XB + kLsMaxCluster * 8;               // CL x sA
   T* AL = static_cast<T*>(a.alpha);             // cap: column norms of T
   T* myA = XA + rank * sA;
   T* myB = XB + rank * 8;
@@ -859,6 +818,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   }
   if (tl && rank == 0 && threadIdx.x == 0) tl[5] = gtimer();
 #undef SGS_TR
+#undef xsync
 }
 
 template <typename T>
@@ -868,42 +828,15 @@ static size_t ls_smem_fixed(int k, int cap, int CL) {
 }
 constexpr size_t kLsSmemMax = 227 * 1024;
 
-// Clusters per LS launch: enough that the CTAs' row slices of T (the columns
-// this launch touches) fit a fixed shared-memory budget.  A function of
-// (k, column) only - never of the allocated capacity - so that streaming and
-// batched factorisations partition identically and agree bit for bit.
-static int ls_groups_host(int k, int CL, int col, size_t esize) {
-  static int cap_g = 0;
-  if (cap_g == 0) {
-    // default one cluster: measured on c1, the cross-cluster handshakes cost
-    // more than the extra shared-memory caching of T saves (tools/timeline.py)
-    const char* env = getenv("SGS_LS_GROUPS");
-    int v = env ? atoi(env) : 1;
-    cap_g = v < 1 ? 1 : (v > kLsMaxGroups ? kLsMaxGroups : v);
-  }
-  int G = 1;
-  while (G < cap_g) {
-    const int64_t rm = (k + (int64_t)CL * G - 1) / ((int64_t)CL * G);
-    if ((size_t)rm * (size_t)(col > 0 ? col : 0) * esize <= (size_t)150 * 1024) break;
-    ++G;
-  }
-  return G;
-}
-
 template <typename T>
 static int launch_ls(const sgs_ls_args* a, cudaStream_t s) {
   const int CL = ls_cluster_size_host(a->k);
-  // the column count that fixes the partition: finalize i / fused (i, i+1) use
-  // i, a solve-only launch for column c uses c - 1 (the fused launch's i)
-  const int gcol = a->do_finalize ? a->col_fin : a->col_sol - 1;
-  const int G = ls_groups_host(a->k, CL, gcol, sizeof(T));
-  const int NT = CL * G;
-  const size_t fixed = ls_smem_fixed<T>(a->k, a->cap, NT);
+  const size_t fixed = ls_smem_fixed<T>(a->k, a->cap, CL);
   if (fixed > kLsSmemMax) {
     set_error("ls_step: k=%d cap=%d needs %zu bytes of shared memory", a->k, a->cap, fixed);
     return SGS_EINVAL;
   }
-  const int RM = (a->k + NT - 1) / NT;
+  const int RM = (a->k + CL - 1) / CL;
   const int ncols_t = a->do_finalize ? a->col_fin : 0;  // solve-only: read T once, no cache
   int cache = (int)((kLsSmemMax - fixed) / ((size_t)RM * sizeof(T)));
   if (cache > ncols_t) cache = ncols_t;
@@ -912,8 +845,6 @@ static int launch_ls(const sgs_ls_args* a, cudaStream_t s) {
   sgs_ls_args aa = *a;
   aa.cache_cols = cache;
   {
-    const int64_t sA = 2 * (int64_t)a->cap + 8;
-    aa.xbar = reinterpret_cast<T*>(a->scratch) + 2 * kLsMaxCTAs * sA + kLsMaxCTAs * 8;
     unsigned long long* tlb = debug_timeline();
     const int col = a->do_finalize ? a->col_fin : a->col_sol;
     aa.timeline = tlb ? tlb + (int64_t)col * 16 + (a->do_finalize ? 0 : 3) : nullptr;
@@ -921,7 +852,7 @@ static int launch_ls(const sgs_ls_args* a, cudaStream_t s) {
   auto kern = ls_step_kernel<T>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (CL > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  return check_ex(launch_ex(kern, dim3(NT), dim3(kLsThreads), smem, s, CL, aa), "ls_step_kernel");
+  return check_ex(launch_ex(kern, dim3(CL), dim3(kLsThreads), smem, s, CL, aa), "ls_step_kernel");
 }
 
 }  // namespace sgs
@@ -1024,7 +955,7 @@ static int ls_mode() {  // 0 = single cluster (default), 1 = grid-wide (SGS_LS_M
 extern "C" int64_t sgs_ls_scratch_elems(int k, int cap) {
   (void)k;
   const int64_t sA = 2 * (int64_t)cap + 8;
-  const int64_t cl = 2 * kLsMaxCTAs * sA + kLsMaxCTAs * 8 + 64;
+  const int64_t cl = 2 * kLsMaxCluster * sA + kLsMaxCluster * 8 + 64;
   const int64_t gr = ls_grid_scratch_elems(cap);
   return cl > gr ? cl : gr;
 }
