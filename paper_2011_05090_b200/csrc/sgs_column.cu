@@ -426,9 +426,6 @@ csr_spmv_srht_kernel(int64_t n, const int32_t* __restrict__ rp, const int32_t* _
 
 }  // namespace sgs
 
-// debug timeline row used by the next SpMV launch (set by sgs_debug_timeline_col)
-static int64_t g_timeline_col = 0;
-extern "C" void sgs_debug_timeline_col(int64_t col) { g_timeline_col = col; }
 
 extern "C" int sgs_csr_spmv_srht(int64_t n, const int32_t* row_ptr, const int32_t* col_idx,
                                  const double* vals, const void* x, int x_dtype,
@@ -445,7 +442,7 @@ extern "C" int sgs_csr_spmv_srht(int64_t n, const int32_t* row_ptr, const int32_
   const int64_t nctas = column_ctas(n);
   const size_t smem = (size_t)(pidx(kColT) + 8 + (k > kSpmvBuf ? k : kSpmvBuf)) * sizeof(double) +
                       (size_t)k * sizeof(int32_t);
-  unsigned long long* tlr = debug_timeline() ? debug_timeline() + g_timeline_col * 16 : nullptr;
+  unsigned long long* tlr = debug_timeline_row();
   cudaError_t err;
   if (x_dtype == SGS_F32) {
     auto kern = csr_spmv_srht_kernel<float>;

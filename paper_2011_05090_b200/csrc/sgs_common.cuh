@@ -100,6 +100,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 unsigned long long* debug_timeline();
+// row of the debug timeline for the current step (sgs_debug_timeline_col), NULL when off
+unsigned long long* debug_timeline_row();
 
 // cudaLaunchKernelEx wrapper: PDL attribute (when enabled) + optional cluster.
 template <typename... KArgs, typename... Args>

@@ -42,6 +42,22 @@ __device__ __forceinline__ void fwht_pass(double* z, int b0) {
   }
 }
 
+// The passes of fwht_tile that remain once the top bits [B, LOGT) are done:
+// the same 3-bit passes, from bit B down.
+template <int LOGT, int B>
+__device__ __forceinline__ void fwht_tile_from(double* z) {
+  int b0 = B;
+#pragma unroll
+  for (int p = 0; p < (B + 2) / 3; ++p) {
+    const int nb = (b0 >= 3) ? 3 : b0;
+    b0 -= nb;
+    if (nb == 3) fwht_pass<LOGT, 3>(z, b0);
+    else if (nb == 2) fwht_pass<LOGT, 2>(z, b0);
+    else fwht_pass<LOGT, 1>(z, b0);
+    __syncthreads();
+  }
+}
+
 template <int LOGT>
 __device__ __forceinline__ void fwht_tile(double* z) {
   // passes of 3 bits from the top down (any bit order gives the transform)

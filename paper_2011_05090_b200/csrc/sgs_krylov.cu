@@ -20,7 +20,11 @@ void set_error(const char* fmt, ...) {
 }
 
 static unsigned long long* g_timeline = nullptr;
+static int64_t g_timeline_col = 0;
 unsigned long long* debug_timeline() { return g_timeline; }
+unsigned long long* debug_timeline_row() {
+  return g_timeline ? g_timeline + g_timeline_col * 16 : nullptr;
+}
 
 bool pdl_enabled() {
   static int v = -1;
@@ -50,26 +54,32 @@ __global__ void __launch_bounds__(256)
 csr_spmv_kernel(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                 const double* __restrict__ vals, const TX* __restrict__ x,
                 const double* __restrict__ xdiv, const double* __restrict__ alpha,
-                double* __restrict__ y, const sgs_status* st) {
+                double* __restrict__ y, const sgs_status* st, unsigned long long* tl) {
   pdl_enter();
   if (status_stopped(st)) return;
+  if (tl && threadIdx.x == 0) atomicMin(tl + 9, gtimer());
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  const int b = __ldg(rp + r), e = __ldg(rp + r + 1);
-  double acc = 0.0;
-  if (xdiv) {
-    const double dv = __ldg(xdiv);
-    for (int q = b; q < e; ++q) {
-      const TX xr = __ldg(x + __ldg(ci + q));
-      TX xn;
-      if constexpr (sizeof(TX) == 4) xn = __double2float_rn((double)xr / dv);
-      else xn = (TX)((double)xr / dv);
-      acc = fma(__ldg(vals + q), (double)xn, acc);
+  if (r < n) {
+    const int b = __ldg(rp + r), e = __ldg(rp + r + 1);
+    double acc = 0.0;
+    if (xdiv) {
+      const double dv = __ldg(xdiv);
+      for (int q = b; q < e; ++q) {
+        const TX xr = __ldg(x + __ldg(ci + q));
+        TX xn;
+        if constexpr (sizeof(TX) == 4) xn = __double2float_rn((double)xr / dv);
+        else xn = (TX)((double)xr / dv);
+        acc = fma(__ldg(vals + q), (double)xn, acc);
+      }
+    } else {
+      for (int q = b; q < e; ++q) acc = fma(__ldg(vals + q), (double)__ldg(x + __ldg(ci + q)), acc);
     }
-  } else {
-    for (int q = b; q < e; ++q) acc = fma(__ldg(vals + q), (double)__ldg(x + __ldg(ci + q)), acc);
+    y[r] = alpha ? acc / __ldg(alpha) : acc;
   }
-  y[r] = alpha ? acc / __ldg(alpha) : acc;
+  if (tl) {
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(tl + 10, gtimer());
+  }
 }
 
 constexpr int kNormBlocks = 296;
@@ -208,6 +218,7 @@ givens_step_kernel(const double* __restrict__ R, int64_t ldr, int i, double* cs,
   if (tl && threadIdx.x == 0) tl[(int64_t)(i + 1) * 16 + 11] = gtimer();
 }
 
+
 __global__ void status_init_kernel(sgs_status* st) {
   st->code = 0;
   st->column = 0;
@@ -236,6 +247,7 @@ extern "C" int sgs_abi_version(void) { return SGS_ABI_VERSION; }
 extern "C" void sgs_debug_timeline(void* buf) {
   g_timeline = static_cast<unsigned long long*>(buf);
 }
+extern "C" void sgs_debug_timeline_col(int64_t col) { g_timeline_col = col; }
 extern "C" const char* sgs_last_error(void) { return g_err; }
 extern "C" uint64_t sgs_launch_count(void) { return g_launches.load(); }
 
@@ -262,10 +274,12 @@ extern "C" int sgs_csr_spmv(int64_t n, const int32_t* row_ptr, const int32_t* co
   const unsigned blocks = (unsigned)((n + 255) / 256);
   if (x_dtype == SGS_F32)
     return check_ex(launch_ex(csr_spmv_kernel<float>, dim3(blocks), dim3(256), 0, s, 1, n, row_ptr,
-                              col_idx, vals, static_cast<const float*>(x), xdiv, alpha, y, st),
+                              col_idx, vals, static_cast<const float*>(x), xdiv, alpha, y, st,
+                              debug_timeline_row()),
                     "csr_spmv_kernel");
   return check_ex(launch_ex(csr_spmv_kernel<double>, dim3(blocks), dim3(256), 0, s, 1, n, row_ptr,
-                            col_idx, vals, static_cast<const double*>(x), xdiv, alpha, y, st),
+                            col_idx, vals, static_cast<const double*>(x), xdiv, alpha, y, st,
+                            debug_timeline_row()),
                   "csr_spmv_kernel");
 }
 

@@ -32,16 +32,21 @@ constexpr int kSrhtCluster = 8;    // CTAs whose k-vector partials are combined 
 // signed sampled entries into a shared k-vector; the 8 CTAs of a cluster then
 // sum their k-vectors through distributed shared memory in rank order, each
 // CTA writing 1/8 of the group partial.  Output: one k-vector per cluster.
+// fp32 inputs (the batched P = Theta W of c1/c4: many columns, many waves):
+// 4 CTAs per SM (32 registers) raises throughput; fp64 inputs keep 40
+// registers - at 32 the spills cost c3's single-column sketch of w more than
+// the extra residency gains (measured both ways).
 template <typename TX, int LOGT>
-__global__ void __launch_bounds__(kSrhtThreads)
+__global__ void __launch_bounds__(kSrhtThreads, sizeof(TX) == 4 ? 4 : 3)
 srht_partials_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local,
                      int64_t row0, int log2_block, const uint32_t* __restrict__ sign_bits,
                      const int32_t* __restrict__ samples, int k, int tiles_per_cta,
                      int64_t ntiles, double* __restrict__ partials,
-                     const sgs_status* st) {
+                     const sgs_status* st, unsigned long long* tl) {
   cg::cluster_group cl = cg::this_cluster();
   pdl_enter();
   if (status_stopped(st)) return;  // uniform across the cluster: nobody writes st here
+  if (tl && threadIdx.x == 0) atomicMin(tl + 12, gtimer());
   constexpr int T = 1 << LOGT;
   extern __shared__ double smem[];
   double* z = smem;                       // pidx(T) entries
@@ -68,18 +73,48 @@ srht_partials_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local,
       for (int j = threadIdx.x; j < k; j += blockDim.x) smp[j] = __ldg(sb + j);
       cur_blk = blk;
     }
-    for (int e = threadIdx.x; e < T; e += blockDim.x) {
-      const int64_t lr = lr0 + e;
-      double v = 0.0;
-      if (lr < n_local) {
-        v = load_as_double(x + lr);
-        const uint32_t word = __ldg(sign_bits + (lr >> 5));
-        if (((word >> (lr & 31)) & 1u) == 0u) v = -v;
+    bool staged = false;
+    if constexpr (LOGT == 12) {
+      if (blockDim.x == kSrhtThreads) {
+      staged = true;
+      // 8 elements per thread, strided by 512: all loads in flight at once, and
+      // the 8 values differ exactly in the top 3 bits, so fwht_tile's first
+      // radix-8 pass runs in registers (same butterflies, same order).
+      constexpr int Q = 8;
+      double v[Q];
+      uint32_t wd[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int64_t lr = lr0 + threadIdx.x + q * kSrhtThreads;
+        v[q] = lr < n_local ? load_as_double(x + lr) : 0.0;
+        wd[q] = lr < n_local ? __ldg(sign_bits + (lr >> 5)) : 1u;
       }
-      z[pidx(e)] = v;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int64_t lr = lr0 + threadIdx.x + q * kSrhtThreads;
+        if (((wd[q] >> (lr & 31)) & 1u) == 0u) v[q] = -v[q];
+      }
+      fwht_reg<3>(v);
+#pragma unroll
+      for (int q = 0; q < Q; ++q) z[pidx(threadIdx.x + q * kSrhtThreads)] = v[q];
+      __syncthreads();
+      fwht_tile_from<LOGT, LOGT - 3>(z);
+      }
     }
-    __syncthreads();
-    fwht_tile<LOGT>(z);
+    if (!staged) {
+      for (int e = threadIdx.x; e < T; e += blockDim.x) {
+        const int64_t lr = lr0 + e;
+        double v = 0.0;
+        if (lr < n_local) {
+          v = load_as_double(x + lr);
+          const uint32_t word = __ldg(sign_bits + (lr >> 5));
+          if (((word >> (lr & 31)) & 1u) == 0u) v = -v;
+        }
+        z[pidx(e)] = v;
+      }
+      __syncthreads();
+      fwht_tile<LOGT>(z);
+    }
     for (int j = threadIdx.x; j < k; j += blockDim.x) {
       const int32_t r = smp[j];
       const double v = z[pidx(r & (T - 1))];
@@ -98,6 +133,7 @@ srht_partials_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local,
     for (int q = 0; q < kSrhtCluster; ++q) s += cl.map_shared_rank(part, q)[j];
     out[j] = s;
   }
+  if (tl && threadIdx.x == 0) atomicMax(tl + 13, gtimer());
   cl.sync();  // keep shared memory alive until every CTA has read it
 }
 
@@ -126,13 +162,15 @@ static int launch_srht_t(const void* X, int64_t ldx, int ncols, int64_t n_local,
   if (smem > 48 * 1024) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
   int threads = kSrhtThreads;
   if (T / 8 < threads) threads = (T / 8 < 64) ? 64 : T / 8;
   if (threads < 256 && k > 1024) threads = 256;
   dim3 grid(nctas, ncols);
   return check_ex(launch_ex(kern, grid, dim3(threads), smem, s, kSrhtCluster,
                             static_cast<const TX*>(X), ldx, n_local, row0, log2_block, sign_bits,
-                            samples, k, tpc, ntiles, partials, st),
+                            samples, k, tpc, ntiles, partials, st, debug_timeline_row()),
                   "srht_partials_kernel");
 }
 

@@ -20,6 +20,7 @@ tl = torch.zeros((m + 3, 16), dtype=torch.int64, device="cuda")
 tl[:, 0] = 2**62
 tl[:, 1] = 2**62
 tl[:, 9] = 2**62
+tl[:, 12] = 2**62
 lib = _lib.load()
 orig = kr._ArnoldiEngine.step
 
@@ -44,10 +45,11 @@ for r in range(3, m - 1):
     giv_done = t[r, 11]
     period = t[r + 1, 9] - t[r, 9]
     gaps = period - spmv - solve - col - fin
-    rows.append((spmv, solve, col, fin, t[r, 7] - t[r, 10], t[r, 1] - t[r, 8], t[r, 4] - t[r, 2],
-                 t[r + 1, 9] - t[r, 5], period))
-names = ["spmv", "ls_solve", "column", "ls_fin", "spmv->solve", "solve->col", "col->fin",
-         "fin->next_spmv", "period"]
+    srht = t[r, 13] - t[r, 12]
+    rows.append((spmv, srht, solve, col, fin, t[r, 12] - t[r, 10], t[r, 7] - t[r, 13],
+                 t[r, 1] - t[r, 8], t[r, 4] - t[r, 2], t[r + 1, 9] - t[r, 5], period))
+names = ["spmv", "srht", "ls_solve", "column", "ls_fin", "spmv->srht", "srht->solve",
+         "solve->col", "col->fin", "fin->next_spmv(givens)", "period"]
 a = np.array(rows)
 out = {f"q{q}": dict(zip(names, [round(float(x), 2) for x in p.mean(0)]))
        for q, p in enumerate(np.array_split(a, 4))}
