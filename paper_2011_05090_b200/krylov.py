@@ -331,10 +331,10 @@ def _operator_norm_estimate(A: SparseMatrix, ws: _Workspace, iters: int = 20,
 class _ArnoldiEngine:
     """Device Arnoldi driver over an RgsState (one stream, no per-step sync).
 
-    With an SRHT sketch on 4096-row tiles a step is five launches: the fused
-    SpMV (x = q'_i / r_ii formed on the fly, 1/alpha, SRHT of w in the
-    epilogue), the LS solve, the fused column kernel (which normalises q'_i in
-    place and sketches q'_{i+1}), the LS finalize and the Givens update.
+    With an SRHT sketch on 4096-row tiles a step is: the in-place
+    normalisation q_i = q'_i / r_ii, the SpMV (1/alpha folded in), the SRHT of
+    w, the LS solve, the fused column kernel (update + sketch of q'_{i+1}), the
+    LS finalize and the Givens update.
     Otherwise the generic path (separate SpMV, sketch and normalisation)."""
 
     def __init__(self, A: SparseMatrix, theta, policy, solver, m: int,
@@ -379,13 +379,16 @@ class _ArnoldiEngine:
         st = self.state
         A, ws = self.A, self.ws
         if self.fused:
-            rii = st._R.data_ptr() + (i * st._cap + i) * 8
+            # q_i = cast(q'_i / r_ii) once, in place (one division per entry
+            # instead of one per stored nonzero in the SpMV); the column kernel
+            # then has no previous column left to normalise
+            st._normalize(i)
             _eff_matvec_into(A, self.M, ws, st._qcol_ptr(i), st.ccode, ws.w, alpha=alpha,
-                             status=st.status, xdiv_ptr=rii)
+                             status=st.status)
             pp, pn, ps = st._sketch_parts(ws.w.data_ptr(), _lib.SGS_F64, A.n, st._parts_p, None)
             st._phi_w(i + 1, ws.w.data_ptr(), _lib.SGS_F64, A.n)
             st._ls(sol=i + 1, p_parts=pp, p_nparts=pn, p_scale=ps)
-            sp, sn, ss = st._column(i + 1, ws.w.data_ptr(), _lib.SGS_F64, True, True)
+            sp, sn, ss = st._column(i + 1, ws.w.data_ptr(), _lib.SGS_F64, False, True)
             phq = st._phi_q_parts(i + 1)
             st._ls(fin=i + 1, s_parts=sp, s_nparts=sn, s_scale=ss)
             st._phi_q_finish(i + 1, phq)
@@ -418,8 +421,9 @@ class _ArnoldiEngine:
                     if int(hb0[0]) != 0:
                         break
         out = st._sync_status()
-        # fused path: the newest committed column is still q'/r_ii unless the
-        # stop was a breakdown (then the column kernel already normalised it)
+        # fused path: the newest committed column is still q'/r_ii (its step's
+        # normalisation never ran, or returned on the stop code) unless the stop
+        # was a breakdown (then that column is the previous step's, normalised)
         if self.fused and out["ncols"] > 0 and out["code"] not in (_lib.ST_BREAKDOWN,
                                                                    _lib.ST_NONFINITE):
             st._normalize(out["ncols"] - 1, guarded=False)
