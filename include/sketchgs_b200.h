@@ -259,6 +259,18 @@ int sgs_givens_step(const double* R, int64_t ldr, int i, double* cs,
                     double* sn, double* g, double* T, int64_t ldt,
                     double* hist, double tol, sgs_status* st, void* stream);
 
+/* Head of one RGMRES step (fused engine): normalise basis column `col` of Q
+ * in place, q = cast(q' / R[col][col]) as RgsState.push step 7
+ * (gram_schmidt.py:330-332), with all blocks but one, and - when gi >= 0 -
+ * the progressive Givens update of step gi (as sgs_givens_step) with the
+ * remaining block, concurrently.  The normalisation does not consult st (the
+ * Givens update may set CONVERGED meanwhile); *norm_flag = col records it.
+ * col < 0: Givens only. */
+int sgs_arnoldi_head(void* Q, int q_dtype, int64_t ldq, int64_t n, int col, const double* R,
+                     int64_t ldr, int* norm_flag, int gi, double* cs, double* sn, double* g,
+                     double* T, int64_t ldt, double* hist, double tol, sgs_status* st,
+                     void* stream);
+
 /* Column-major transpose for staging host row-major inputs:
  * dst[c*ldd + r] = src[r*lds + c], r < rows, c < cols. */
 int sgs_transpose(const void* src, int64_t lds, void* dst, int64_t ldd,

@@ -94,6 +94,9 @@ _SIGS = {
     "sgs_power_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
     "sgs_givens_step": (c_int, [c_void_p, c_int64, c_int, c_void_p, c_void_p, c_void_p,
                                 c_void_p, c_int64, c_void_p, c_double, c_void_p, c_void_p]),
+    "sgs_arnoldi_head": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_void_p, c_int64,
+                                 c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
+                                 c_int64, c_void_p, c_double, c_void_p, c_void_p]),
     "sgs_transpose": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_int,
                               c_void_p]),
     "sgs_ilu0_analysis_work_elems": (c_int64, [c_int64]),

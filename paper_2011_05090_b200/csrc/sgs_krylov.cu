@@ -166,12 +166,11 @@ __global__ void cos_init_kernel(double* v, int64_t n) {
 // memory.  Products and sums are not contracted so the arithmetic matches
 // numpy's scalar expressions.
 constexpr int kGivMax = 4096;
-__global__ void __launch_bounds__(256)
-givens_step_kernel(const double* __restrict__ R, int64_t ldr, int i, double* cs, double* sn,
-                   double* g, double* T, int64_t ldt, double* hist, double tol, sgs_status* st,
-                   unsigned long long* tl) {
-  pdl_enter();
-  if (status_stopped(st)) return;
+// One progressive Givens update by the calling block (all its threads).
+__device__ __forceinline__ void givens_update(const double* __restrict__ R, int64_t ldr, int i,
+                                              double* cs, double* sn, double* g, double* T,
+                                              int64_t ldt, double* hist, double tol,
+                                              sgs_status* st, unsigned long long* tl) {
   extern __shared__ double gsm[];
   double* h = gsm;            // i + 2
   double* c_s = gsm + i + 2;  // i
@@ -216,6 +215,41 @@ givens_step_kernel(const double* __restrict__ R, int64_t ldr, int i, double* cs,
   double* Tc = T + (int64_t)i * ldt;
   for (int j = threadIdx.x; j < i + 2; j += blockDim.x) Tc[j] = h[j];
   if (tl && threadIdx.x == 0) tl[(int64_t)(i + 1) * 16 + 11] = gtimer();
+}
+
+__global__ void __launch_bounds__(256)
+givens_step_kernel(const double* __restrict__ R, int64_t ldr, int i, double* cs, double* sn,
+                   double* g, double* T, int64_t ldt, double* hist, double tol, sgs_status* st,
+                   unsigned long long* tl) {
+  pdl_enter();
+  if (status_stopped(st)) return;
+  givens_update(R, ldr, i, cs, sn, g, T, ldt, hist, tol, st, tl);
+}
+
+// Head of an RGMRES step: the last block performs the Givens update of step
+// gi (if gi >= 0) while all other blocks normalise basis column `col` in
+// place.  The normalising blocks ignore the status block on purpose - the
+// Givens update may set CONVERGED concurrently, and a partly normalised
+// column must never happen; *norm_flag = col records what was normalised.
+template <typename TQ>
+__global__ void __launch_bounds__(256)
+arnoldi_head_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int col, int* norm_flag, int gi,
+                    const double* __restrict__ R, int64_t ldr, double* cs, double* sn, double* g,
+                    double* T, int64_t ldt, double* hist, double tol, sgs_status* st,
+                    unsigned long long* tl) {
+  pdl_enter();
+  if (gi >= 0 && blockIdx.x == gridDim.x - 1) {
+    if (!status_stopped(st)) givens_update(R, ldr, gi, cs, sn, g, T, ldt, hist, tol, st, tl);
+    return;
+  }
+  if (col < 0) return;
+  const int nb = gridDim.x - (gi >= 0 ? 1 : 0);
+  const double rjj = R[(int64_t)col * ldr + col];
+  TQ* q = Q + (int64_t)col * ldq;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)nb * blockDim.x)
+    q[r] = cvt<TQ>((double)q[r] / rjj);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *norm_flag = col;
 }
 
 
@@ -352,6 +386,35 @@ extern "C" int sgs_power_step(const double* w, const double* nrm, double* v, dou
   if (rc) return rc;
   power_step_kernel<<<grid_for(n), 256, 0, s>>>(w, nrm, v, sigma, n);
   return check_launch("power_step_kernel");
+}
+
+extern "C" int sgs_arnoldi_head(void* Q, int q_dtype, int64_t ldq, int64_t n, int col,
+                                const double* R, int64_t ldr, int* norm_flag, int gi, double* cs,
+                                double* sn, double* g, double* T, int64_t ldt, double* hist,
+                                double tol, sgs_status* st, void* stream) {
+  SGS_REQUIRE(R && st && n >= 1 && (col < 0 || (Q && norm_flag && ldq >= n && col < ldr)),
+              "arnoldi_head: bad args");
+  SGS_REQUIRE(gi < 0 || (cs && sn && g && T && hist && ldr >= gi + 2 && ldt >= gi + 2 &&
+                         gi + 2 <= kGivMax),
+              "arnoldi_head: bad Givens args");
+  const size_t smem = gi >= 0 ? (size_t)(3 * gi + 2) * sizeof(double) : 0;
+  const unsigned nb = (col >= 0 ? grid_for(n) : 0) + (gi >= 0 ? 1 : 0);
+  if (nb == 0) return SGS_OK;
+  cudaStream_t s = as_stream(stream);
+  if (q_dtype == SGS_F32) {
+    auto kern = arnoldi_head_kernel<float>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return check_ex(launch_ex(kern, dim3(nb), dim3(256), smem, s, 1, static_cast<float*>(Q), ldq, n,
+                              col, norm_flag, gi, R, ldr, cs, sn, g, T, ldt, hist, tol, st,
+                              debug_timeline()),
+                    "arnoldi_head_kernel");
+  }
+  auto kern = arnoldi_head_kernel<double>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return check_ex(launch_ex(kern, dim3(nb), dim3(256), smem, s, 1, static_cast<double*>(Q), ldq, n,
+                            col, norm_flag, gi, R, ldr, cs, sn, g, T, ldt, hist, tol, st,
+                            debug_timeline()),
+                  "arnoldi_head_kernel");
 }
 
 extern "C" int sgs_givens_step(const double* R, int64_t ldr, int i, double* cs, double* sn,

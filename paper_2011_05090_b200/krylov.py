@@ -331,10 +331,10 @@ def _operator_norm_estimate(A: SparseMatrix, ws: _Workspace, iters: int = 20,
 class _ArnoldiEngine:
     """Device Arnoldi driver over an RgsState (one stream, no per-step sync).
 
-    With an SRHT sketch on 4096-row tiles a step is: the in-place
-    normalisation q_i = q'_i / r_ii, the SpMV (1/alpha folded in), the SRHT of
-    w, the LS solve, the fused column kernel (update + sketch of q'_{i+1}), the
-    LS finalize and the Givens update.
+    With an SRHT sketch on 4096-row tiles a step is: the head (in-place
+    normalisation q_i = q'_i / r_ii together with the previous step's Givens
+    update), the SpMV (1/alpha folded in), the SRHT of w, the LS solve, the
+    fused column kernel (update + sketch of q'_{i+1}) and the LS finalize.
     Otherwise the generic path (separate SpMV, sketch and normalisation)."""
 
     def __init__(self, A: SparseMatrix, theta, policy, solver, m: int,
@@ -355,6 +355,8 @@ class _ArnoldiEngine:
         self.g = torch.zeros(m + 2, dtype=torch.float64, device=dev)
         self.T = torch.zeros((m + 1, m + 2), dtype=torch.float64, device=dev)  # T[i] = column i
         self.hist = torch.zeros(m + 1, dtype=torch.float64, device=dev)
+        self.norm_flag = torch.full((1,), -1, dtype=torch.int32, device=dev)
+        self._owed = None  # step whose Givens update rides on the next step's head
 
     def start(self, b_dev: torch.Tensor, b_norm_ptr) -> None:
         """Push b (divided by ||b|| when b_norm_ptr is given) as column 0."""
@@ -379,10 +381,17 @@ class _ArnoldiEngine:
         st = self.state
         A, ws = self.A, self.ws
         if self.fused:
-            # q_i = cast(q'_i / r_ii) once, in place (one division per entry
-            # instead of one per stored nonzero in the SpMV); the column kernel
-            # then has no previous column left to normalise
-            st._normalize(i)
+            # step head: q_i = cast(q'_i / r_ii) once, in place (one division per
+            # entry instead of one per stored nonzero in the SpMV; the column
+            # kernel then has no previous column left to normalise), and the
+            # Givens update of step i-1 in the same launch (sgs_arnoldi_head)
+            gi = -1 if self._owed is None else self._owed
+            self._owed = None
+            call("sgs_arnoldi_head", st._Q.data_ptr(), st.ccode, st.ldq, A.n, i,
+                 st._R.data_ptr(), st._cap, self.norm_flag.data_ptr(), gi, self.cs.data_ptr(),
+                 self.sn.data_ptr(), self.g.data_ptr(), self.T.data_ptr(), self.T.shape[1],
+                 self.hist.data_ptr(), -1.0 if tol is None else float(tol), st.status.ptr,
+                 stream_ptr())
             _eff_matvec_into(A, self.M, ws, st._qcol_ptr(i), st.ccode, ws.w, alpha=alpha,
                              status=st.status)
             pp, pn, ps = st._sketch_parts(ws.w.data_ptr(), _lib.SGS_F64, A.n, st._parts_p, None)
@@ -398,10 +407,17 @@ class _ArnoldiEngine:
                              status=st.status)
             st._push_async(ws.w)
         if tol is not None or alpha is not None:
-            call("sgs_givens_step", st._R.data_ptr(), st._cap, i, self.cs.data_ptr(),
-                 self.sn.data_ptr(), self.g.data_ptr(), self.T.data_ptr(), self.T.shape[1],
-                 self.hist.data_ptr(), -1.0 if tol is None else float(tol), st.status.ptr,
-                 stream_ptr())
+            if self.fused:
+                self._owed = i
+            else:
+                self._givens(i, tol)
+
+    def _givens(self, i: int, tol: float | None) -> None:
+        st = self.state
+        call("sgs_givens_step", st._R.data_ptr(), st._cap, i, self.cs.data_ptr(),
+             self.sn.data_ptr(), self.g.data_ptr(), self.T.data_ptr(), self.T.shape[1],
+             self.hist.data_ptr(), -1.0 if tol is None else float(tol), st.status.ptr,
+             stream_ptr())
 
     def run(self, alpha, tol) -> dict:
         """Steps 0..m-1 with periodic status polls; returns the final status."""
@@ -420,12 +436,14 @@ class _ArnoldiEngine:
                     ev0.synchronize()
                     if int(hb0[0]) != 0:
                         break
+        if self._owed is not None:  # the last step's Givens update (no head follows)
+            self._givens(self._owed, tol)
+            self._owed = None
         out = st._sync_status()
-        # fused path: the newest committed column is still q'/r_ii (its step's
-        # normalisation never ran, or returned on the stop code) unless the stop
-        # was a breakdown (then that column is the previous step's, normalised)
-        if self.fused and out["ncols"] > 0 and out["code"] not in (_lib.ST_BREAKDOWN,
-                                                                   _lib.ST_NONFINITE):
+        # fused path: columns are normalised by the step heads; the newest
+        # committed one is still q'/r_ii unless a head (run after a stop, or a
+        # breakdown that left the previous column newest) already covered it
+        if self.fused and out["ncols"] > 0 and int(self.norm_flag) < out["ncols"] - 1:
             st._normalize(out["ncols"] - 1, guarded=False)
         return out
 
