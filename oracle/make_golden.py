@@ -67,13 +67,40 @@ def ilu_fixtures(sg):
     np.savez_compressed(os.path.join(OUT, "ilu.npz"), **d)
 
 
+def cert_fixtures(sg):
+    """omega_bar / epsilon_of / certify_factorization (certification.py, sketch.py:213-228)."""
+    d = {}
+    n, dcols = 1024, 8
+    theta = sg.make_sketch(sg.SketchKind.PSRHT, 96, n, seed=3)
+    rng = np.random.default_rng(2024)
+    for t in range(3):
+        V = rng.standard_normal((n, dcols))
+        phi = sg.make_certification_sketch(
+            sg.CertificationParams(eps_star=0.25, delta_star=1e-3, phi_seed=t), n)
+        Vt, Vp = theta.apply_block(V), phi.apply_block(V)
+        d[f"V{t}"], d[f"Vt{t}"], d[f"Vp{t}"] = V, Vt, Vp
+        d[f"ob{t}"] = sg.omega_bar(Vt, Vp, 0.25)
+        d[f"om{t}"] = sg.epsilon_of(theta, V)
+    W = rng.standard_normal((n, 10))
+    th = sg.make_sketch(sg.SketchKind.PSRHT, 128, n, seed=0)
+    phi = sg.make_certification_sketch(sg.CertificationParams(eps_star=0.25), n)
+    f, _ = sg.rgs_factorize(W, th, sg.UNIFIED64, phi=phi)
+    res = sg.certify_factorization(f, eps_star=0.25, u_crs=sg.UNIFIED64.u_crs)
+    d.update({"cf_W": W, "cf_S": f.S, "cf_Sphi": f.S_phi, "cf_P": f.P, "cf_Pphi": f.P_phi,
+              "cf_Q": f.Q, "cf_obq": res.omega_bar_q, "cf_obw": res.omega_bar_w,
+              "cf_mq": res.margin_q, "cf_mw": res.margin_w})
+    d["eps_inv"] = np.array([sg.eps_star_for_dim(sg.vector_certificate_dim(e, 1e-3), 1e-3)
+                             for e in (0.05, 0.1, 0.25, 0.5)])
+    np.savez_compressed(os.path.join(OUT, "cert.npz"), **d)
+
+
 def main(only=None):
     sys.path.insert(0, REF)
     import sketchgs as sg
-    if only == "ilu":
+    if only in ("ilu", "cert"):
         os.makedirs(OUT, exist_ok=True)
-        ilu_fixtures(sg)
-        print("ilu fixtures written to", os.path.abspath(OUT))
+        (ilu_fixtures if only == "ilu" else cert_fixtures)(sg)
+        print(only, "fixtures written to", os.path.abspath(OUT))
         return
     sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
     from paper_2011_05090_b200.workloads import make_w, convdiff3d, rhs_gaussian
@@ -184,6 +211,7 @@ def main(only=None):
               "cd_hist": r3.residual_history})
     np.savez_compressed(os.path.join(OUT, "krylov.npz"), **d)
     ilu_fixtures(sg)
+    cert_fixtures(sg)
     print("golden fixtures written to", os.path.abspath(OUT))
 
 

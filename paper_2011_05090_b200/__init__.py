@@ -16,6 +16,10 @@ from .gram_schmidt import (BREAKDOWN_FACTOR, HOUSEHOLDER_QR, BreakdownError, GsV
                            loss_of_orthogonality, rgs_factorize)
 from .krylov import (ArnoldiDecomposition, GmresResult, Ilu0Preconditioner, RestartedResult,
                      SparseMatrix, arnoldi, gmres, gmres_restarted, ilu0)
+from .certification import (CertificationParams, CertificationResult, EmbeddingParams,
+                            certify_factorization, epsilon_of, eps_star_for_dim,
+                            make_certification_sketch, omega_bar, omega_bar_sharpness,
+                            required_sketch_dim, rounding_sketch_trial, vector_certificate_dim)
 
 __version__ = "0.1.0"
 
@@ -26,5 +30,8 @@ __all__ = [
     "LsqSolver", "QrFactors", "RgsState", "StabilityCertificate", "certificates",
     "loss_of_orthogonality", "rgs_factorize", "ArnoldiDecomposition", "GmresResult",
     "RestartedResult", "SparseMatrix", "Ilu0Preconditioner", "ilu0", "arnoldi", "gmres",
-    "gmres_restarted",
+    "gmres_restarted", "CertificationParams", "CertificationResult", "EmbeddingParams",
+    "certify_factorization", "epsilon_of", "eps_star_for_dim", "make_certification_sketch",
+    "omega_bar", "omega_bar_sharpness", "required_sketch_dim", "rounding_sketch_trial",
+    "vector_certificate_dim",
 ]

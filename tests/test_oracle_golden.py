@@ -131,3 +131,30 @@ def test_oracle_preconditioned_gmres_matches_reference():
                         precond=pre2)
     assert out2["iterations"] == int(g["pr_its"])
     assert np.array_equal(out2["x"], g["pr_x"])
+
+
+def test_oracle_certification_matches_reference():
+    from oracle import oracle_certify, oracle_epsilon_of, oracle_omega_bar
+    g = golden("cert.npz")
+    th = OracleSketch("psrht", 96, 1024, 3)
+    for t in range(3):
+        assert oracle_omega_bar(g[f"Vt{t}"], g[f"Vp{t}"], 0.25) == float(g[f"ob{t}"])
+        assert oracle_epsilon_of(th, g[f"V{t}"]) == float(g[f"om{t}"])
+    r = oracle_certify(g["cf_S"], g["cf_Sphi"], g["cf_P"], g["cf_Pphi"], 0.25, 2.0 ** -53)
+    assert r["omega_bar_q"] == float(g["cf_obq"]) and r["omega_bar_w"] == float(g["cf_obw"])
+    assert r["margin_q"] == float(g["cf_mq"]) and r["margin_w"] == float(g["cf_mw"])
+
+
+def test_sizing_helpers_match_reference():
+    # host arithmetic of the package (no device work)
+    import paper_2011_05090_b200 as sg
+    g = golden("cert.npz")
+    got = [sg.eps_star_for_dim(sg.vector_certificate_dim(e, 1e-3), 1e-3)
+           for e in (0.05, 0.1, 0.25, 0.5)]
+    assert np.array_equal(np.array(got), g["eps_inv"])
+    assert sg.vector_certificate_dim(0.25, 1e-3) == 584  # reference test_certification.py:13
+    assert sg.CertificationParams(k_phi=100).dimension() == 100
+    with pytest.raises(ValueError):
+        sg.eps_star_for_dim(1, 1e-3)
+    with pytest.raises(ValueError):
+        sg.EmbeddingParams(1.5, 0.1, 3)
