@@ -32,12 +32,11 @@ constexpr int kSrhtCluster = 8;    // CTAs whose k-vector partials are combined 
 // signed sampled entries into a shared k-vector; the 8 CTAs of a cluster then
 // sum their k-vectors through distributed shared memory in rank order, each
 // CTA writing 1/8 of the group partial.  Output: one k-vector per cluster.
-// fp32 inputs (the batched P = Theta W of c1/c4: many columns, many waves):
-// 4 CTAs per SM (32 registers) raises throughput; fp64 inputs keep 40
-// registers - at 32 the spills cost c3's single-column sketch of w more than
-// the extra residency gains (measured both ways).
+// 4 CTAs per SM (32 registers, the tile's sign words staged in shared memory
+// instead of registers): c3's 512-tile sketch of w runs in one wave of 592
+// slots instead of 444 + 68, and the batched P = Theta W gains residency.
 template <typename TX, int LOGT>
-__global__ void __launch_bounds__(kSrhtThreads, sizeof(TX) == 4 ? 4 : 3)
+__global__ void __launch_bounds__(kSrhtThreads, 4)
 srht_partials_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local,
                      int64_t row0, int log2_block, const uint32_t* __restrict__ sign_bits,
                      const int32_t* __restrict__ samples, int k, int tiles_per_cta,
@@ -52,6 +51,7 @@ srht_partials_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local,
   double* z = smem;                       // pidx(T) entries
   double* part = smem + pidx(T) + 8;      // k entries
   int32_t* smp = reinterpret_cast<int32_t*>(part + k);  // k entries
+  uint32_t* sgn = reinterpret_cast<uint32_t*>(smp + k);  // T / 32 sign words (staged path)
   const int col = blockIdx.y;
   const int ngroups = gridDim.x / kSrhtCluster;
   const TX* x = X + (int64_t)col * ldx;
@@ -81,18 +81,23 @@ srht_partials_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local,
       // the 8 values differ exactly in the top 3 bits, so fwht_tile's first
       // radix-8 pass runs in registers (same butterflies, same order).
       constexpr int Q = 8;
+      // the tile's 128 sign words once into shared memory (lr0 is a multiple
+      // of 4096, so word w of the tile covers rows lr0 + 32 w .. + 31)
+      if (threadIdx.x < T / 32) {
+        const int64_t lw = lr0 + 32 * (int64_t)threadIdx.x;
+        sgn[threadIdx.x] = lw < n_local ? __ldg(sign_bits + (lw >> 5)) : ~0u;
+      }
       double v[Q];
-      uint32_t wd[Q];
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
         const int64_t lr = lr0 + threadIdx.x + q * kSrhtThreads;
         v[q] = lr < n_local ? load_as_double(x + lr) : 0.0;
-        wd[q] = lr < n_local ? __ldg(sign_bits + (lr >> 5)) : 1u;
       }
+      __syncthreads();
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
-        const int64_t lr = lr0 + threadIdx.x + q * kSrhtThreads;
-        if (((wd[q] >> (lr & 31)) & 1u) == 0u) v[q] = -v[q];
+        const int e = threadIdx.x + q * kSrhtThreads;
+        if (((sgn[e >> 5] >> (e & 31)) & 1u) == 0u) v[q] = -v[q];
       }
       fwht_reg<3>(v);
 #pragma unroll
@@ -157,7 +162,8 @@ static int launch_srht_t(const void* X, int64_t ldx, int ncols, int64_t n_local,
                          int k, double* partials, const sgs_status* st, cudaStream_t s,
                          int tpc, int64_t ntiles, int nctas) {
   constexpr int T = 1 << LOGT;
-  const size_t smem = (size_t)(T + T / 8 + 8 + k) * sizeof(double) + (size_t)k * sizeof(int32_t);
+  const size_t smem = (size_t)(T + T / 8 + 8 + k) * sizeof(double) + (size_t)k * sizeof(int32_t) +
+                      (size_t)(T / 32) * sizeof(uint32_t);
   auto kern = srht_partials_kernel<TX, LOGT>;
   if (smem > 48 * 1024) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
