@@ -243,6 +243,8 @@ int sgs_cast_div(const void* src, int src_dtype, void* dst, int dst_dtype,
                  const double* den, int64_t n, void* stream);
 /* v[r] = cos(r + 1): start vector of _operator_norm_estimate (krylov.py:218) */
 int sgs_cos_init(double* v, int64_t n, void* stream);
+/* The same start vector's entries [first, first + n) (a rank's row block). */
+int sgs_cos_init_at(double* v, int64_t n, int64_t first, void* stream);
 
 /* Power-iteration step of _operator_norm_estimate (krylov.py:213-226):
  * given w = A v and ||w|| in nrm[0], sets v = w / ||w|| and sigma[0] = ||w||;

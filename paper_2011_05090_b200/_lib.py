@@ -91,6 +91,7 @@ _SIGS = {
     "sgs_rsub": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "sgs_cast_div": (c_int, [c_void_p, c_int, c_void_p, c_int, c_void_p, c_int64, c_void_p]),
     "sgs_cos_init": (c_int, [c_void_p, c_int64, c_void_p]),
+    "sgs_cos_init_at": (c_int, [c_void_p, c_int64, c_int64, c_void_p]),
     "sgs_power_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
     "sgs_givens_step": (c_int, [c_void_p, c_int64, c_int, c_void_p, c_void_p, c_void_p,
                                 c_void_p, c_int64, c_void_p, c_double, c_void_p, c_void_p]),

@@ -154,10 +154,10 @@ __global__ void power_commit_kernel(const double* nrm, double* sigma) {
   if (*nrm != 0.0) *sigma = *nrm;
 }
 
-__global__ void cos_init_kernel(double* v, int64_t n) {
+__global__ void cos_init_kernel(double* v, int64_t n, int64_t first) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
        r += (int64_t)gridDim.x * blockDim.x)
-    v[r] = cos((double)r + 1.0);
+    v[r] = cos((double)(first + r) + 1.0);
 }
 
 // One progressive Givens step (krylov.py:282-301).  The O(i) rotation chain
@@ -371,9 +371,13 @@ extern "C" int sgs_cast_div(const void* src, int src_dtype, void* dst, int dst_d
 }
 
 extern "C" int sgs_cos_init(double* v, int64_t n, void* stream) {
-  SGS_REQUIRE(v && n >= 0, "cos_init: bad args");
+  return sgs_cos_init_at(v, n, 0, stream);
+}
+
+extern "C" int sgs_cos_init_at(double* v, int64_t n, int64_t first, void* stream) {
+  SGS_REQUIRE(v && n >= 0 && first >= 0, "cos_init: bad args");
   if (n == 0) return SGS_OK;
-  cos_init_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(v, n);
+  cos_init_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(v, n, first);
   return check_launch("cos_init_kernel");
 }
 

@@ -29,6 +29,29 @@ class TorchComm:
     def allreduce_(self, t: torch.Tensor) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
 
+    def allgather_rows(self, local: torch.Tensor, counts: list[int], out: torch.Tensor) -> None:
+        """out[:sum(counts)] = the ranks' row blocks in rank order.  Blocks are
+        padded to max(counts); shard_rows gives every rank but the last the
+        same size, so the padded concatenation trimmed to n is the vector."""
+        nmax = max(counts)
+        world = self.world
+        buf = out.new_empty((world, nmax))
+        mine = out.new_zeros(nmax)
+        mine[:local.numel()].copy_(local)
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_gather_into_tensor(buf.view(-1), mine, group=self.group)
+        else:
+            dist.all_gather(list(buf.unbind(0)), mine, group=self.group)
+        flat = buf.view(-1)
+        n = sum(counts)
+        if all(c == nmax for c in counts[:-1]):
+            out[:n].copy_(flat[:n])
+        else:
+            o = 0
+            for r, c in enumerate(counts):
+                out[o:o + c].copy_(buf[r, :c])
+                o += c
+
 
 def init_from_env(backend: str = "nccl") -> TorchComm | None:
     """Initialise the default process group from torchrun's environment

@@ -115,6 +115,33 @@ class SparseMatrix:
     def __post_init__(self):
         self.__dict__.setdefault("_dev_cache", {})
 
+    def row_block(self, row0: int, n_rows: int, device=None) -> "_RowBlock":
+        """Rows [row0, row0 + n_rows) of the operator (global column indices),
+        for a row-sharded solve."""
+        return _RowBlock(self, row0, n_rows, device)
+
+
+class _RowBlock:
+    """A contiguous row block of a SparseMatrix on the device; its SpMV takes
+    the full input vector and writes the block's rows."""
+
+    def __init__(self, A: SparseMatrix, row0: int, n_rows: int, device=None):
+        _lib.require_cuda()
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None \
+            else torch.device(device)
+        lo, hi = int(A.row_ptr[row0]), int(A.row_ptr[row0 + n_rows])
+        rp = np.asarray(A.row_ptr[row0:row0 + n_rows + 1], dtype=np.int64) - lo
+        self.n, self.n_rows, self.row0 = A.n, n_rows, row0
+        self.rp = torch.from_numpy(rp.astype(np.int32)).to(dev)
+        self.ci = torch.from_numpy(np.asarray(A.col_idx[lo:hi], dtype=np.int32)).to(dev)
+        self.va = torch.from_numpy(np.asarray(A.values[lo:hi], dtype=np.float64)).to(dev)
+
+    def spmv_into(self, x_ptr: int, x_code: int, y: torch.Tensor, alpha=None, status=None):
+        call("sgs_csr_spmv", self.n_rows, self.rp.data_ptr(), self.ci.data_ptr(),
+             self.va.data_ptr(), x_ptr, x_code, None,
+             alpha.data_ptr() if alpha is not None else None, y.data_ptr(),
+             status.ptr if status is not None else None, stream_ptr())
+
 
 class Ilu0Preconditioner:
     """Zero-fill incomplete LU factors on A's pattern (krylov.py:86-100).
@@ -298,6 +325,45 @@ class _Workspace:
              self.nrm[out_slot:].data_ptr(), self.work.data_ptr(), stream_ptr())
 
 
+class _Dist:
+    """Row sharding of an RGMRES solve: this rank owns
+    operator rows [row0, row0 + n_loc) and the same rows of every n-vector
+    (shard_rows, aligned to the sketch's tiles).  The RGS state is sharded as
+    in RgsState(comm=...): one k-vector all-reduce per sketch, replicated LS
+    and Givens.  The SpMV all-gathers its input vector; norms all-reduce
+    their squares."""
+
+    def __init__(self, comm, A: SparseMatrix, align: int, device):
+        from .workloads import shard_rows
+        self.comm = comm
+        self.n = A.n
+        self.counts = [shard_rows(A.n, comm.world, r, align)[1] for r in range(comm.world)]
+        self.row0, self.n_loc = shard_rows(A.n, comm.world, comm.rank, align)
+        if self.n_loc < 1:
+            raise ValueError("more ranks than row blocks")
+        self.block = A.row_block(self.row0, self.n_loc, device)
+        self.device = device
+        self._full = {}
+
+    def full(self, x_local: torch.Tensor) -> torch.Tensor:
+        buf = self._full.get(x_local.dtype)
+        if buf is None:
+            buf = self._full[x_local.dtype] = torch.empty(self.n, dtype=x_local.dtype,
+                                                          device=self.device)
+        self.comm.allgather_rows(x_local, self.counts, buf)
+        return buf
+
+    def norm_(self, nrm: torch.Tensor, slot: int) -> None:
+        """nrm[slot] holds this rank's norm; make it the global one."""
+        t = nrm[slot:slot + 1]
+        sq = t * t
+        self.comm.allreduce_(sq)
+        torch.sqrt(sq, out=t)
+
+    def local(self, v_full: torch.Tensor) -> torch.Tensor:
+        return v_full[self.row0:self.row0 + self.n_loc]
+
+
 def _eff_matvec_into(A: SparseMatrix, M, ws: _Workspace, x_ptr: int, x_code: int,
                      out: torch.Tensor, alpha=None, status=None, xdiv_ptr=None) -> None:
     """out = A M^{-1} x (/ alpha): the right-preconditioned operator of
@@ -312,17 +378,24 @@ def _eff_matvec_into(A: SparseMatrix, M, ws: _Workspace, x_ptr: int, x_code: int
 
 
 def _operator_norm_estimate(A: SparseMatrix, ws: _Workspace, iters: int = 20,
-                            M=None) -> torch.Tensor:
+                            M=None, dist: _Dist | None = None) -> torch.Tensor:
     """Device power iteration (krylov.py:213-226) on A M^{-1}; returns a
     1-element device tensor (-1 when the reference would return 0.0)."""
-    n = A.n
+    n = A.n if dist is None else dist.n_loc
     sigma = torch.ones(1, dtype=torch.float64, device=ws.v.device)
-    call("sgs_cos_init", ws.v.data_ptr(), n, stream_ptr())
+    call("sgs_cos_init_at", ws.v.data_ptr(), n, 0 if dist is None else dist.row0, stream_ptr())
     ws.norm(ws.v, 0)
+    if dist is not None:
+        dist.norm_(ws.nrm, 0)
     call("sgs_scale", ws.v.data_ptr(), 1.0, ws.nrm.data_ptr(), 1, ws.v.data_ptr(), n, stream_ptr())
     for _ in range(iters):
-        _eff_matvec_into(A, M, ws, ws.v.data_ptr(), _lib.SGS_F64, ws.w)
+        if dist is None:
+            _eff_matvec_into(A, M, ws, ws.v.data_ptr(), _lib.SGS_F64, ws.w)
+        else:
+            dist.block.spmv_into(dist.full(ws.v).data_ptr(), _lib.SGS_F64, ws.w)
         ws.norm(ws.w, 1)
+        if dist is not None:
+            dist.norm_(ws.nrm, 1)
         call("sgs_power_step", ws.w.data_ptr(), ws.nrm[1:].data_ptr(), ws.v.data_ptr(),
              sigma.data_ptr(), n, stream_ptr())
     return sigma
@@ -338,18 +411,23 @@ class _ArnoldiEngine:
     Otherwise the generic path (separate SpMV, sketch and normalisation)."""
 
     def __init__(self, A: SparseMatrix, theta, policy, solver, m: int,
-                 breakdown_factor: float = BREAKDOWN_FACTOR, phi=None, M=None):
+                 breakdown_factor: float = BREAKDOWN_FACTOR, phi=None, M=None,
+                 dist: _Dist | None = None):
         self.A = A
         self.M = M
         self.m = m
+        self.dist = dist
+        shard = {} if dist is None else {"comm": dist.comm, "row0": dist.row0,
+                                         "n_local": dist.n_loc}
         self.state = RgsState(theta, policy, solver, phi=phi, capacity=m + 2,
-                              breakdown_factor=breakdown_factor)
+                              breakdown_factor=breakdown_factor, **shard)
         st = self.state
         if st.n != A.n:
             raise ValueError("sketch ambient dimension does not match the operator")
         self.fused = st.fused
+        self.n_loc = st.n_local
         dev = st.device
-        self.ws = _Workspace(A.n, dev)
+        self.ws = _Workspace(self.n_loc, dev)
         self.cs = torch.zeros(m + 1, dtype=torch.float64, device=dev)
         self.sn = torch.zeros_like(self.cs)
         self.g = torch.zeros(m + 2, dtype=torch.float64, device=dev)
@@ -358,16 +436,28 @@ class _ArnoldiEngine:
         self.norm_flag = torch.full((1,), -1, dtype=torch.int32, device=dev)
         self._owed = None  # step whose Givens update rides on the next step's head
 
+    def _matvec(self, i: int, out: torch.Tensor, alpha, status) -> None:
+        """out = (A M^{-1} q_i) / alpha over this rank's rows."""
+        st = self.state
+        if self.dist is None:
+            _eff_matvec_into(self.A, self.M, self.ws, st._qcol_ptr(i), st.ccode, out,
+                             alpha=alpha, status=status)
+        else:
+            xf = self.dist.full(st._Q[i, :self.n_loc])
+            self.dist.block.spmv_into(xf.data_ptr(), st.ccode, out, alpha=alpha, status=status)
+
     def start(self, b_dev: torch.Tensor, b_norm_ptr) -> None:
-        """Push b (divided by ||b|| when b_norm_ptr is given) as column 0."""
-        st, n = self.state, self.A.n
+        """Push b (this rank's rows; divided by ||b|| when b_norm_ptr is given)
+        as column 0."""
+        st, n = self.state, self.n_loc
         bn = self.ws.v
         call("sgs_cast_div", b_dev.data_ptr(), _lib.SGS_F64, bn.data_ptr(), _lib.SGS_F64,
              b_norm_ptr, n, stream_ptr())
         if not self.fused:
             st._push_async(bn)
             return
-        pp, pn, ps = st._sketch_parts(bn.data_ptr(), _lib.SGS_F64, n, st._parts_p, None)
+        pp, pn, ps = st._sketch_parts(bn.data_ptr(), _lib.SGS_F64, n, st._parts_p,
+                                      getattr(st, "_kvec_p", None))
         call("sgs_partials_reduce", pp, pn, st.k, 1, ps, st._P.data_ptr(), st.fcode, st.k,
              st.status.ptr, stream_ptr())
         st._phi_w(0, bn.data_ptr(), _lib.SGS_F64, n)
@@ -387,15 +477,15 @@ class _ArnoldiEngine:
             # Givens update of step i-1 in the same launch (sgs_arnoldi_head)
             gi = -1 if self._owed is None else self._owed
             self._owed = None
-            call("sgs_arnoldi_head", st._Q.data_ptr(), st.ccode, st.ldq, A.n, i,
+            call("sgs_arnoldi_head", st._Q.data_ptr(), st.ccode, st.ldq, self.n_loc, i,
                  st._R.data_ptr(), st._cap, self.norm_flag.data_ptr(), gi, self.cs.data_ptr(),
                  self.sn.data_ptr(), self.g.data_ptr(), self.T.data_ptr(), self.T.shape[1],
                  self.hist.data_ptr(), -1.0 if tol is None else float(tol), st.status.ptr,
                  stream_ptr())
-            _eff_matvec_into(A, self.M, ws, st._qcol_ptr(i), st.ccode, ws.w, alpha=alpha,
-                             status=st.status)
-            pp, pn, ps = st._sketch_parts(ws.w.data_ptr(), _lib.SGS_F64, A.n, st._parts_p, None)
-            st._phi_w(i + 1, ws.w.data_ptr(), _lib.SGS_F64, A.n)
+            self._matvec(i, ws.w, alpha, st.status)
+            pp, pn, ps = st._sketch_parts(ws.w.data_ptr(), _lib.SGS_F64, self.n_loc,
+                                          st._parts_p, getattr(st, "_kvec_p", None))
+            st._phi_w(i + 1, ws.w.data_ptr(), _lib.SGS_F64, self.n_loc)
             st._ls(sol=i + 1, p_parts=pp, p_nparts=pn, p_scale=ps)
             sp, sn, ss = st._column(i + 1, ws.w.data_ptr(), _lib.SGS_F64, False, True)
             phq = st._phi_q_parts(i + 1)
@@ -403,8 +493,7 @@ class _ArnoldiEngine:
             st._phi_q_finish(i + 1, phq)
             st.m = i + 2
         else:
-            _eff_matvec_into(A, self.M, ws, st._qcol_ptr(i), st.ccode, ws.w, alpha=alpha,
-                             status=st.status)
+            self._matvec(i, ws.w, alpha, st.status)
             st._push_async(ws.w)
         if tol is not None or alpha is not None:
             if self.fused:
@@ -448,17 +537,33 @@ class _ArnoldiEngine:
         return out
 
 
+def _make_dist(comm, A: SparseMatrix, theta, M) -> _Dist | None:
+    if comm is None:
+        return None
+    if M is not None:
+        raise NotImplementedError("ILU(0) preconditioning is single-GPU (its sweeps run in "
+                                  "global dependency order)")
+    from .sketch import as_device_sketch
+    device = torch.device("cuda", torch.cuda.current_device())
+    return _Dist(comm, A, as_device_sketch(theta).row_align(), device)
+
+
 def arnoldi(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, theta=None,
             policy: PrecisionPolicy = MIXED32_64, solver: LsqSolver = HOUSEHOLDER_QR,
-            phi=None) -> ArnoldiDecomposition:
-    """m-step RGS-Arnoldi (krylov.py:176-199); fewer columns on a lucky breakdown."""
+            phi=None, *, comm=None) -> ArnoldiDecomposition:
+    """m-step RGS-Arnoldi (krylov.py:176-199); fewer columns on a lucky
+    breakdown.  With ``comm`` the rows are sharded across the ranks (b is the
+    full vector on every rank; Q holds this rank's rows, H and R are
+    replicated)."""
     _check_variant(variant)
     if theta is None:
         raise ValueError("the randomized variant needs a sketch operator")
-    eng = _ArnoldiEngine(A, theta, policy, solver, m, phi=phi)
+    _lib.require_cuda()
+    dist = _make_dist(comm, A, theta, None)
+    eng = _ArnoldiEngine(A, theta, policy, solver, m, phi=phi, dist=dist)
     st = eng.state
     b_dev = _to_device_f64(b, A.n, st.device)
-    eng.start(b_dev, None)
+    eng.start(b_dev if dist is None else dist.local(b_dev).contiguous(), None)
     s0 = eng.run(alpha=None, tol=None)
     breakdown = s0["code"] in (_lib.ST_BREAKDOWN, _lib.ST_NONFINITE)
     if s0["code"] == _lib.ST_RANK:
@@ -472,9 +577,13 @@ def arnoldi(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, thet
 
 def gmres(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, theta=None,
           policy: PrecisionPolicy = MIXED32_64, solver: LsqSolver = HOUSEHOLDER_QR,
-          preconditioner=None, tol: float | None = None, phi=None) -> GmresResult:
+          preconditioner=None, tol: float | None = None, phi=None, *,
+          comm=None) -> GmresResult:
     """Single-cycle RGS-GMRES(m) with progressive Givens rotations (krylov.py:229-319),
-    right-preconditioned by an ILU(0) ``preconditioner`` when given."""
+    right-preconditioned by an ILU(0) ``preconditioner`` when given.  With
+    ``comm`` (distributed.TorchComm) the operator rows and every n-vector are
+    sharded across the ranks (one tile-aligned row block each); b is the full
+    vector on every rank and so is the returned x."""
     _check_variant(variant)
     M = _as_preconditioner(preconditioner)
     if theta is None:
@@ -482,21 +591,26 @@ def gmres(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, theta=
     _lib.require_cuda()
     device = torch.device("cuda", torch.cuda.current_device())
     return_numpy = not (isinstance(b, torch.Tensor) and b.is_cuda)
+    dist = _make_dist(comm, A, theta, M)
     b_dev = _to_device_f64(b, A.n, device)
-    ws0 = _Workspace(A.n, device)
-    ws0.norm(b_dev, 0)
+    b_loc = b_dev if dist is None else dist.local(b_dev).contiguous()
+    n_loc = A.n if dist is None else dist.n_loc
+    ws0 = _Workspace(n_loc, device)
+    ws0.norm(b_loc, 0)
+    if dist is not None:
+        dist.norm_(ws0.nrm, 0)
     b_norm = float(ws0.nrm[0])  # host sync: the zero-rhs branch needs it
     if b_norm == 0.0:
         x0 = np.zeros(A.n) if return_numpy else torch.zeros(A.n, dtype=torch.float64,
                                                              device=device)
         return GmresResult(x=x0, residual_history=np.zeros(0), final_residual=0.0,
                            iterations=0, converged=True, breakdown=False)
-    eng = _ArnoldiEngine(A, theta, policy, solver, m, phi=phi, M=M)
+    eng = _ArnoldiEngine(A, theta, policy, solver, m, phi=phi, M=M, dist=dist)
     st = eng.state
-    alpha = _operator_norm_estimate(A, eng.ws, M=M)
+    alpha = _operator_norm_estimate(A, eng.ws, M=M, dist=dist)
     if float(alpha) <= 0.0:
         raise np.linalg.LinAlgError("operator norm estimate is zero")
-    eng.start(b_dev, ws0.nrm.data_ptr())
+    eng.start(b_loc, ws0.nrm.data_ptr())
     s1 = eng.run(alpha=alpha, tol=tol)
     code = s1["code"]
     if code == _lib.ST_RANK:
@@ -506,25 +620,31 @@ def gmres(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, theta=
     breakdown = code in (_lib.ST_BREAKDOWN, _lib.ST_NONFINITE)
     k = s1["iters"]
     hist = eng.hist[:k].cpu().numpy()
-    x = torch.zeros(A.n, dtype=torch.float64, device=device)
+    x = torch.zeros(n_loc, dtype=torch.float64, device=device)
     if k > 0:
         T = eng.T[:k, :k].t().cpu().numpy()
         g = eng.g[:k].cpu().numpy()
         y = scipy.linalg.solve_triangular(T, g, lower=False)
         yd = torch.from_numpy(y).to(device)
-        z = torch.empty(A.n, dtype=torch.float64, device=device)
-        call("sgs_gemv_f64", st._Q.data_ptr(), st.ccode, st.ldq, A.n, k, yd.data_ptr(),
+        z = torch.empty(n_loc, dtype=torch.float64, device=device)
+        call("sgs_gemv_f64", st._Q.data_ptr(), st.ccode, st.ldq, n_loc, k, yd.data_ptr(),
              z.data_ptr(), stream_ptr())
-        call("sgs_scale", z.data_ptr(), b_norm, alpha.data_ptr(), 0, x.data_ptr(), A.n,
+        call("sgs_scale", z.data_ptr(), b_norm, alpha.data_ptr(), 0, x.data_ptr(), n_loc,
              stream_ptr())
         if M is not None:  # x = M^{-1} x_tilde (krylov.py:309-310)
             M.solve_into(x.data_ptr(), _lib.SGS_F64, z)
             x = z
     # true residual ||b - A x|| / ||b|| in binary64
     ax = eng.ws.w
-    A.spmv_into(x.data_ptr(), _lib.SGS_F64, ax)
-    call("sgs_rsub", b_dev.data_ptr(), ax.data_ptr(), A.n, stream_ptr())
+    if dist is None:
+        A.spmv_into(x.data_ptr(), _lib.SGS_F64, ax)
+    else:
+        x = dist.full(x).clone()
+        dist.block.spmv_into(x.data_ptr(), _lib.SGS_F64, ax)
+    call("sgs_rsub", b_loc.data_ptr(), ax.data_ptr(), n_loc, stream_ptr())
     eng.ws.norm(ax, 2)
+    if dist is not None:
+        dist.norm_(eng.ws.nrm, 2)
     true_res = float(eng.ws.nrm[2]) / b_norm
     converged = (true_res <= max(tol, 0.0)) if tol is not None else False
     return GmresResult(x=x.cpu().numpy() if return_numpy else x,
@@ -544,36 +664,52 @@ class RestartedResult:
 
 def gmres_restarted(A: SparseMatrix, b, theta, policy: PrecisionPolicy = MIXED32_64,
                     restart: int = 300, max_iters: int = 3000, tol: float = 1e-8,
-                    solver: LsqSolver = HOUSEHOLDER_QR, preconditioner=None) -> RestartedResult:
+                    solver: LsqSolver = HOUSEHOLDER_QR, preconditioner=None, *,
+                    comm=None) -> RestartedResult:
     """Restarted RGMRES(restart) for BASELINE config 3 (the reference is
     single-cycle, krylov.py:236-241; the wrapper is shared verbatim with the
     oracle): each cycle runs gmres(A, r, min(restart, max_iters - its), tol =
     tol * ||b|| / ||r||), then x += dx and r = b - A x in binary64; stop at
-    ||r|| / ||b|| <= tol or its >= max_iters."""
+    ||r|| / ||b|| <= tol or its >= max_iters.  ``comm``: row-sharded, as gmres."""
     _lib.require_cuda()
     device = torch.device("cuda", torch.cuda.current_device())
     return_numpy = not (isinstance(b, torch.Tensor) and b.is_cuda)
+    M = _as_preconditioner(preconditioner)
+    dist = _make_dist(comm, A, theta, M)
+    n_loc = A.n if dist is None else dist.n_loc
     b_dev = _to_device_f64(b, A.n, device)
-    ws = _Workspace(A.n, device)
-    ws.norm(b_dev, 0)
-    b_norm = float(ws.nrm[0])
+    b_loc = b_dev if dist is None else dist.local(b_dev).contiguous()
+    ws = _Workspace(n_loc, device)
+
+    def rnorm(v, slot):
+        ws.norm(v, slot)
+        if dist is not None:
+            dist.norm_(ws.nrm, slot)
+        return float(ws.nrm[slot])
+
+    b_norm = rnorm(b_loc, 0)
     x = torch.zeros(A.n, dtype=torch.float64, device=device)
     r = b_dev.clone()
+    r_loc = torch.empty(n_loc, dtype=torch.float64, device=device)
     its, cycles = 0, []
     r_norm = b_norm
-    M = _as_preconditioner(preconditioner)
     while True:
         if b_norm == 0.0 or r_norm / b_norm <= tol or its >= max_iters:
             break
         res = gmres(A, r, m=min(restart, max_iters - its), theta=theta, policy=policy,
-                    solver=solver, tol=tol * b_norm / r_norm, preconditioner=M)
+                    solver=solver, tol=tol * b_norm / r_norm, preconditioner=M, comm=comm)
         cycles.append(res.iterations)
         its += res.iterations
         x += res.x
-        A.spmv_into(x.data_ptr(), _lib.SGS_F64, r)
-        call("sgs_rsub", b_dev.data_ptr(), r.data_ptr(), A.n, stream_ptr())
-        ws.norm(r, 1)
-        r_norm = float(ws.nrm[1])
+        if dist is None:
+            A.spmv_into(x.data_ptr(), _lib.SGS_F64, r)
+            call("sgs_rsub", b_dev.data_ptr(), r.data_ptr(), A.n, stream_ptr())
+            r_norm = rnorm(r, 1)
+        else:
+            dist.block.spmv_into(x.data_ptr(), _lib.SGS_F64, r_loc)
+            call("sgs_rsub", b_loc.data_ptr(), r_loc.data_ptr(), n_loc, stream_ptr())
+            r_norm = rnorm(r_loc, 1)
+            r.copy_(dist.full(r_loc))
         if res.iterations == 0:
             break
     rel = r_norm / b_norm if b_norm else 0.0
