@@ -388,7 +388,11 @@ def run_gmres(args):
     import paper_2011_05090_b200 as sg
     import paper_2011_05090_b200.gram_schmidt as gsm
     from paper_2011_05090_b200 import _lib
+    from paper_2011_05090_b200.distributed import init_from_env
     from paper_2011_05090_b200.workloads import CONFIGS, convdiff3d, rhs_gaussian
+    comm = init_from_env(os.environ.get("SGS_DIST_BACKEND", "nccl"))
+    if comm is not None:
+        return run_gmres_sharded(args, comm)
     cfg = CONFIGS["c3"]
     N = cfg["grid"]
     rp, ci, va = convdiff3d(N, (cfg["beta"],) * 3)
@@ -487,6 +491,62 @@ def run_gmres(args):
                                  "l2": "inputs larger than L2 (basis, CSR >> 126 MB)"},
                       "results": out, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                       "gpu_launches": out["f64"]["gpu_launches"], "clocks": clk}), flush=True)
+
+
+def run_gmres_sharded(args, comm):
+    """c3 at N > 1: row-sharded restarted RGMRES (strong scaling over n = 2^21
+    rows); steps/s of the whole job, device time as the max over ranks."""
+    import torch
+    import paper_2011_05090_b200 as sg
+    from paper_2011_05090_b200 import _lib
+    from paper_2011_05090_b200.workloads import CONFIGS, convdiff3d, rhs_gaussian
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    cfg = CONFIGS["c3"]
+    N = cfg["grid"]
+    rp, ci, va = convdiff3d(N, (cfg["beta"],) * 3)
+    A = sg.SparseMatrix(n=N ** 3, row_ptr=rp, col_idx=ci, values=va)
+    b = torch.from_numpy(rhs_gaussian(A.n, 0)).cuda()
+    th = sg.make_sketch(sg.SketchKind.PSRHT, cfg["k"], A.n, 0)
+    th.device_data()
+    out = {}
+    clocks = Clocks(local)
+    for pname in ("f64", "mixed"):
+        pol = sg.policy_from_name(pname)
+        solve = lambda: sg.gmres_restarted(A, b, th, pol, cfg["restart"],  # noqa: E731
+                                           cfg["max_iters"], cfg["tol"], comm=comm)
+        for _ in range(args.warmup):
+            solve()
+        torch.cuda.synchronize()
+        torch.distributed.barrier()
+        lc0 = _lib.launch_count()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        its = 0
+        for _ in range(args.steps):
+            res = solve()
+            its += res.iterations
+        e1.record()
+        torch.cuda.synchronize()
+        ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(ms, op=torch.distributed.ReduceOp.MAX)
+        ms = float(ms)
+        out[pname] = {"steps_per_s": its / (ms / 1e3), "iterations": res.iterations,
+                      "cycles": res.cycles, "relres": res.final_residual,
+                      "ms_per_solve": ms / args.steps,
+                      "gpu_launches": _lib.launch_count() - lc0}
+    clk = clocks.stop()
+    if comm.rank == 0:
+        print(json.dumps({"metric": "RGMRES Arnoldi steps/s", "value": out["f64"]["steps_per_s"],
+                          "unit": "steps/s", "n_gpus": comm.world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": out["f64"]["ms_per_solve"],
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                          "dtype": "f64", "data": "synthetic",
+                          "config": {"workload": "c3", **cfg,
+                                     "parallelism": f"row-shard x{comm.world}"},
+                          "results": out, "gpu_launches": out["f64"]["gpu_launches"],
+                          "clocks": clk}), flush=True)
+    torch.distributed.destroy_process_group()
 
 
 def main():
