@@ -226,6 +226,7 @@ givens_step_kernel(const double* __restrict__ R, int64_t ldr, int i, double* cs,
   givens_update(R, ldr, i, cs, sn, g, T, ldt, hist, tol, st, tl);
 }
 
+constexpr int kHeadPer = 4;
 // Head of an RGMRES step: the last block performs the Givens update of step
 // gi (if gi >= 0) while all other blocks normalise basis column `col` in
 // place.  The normalising blocks ignore the status block on purpose - the
@@ -243,12 +244,22 @@ arnoldi_head_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int col, int* no
     return;
   }
   if (col < 0) return;
-  const int nb = gridDim.x - (gi >= 0 ? 1 : 0);
   const double rjj = R[(int64_t)col * ldr + col];
   TQ* q = Q + (int64_t)col * ldq;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
-       r += (int64_t)nb * blockDim.x)
-    q[r] = cvt<TQ>((double)q[r] / rjj);
+  // kHeadPer elements per thread, all loads issued before the divisions (a
+  // grid-stride loop here waits one memory latency per element)
+  const int64_t r0 = (int64_t)blockIdx.x * blockDim.x * kHeadPer + threadIdx.x;
+  TQ v[kHeadPer];
+#pragma unroll
+  for (int u = 0; u < kHeadPer; ++u) {
+    const int64_t r = r0 + (int64_t)u * blockDim.x;
+    v[u] = r < n ? q[r] : TQ(0);
+  }
+#pragma unroll
+  for (int u = 0; u < kHeadPer; ++u) {
+    const int64_t r = r0 + (int64_t)u * blockDim.x;
+    if (r < n) q[r] = cvt<TQ>((double)v[u] / rjj);
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) *norm_flag = col;
 }
 
@@ -402,7 +413,8 @@ extern "C" int sgs_arnoldi_head(void* Q, int q_dtype, int64_t ldq, int64_t n, in
                          gi + 2 <= kGivMax),
               "arnoldi_head: bad Givens args");
   const size_t smem = gi >= 0 ? (size_t)(3 * gi + 2) * sizeof(double) : 0;
-  const unsigned nb = (col >= 0 ? grid_for(n) : 0) + (gi >= 0 ? 1 : 0);
+  const unsigned nb = (col >= 0 ? (unsigned)((n + 256 * kHeadPer - 1) / (256 * kHeadPer)) : 0) +
+                      (gi >= 0 ? 1 : 0);
   if (nb == 0) return SGS_OK;
   cudaStream_t s = as_stream(stream);
   if (q_dtype == SGS_F32) {
