@@ -217,17 +217,6 @@ int sgs_csr_spmv(int64_t n, const int32_t* row_ptr, const int32_t* col_idx,
                  const double* alpha, double* y, const sgs_status* st,
                  void* stream);
 
-/* Fused RGMRES operator step: y = (A x) / alpha[0] with x = cast(q / xdiv[0])
- * formed on the fly (xdiv == NULL: x as given), plus, when do_sketch != 0, the
- * P-SRHT of y in the epilogue (partials as sgs_rgs_update_srht,
- * sgs_column_nparts(n) of them).  krylov.py:276 + gram_schmidt.py:303. */
-int sgs_csr_spmv_srht(int64_t n, const int32_t* row_ptr, const int32_t* col_idx,
-                      const double* vals, const void* x, int x_dtype,
-                      const double* xdiv, const double* alpha, double* y,
-                      int do_sketch, int64_t row0, int log2_block,
-                      const uint32_t* sign_bits, const int32_t* samples, int k,
-                      double* partials, const sgs_status* st, void* stream);
-
 /* deterministic ||x||_2 (fp64 or fp32 input, fp64 result on device) */
 int sgs_norm2(const void* x, int x_dtype, int64_t n, double* out, double* work,
               void* stream);

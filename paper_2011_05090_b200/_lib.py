@@ -82,9 +82,6 @@ _SIGS = {
     "sgs_ls_step": (c_int, [POINTER(LsArgs), c_void_p]),
     "sgs_csr_spmv": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p,
                              c_void_p, c_void_p, c_void_p, c_void_p]),
-    "sgs_csr_spmv_srht": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p,
-                                  c_void_p, c_void_p, c_int, c_int64, c_int, c_void_p, c_void_p,
-                                  c_int, c_void_p, c_void_p, c_void_p]),
     "sgs_norm2": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_void_p, c_void_p]),
     "sgs_norm2_work_elems": (c_int64, [c_int64]),
     "sgs_scale": (c_int, [c_void_p, c_double, c_void_p, c_int, c_void_p, c_int64, c_void_p]),

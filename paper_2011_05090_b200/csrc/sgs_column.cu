@@ -311,151 +311,3 @@ extern "C" int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n,
 #undef SGS_COL
   return check_ex(err, "rgs_column_kernel");
 }
-
-// ===========================================================================
-// Fused RGMRES operator step: w = (A x) / alpha with x = cast(q'_i / r_ii)
-// formed on the fly from the not yet normalised basis column (the same
-// rounding the next column kernel applies when it normalises q'_i in place),
-// followed by the P-SRHT of w in the epilogue (krylov.py:276 then
-// gram_schmidt.py:303).  One CTA per 4096-row tile, 8-CTA clusters, one
-// partial k-vector per cluster.  Rows are assigned to consecutive lanes so the
-// CSR streams coalesce; the tile then goes through the shared-memory FWHT.
-namespace sgs {
-
-constexpr int kSpmvBuf = 4096;  // products per 512-row chunk held in shared memory
-
-template <typename TX>
-__global__ void __launch_bounds__(kColThreads)
-csr_spmv_srht_kernel(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                     const double* __restrict__ vals, const TX* __restrict__ x,
-                     const double* __restrict__ xdiv, const double* __restrict__ alpha,
-                     double* __restrict__ y, int do_sketch, int64_t row0, int log2_block,
-                     const uint32_t* __restrict__ sign_bits, const int32_t* __restrict__ samples,
-                     int k, double* __restrict__ partials, const sgs_status* st,
-                     unsigned long long* tl) {
-  cg::cluster_group cl = cg::this_cluster();
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* z = reinterpret_cast<double*>(smem_raw);  // pidx(4096) + 8
-  double* part = z + pidx(kColT) + 8;               // max(k, kSpmvBuf)
-  int32_t* smp = reinterpret_cast<int32_t*>(part + (k > kSpmvBuf ? k : kSpmvBuf));
-  const int tid = threadIdx.x;
-  const int64_t lr0 = (int64_t)blockIdx.x * kColT;
-  const bool active = lr0 < n;
-  const int64_t g0 = row0 + lr0;
-  const int64_t blk = g0 >> log2_block;
-  const int64_t h = (g0 & ((int64_t(1) << log2_block) - 1)) >> kColLogT;
-  if (do_sketch && active) {
-    const int32_t* sb = samples + blk * (int64_t)k;
-    for (int j = tid; j < k; j += blockDim.x) smp[j] = __ldg(sb + j);
-  }
-  pdl_enter();
-  if (tl && threadIdx.x == 0) atomicMin(tl + 9, gtimer());
-  if (status_stopped(st)) return;  // uniform (nobody writes st here)
-  const double dv = xdiv ? *xdiv : 1.0;
-  const double al = alpha ? *alpha : 1.0;
-  auto xval = [&](int32_t c) -> double {
-    const TX xr = x[c];
-    return xdiv ? (double)cvt<TX>((double)xr / dv) : (double)xr;
-  };
-  if (active) {
-    // CSR-stream: the tile's rows in chunks of 512 rows; the chunk's nonzeros
-    // are swept by all threads (coalesced vals / col_idx) into shared-memory
-    // products, then each thread sums its row in CSR order.  Chunks whose
-    // nonzeros exceed the product buffer fall back to thread-per-row.
-    double* prod = part;  // reuse: k + extra doubles sized by the host (kSpmvBuf)
-    for (int c0 = 0; c0 < kColT; c0 += kColThreads) {
-      const int64_t ra = lr0 + c0;
-      const int64_t rbnd = min(ra + kColThreads, n);
-      const int e = c0 + tid;
-      const int64_t r = ra + tid;
-      double v = 0.0;
-      if (ra < n) {
-        const int64_t e0 = __ldg(rp + ra), e1 = __ldg(rp + rbnd);
-        const bool stream = (e1 - e0) <= kSpmvBuf;
-        __syncthreads();  // previous chunk's products consumed
-        if (stream) {
-          for (int64_t q = e0 + tid; q < e1; q += kColThreads)
-            prod[q - e0] = __ldg(vals + q) * xval(__ldg(ci + q));
-        }
-        __syncthreads();
-        if (r < n) {
-          const int b = __ldg(rp + r), eidx = __ldg(rp + r + 1);
-          double acc = 0.0;
-          if (stream)
-            for (int q = b; q < eidx; ++q) acc += prod[q - e0];
-          else
-            for (int q = b; q < eidx; ++q) acc += __ldg(vals + q) * xval(__ldg(ci + q));
-          const double yv = alpha ? acc / al : acc;
-          y[r] = yv;
-          if (do_sketch) {
-            const uint32_t word = __ldg(sign_bits + (r >> 5));
-            v = ((word >> (r & 31)) & 1u) ? yv : -yv;
-          }
-        }
-      }
-      if (do_sketch) z[pidx(e)] = v;
-    }
-  }
-  if (!do_sketch) return;
-  __syncthreads();
-  if (active) {
-    fwht_tile<kColLogT>(z);
-    for (int j = tid; j < k; j += blockDim.x) {
-      const int32_t rr = smp[j];
-      const double v = z[pidx(rr & (kColT - 1))];
-      const int64_t rh = (int64_t)(rr >> kColLogT);
-      part[j] = (__popcll(rh & h) & 1) ? -v : v;
-    }
-  } else {
-    for (int j = tid; j < k; j += blockDim.x) part[j] = 0.0;
-  }
-  cl.sync();
-  const int rank = (int)cl.block_rank();
-  const int j0 = (int)(((int64_t)rank * k) / kColCluster);
-  const int j1 = (int)(((int64_t)(rank + 1) * k) / kColCluster);
-  double* outp = partials + (int64_t)(blockIdx.x / kColCluster) * k;
-  for (int j = j0 + tid; j < j1; j += blockDim.x) {
-    double s = 0.0;
-#pragma unroll
-    for (int q2 = 0; q2 < kColCluster; ++q2) s += cl.map_shared_rank(part, q2)[j];
-    outp[j] = s;
-  }
-  cl.sync();
-  if (tl && threadIdx.x == 0) atomicMax(tl + 10, gtimer());
-}
-
-}  // namespace sgs
-
-
-extern "C" int sgs_csr_spmv_srht(int64_t n, const int32_t* row_ptr, const int32_t* col_idx,
-                                 const double* vals, const void* x, int x_dtype,
-                                 const double* xdiv, const double* alpha, double* y,
-                                 int do_sketch, int64_t row0, int log2_block,
-                                 const uint32_t* sign_bits, const int32_t* samples, int k,
-                                 double* partials, const sgs_status* st, void* stream) {
-  SGS_REQUIRE(n >= 1 && row_ptr && col_idx && vals && x && y, "spmv_srht: bad args");
-  SGS_REQUIRE(!do_sketch || (sign_bits && samples && partials && k >= 1 && k <= 8192),
-              "spmv_srht: sketch arguments");
-  SGS_REQUIRE(!do_sketch || (log2_block >= kColLogT && (row0 % kColT) == 0),
-              "spmv_srht: needs 4096-row tiles");
-  cudaStream_t s = as_stream(stream);
-  const int64_t nctas = column_ctas(n);
-  const size_t smem = (size_t)(pidx(kColT) + 8 + (k > kSpmvBuf ? k : kSpmvBuf)) * sizeof(double) +
-                      (size_t)k * sizeof(int32_t);
-  unsigned long long* tlr = debug_timeline_row();
-  cudaError_t err;
-  if (x_dtype == SGS_F32) {
-    auto kern = csr_spmv_srht_kernel<float>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    err = launch_ex(kern, dim3((unsigned)nctas), dim3(kColThreads), smem, s, kColCluster, n,
-                    row_ptr, col_idx, vals, static_cast<const float*>(x), xdiv, alpha, y,
-                    do_sketch, row0, log2_block, sign_bits, samples, k, partials, st, tlr);
-  } else {
-    auto kern = csr_spmv_srht_kernel<double>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    err = launch_ex(kern, dim3((unsigned)nctas), dim3(kColThreads), smem, s, kColCluster, n,
-                    row_ptr, col_idx, vals, static_cast<const double*>(x), xdiv, alpha, y,
-                    do_sketch, row0, log2_block, sign_bits, samples, k, partials, st, tlr);
-  }
-  return check_ex(err, "csr_spmv_srht_kernel");
-}

@@ -938,26 +938,11 @@ extern "C" int sgs_transpose(const void* src, int64_t lds, void* dst, int64_t ld
   return check_launch("transpose_kernel");
 }
 
-namespace sgs {
-int launch_ls_grid(const sgs_ls_args* a, cudaStream_t s);
-int64_t ls_grid_scratch_elems(int cap);
-int ls_grid_size(int k);
-static int ls_mode() {  // 0 = single cluster (default), 1 = grid-wide (SGS_LS_MODE=grid)
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SGS_LS_MODE");
-    v = (e && e[0] == 'g') ? 1 : 0;
-  }
-  return v;
-}
-}  // namespace sgs
 
 extern "C" int64_t sgs_ls_scratch_elems(int k, int cap) {
   (void)k;
   const int64_t sA = 2 * (int64_t)cap + 8;
-  const int64_t cl = 2 * kLsMaxCluster * sA + kLsMaxCluster * 8 + 64;
-  const int64_t gr = ls_grid_scratch_elems(cap);
-  return cl > gr ? cl : gr;
+  return 2 * kLsMaxCluster * sA + kLsMaxCluster * 8 + 64;
 }
 
 extern "C" int sgs_ls_cluster_size(int k) { return ls_cluster_size_host(k); }
@@ -973,7 +958,6 @@ extern "C" int sgs_ls_step(const sgs_ls_args* a, void* stream) {
   SGS_REQUIRE(!(a->do_finalize && a->do_solve) || a->col_sol == a->col_fin + 1,
               "ls_step: fused solve must target the next column");
   cudaStream_t s = as_stream(stream);
-  if (ls_mode() == 1) return launch_ls_grid(a, s);
   if (a->fine_dtype == SGS_F64) return launch_ls<double>(a, s);
   if (a->fine_dtype == SGS_F32) return launch_ls<float>(a, s);
   set_error("ls_step: bad fine dtype");

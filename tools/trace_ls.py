@@ -16,13 +16,9 @@ for rep in range(2):
     st._trace = torch.zeros((m + 1, 16), dtype=torch.int64, device="cuda")
     st.factorize_columns(W, W.shape[1], m)
 tr = st._trace[:m].cpu().numpy().astype(np.float64)
-import os as _os
-if not _os.environ.get("SGS_LS_MODE", "cluster").startswith("g"):
-    names = {1: "prewait(cache,z,y)", 2: "wait", 3: "reduce_parts", 4: "exch1", 5: "gather+s+matvec",
-             6: "exch2", 7: "reorth", 8: "rinv_col", 9: "solve_prep", 10: "store"}
-else:
-    names = {1: "reduce_parts", 2: "coldot+B1", 3: "reduce_scatter+B2", 4: "gather+t", 5: "B3",
-             6: "reorth+rinv_col", 7: "solve_prep", 8: "trmv_store"}
+names = {1: "prewait(cache,z,y)", 2: "wait", 3: "reduce_parts", 4: "exch1",
+         5: "gather+s+matvec", 6: "exch2", 7: "reorth/fast path", 8: "rinv_col",
+         9: "solve_prep", 10: "store"}
 LAST = max(names)
 out = {}
 for dec, rows in enumerate(np.array_split(tr[1:-1], 5)):
