@@ -194,7 +194,8 @@ typedef struct sgs_ls_args {
   long long* trace;      /* optional (NULL): clock64() at phase boundaries, CTA 0 */
   int cache_cols;        /* set by the library: columns of T cached in shared memory */
   unsigned long long* timeline;  /* set by the library (debug timeline) */
-  int* t_pend;           /* optional (NULL: off): column of T whose formation is deferred, -1 none */
+  int* t_pend;           /* optional (NULL: off), 2 ints, -1 = none: [0] column of T whose formation
+                            is deferred, [1] last column finalized without forming t */
   void* t_coef;          /* cap, fine: its projection coefficients (with t_pend).  A finalize
                             that sees no cancellation (||t||^2 >= ||s||^2/2 by Pythagoras)
                             publishes r without forming t = s - T c; the next launch forms

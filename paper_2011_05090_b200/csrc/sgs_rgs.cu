@@ -470,6 +470,34 @@ struct LsSmem {
   }
 };
 
+// The deferred T column of the previous finalize (its own register budget:
+// inlined, it pushed the LS kernel into spilling).  Loads that column's c1
+// (and c2 = c1 / alpha) into shared memory and, when pend >= 0, forms
+// T[:, pend] = S[:, pend] - T[:, :pend] c2 for this CTA's rows (the explicit
+// path's arithmetic), also into the cache slot.  Ends with a block barrier.
+template <typename T>
+__device__ __forceinline__ void ls_deferred_column(const T* coef, int pend, int ncoef, const T* AL,
+                                                const T* S, T* Tm, ColSrc<T> TS, T* sq, int RM,
+                                                int ncache, int k, int ra, int nr, T* c1, T* c2,
+                                                T* vt, T* tmp, T* red) {
+  for (int j = threadIdx.x; j < ncoef; j += blockDim.x) {
+    const T cj = __ldcg(coef + j);
+    c1[j] = cj;                       // kept for a solve-only launch (identity)
+    c2[j] = cj / __ldcg(AL + j);      // as the explicit path: coefficient on T_j
+  }
+  __syncthreads();
+  if (pend < 0) return;
+  for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vt[rr] = S[(int64_t)pend * k + ra + rr];
+  __syncthreads();
+  if (pend > 0) ls_rows_gemv<T>(TS, nr, pend, c2, tmp, red);  // columns < pend only
+  for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
+    const T tv = pend > 0 ? vt[rr] - tmp[rr] : vt[rr];
+    Tm[(int64_t)pend * k + ra + rr] = tv;
+    if (pend < ncache) sq[(int64_t)pend * RM + rr] = tv;
+  }
+  __syncthreads();
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   cg::cluster_group cl = cg::this_cluster();
@@ -537,7 +565,10 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   // t = s - T[:, :pend] c2, rows of this CTA, from the shared-memory cache).
   // Idempotent, so a launch that stops early and leaves t_pend set only makes
   // the next one redo it.
+  // t_pend[0]: column still to be formed; t_pend[1]: last column finalized on
+  // the fast path (its c1 / s' are in t_coef) - kept when [0] is cleared
   const int pend = a.t_pend ? *reinterpret_cast<volatile const int*>(a.t_pend) : -1;
+  const int last_fast = a.t_pend ? *reinterpret_cast<volatile const int*>(a.t_pend + 1) : -1;
   const int ncols_t = a.do_finalize ? a.col_fin : a.col_sol;  // columns of T in use
   const int ncache = min(ncols_t, a.cache_cols);
   for (int e = threadIdx.x; e < ncache * nr; e += blockDim.x) {
@@ -545,22 +576,13 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     if (j != pend) sq[(int64_t)j * RM + rr] = Tm[(int64_t)j * k + ra + rr];
   }
   const ColSrc<T> TS{sq, RM, ncache, Tm + ra, (int64_t)k};
-  if (pend >= 0 && code0 == 0) {
-    const T* coef = static_cast<const T*>(a.t_coef);  // [c1 (cap) | s' (k)] of column pend
-    for (int j = threadIdx.x; j < pend; j += blockDim.x) {
-      const T cj = __ldcg(coef + j);
-      c1[j] = cj;                       // kept for a solve-only launch (identity below)
-      c2[j] = cj / __ldcg(AL + j);      // as the explicit path: coefficient on T_j
-    }
-    for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vt[rr] = S[(int64_t)pend * k + ra + rr];
-    __syncthreads();
-    if (pend > 0) ls_rows_gemv<T>(TS, nr, pend, c2, tmp, red);  // columns < pend only
-    for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
-      const T tv = pend > 0 ? vt[rr] - tmp[rr] : vt[rr];
-      Tm[(int64_t)pend * k + ra + rr] = tv;
-      if (pend < ncache) sq[(int64_t)pend * RM + rr] = tv;
-    }
-  }
+  // a solve-only launch whose newest column was finalized on the fast path
+  // evaluates z by the identity below and needs that column's c1 (even when
+  // an earlier launch - e.g. a push that broke down - already formed T)
+  const bool need_c1 = !a.do_finalize && a.do_solve && last_fast >= 0 && last_fast == a.col_sol - 1;
+  if ((pend >= 0 || need_c1) && code0 == 0)
+    ls_deferred_column<T>(static_cast<const T*>(a.t_coef), pend, pend >= 0 ? pend : last_fast, AL,
+                          S, Tm, TS, sq, RM, ncache, k, ra, nr, c1, c2, vt, tmp, red);
   __syncthreads();
   int s0 = 0, s1 = 0;  // output slice of the solve: [0, c) for c = col_sol
   if (a.do_solve) slice(a.col_sol, s0, s1);
@@ -668,7 +690,10 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
         if (rank == 0) {
           T* coef = static_cast<T*>(a.t_coef);
           for (int j = threadIdx.x; j < nq; j += blockDim.x) coef[j] = c1[j];
-          if (threadIdx.x == 0) *a.t_pend = i;
+          if (threadIdx.x == 0) {
+            a.t_pend[0] = i;
+            a.t_pend[1] = i;
+          }
         }
       }
     }
@@ -724,7 +749,10 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
       tt = bc[4];
       tp = bc[5];
     }
-    if (defer && rank == 0 && threadIdx.x == 0) *a.t_pend = -1;  // T[:, i] stored
+    if (defer && rank == 0 && threadIdx.x == 0) {  // T[:, i] stored, z by explicit dot
+      a.t_pend[0] = -1;
+      a.t_pend[1] = -1;
+    }
     }  // explicit_t
     SGS_TR(7);
     alpha = sqrt(tt);
@@ -780,7 +808,10 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
       // Newest column deferred by its finalize: z from the same identity and
       // arithmetic as the fused launch (t^T p = s'^T p / r_ii - sum_j c1_j zc_j),
       // so streaming push and batch factorisation stay bit-identical.
-      const bool idz = a.t_pend != nullptr && pend >= 0 && pend == c - 1;
+      // re-read (unchanged within a solve-only launch) instead of keeping a
+      // register live across the whole kernel
+      const int last_fast_c = a.t_pend ? *reinterpret_cast<volatile const int*>(a.t_pend + 1) : -1;
+      const bool idz = last_fast_c >= 0 && last_fast_c == c - 1;
       if (idz) {
         const T* sprime = static_cast<const T*>(a.t_coef) + cap;
         T l2 = T(0);
@@ -791,7 +822,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
       ls_coldot<T, 1>(TS, nr, 0, c, vp, nullptr, myA + 8 + cap, nullptr);
       xsync();
       // every CTA has read t_pend (pre-wait) and formed its rows of it
-      if (!a.do_finalize && pend >= 0 && rank == 0 && threadIdx.x == 0) *a.t_pend = -1;
+      if (!a.do_finalize && a.t_pend != nullptr && rank == 0 && threadIdx.x == 0) a.t_pend[0] = -1;
       ls_gather<T>(XA + 8 + cap, sA, CL, 0, c, AL, zc);
       if (idz && threadIdx.x == 0) bc[2] = ls_slot_sum(XA + 2, sA, CL);
       __syncthreads();

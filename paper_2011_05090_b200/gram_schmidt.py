@@ -3,21 +3,23 @@
 Interface mirror of the reference's ``gram_schmidt.py`` (RgsState
 ``:228-347``, rgs_factorize ``:350-375``, certificates ``:474-487``,
 BreakdownError ``:35-43``).  Per column the device runs, on torch's current
-stream and without host synchronisation:
+stream and without host synchronisation (SRHT sketches on 4096-row tiles):
 
-1. ``sgs_ls_step`` (solve): r = argmin ||S_{i-1} r - p_i|| (step 2),
-2. ``sgs_rgs_update``: q'_i = w_i - Q_{i-1} r in the coarse format (step 3),
-   normalising q'_{i-1} in the same pass in batch mode,
-3. the sketch partials of q'_i (step 4),
-4. ``sgs_ls_step`` (finalize): r_ii, breakdown guard, S, R, LS append
-   (steps 5-7).
+1. ``sgs_rgs_update_srht``: q'_i = w_i - Q_{i-1} r in the coarse format
+   (step 3), normalising q'_{i-1} in the same pass, with the sketch partials
+   of q'_i in the epilogue (step 4);
+2. ``sgs_ls_step``: finalize column i - r_ii, breakdown guard, S, R and the
+   LS append (steps 5-7) - fused with the solve for column i+1 (step 2),
+   whose work on the existing columns runs before the dependency wait.
 
 In ``rgs_factorize`` the sketches P = Theta W of all columns are computed up
-front in batched launches (bit-identical to per-column sketches), and the
-solve for column i+1 is fused into the finalize launch of column i, so a
-column costs three kernel launches.  Breakdown and rank deficiency are
-recorded on the device and raised at the next synchronisation with the
-reference's exception types and column numbers.
+front in batched launches (bit-identical to per-column sketches), so a column
+costs two launches; ``push`` (streaming) issues the solve and the finalize
+as separate launches with the same arithmetic, so both paths agree bit for
+bit.  Other sketch kinds take the generic path (separate update, sketch and
+normalisation kernels).  Breakdown and rank deficiency are recorded on the
+device and raised at the next synchronisation with the reference's exception
+types and column numbers.
 """
 
 from __future__ import annotations
@@ -252,7 +254,7 @@ class RgsState:
             self._tcoef[:oc_] = old_coef[:oc_]
             self._tcoef[cap:] = old_coef[oc_:]
         if "_tpend" not in self.__dict__:
-            self._tpend = torch.full((1,), -1, dtype=torch.int32, device=dev)
+            self._tpend = torch.full((2,), -1, dtype=torch.int32, device=dev)
         self._rc = torch.zeros(cap, dtype=self.cdt, device=dev)
         if old is not None:
             Q, R, S, P, Qs, Rinv, alpha, oc = old

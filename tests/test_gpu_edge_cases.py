@@ -84,3 +84,27 @@ def test_gmres_breakdown_after_two_steps(cuda, rng):
     ref = oracle_gmres(lambda v: As @ v, n, b, 10, OracleSketch("psrht", 64, n, 0), "f64")
     assert res.breakdown == ref["breakdown"] and res.iterations == ref["iterations"]
     assert abs(res.final_residual - ref["final_residual"]) < 1e-8
+
+
+@pytest.mark.parametrize("policy", ["f64", "mixed"])
+def test_push_after_breakdown_is_unaffected(cuda, rng, policy):
+    # gram_schmidt.py:323-326: the failed push leaves the state unchanged, so
+    # the next columns factorise exactly as if it had never been pushed
+    n, k = 5000, 64
+    W = rng.standard_normal((n, 6))
+    th = sg.make_sketch(sg.SketchKind.PSRHT, k, n, 1)
+    pol = sg.policy_from_name(policy)
+    a = sg.RgsState(th, pol)
+    b = sg.RgsState(th, pol)
+    for j in range(3):
+        a.push(W[:, j])
+        b.push(W[:, j])
+    bad = W[:, 0] + 2.0 * W[:, 1]  # in the span: r_ii ~ rounding level
+    with pytest.raises(sg.BreakdownError) as e:
+        a.push(bad)
+    assert e.value.column == 4
+    for j in range(3, 6):
+        a.push(W[:, j])
+        b.push(W[:, j])
+    for name in ("Q", "R", "S", "P"):
+        assert np.array_equal(getattr(a, name), getattr(b, name)), name
