@@ -276,11 +276,37 @@ dense_gemv_kernel(const double* __restrict__ thetaT, int64_t ldt, int k,
   }
 }
 
-// split-K GEMM tile: 128 sketch rows (j) x 64 columns (c), 8 data rows per stage,
-// 256 threads each owning 8 (j) x 4 (c) outputs; per output the chain is the
-// ascending-row FMA of dense_gemv_kernel, so P = Theta W is bit-identical to
-// per-column sketches.
-constexpr int kGBJ = 128, kGBC = 64, kGBR = 8;
+// split-K GEMM tile: 128 sketch rows (j) x 64 columns (c), 256 threads each
+// owning 8 (j) x 4 (c) outputs; per output the chain is the ascending-row FMA
+// of dense_gemv_kernel over the same row chunk, so P = Theta W is
+// bit-identical to per-column sketches.  Operands stream through a
+// kGBS-stage cp.async pipeline of kGBR-row stages (16-byte copies for the
+// rows of Theta^T, element copies for the column-major W, whose part
+// boundaries are not aligned); W is kept transposed in shared memory, padded
+// against bank conflicts.
+constexpr int kGBJ = 128, kGBC = 64, kGBR = 16, kGBS = 3, kGBP = kGBR + 1;
+
+__device__ __forceinline__ uint32_t smem_u32a(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+template <int B>
+__device__ __forceinline__ void cp_async_el(void* dst, const void* src, bool pred) {
+  const int sz = pred ? B : 0;  // src-size 0: zero-fill, nothing read
+  if constexpr (B == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32a(dst)), "l"(src),
+                 "r"(sz) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(smem_u32a(dst)), "l"(src),
+                 "n"(B), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <typename TX>
+constexpr size_t dense_gemm_smem() {
+  return (size_t)kGBS * kGBR * kGBJ * sizeof(double) + (size_t)kGBS * kGBC * kGBP * sizeof(TX);
+}
 
 template <typename TX>
 __global__ void __launch_bounds__(256)
@@ -289,8 +315,10 @@ dense_gemm_kernel(const double* __restrict__ thetaT, int64_t ldt, int k,
                   double* __restrict__ partials, const sgs_status* st) {
   pdl_enter();
   if (status_stopped(st)) return;
-  __shared__ __align__(16) double As[2][kGBR][kGBJ];
-  __shared__ __align__(16) double Bs[2][kGBR][kGBC];
+  extern __shared__ __align__(16) unsigned char gsm_raw[];
+  double (*As)[kGBR][kGBJ] = reinterpret_cast<double (*)[kGBR][kGBJ]>(gsm_raw);
+  TX (*Bt)[kGBC][kGBP] = reinterpret_cast<TX (*)[kGBC][kGBP]>(
+      gsm_raw + (size_t)kGBS * kGBR * kGBJ * sizeof(double));
   const int jt = blockIdx.x * kGBJ, ct = blockIdx.y * kGBC;
   const int p = blockIdx.z, nparts = gridDim.z;
   const int64_t r0 = chunk_begin(n, nparts, p), r1 = chunk_begin(n, nparts, p + 1);
@@ -302,39 +330,53 @@ dense_gemm_kernel(const double* __restrict__ thetaT, int64_t ldt, int k,
   for (int a = 0; a < 8; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  auto load_stage = [&](int buf, int64_t rs) {
-    const int nrow = (int)min((int64_t)kGBR, r1 - rs);
-    for (int e = threadIdx.x; e < kGBR * kGBJ; e += blockDim.x) {
-      const int rr = e / kGBJ, jj = e % kGBJ;
-      As[buf][rr][jj] = (rr < nrow && jt + jj < k) ? __ldg(thetaT + (rs + rr) * ldt + jt + jj) : 0.0;
+  const int nst = (int)((r1 - r0 + kGBR - 1) / kGBR);
+  auto issue = [&](int sidx) {
+    if (sidx < nst) {
+      const int buf = sidx % kGBS;
+      const int64_t rs = r0 + (int64_t)sidx * kGBR;
+      // Theta^T: kGBR rows x kGBJ doubles, 16-byte chunks (ldt even, zero padded)
+#pragma unroll
+      for (int u = 0; u < kGBR * kGBJ / 2 / 256; ++u) {
+        const int e = threadIdx.x + u * 256;
+        const int rr = e / (kGBJ / 2), jj = 2 * (e % (kGBJ / 2));
+        const bool ok = rs + rr < r1 && jt + jj < ldt;
+        const double* src = ok ? thetaT + (rs + rr) * ldt + jt + jj : thetaT;
+        cp_async_el<16>(&As[buf][rr][jj], src, ok);
+      }
+      // W: kGBC columns x kGBR rows, one element per copy, stored transposed
+#pragma unroll
+      for (int u = 0; u < kGBR * kGBC / 256; ++u) {
+        const int e = threadIdx.x + u * 256;
+        const int cc = e / kGBR, rr = e % kGBR;
+        const bool ok = rs + rr < r1 && ct + cc < ncols;
+        const TX* src = ok ? X + (int64_t)(ct + cc) * ldx + rs + rr : X;
+        cp_async_el<sizeof(TX)>(&Bt[buf][cc][rr], src, ok);
+      }
     }
-    for (int e = threadIdx.x; e < kGBR * kGBC; e += blockDim.x) {
-      const int cc = e / kGBR, rr = e % kGBR;
-      Bs[buf][rr][cc] = (rr < nrow && ct + cc < ncols)
-                            ? (double)__ldg(X + (int64_t)(ct + cc) * ldx + rs + rr) : 0.0;
-    }
+    cp_async_commit();  // one group per stage slot, even when empty
   };
-  int buf = 0;
-  if (r0 < r1) load_stage(0, r0);
-  __syncthreads();
-  for (int64_t rs = r0; rs < r1; rs += kGBR) {
-    const int nrow = (int)min((int64_t)kGBR, r1 - rs);
-    if (rs + kGBR < r1) load_stage(buf ^ 1, rs + kGBR);
+#pragma unroll
+  for (int q = 0; q < kGBS - 1; ++q) issue(q);
+  for (int sidx = 0; sidx < nst; ++sidx) {
+    cp_async_wait<kGBS - 2>();
+    __syncthreads();          // stage sidx landed; stage sidx-1's buffer is free
+    issue(sidx + kGBS - 1);
+    const int buf = sidx % kGBS;
+    const int nrow = (int)min((int64_t)kGBR, r1 - (r0 + (int64_t)sidx * kGBR));
     for (int rr = 0; rr < nrow; ++rr) {  // ascending rows: the GEMV's chain
       const double4 a0 = *reinterpret_cast<const double4*>(&As[buf][rr][tx * 4]);
       const double4 a1 = *reinterpret_cast<const double4*>(&As[buf][rr][64 + tx * 4]);
-      const double2 b0 = *reinterpret_cast<const double2*>(&Bs[buf][rr][ty * 2]);
-      const double2 b1 = *reinterpret_cast<const double2*>(&Bs[buf][rr][32 + ty * 2]);
       const double av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const double bv[4] = {b0.x, b0.y, b1.x, b1.y};
+      const double bv[4] = {(double)Bt[buf][ty * 2][rr], (double)Bt[buf][ty * 2 + 1][rr],
+                            (double)Bt[buf][32 + ty * 2][rr], (double)Bt[buf][33 + ty * 2][rr]};
 #pragma unroll
       for (int a = 0; a < 8; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
     }
-    __syncthreads();
-    buf ^= 1;
   }
+  cp_async_wait<0>();
 #pragma unroll
   for (int a = 0; a < 8; ++a) {
     const int j = jt + (a < 4 ? tx * 4 + a : 64 + tx * 4 + a - 4);
@@ -619,8 +661,11 @@ static int launch_dense(const double* thetaT, int64_t ldt, int k, const void* X,
     return check_ex(e, "dense_gemv_kernel");
   }
   dim3 grid((k + kGBJ - 1) / kGBJ, (ncols + kGBC - 1) / kGBC, np);
-  return check_ex(launch_ex(dense_gemm_kernel<TX>, grid, dim3(256), 0, s, 1, thetaT, ldt, k, x,
-                            ldx, ncols, n, partials, st), "dense_gemm_kernel");
+  constexpr size_t smem = dense_gemm_smem<TX>();
+  cudaFuncSetAttribute(dense_gemm_kernel<TX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  return check_ex(launch_ex(dense_gemm_kernel<TX>, grid, dim3(256), smem, s, 1, thetaT, ldt, k,
+                            x, ldx, ncols, n, partials, st), "dense_gemm_kernel");
 }
 
 extern "C" int sgs_dense_partials(const double* thetaT, int64_t ldt, int k, const void* X,
