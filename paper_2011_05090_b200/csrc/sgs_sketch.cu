@@ -518,7 +518,7 @@ dense_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW*
 #pragma unroll
   for (int q = 0; q < QP; ++q) acc2[q] = make_double2(0.0, 0.0);
   int64_t r = r0;
-  constexpr int U = (QP <= 2) ? 8 : 4;
+  constexpr int U = (QP == 1) ? 16 : (QP <= 2) ? 8 : 4;  // Theta rows in flight
   for (; r + U <= r1; r += U) {
     double2 tv[U][QP];
 #pragma unroll
