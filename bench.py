@@ -289,7 +289,7 @@ def run_qr(args, cfg_name):
         except Exception:
             pass
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": traffic, "traffic_note": traffic_note, "kernel": "rgs_column_kernel (update + SRHT epilogue)" if cfg["kind"] != "gaussian" else "rgs_update_kernel + dense_gemv_kernel (Theta stream)",
+                "frac": round(ach / peak, 4), "traffic": traffic, "traffic_note": traffic_note, "kernel": "rgs_column_kernel (update + SRHT epilogue)" if cfg["kind"] != "gaussian" else "dense_ring_kernel (Q + Theta^T through a TMA bulk-copy ring)",
                 "peak_source": peak_kind,
                 "share_of_step": round(tot_ms / ms, 4),
                 "launches": len(evs), "avg_launch_us": round(1e3 * tot_ms / len(evs), 2)}

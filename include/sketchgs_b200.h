@@ -94,6 +94,9 @@ int sgs_srht_partials(const void* X, int x_dtype, int64_t ldx, int ncols,
  * ncols>1 a split-K GEMM; both accumulate each chunk in ascending row order,
  * so apply_block is bit-identical to apply. */
 int sgs_dense_nparts(int64_t n);
+/* Partial k-vectors per column written by sgs_rgs_update_dense (its own
+ * 16-row-aligned chunking, about two chunks per SM). */
+int sgs_dense_column_nparts(int64_t n_local, int k);
 int sgs_dense_partials(const double* thetaT, int64_t ldt, int k,
                        const void* X, int x_dtype, int64_t ldx, int ncols,
                        int64_t n, double* partials, const sgs_status* st,

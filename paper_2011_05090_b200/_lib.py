@@ -57,6 +57,7 @@ _SIGS = {
     "sgs_srht_partials": (c_int, [c_void_p, c_int, c_int64, c_int, c_int64, c_int64, c_int,
                                   c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
     "sgs_dense_nparts": (c_int, [c_int64]),
+    "sgs_dense_column_nparts": (c_int, [c_int64, c_int]),
     "sgs_dense_partials": (c_int, [c_void_p, c_int64, c_int, c_void_p, c_int, c_int64, c_int,
                                    c_int64, c_void_p, c_void_p, c_void_p]),
     "sgs_partials_reduce": (c_int, [c_void_p, c_int, c_int, c_int, c_double, c_void_p, c_int,

@@ -16,6 +16,9 @@
 #include "sgs_common.cuh"
 #include "sgs_fwht.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace cg = cooperative_groups;
 
 namespace sgs {
@@ -259,9 +262,277 @@ static int64_t column_ctas(int64_t n_local) {
   return (nt + kColCluster - 1) / kColCluster * kColCluster;
 }
 
+// ===========================================================================
+// Fused dense-sketch column kernel (Gaussian / Rademacher Theta, step 3 + the
+// sketch of step 4 as Theta^T rows): one CTA per row chunk streams, through a
+// ring of TMA bulk copies, first the chunk's segments of Q[:, :i] (grouped
+// several columns per stage) and then the chunk's rows of Theta^T (contiguous,
+// several rows per stage).  q'_i = cast(w) - Q r accumulates per row in column
+// order; the GEMV sum_r Theta[:, r] q'_r accumulates per sketch row in row
+// order - the chains of the register version.  Chunks are 16-row aligned (the
+// bulk copies need 16-byte aligned sources), one partial k-vector per chunk.
+constexpr int kDcStageBytes = 53248;  // large bulk copies: measured best (c0)
+constexpr int kDcStages = 2;
+constexpr int kDcMaxRPT = 4;  // chunk rows per thread
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* mb) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mb)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* mb, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_copy_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* mb, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(mb)),
+      "l"(policy) : "memory");
+}
+
+template <typename TQ, typename TW, int QP>
+__global__ void __launch_bounds__(512)
+dense_ring_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* __restrict__ w,
+                  const TQ* __restrict__ rc, int normalize_prev, const double* __restrict__ R,
+                  int64_t ldr, int do_sketch, const double* __restrict__ thetaT, int64_t ldt,
+                  int k, double* __restrict__ partials, int64_t chunk, int stage_bytes,
+                  const sgs_status* st) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* ring = smem_raw;  // kDcStages x stage_bytes
+  double* xq = reinterpret_cast<double*>(smem_raw + (size_t)kDcStages * stage_bytes);  // chunk
+  TQ* rs = reinterpret_cast<TQ*>(xq + chunk);                                           // i
+  // full[s]: the stage's bytes landed; empty[s]: every warp has read it
+  __shared__ uint64_t full[kDcStages], empty[kDcStages];
+  const int tid = threadIdx.x, T = blockDim.x;
+  const int nwarps = T >> 5;
+  const int p = blockIdx.x;
+  const int64_t r0 = (int64_t)p * chunk;
+  const int nr = (int)min(chunk, n - r0);
+  const int nplain = (i == 0) ? 0 : (normalize_prev ? i - 1 : i);
+  const uint32_t segb = (uint32_t)(((size_t)nr * sizeof(TQ) + 15) / 16 * 16);
+  const int G = max(1, stage_bytes / (int)segb);               // Q columns per stage
+  const uint32_t rowb = (uint32_t)(ldt * sizeof(double));
+  const int Rr = max(1, stage_bytes / (int)rowb);               // Theta rows per stage
+  const int n1 = (nplain + G - 1) / G;
+  const int n2 = do_sketch ? (nr + Rr - 1) / Rr : 0;
+  const int ntot = n1 + n2;
+  uint64_t policy = 0;
+  if (tid == 0) {
+    for (int q = 0; q < kDcStages; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], nwarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  }
+  __syncthreads();
+  auto issue = [&](int t) {
+    unsigned char* buf = ring + (size_t)(t % kDcStages) * stage_bytes;
+    uint64_t* mb = &full[t % kDcStages];
+    if (t < n1) {
+      const int j0 = t * G, j1 = min(nplain, j0 + G);
+      mbar_expect(mb, (uint32_t)(j1 - j0) * segb);
+      for (int j = j0; j < j1; ++j)
+        tma_copy_1d(buf + (size_t)(j - j0) * segb, Q + (int64_t)j * ldq + r0, segb, mb, policy);
+    } else {
+      const int rr0 = (t - n1) * Rr, rr1 = min(nr, rr0 + Rr);
+      const uint32_t bytes = (uint32_t)(rr1 - rr0) * rowb;
+      mbar_expect(mb, bytes);
+      tma_copy_1d(buf, thetaT + (r0 + rr0) * ldt, bytes, mb, policy);
+    }
+  };
+  // Q[:, :nplain] and Theta are final before the predecessor started, w is an
+  // input: the ring prologue and the w rows go out before the dependency wait
+  if (tid == 0)
+    for (int t = 0; t < kDcStages && t < ntot; ++t) issue(t);
+  TQ wv[kDcMaxRPT];
+#pragma unroll
+  for (int u = 0; u < kDcMaxRPT; ++u) {
+    const int lr = tid + u * T;
+    wv[u] = lr < nr ? cvt<TQ>(__ldcs(w + r0 + lr)) : TQ(0);
+  }
+  pdl_enter();
+  if (status_stopped(st)) {  // uniform; drain the prologue before leaving
+    if (tid == 0)
+      for (int t = 0; t < kDcStages && t < ntot; ++t) mbar_wait(&full[t], 0u);
+    __syncthreads();
+    return;
+  }
+  for (int j = tid; j < i; j += T) rs[j] = rc[j];
+  __syncthreads();
+  TQ acc[kDcMaxRPT];
+#pragma unroll
+  for (int u = 0; u < kDcMaxRPT; ++u) acc[u] = TQ(0);
+  const int kp = (k + 1) >> 1;
+  double2 acc2[QP];
+#pragma unroll
+  for (int q = 0; q < QP; ++q) acc2[q] = make_double2(0.0, 0.0);
+  auto finish_update = [&]() {  // q'_i for the chunk; the Theta stages read xq
+#pragma unroll
+    for (int u = 0; u < kDcMaxRPT; ++u) {
+      const int lr = tid + u * T;
+      if (lr >= nr) continue;
+      const int64_t r = r0 + lr;
+      TQ a = acc[u];
+      if (i > 0 && normalize_prev) {
+        const int jj = i - 1;
+        TQ* cp = Q + (int64_t)jj * ldq + r;
+        const TQ qn = cvt<TQ>((double)*cp / R[(int64_t)jj * ldr + jj]);
+        *cp = qn;
+        a = fma(qn, rs[jj], a);
+      }
+      const TQ out = wv[u] - a;
+      Q[(int64_t)i * ldq + r] = out;
+      xq[lr] = (double)out;
+    }
+    __syncthreads();
+  };
+  if (n1 == 0) finish_update();
+  for (int t = 0; t < ntot; ++t) {
+    const int sidx = t % kDcStages;
+    const uint32_t ph = (uint32_t)((t / kDcStages) & 1);
+    // producer: refill the slot released kDcStages stages ago, as soon as every
+    // warp has read it (no block barrier on the consumers' path)
+    if (tid == 0 && t >= 1 && t - 1 + kDcStages < ntot) {
+      const int tr = t - 1;
+      mbar_wait(&empty[tr % kDcStages], (uint32_t)((tr / kDcStages) & 1));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(tr + kDcStages);
+    }
+    mbar_wait(&full[sidx], ph);
+    const unsigned char* buf = ring + (size_t)sidx * stage_bytes;
+    if (t < n1) {
+      const int j0 = t * G, j1 = min(nplain, j0 + G);
+      for (int j = j0; j < j1; ++j) {
+        const TQ* col = reinterpret_cast<const TQ*>(buf + (size_t)(j - j0) * segb);
+        const TQ c = rs[j];
+#pragma unroll
+        for (int u = 0; u < kDcMaxRPT; ++u) {
+          const int lr = tid + u * T;
+          if (lr < nr) acc[u] = fma(col[lr], c, acc[u]);
+        }
+      }
+    } else {
+      const int rr0 = (t - n1) * Rr, rr1 = min(nr, rr0 + Rr);
+      for (int rr = rr0; rr < rr1; ++rr) {
+        const double xv = xq[rr];
+        const double2* trow = reinterpret_cast<const double2*>(buf + (size_t)(rr - rr0) * rowb);
+#pragma unroll
+        for (int q = 0; q < QP; ++q) {
+          const int jj = tid + q * T;
+          if (jj < kp) {
+            const double2 tv = trow[jj];
+            acc2[q].x = fma(tv.x, xv, acc2[q].x);
+            acc2[q].y = fma(tv.y, xv, acc2[q].y);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[sidx]);  // this warp is done with stage t
+    if (t == n1 - 1) finish_update();
+  }
+  if (!do_sketch) return;
+  double* outp = partials + (int64_t)p * k;
+#pragma unroll
+  for (int q = 0; q < QP; ++q) {
+    const int jj = tid + q * T;
+    if (2 * jj < k) outp[2 * jj] = acc2[q].x;
+    if (2 * jj + 1 < k) outp[2 * jj + 1] = acc2[q].y;
+  }
+}
+
+// Row chunking of dense_ring_kernel: about two chunks per SM, 16-row aligned,
+// at most kDcMaxRPT rows per thread.
+static void dense_ring_geom(int64_t n, int threads, int64_t* chunk, int* np) {
+  int64_t c = (n + 2 * (int64_t)sm_count() - 1) / (2 * (int64_t)sm_count());
+  const int64_t cmax = (int64_t)kDcMaxRPT * threads / 16 * 16;
+  if (c > cmax) c = cmax;
+  c = (c + 15) / 16 * 16;
+  if (c < 16) c = 16;
+  *chunk = c;
+  *np = (int)((n + c - 1) / c);
+}
+
+static int dense_ring_threads(int k) {
+  const int kp = (k + 1) / 2;
+  int threads = ((kp + 31) / 32) * 32;
+  if (threads < 256) threads = 256;
+  if (threads > 512) threads = 512;
+  return threads;
+}
+
+template <typename TQ, typename TW>
+static int launch_dense_ring(void* Q, int64_t ldq, int64_t n, int i, const void* w,
+                             const void* r_crs, int normalize_prev, const double* R, int64_t ldr,
+                             int do_sketch, const double* thetaT, int64_t ldt, int k,
+                             double* partials, const sgs_status* st, cudaStream_t s) {
+  const int threads = dense_ring_threads(k);
+  const int kp = (k + 1) / 2;
+  const int qp = (kp + threads - 1) / threads;
+  int64_t chunk;
+  int np;
+  dense_ring_geom(n, threads, &chunk, &np);
+  const int stage_bytes = (int)std::max<int64_t>(kDcStageBytes, ((int64_t)ldt * 8 + 15) / 16 * 16);
+  const size_t smem = (size_t)kDcStages * stage_bytes + (size_t)chunk * 8 +
+                      (size_t)(i > 0 ? i : 1) * sizeof(TQ);
+  if (smem > 227 * 1024) {
+    set_error("dense column: k=%d / i=%d need %zu bytes of shared memory", k, i, smem);
+    return SGS_EINVAL;
+  }
+  cudaError_t e;
+#define SGS_DR(QPV)                                                                              \
+  do {                                                                                           \
+    auto kern = dense_ring_kernel<TQ, TW, QPV>;                                                  \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
+    e = launch_ex(kern, dim3(np), dim3(threads), smem, s, 1, static_cast<TQ*>(Q), ldq, n, i,     \
+                  static_cast<const TW*>(w), static_cast<const TQ*>(r_crs), normalize_prev, R,   \
+                  ldr, do_sketch, thetaT, ldt, k, partials, chunk, stage_bytes, st);             \
+  } while (0)
+  if (qp <= 1) SGS_DR(1);
+  else if (qp <= 2) SGS_DR(2);
+  else if (qp <= 4) SGS_DR(4);
+  else if (qp <= 8) SGS_DR(8);
+  else {
+    set_error("dense column: k=%d too large", k);
+    return SGS_EINVAL;
+  }
+#undef SGS_DR
+  return check_ex(e, "dense_ring_kernel");
+}
+
 }  // namespace sgs
 
 using namespace sgs;
+
+extern "C" int sgs_dense_column_nparts(int64_t n_local, int k) {
+  if (n_local < 1 || k < 1) return 0;
+  int64_t chunk;
+  int np;
+  dense_ring_geom(n_local, dense_ring_threads(k), &chunk, &np);
+  return np;
+}
+
+extern "C" int sgs_rgs_update_dense(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
+                                    const void* w, int w_dtype, const void* r_crs,
+                                    int normalize_prev, const double* R, int64_t ldr,
+                                    int do_sketch, const double* thetaT, int64_t ldt, int k,
+                                    double* partials, const sgs_status* st, void* stream) {
+  SGS_REQUIRE(Q && w && (i == 0 || r_crs) && n >= 1 && i >= 0, "update_dense: bad args");
+  SGS_REQUIRE(!normalize_prev || (i > 0 && R), "update_dense: normalize_prev needs R");
+  SGS_REQUIRE(!do_sketch || (thetaT && partials && ldt >= k && (ldt % 2) == 0 &&
+                             ((uintptr_t)thetaT & 15) == 0), "update_dense: sketch args");
+  SGS_REQUIRE(((uintptr_t)Q & 15) == 0 && (ldq % 16) == 0, "update_dense: Q alignment");
+  cudaStream_t s = as_stream(stream);
+#define SGS_DCL(TQ, TW)                                                                          return launch_dense_ring<TQ, TW>(Q, ldq, n, i, w, r_crs, normalize_prev, R, ldr, do_sketch,                                      thetaT, ldt, k, partials, st, s)
+  if (q_dtype == SGS_F32 && w_dtype == SGS_F32) SGS_DCL(float, float);
+  if (q_dtype == SGS_F32 && w_dtype == SGS_F64) SGS_DCL(float, double);
+  if (q_dtype == SGS_F64 && w_dtype == SGS_F32) SGS_DCL(double, float);
+  if (q_dtype == SGS_F64 && w_dtype == SGS_F64) SGS_DCL(double, double);
+#undef SGS_DCL
+  set_error("update_dense: bad dtype");
+  return SGS_EINVAL;
+}
 
 extern "C" int sgs_column_nparts(int64_t n_local) {
   return n_local < 1 ? 0 : (int)(column_ctas(n_local) / kColCluster);

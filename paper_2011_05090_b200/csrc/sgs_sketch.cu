@@ -441,162 +441,6 @@ static int launch_fwht_tile(double* X, int64_t ldx, int64_t ntile, int ncols, cu
 }
 
 
-// ---------------------------------------------------------------------------
-// Fused column kernel for dense sketches (Gaussian / Rademacher, BASELINE
-// config 0): step 3 of push for the CTA's row chunk (the chunks of the dense
-// sketch, chunk_begin), q' kept in shared memory, then step 4 as the GEMV of
-// Theta^T[chunk, :] with q' - the same ascending-row FMA chain as
-// dense_gemv_kernel, so the sketch is bit-identical to the stand-alone one.
-template <typename TQ, typename TW, int QP>
-__global__ void __launch_bounds__(512)
-dense_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* __restrict__ w,
-                    const TQ* __restrict__ rc, int normalize_prev, const double* __restrict__ R,
-                    int64_t ldr, int do_sketch, const double* __restrict__ thetaT, int64_t ldt,
-                    int k, double* __restrict__ partials, const sgs_status* st) {
-  pdl_enter();
-  if (status_stopped(st)) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  TQ* rs = reinterpret_cast<TQ*>(smem_raw);                       // i coefficients
-  double* xq = reinterpret_cast<double*>(smem_raw + ((size_t)(i > 0 ? i : 1) * sizeof(TQ) + 15) / 16 * 16);
-  const int p = blockIdx.x, nparts = gridDim.x;
-  const int64_t r0 = chunk_begin(n, nparts, p), r1 = chunk_begin(n, nparts, p + 1);
-  for (int j = threadIdx.x; j < i; j += blockDim.x) rs[j] = rc[j];
-  __syncthreads();
-  const int nplain = (i == 0) ? 0 : (normalize_prev ? i - 1 : i);
-  // rows of the chunk in passes of 2 x blockDim, each a single sweep over the columns
-  constexpr int RPT = 2;
-  for (int64_t base = r0; base < r1; base += (int64_t)RPT * blockDim.x) {
-  int64_t rr[RPT];
-  bool ok[RPT];
-#pragma unroll
-  for (int u = 0; u < RPT; ++u) {
-    rr[u] = base + threadIdx.x + (int64_t)u * blockDim.x;
-    ok[u] = rr[u] < r1;
-  }
-  TQ acc[RPT];
-#pragma unroll
-  for (int u = 0; u < RPT; ++u) acc[u] = TQ(0);
-  if (ok[0]) {
-    int j = 0;
-    for (; j + 8 <= nplain; j += 8) {
-      TQ q[8][RPT];
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-#pragma unroll
-        for (int u = 0; u < RPT; ++u)
-          q[c][u] = ok[u] ? __ldcs(Q + (int64_t)(j + c) * ldq + rr[u]) : TQ(0);
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-#pragma unroll
-        for (int u = 0; u < RPT; ++u) acc[u] = fma(q[c][u], rs[j + c], acc[u]);
-    }
-    for (; j < nplain; ++j)
-#pragma unroll
-      for (int u = 0; u < RPT; ++u)
-        if (ok[u]) acc[u] = fma(__ldcs(Q + (int64_t)j * ldq + rr[u]), rs[j], acc[u]);
-  }
-#pragma unroll
-  for (int u = 0; u < RPT; ++u) {
-    if (!ok[u]) continue;
-    const int64_t r = rr[u];
-    if (i > 0 && normalize_prev) {
-      const int jj = i - 1;
-      TQ* cp = Q + (int64_t)jj * ldq + r;
-      const TQ qn = cvt<TQ>((double)*cp / R[(int64_t)jj * ldr + jj]);
-      *cp = qn;
-      acc[u] = fma(qn, rs[jj], acc[u]);
-    }
-    const TQ out = cvt<TQ>(__ldcs(w + r)) - acc[u];
-    Q[(int64_t)i * ldq + r] = out;
-    xq[r - r0] = (double)out;
-  }
-  }  // row passes
-  if (!do_sketch) return;
-  __syncthreads();
-  const int kp = (k + 1) >> 1;
-  double2 acc2[QP];
-#pragma unroll
-  for (int q = 0; q < QP; ++q) acc2[q] = make_double2(0.0, 0.0);
-  int64_t r = r0;
-  constexpr int U = (QP == 1) ? 16 : (QP <= 2) ? 8 : 4;  // Theta rows in flight
-  for (; r + U <= r1; r += U) {
-    double2 tv[U][QP];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int q = 0; q < QP; ++q) {
-        const int jj = threadIdx.x + q * blockDim.x;
-        tv[u][q] = jj < kp ? __ldcs(reinterpret_cast<const double2*>(thetaT + (r + u) * ldt) + jj)
-                           : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const double xv = xq[r + u - r0];
-#pragma unroll
-      for (int q = 0; q < QP; ++q) {
-        acc2[q].x = fma(tv[u][q].x, xv, acc2[q].x);
-        acc2[q].y = fma(tv[u][q].y, xv, acc2[q].y);
-      }
-    }
-  }
-  for (; r < r1; ++r) {
-    const double xv = xq[r - r0];
-#pragma unroll
-    for (int q = 0; q < QP; ++q) {
-      const int jj = threadIdx.x + q * blockDim.x;
-      if (jj < kp) {
-        const double2 tv = __ldcs(reinterpret_cast<const double2*>(thetaT + r * ldt) + jj);
-        acc2[q].x = fma(tv.x, xv, acc2[q].x);
-        acc2[q].y = fma(tv.y, xv, acc2[q].y);
-      }
-    }
-  }
-  double* outp = partials + (int64_t)p * k;
-#pragma unroll
-  for (int q = 0; q < QP; ++q) {
-    const int jj = threadIdx.x + q * blockDim.x;
-    if (2 * jj < k) outp[2 * jj] = acc2[q].x;
-    if (2 * jj + 1 < k) outp[2 * jj + 1] = acc2[q].y;
-  }
-}
-
-template <typename TQ, typename TW>
-static int launch_dense_column(void* Q, int64_t ldq, int64_t n, int i, const void* w,
-                               const void* r_crs, int normalize_prev, const double* R,
-                               int64_t ldr, int do_sketch, const double* thetaT, int64_t ldt,
-                               int k, double* partials, const sgs_status* st, cudaStream_t s) {
-  const int np = dense_nparts_host(n);
-  const int kp = (k + 1) / 2;
-  int threads = ((kp + 31) / 32) * 32;
-  if (threads < 256) threads = 256;
-  if (threads > 512) threads = 512;
-  const int qp = (kp + threads - 1) / threads;
-  const int64_t maxchunk = (n + np - 1) / np + 1;
-  if ((size_t)maxchunk * 8 > 160 * 1024) {
-    set_error("dense column: row chunk %lld too large for shared memory", (long long)maxchunk);
-    return SGS_EINVAL;
-  }
-  const size_t smem = ((size_t)(i > 0 ? i : 1) * sizeof(TQ) + 15) / 16 * 16 + (size_t)maxchunk * 8;
-  cudaError_t e;
-#define SGS_DC(QPV)                                                                             \
-  do {                                                                                          \
-    auto kern = dense_column_kernel<TQ, TW, QPV>;                                               \
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
-    e = launch_ex(kern, dim3(np), dim3(threads), smem, s, 1, static_cast<TQ*>(Q), ldq, n, i,    \
-                  static_cast<const TW*>(w), static_cast<const TQ*>(r_crs), normalize_prev, R,  \
-                  ldr, do_sketch, thetaT, ldt, k, partials, st);                                \
-  } while (0)
-  if (qp <= 1) SGS_DC(1);
-  else if (qp <= 2) SGS_DC(2);
-  else if (qp <= 4) SGS_DC(4);
-  else if (qp <= 8) SGS_DC(8);
-  else {
-    set_error("dense column: k=%d too large", k);
-    return SGS_EINVAL;
-  }
-#undef SGS_DC
-  return check_ex(e, "dense_column_kernel");
-}
 
 }  // namespace sgs
 
@@ -757,24 +601,3 @@ extern "C" int sgs_fwht(double* X, int64_t s_len, int ncols, int64_t ldx, void* 
   return SGS_OK;
 }
 
-extern "C" int sgs_rgs_update_dense(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
-                                    const void* w, int w_dtype, const void* r_crs,
-                                    int normalize_prev, const double* R, int64_t ldr,
-                                    int do_sketch, const double* thetaT, int64_t ldt, int k,
-                                    double* partials, const sgs_status* st, void* stream) {
-  SGS_REQUIRE(Q && w && (i == 0 || r_crs) && n >= 1 && i >= 0, "update_dense: bad args");
-  SGS_REQUIRE(!normalize_prev || (i > 0 && R), "update_dense: normalize_prev needs R");
-  SGS_REQUIRE(!do_sketch || (thetaT && partials && ldt >= k && (ldt % 2) == 0 &&
-                             ((uintptr_t)thetaT & 15) == 0), "update_dense: sketch args");
-  cudaStream_t s = as_stream(stream);
-#define SGS_DCL(TQ, TW)                                                                        \
-  return launch_dense_column<TQ, TW>(Q, ldq, n, i, w, r_crs, normalize_prev, R, ldr, do_sketch, \
-                                     thetaT, ldt, k, partials, st, s)
-  if (q_dtype == SGS_F32 && w_dtype == SGS_F32) SGS_DCL(float, float);
-  if (q_dtype == SGS_F32 && w_dtype == SGS_F64) SGS_DCL(float, double);
-  if (q_dtype == SGS_F64 && w_dtype == SGS_F32) SGS_DCL(double, float);
-  if (q_dtype == SGS_F64 && w_dtype == SGS_F64) SGS_DCL(double, double);
-#undef SGS_DCL
-  set_error("update_dense: bad dtype");
-  return SGS_EINVAL;
-}

@@ -202,8 +202,12 @@ class RgsState:
         # fused update + sketch column kernel for SRHT kinds with 4096-row tiles
         self.fused = (not self.theta.is_dense and self.theta.log2_block >= 12
                       and self.row0 % 4096 == 0)
-        self.nparts_q = (int(_lib.load().sgs_column_nparts(self.n_local)) if self.fused
-                         else self.nparts)
+        if self.fused:
+            self.nparts_q = int(_lib.load().sgs_column_nparts(self.n_local))
+        elif self.theta.is_dense:  # the dense column kernel's own row chunks
+            self.nparts_q = int(_lib.load().sgs_dense_column_nparts(self.n_local, self.k))
+        else:
+            self.nparts_q = self.nparts
         self._cap = 0
         self._alloc(max(int(capacity), 2))
         self._parts_s = torch.empty((self.nparts_q, self.k), dtype=torch.float64,
@@ -351,7 +355,7 @@ class RgsState:
                  self._R.data_ptr(), self._cap, 1 if sketch else 0,
                  d["thetaT"].data_ptr() + self.row0 * d["ldt"] * 8, d["ldt"], self.k,
                  self._parts_s.data_ptr(), self.status.ptr, stream_ptr())
-            return self._combine(self._parts_s, self.nparts, kvec) if sketch else None
+            return self._combine(self._parts_s, self.nparts_q, kvec) if sketch else None
         self._update(i, w_ptr, w_code, normalize_prev)
         if not sketch:
             return None
