@@ -85,6 +85,9 @@ def _pack_signs(signs: np.ndarray) -> np.ndarray:
     return bits.view("<u4").astype(np.uint32)
 
 
+MAX_SRHT_ROWS = 8192  # shared-memory bound of the SRHT kernels (BASELINE uses k <= 3000)
+
+
 class SketchOperator:
     """A seeded k x n embedding applied on the GPU without forming it when
     structured (P-SRHT kinds) or as a dense fp64 stream (Gaussian/Rademacher)."""
@@ -97,6 +100,10 @@ class SketchOperator:
                           stacklevel=3)
         if not isinstance(kind, SketchKind):
             raise TypeError(f"unknown sketch kind {kind!r}")
+        if kind in (SketchKind.PSRHT, SketchKind.BLOCK_SRHT) and k > MAX_SRHT_ROWS:
+            # each CTA keeps the k-vector and the sample rows in shared memory
+            raise ValueError(f"P-SRHT sketches support k <= {MAX_SRHT_ROWS} rows on the "
+                             f"B200 kernels (got k={k})")
         self.kind = kind
         self.k = int(k)
         self.n = int(n)

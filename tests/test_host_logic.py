@@ -133,3 +133,10 @@ def test_oracle_sketch_agrees_with_package_construction():
     op = sg.make_sketch(sg.SketchKind.PSRHT, 12, 100, 4)
     orc = OracleSketch("psrht", 12, 100, 4)
     assert np.array_equal(op.signs, orc.signs) and np.array_equal(op.sample_indices, orc.samples)
+
+
+def test_srht_rows_limit_is_explicit():
+    import paper_2011_05090_b200 as sg
+    from paper_2011_05090_b200.sketch import MAX_SRHT_ROWS
+    with pytest.raises(ValueError, match="k <= 8192"):
+        sg.make_sketch(sg.SketchKind.PSRHT, MAX_SRHT_ROWS + 1, 1 << 20, 0)
