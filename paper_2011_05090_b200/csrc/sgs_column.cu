@@ -75,7 +75,7 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
                   const double* __restrict__ R, int64_t ldr, int do_sketch, int64_t row0,
                   int log2_block, const uint32_t* __restrict__ sign_bits,
                   const int32_t* __restrict__ samples, int k, double* __restrict__ partials,
-                  const sgs_status* st, unsigned long long* tl) {
+                  const sgs_status* st, unsigned long long* tl, int pf_cols) {
   cg::cluster_group cl = cg::this_cluster();
   if (tl && threadIdx.x == 0) atomicMin(tl + (int64_t)i * 16 + 0, gtimer());
   constexpr int V = VecT<TQ>::N;                  // rows per vector (4 fp32, 2 fp64)
@@ -121,6 +121,12 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
   if (tid == 0 && active)
     for (int j = 0; j < S && j < nplain; ++j)
       tma_load_1d(ring + (size_t)j * kColT, Q + (int64_t)j * ldq + lr0, bytes, &mbar[j], policy);
+  // The predecessor LS launch keeps HBM idle while it solves: pull the next
+  // pf_cols columns of this tile into L2 meanwhile (one bulk prefetch per thread).
+  if (active && tid >= 32 && tid - 32 < pf_cols && S + tid - 32 < nplain)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                     Q + (int64_t)(S + tid - 32) * ldq + lr0),
+                 "r"(bytes) : "memory");
   int64_t rows[NH];
 #pragma unroll
   for (int hh = 0; hh < NH; ++hh)
@@ -561,6 +567,16 @@ extern "C" int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n,
                       (size_t)(i > 0 ? i : 1) * esz;
   SGS_REQUIRE(smem <= 227 * 1024, "update_srht: i=%d k=%d needs %zu bytes of shared memory", i,
               k, smem);
+  // L2 prefetch budget for the columns behind the ring prologue, spread over
+  // the first wave of tiles
+  static const long pf_bytes = [] {
+    const char* e = getenv("SGS_COL_PF_MB");
+    return (e ? atol(e) : 64L) << 20;
+  }();
+  // (single-wave grids only: later waves start after the wait and just stream)
+  const int pf = nctas > 2 * 148 ? 0
+                                  : (int)std::min<int64_t>(kColThreads - 32,
+                                                           pf_bytes / (nctas * kColT * esz));
   cudaError_t err = cudaSuccess;
 #define SGS_COL(TQ, TW)                                                                       \
   do {                                                                                        \
@@ -569,7 +585,7 @@ extern "C" int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n,
     err = launch_ex(kern, dim3((unsigned)nctas), dim3(kColThreads), smem, s, kColCluster,     \
                     static_cast<TQ*>(Q), ldq, n, i, static_cast<const TW*>(w),                \
                     static_cast<const TQ*>(r_crs), normalize_prev, R, ldr, do_sketch, row0,  \
-                    log2_block, sign_bits, samples, k, partials, st, debug_timeline());       \
+                    log2_block, sign_bits, samples, k, partials, st, debug_timeline(), pf);   \
   } while (0)
   if (q_dtype == SGS_F32 && w_dtype == SGS_F32) SGS_COL(float, float);
   else if (q_dtype == SGS_F32 && w_dtype == SGS_F64) SGS_COL(float, double);

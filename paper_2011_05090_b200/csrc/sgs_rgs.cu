@@ -558,6 +558,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   // CTA's rows of T and, in the fused QR path, the whole solve except the last
   // column's term run while the predecessor column kernel is still streaming Q.
   SGS_TR(0);
+  if (a.timeline && rank == 0 && threadIdx.x == 0) a.timeline[6] = gtimer();
   const int64_t code0 = *reinterpret_cast<volatile const int64_t*>(&a.st->code);
   double dmax = a.st->diag_max, dmin = a.st->diag_min;
   // The previous finalize may have deferred its T column: form it now, while
@@ -571,10 +572,28 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   const int last_fast = a.t_pend ? *reinterpret_cast<volatile const int*>(a.t_pend + 1) : -1;
   const int ncols_t = a.do_finalize ? a.col_fin : a.col_sol;  // columns of T in use
   const int ncache = min(ncols_t, a.cache_cols);
-  for (int e = threadIdx.x; e < ncache * nr; e += blockDim.x) {
-    const int j = e / nr, rr = e - j * nr;
-    if (j != pend) sq[(int64_t)j * RM + rr] = Tm[(int64_t)j * k + ra + rr];
+  {  // warp per column, 4 columns x 3 row groups of loads in flight per lane
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int rb0 = 0; rb0 < nr; rb0 += 96)
+      for (int j0 = wid * 4; j0 < ncache; j0 += nw * 4) {
+        T v[4][3];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int r = 0; r < 3; ++r) {
+            const int j = j0 + c, rr = rb0 + lane + 32 * r;
+            v[c][r] = (j < ncache && rr < nr) ? Tm[(int64_t)j * k + ra + rr] : T(0);
+          }
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int r = 0; r < 3; ++r) {
+            const int j = j0 + c, rr = rb0 + lane + 32 * r;
+            if (j < ncache && j != pend && rr < nr) sq[(int64_t)j * RM + rr] = v[c][r];
+          }
+      }
   }
+  SGS_TR(11);
   const ColSrc<T> TS{sq, RM, ncache, Tm + ra, (int64_t)k};
   // a solve-only launch whose newest column was finalized on the fast path
   // evaluates z by the identity below and needs that column's c1 (even when
@@ -584,6 +603,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     ls_deferred_column<T>(static_cast<const T*>(a.t_coef), pend, pend >= 0 ? pend : last_fast, AL,
                           S, Tm, TS, sq, RM, ncache, k, ra, nr, c1, c2, vt, tmp, red);
   __syncthreads();
+  SGS_TR(12);
   int s0 = 0, s1 = 0;  // output slice of the solve: [0, c) for c = col_sol
   if (a.do_solve) slice(a.col_sol, s0, s1);
   if (fused && code0 == 0) {
@@ -593,6 +613,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     if (i > 0) {
       ls_coldot<T, 1>(TS, nr, 0, i, vp, nullptr, myA + 8 + cap, nullptr);
       xsync();
+      SGS_TR(13);
       ls_gather<T>(XA + 8 + cap, sA, CL, 0, i, AL, zc);
       __syncthreads();
       ls_matvec<T, true>(Rinv, cap, s0, s1, i, zc, yv, red);  // y = R_S^{-1}[:, :i] z[:i]

@@ -34,12 +34,20 @@ for i in range(2, m - 1):
     gap_col_to_ls = t[i, 4] - t[i, 2]      # LS passes its wait after the column kernel's last exit
     gap_ls_to_col = t[i + 1, 1] - t[i, 5]  # next column kernel passes its wait after the LS exit
     period = t[i + 1, 1] - t[i, 1]
-    rows.append((col_run, ls_post, gap_col_to_ls, gap_ls_to_col, period))
+    window = t[i + 1, 1] - t[i + 1, 0]     # next column kernel: entry -> past its wait
+    ls_to_entry = t[i + 1, 0] - t[i, 4]    # LS past its wait -> next column kernel entry
+    ls_entry = t[i, 6] - t[i, 2]           # LS entry relative to the column kernel's last exit
+    ls_pre = t[i, 3] - t[i, 2]             # LS pre-wait work done, relative to that exit
+    rows.append((col_run, ls_post, gap_col_to_ls, gap_ls_to_col, period, window, ls_to_entry,
+                 ls_entry, ls_pre))
 a = np.array(rows)
 out = {}
 for q, part in enumerate(np.array_split(a, 5)):
     out[f"quintile{q}"] = dict(zip(["col_run", "ls_post", "col_exit->ls_go", "ls_exit->col_go",
-                                    "period"], [round(float(x), 2) for x in part.mean(0)]))
-out["mean"] = dict(zip(["col_run", "ls_post", "col_exit->ls_go", "ls_exit->col_go", "period"],
+                                    "period", "prewait_window", "ls_go->col_entry",
+                                    "ls_entry-col_exit", "ls_ready-col_exit"],
+                                   [round(float(x), 2) for x in part.mean(0)]))
+out["mean"] = dict(zip(["col_run", "ls_post", "col_exit->ls_go", "ls_exit->col_go", "period",
+                        "prewait_window", "ls_go->col_entry", "ls_entry-col_exit", "ls_ready-col_exit"],
                        [round(float(x), 2) for x in a.mean(0)]))
 print(json.dumps(out, indent=1))

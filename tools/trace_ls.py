@@ -33,4 +33,11 @@ for dec, rows in enumerate(np.array_split(tr[1:-1], 5)):
     d["total_us"] = round(float(np.mean(rows[:, LAST] - rows[:, 0])) / 1.965e3, 2)
     d["post_wait_us"] = round(float(np.mean(rows[:, LAST] - rows[:, 2])) / 1.965e3, 2)
     out[f"quintile{dec}"] = d
+for dec, rows in enumerate(np.array_split(tr[1:-1], 5)):
+    d = out[f"quintile{dec}"]
+    cyc = lambda a, b: round(float(np.mean(rows[:, b] - rows[:, a])) / 1.965e3, 2)  # noqa: E731
+    d["pre:cache"] = cyc(0, 11)
+    d["pre:deferred"] = cyc(11, 12)
+    d["pre:coldot"] = cyc(12, 13)
+    d["pre:gather+matvec"] = cyc(13, 1)
 print(json.dumps(out, indent=1))
