@@ -53,6 +53,21 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       "l"(policy) : "memory");
 }
 
+__device__ __forceinline__ void l2_prefetch(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// L2 prefetch budget (bytes) of the SRHT column kernel's pre-wait prologue:
+// about what one LS launch's latency lets HBM move (SGS_COL_PF_MB overrides;
+// measured at c1.  The dense ring kernel measured slower with it at c0.)
+static long col_pf_bytes() {
+  static const long b = [] {
+    const char* e = getenv("SGS_COL_PF_MB");
+    return (e ? atol(e) : 64L) << 20;
+  }();
+  return b;
+}
+
 template <typename TQ> struct ColCfg;
 template <> struct ColCfg<float> { static constexpr int kStages = 4; };
 template <> struct ColCfg<double> { static constexpr int kStages = 3; };
@@ -124,9 +139,7 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
   // The predecessor LS launch keeps HBM idle while it solves: pull the next
   // pf_cols columns of this tile into L2 meanwhile (one bulk prefetch per thread).
   if (active && tid >= 32 && tid - 32 < pf_cols && S + tid - 32 < nplain)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                     Q + (int64_t)(S + tid - 32) * ldq + lr0),
-                 "r"(bytes) : "memory");
+    l2_prefetch(Q + (int64_t)(S + tid - 32) * ldq + lr0, bytes);
   int64_t rows[NH];
 #pragma unroll
   for (int hh = 0; hh < NH; ++hh)
@@ -567,16 +580,11 @@ extern "C" int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n,
                       (size_t)(i > 0 ? i : 1) * esz;
   SGS_REQUIRE(smem <= 227 * 1024, "update_srht: i=%d k=%d needs %zu bytes of shared memory", i,
               k, smem);
-  // L2 prefetch budget for the columns behind the ring prologue, spread over
-  // the first wave of tiles
-  static const long pf_bytes = [] {
-    const char* e = getenv("SGS_COL_PF_MB");
-    return (e ? atol(e) : 64L) << 20;
-  }();
+  // L2 prefetch of the columns behind the ring prologue, spread over the tiles
   // (single-wave grids only: later waves start after the wait and just stream)
   const int pf = nctas > 2 * 148 ? 0
                                   : (int)std::min<int64_t>(kColThreads - 32,
-                                                           pf_bytes / (nctas * kColT * esz));
+                                                           col_pf_bytes() / (nctas * kColT * esz));
   cudaError_t err = cudaSuccess;
 #define SGS_COL(TQ, TW)                                                                       \
   do {                                                                                        \

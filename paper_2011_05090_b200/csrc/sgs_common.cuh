@@ -77,6 +77,29 @@ __device__ __forceinline__ T block_sum(T v, T* red) {
   return t;
 }
 
+// Two block sums sharing one barrier pair; each value follows block_sum's
+// order exactly.  `red` must hold 2 * blockDim/32 elements.
+template <typename T>
+__device__ __forceinline__ void block_sum2(T& a, T& b, T* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  __syncthreads();
+  if (lane == 0) {
+    red[warp] = a;
+    red[nw + warp] = b;
+  }
+  __syncthreads();
+  T ta = T(0), tb = T(0);
+  for (int w = 0; w < nw; ++w) {
+    ta += red[w];
+    tb += red[nw + w];
+  }
+  a = ta;
+  b = tb;
+}
+
 // ---- programmatic dependent launch (PDL) ---------------------------------------
 // Every hot-loop kernel is launched with programmatic stream serialisation: it
 // may be scheduled while its predecessor drains, waits here before touching

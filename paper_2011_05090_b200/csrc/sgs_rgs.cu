@@ -443,8 +443,12 @@ __device__ __noinline__ void ls_reduce_parts(const double* parts, int nparts, in
 // Cluster sum of one scalar per CTA from slots[q*stride] (ascending q).
 template <typename T>
 __device__ __forceinline__ T ls_slot_sum(const T* slots, int64_t stride, int CL) {
+  T v[kLsMaxCluster];  // all loads in flight, summed in ascending q
+#pragma unroll
+  for (int q = 0; q < kLsMaxCluster; ++q) v[q] = q < CL ? __ldcg(slots + (int64_t)q * stride) : T(0);
   T s = T(0);
-  for (int q = 0; q < CL; ++q) s += __ldcg(slots + (int64_t)q * stride);
+#pragma unroll
+  for (int q = 0; q < kLsMaxCluster; ++q) if (q < CL) s += v[q];
   return s;
 }
 
@@ -622,6 +626,13 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
       __syncthreads();
     }
   }
+  if (a.do_finalize && code0 == 0) {  // ||p_i||^2 over this CTA's rows: P is an input
+    const int64_t pi = (int64_t)a.col_fin * k + ra;
+    T l1 = T(0);
+    for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) l1 = fma(P[pi + rr], P[pi + rr], l1);
+    l1 = block_sum(l1, red);
+    if (threadIdx.x == 0) bc[6] = l1;
+  }
   SGS_TR(1);
   unsigned long long* tl = a.timeline;
   if (tl && rank == 0 && threadIdx.x == 0) tl[3] = gtimer();
@@ -643,17 +654,14 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     SGS_TR(3);
     // ---- exchange #1: ||s'||^2, ||p_i||^2, T^T s' --------------------------------
     const bool defer = a.t_pend != nullptr;
-    T l0 = T(0), l1 = T(0), l2 = T(0);
+    T l0 = T(0), l2 = T(0);
     for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
-      const T pv = P[(int64_t)i * k + ra + rr];
       l0 = fma(vs[rr], vs[rr], l0);
-      l1 = fma(pv, pv, l1);
       if (defer && fused) l2 = fma(vs[rr], vp[rr], l2);  // s'^T p_{i+1}
     }
-    l0 = block_sum(l0, red);
-    l1 = block_sum(l1, red);
-    if (defer && fused) l2 = block_sum(l2, red);
-    if (threadIdx.x == 0) { myA[0] = l0; myA[1] = l1; myA[2] = l2; }
+    if (defer && fused) block_sum2(l0, l2, red);
+    else l0 = block_sum(l0, red);
+    if (threadIdx.x == 0) { myA[0] = l0; myA[1] = bc[6]; myA[2] = l2; }  // bc[6]: ||p_i||^2
     if (nq > 0) ls_coldot<T, 1>(TS, nr, 0, nq, vs, nullptr, myA + 8, nullptr);
     xsync();
     SGS_TR(4);
