@@ -169,6 +169,15 @@ def run_qr(args, cfg_name):
     dev = torch.device("cuda", local)
     cfg = CONFIGS[cfg_name]
     n, m, k = cfg["n"], cfg["m"], cfg["k"]
+    if cfg_name == "c4" and world < 4 and args.columns is None:
+        # W and Q are 201 GB each in fp32 (BASELINE configs[4]: 4 and 8 GPUs only)
+        if rank == 0:
+            print(json.dumps({"metric": "RGS-QR columns/s", "impl": "ours", "n_gpus": world,
+                              "unavailable": "c4 needs >= 4 GPUs (W and Q are 201 GB each)"}),
+                  flush=True)
+        return
+    if args.columns is not None:  # functional runs of a config's shapes with fewer columns
+        m = args.columns
     pol = sg.policy_from_name(cfg["policy"])
     bf = cfg["breakdown_factor"]
     kw = {"block_log2": cfg["block_log2"]} if "block_log2" in cfg else {}
@@ -296,7 +305,8 @@ def run_qr(args, cfg_name):
 
     # ---- e2e through the public API (pinned host W -> factors on the host)
     e2e = None
-    if not args.no_e2e:
+    # c4's pinned host shard would be 50 GB per rank: no end-to-end leg there
+    if not args.no_e2e and cfg_name != "c4":
         del graph, gstate
         torch.cuda.empty_cache()
         pin = torch.empty((m, n_loc), dtype=wdt, pin_memory=True)
@@ -344,7 +354,8 @@ def run_qr(args, cfg_name):
             "vs_baseline": None,
             "dtype": "f32 (Q, update) / f64 (sketch, LS)" if cfg["policy"] == "mixed" else "f64",
             "data": "synthetic (W = G diag(sigma) V^T generated on device, seeded)",
-            "config": {"workload": cfg_name + ("-weak" if weak else ""), "n": n, "m": m, "k": k,
+            "config": {"workload": cfg_name + ("-weak" if weak else "")
+                                   + (f"-m{m}" if args.columns is not None else ""), "n": n, "m": m, "k": k,
                        "sketch": cfg["kind"], "policy": cfg["policy"], "breakdown_factor": bf,
                        "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
                        **({"weak": f"n = {world} x {n_per_gpu} rows (~{n_per_gpu} per GPU); "
@@ -558,6 +569,9 @@ def main():
     ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
                     help="N > 1 on c1: weak (1e6 rows per GPU, default) or strong (n = 1e6 split)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--columns", type=int, default=None,
+                    help="override the config's column count (functional runs; the workload "
+                         "name records it)")
     ap.add_argument("--cpu-cols", type=int, default=24)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
