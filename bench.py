@@ -305,12 +305,23 @@ def run_qr(args, cfg_name):
 
     # ---- e2e through the public API (pinned host W -> factors on the host)
     e2e = None
-    # c4's pinned host shard would be 50 GB per rank: no end-to-end leg there
-    if not args.no_e2e and cfg_name != "c4":
+    e2e_note = None
+    # pinned host W and host Q (plus R, S, P) per rank: skip the leg when the
+    # host cannot hold them with a margin (c4: 50 GB per rank; c2: 62.5 GB)
+    import psutil
+    # (torch's pinned allocator rounds each buffer up to a power of two)
+    buf = 1 << int(np.ceil(np.log2(n_loc * m * (4 if wdt == torch.float32 else 8))))
+    need = 2 * buf * (world if comm else 1)
+    if not args.no_e2e and psutil.virtual_memory().available < 1.25 * need:
+        e2e_note = (f"skipped: pinned host W + Q need {need / 2**30:.0f} GiB, "
+                    f"{psutil.virtual_memory().available / 2**30:.0f} GiB available")
+    elif not args.no_e2e:
         del graph, gstate
         torch.cuda.empty_cache()
         pin = torch.empty((m, n_loc), dtype=wdt, pin_memory=True)
         pin.copy_(Wt[:, :n_loc])
+        del Wt  # c2: the device W (62.5 GB) would not fit next to the call's own W and Q
+        torch.cuda.empty_cache()
         Wh = pin.numpy().T  # (n_loc, m) Fortran-ordered numpy view of pinned memory
         kw_sh = {"comm": comm, "row0": row0} if comm else {}
 
@@ -318,12 +329,15 @@ def run_qr(args, cfg_name):
             return sg.rgs_factorize(Wh, th, pol, with_certificate=False, breakdown_factor=bf,
                                     **kw_sh)
 
+        f = None
         for _ in range(2):  # allocates the pinned output buffers once
+            f = None  # the previous result's buffers are reused only once released
             f, _ = e2e_call()
         barrier()
         t0 = time.perf_counter()
         ne = max(1, min(args.steps, 3))
         for _ in range(ne):
+            f = None
             f, _ = e2e_call()
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) / ne
@@ -365,7 +379,8 @@ def run_qr(args, cfg_name):
             "hbm_gbs_whole_step": round(hbm_gbs, 1),
             "hbm_frac_whole_step": round(hbm_gbs / (peak * world), 4),
             "alg_bytes_per_step": alg,
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            **({"e2e_note": e2e_note} if e2e_note else {}), "gpu_launches": launches,
             "clocks": clk,
         }), flush=True)
     if comm:
