@@ -306,6 +306,7 @@ class RgsState:
     _trace = None  # optional (cap, 16) int64 device tensor: per-column LS phase clocks
     _e2e_late = (192, 64)  # pipelined path: (column from which chunks grow, late chunk cap)
     _e2e_ship = 8          # pipelined path: Q columns per D2H copy
+    _e2e_tail = 32         # pipelined path: last columns shipped two at a time
 
     def _trace_ptr(self, col):
         t = self._trace
@@ -649,12 +650,25 @@ class RgsState:
             with torch.cuda.stream(d2h):
                 Qh[c0:c1].copy_(self._Q[c0:c1, :n], non_blocking=True)
 
+        Ph, Parr = _pinned_buffer((m, k), self.fdt)
+
+        def ship_p():  # P is final once the last chunk is sketched
+            ev = torch.cuda.Event()
+            ev.record(comp)
+            d2h.wait_event(ev)
+            with torch.cuda.stream(d2h):
+                Ph.copy_(self._P[:m], non_blocking=True)
+
         sketch_chunk(0)
+        if nchunks == 1:
+            ship_p()
         shipped, ship_chunk = 0, self._e2e_ship
         for i in range(m):
             nxt = i + 1
             if nxt < m and bounds[chunk_of[nxt]] == nxt:
                 sketch_chunk(int(chunk_of[nxt]))
+                if int(chunk_of[nxt]) == nchunks - 1:
+                    ship_p()
             sol = nxt if nxt < m else None
             if i == 0:
                 self._column(0, base, wc, False, False)
@@ -662,16 +676,17 @@ class RgsState:
             else:
                 spp, snp, ssc = self._column(i, base + i * n * esz, wc, True, True)
                 self._ls(fin=i, s_parts=spp, s_nparts=snp, s_scale=ssc, sol=sol)
-                # columns < i are final once the column kernel i has normalised i-1
-                if i - shipped >= ship_chunk:
-                    ship(shipped, shipped + ship_chunk)
-                    shipped += ship_chunk
+                # columns < i are final once the column kernel i has normalised
+                # i-1; finer copies over the last columns keep the tail short
+                step = ship_chunk if i < m - self._e2e_tail else min(ship_chunk, 2)
+                if i - shipped >= step:
+                    ship(shipped, shipped + step)
+                    shipped += step
         self._normalize(m - 1)
-        # the tail: last Q columns and R, S, P into pinned buffers on the copy
+        # the tail: last Q columns and R, S into pinned buffers on the copy
         # stream (pageable .cpu() copies of R/S/P cost ~3.5 ms at c1)
         Rh, Rarr = _pinned_buffer((m, m), torch.float64)
         Sh, Sarr = _pinned_buffer((m, k), self.fdt)
-        Ph, Parr = _pinned_buffer((m, k), self.fdt)
         ev = torch.cuda.Event()
         ev.record(comp)
         d2h.wait_event(ev)
@@ -680,7 +695,6 @@ class RgsState:
                 Qh[shipped:m].copy_(self._Q[shipped:m, :n], non_blocking=True)
             Rh.copy_(self._R[:m, :m], non_blocking=True)
             Sh.copy_(self._S[:m], non_blocking=True)
-            Ph.copy_(self._P[:m], non_blocking=True)
         comp.wait_stream(d2h)
         st = self._sync_status()
         if st["code"]:
