@@ -429,21 +429,24 @@ def run_gmres(args):
     b = torch.from_numpy(b_host).cuda()
     th = sg.make_sketch(sg.SketchKind.PSRHT, cfg["k"], n, 0)
     th.device_data()
-    solve = lambda pol, rhs: sg.gmres_restarted(A, rhs, th, pol, cfg["restart"],  # noqa: E731
-                                                cfg["max_iters"], cfg["tol"])
+    solve = lambda pol, rhs, lagged=False: sg.gmres_restarted(  # noqa: E731
+        A, rhs, th, pol, cfg["restart"], cfg["max_iters"], cfg["tol"], lagged=lagged)
     out = {}
     clocks = Clocks(0)
-    for pname in ("f64", "mixed"):
-        pol = sg.policy_from_name(pname)
+    # standard RGS-Arnoldi (the reference's algorithm) for both bases, then the
+    # one-synchronisation variant as "<basis>_lagged"
+    for pname in ("f64", "mixed", "f64_lagged", "mixed_lagged"):
+        pol = sg.policy_from_name(pname.split("_")[0])
+        lag = pname.endswith("_lagged")
         for _ in range(args.warmup):
-            solve(pol, b)
+            solve(pol, b, lag)
         torch.cuda.synchronize()
         lc0 = _lib.launch_count()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         its = 0
         for _ in range(args.steps):
-            res = solve(pol, b)
+            res = solve(pol, b, lag)
             its += res.iterations
         e1.record()
         torch.cuda.synchronize()
@@ -458,10 +461,10 @@ def run_gmres(args):
     evs = []
     orig = gsm.RgsState._column
 
-    def timed_column(self, i, w_ptr, w_code, normalize_prev, sketch):
+    def timed_column(self, i, w_ptr, w_code, normalize_prev, sketch, **kw):
         a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a_.record()
-        r = orig(self, i, w_ptr, w_code, normalize_prev, sketch)
+        r = orig(self, i, w_ptr, w_code, normalize_prev, sketch, **kw)
         b_.record()
         evs.append((i, a_, b_))
         return r

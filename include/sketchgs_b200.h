@@ -134,11 +134,13 @@ int sgs_rgs_update(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
  * epilogue, without re-reading q'.  One CTA per 4096-row tile (requires
  * log2_block >= 12 and row0 % 4096 == 0), Q streamed through a TMA bulk-copy
  * ring; partials as sgs_srht_partials, one k-vector per 8-CTA cluster,
- * sgs_column_nparts(n_local) of them. */
+ * sgs_column_nparts(n_local) of them.  w_div != NULL (device scalar): the
+ * column is cast(w / w_div[0]) - the lagged w_{i} = A q'_{i-1} / r_{i-1,i-1}
+ * of the one-synchronisation Arnoldi. */
 int sgs_column_nparts(int64_t n_local);
 int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
-                        const void* w, int w_dtype, const void* r_crs,
-                        int normalize_prev, const double* R, int64_t ldr,
+                        const void* w, int w_dtype, const double* w_div /* nullable */,
+                        const void* r_crs, int normalize_prev, const double* R, int64_t ldr,
                         int do_sketch, int64_t row0, int log2_block,
                         const uint32_t* sign_bits, const int32_t* samples, int k,
                         double* partials, const sgs_status* st, void* stream);
@@ -204,6 +206,9 @@ typedef struct sgs_ls_args {
                             publishes r without forming t = s - T c; the next launch forms
                             T[:, t_pend] before its dependency wait, overlapping the column
                             kernel.  Bit-identical T; alpha from the Pythagorean norm. */
+  int p_lag;             /* finalize + solve with p_partials: they hold p' = Theta A q'_fin of the
+                            one-synchronisation Arnoldi, p = p' / r_fin,fin
+                            (stored to P[:, col_sol]); the solve runs after the one exchange */
 } sgs_ls_args;
 
 int64_t sgs_ls_scratch_elems(int k, int cap);

@@ -21,7 +21,8 @@ order, so with single-threaded BLAS it reproduces the reference bit for bit
 
 from .ref_sketch import OracleSketch, fwht_ref, psrht_setup
 from .ref_rgs import OracleRgs, householder_lsq, oracle_certificates, oracle_rgs_factorize
-from .ref_krylov import (OracleIlu0, csr_matvec, oracle_arnoldi, oracle_gmres, oracle_gmres_restarted,
+from .ref_krylov import (OracleIlu0, csr_matvec, oracle_arnoldi, oracle_gmres, oracle_gmres_lagged,
+                         oracle_gmres_restarted,
                          power_norm_estimate)
 from .metrics import factor_metrics, rel_diff
 from .ref_cert import oracle_certify, oracle_epsilon_of, oracle_omega_bar

@@ -41,6 +41,7 @@ class LsArgs(ctypes.Structure):
         ("Qs", c_void_p), ("Rinv", c_void_p), ("alpha", c_void_p), ("scratch", c_void_p),
         ("r_crs", c_void_p), ("st", c_void_p), ("trace", c_void_p), ("cache_cols", c_int),
         ("timeline", c_void_p), ("t_pend", c_void_p), ("t_coef", c_void_p),
+        ("p_lag", c_int),
     ]
 
 
@@ -69,7 +70,7 @@ _SIGS = {
                                c_void_p, c_int, c_void_p, c_int64, c_void_p, c_void_p]),
     "sgs_column_nparts": (c_int, [c_int64]),
     "sgs_rgs_update_srht": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_void_p, c_int,
-                                    c_void_p, c_int, c_void_p, c_int64, c_int, c_int64, c_int,
+                                    c_void_p, c_void_p, c_int, c_void_p, c_int64, c_int, c_int64, c_int,
                                     c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
     "sgs_rgs_update_dense": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_void_p, c_int,
                                      c_void_p, c_int, c_void_p, c_int64, c_int, c_void_p,

@@ -86,7 +86,8 @@ __host__ __device__ constexpr size_t col_ring_bytes() {
 template <typename TQ, typename TW>
 __global__ void __launch_bounds__(kColThreads)
 rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
-                  const TW* __restrict__ w, const TQ* __restrict__ rc, int normalize_prev,
+                  const TW* __restrict__ w, const double* __restrict__ w_div,
+                  const TQ* __restrict__ rc, int normalize_prev,
                   const double* __restrict__ R, int64_t ldr, int do_sketch, int64_t row0,
                   int log2_block, const uint32_t* __restrict__ sign_bits,
                   const int32_t* __restrict__ samples, int k, double* __restrict__ partials,
@@ -145,12 +146,24 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
   for (int hh = 0; hh < NH; ++hh)
     rows[hh] = lr0 + (int64_t)hh * (kColThreads * V) + (int64_t)tid * V;
   TQ wv[NH][V];
+  if (w_div == nullptr) {
 #pragma unroll
-  for (int hh = 0; hh < NH; ++hh)
+    for (int hh = 0; hh < NH; ++hh)
 #pragma unroll
-    for (int v = 0; v < V; ++v)
-      wv[hh][v] = (rows[hh] + v < n) ? cvt<TQ>(__ldcs(w + rows[hh] + v)) : TQ(0);
+      for (int v = 0; v < V; ++v)
+        wv[hh][v] = (rows[hh] + v < n) ? cvt<TQ>(__ldcs(w + rows[hh] + v)) : TQ(0);
+  }
   pdl_enter();
+  if (w_div != nullptr) {
+    // one-synchronisation Arnoldi: w = cast((A q'_{i-1} / alpha) / r_{i-1,i-1}),
+    // the divisor finalized by the predecessor launch
+    const double d = *w_div;
+#pragma unroll
+    for (int hh = 0; hh < NH; ++hh)
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        wv[hh][v] = (rows[hh] + v < n) ? cvt<TQ>((double)__ldcs(w + rows[hh] + v) / d) : TQ(0);
+  }
   if (tl && threadIdx.x == 0) atomicMin(tl + (int64_t)i * 16 + 1, gtimer());
   if (status_stopped(st)) {  // uniform over the grid; drain the prologue before leaving
     if (tid == 0 && active)
@@ -558,9 +571,9 @@ extern "C" int sgs_column_nparts(int64_t n_local) {
 }
 
 extern "C" int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
-                                   const void* w, int w_dtype, const void* r_crs,
-                                   int normalize_prev, const double* R, int64_t ldr,
-                                   int do_sketch, int64_t row0, int log2_block,
+                                   const void* w, int w_dtype, const double* w_div,
+                                   const void* r_crs, int normalize_prev, const double* R,
+                                   int64_t ldr, int do_sketch, int64_t row0, int log2_block,
                                    const uint32_t* sign_bits, const int32_t* samples, int k,
                                    double* partials, const sgs_status* st, void* stream) {
   SGS_REQUIRE(Q && w, "update_srht: null pointer");
@@ -591,7 +604,7 @@ extern "C" int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n,
     auto kern = rgs_column_kernel<TQ, TW>;                                                    \
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
     err = launch_ex(kern, dim3((unsigned)nctas), dim3(kColThreads), smem, s, kColCluster,     \
-                    static_cast<TQ*>(Q), ldq, n, i, static_cast<const TW*>(w),                \
+                    static_cast<TQ*>(Q), ldq, n, i, static_cast<const TW*>(w), w_div,        \
                     static_cast<const TQ*>(r_crs), normalize_prev, R, ldr, do_sketch, row0,  \
                     log2_block, sign_bits, samples, k, partials, st, debug_timeline(), pf);   \
   } while (0)

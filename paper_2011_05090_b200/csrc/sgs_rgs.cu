@@ -514,6 +514,9 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   const int nr = rb - ra;
   const int RM = (k + CL - 1) / CL;
   const bool fused = a.do_finalize && a.do_solve;
+  // one-synchronisation Arnoldi: p'_{i+1} = Theta A q'_i
+  // arrives as partials with s'_i, and p_{i+1} = p'_{i+1} / r_ii
+  const bool lag = fused && a.p_lag && a.p_partials != nullptr;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LsSmem<T> L(smem_raw, RM, cap);
@@ -610,7 +613,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   SGS_TR(12);
   int s0 = 0, s1 = 0;  // output slice of the solve: [0, c) for c = col_sol
   if (a.do_solve) slice(a.col_sol, s0, s1);
-  if (fused && code0 == 0) {
+  if (fused && !lag && code0 == 0) {
     const int i = a.col_fin;  // solve for c = i + 1 uses T[:, :i] now, T[:, i] later
     for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vp[rr] = P[(int64_t)(i + 1) * k + ra + rr];
     __syncthreads();
@@ -650,6 +653,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     } else {
       ls_reduce_parts<T>(a.s_partials, a.s_nparts, k, ra, nr, a.s_scale, vs, dred);
     }
+    if (lag) ls_reduce_parts<T>(a.p_partials, a.p_nparts, k, ra, nr, a.p_scale, vp, dred);  // p'
     __syncthreads();
     SGS_TR(3);
     // ---- exchange #1: ||s'||^2, ||p_i||^2, T^T s' --------------------------------
@@ -662,11 +666,15 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     if (defer && fused) block_sum2(l0, l2, red);
     else l0 = block_sum(l0, red);
     if (threadIdx.x == 0) { myA[0] = l0; myA[1] = bc[6]; myA[2] = l2; }  // bc[6]: ||p_i||^2
-    if (nq > 0) ls_coldot<T, 1>(TS, nr, 0, nq, vs, nullptr, myA + 8, nullptr);
+    if (nq > 0) {
+      if (lag) ls_coldot<T, 2>(TS, nr, 0, nq, vs, vp, myA + 8, myA + 8 + cap);  // + T^T p'
+      else ls_coldot<T, 1>(TS, nr, 0, nq, vs, nullptr, myA + 8, nullptr);
+    }
     xsync();
     SGS_TR(4);
     if (threadIdx.x < 3) bc[threadIdx.x] = ls_slot_sum(XA + threadIdx.x, sA, CL);
     if (nq > 0) ls_gather<T>(XA + 8, sA, CL, 0, nq, AL, c1);  // T^T s' / alpha
+    if (lag && nq > 0) ls_gather<T>(XA + 8 + cap, sA, CL, 0, nq, AL, zc);  // T^T p' / alpha
     __syncthreads();
     const double r_ii = (double)sqrt(bc[0]);
     const double tol = a.bf_ucrs * (double)sqrt(bc[1]);
@@ -680,6 +688,23 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
       return;
     }
     const T rT = (T)r_ii;
+    T sp_dot = bc[2];  // s'^T p_{i+1}
+    if (lag) {  // p_{i+1} = p'_{i+1} / r_ii; Q_s^T p and s'^T p follow linearly
+      sp_dot = bc[2] / rT;
+      for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
+        const T pv = vp[rr] / rT;
+        vp[rr] = pv;
+        P[(int64_t)(i + 1) * k + ra + rr] = pv;
+      }
+      for (int j = threadIdx.x; j < nq; j += blockDim.x) zc[j] = zc[j] / rT;
+      __syncthreads();
+      if (nq > 0) {
+        ls_matvec<T, true>(Rinv, cap, s0, s1, nq, zc, yv, red);  // y = R_S^{-1}[:, :i] z[:i]
+      } else {
+        for (int o = s0 + threadIdx.x; o < s1; o += blockDim.x) yv[o - s0] = T(0);
+        __syncthreads();
+      }
+    }
     T* sprime = defer ? static_cast<T*>(a.t_coef) + cap : nullptr;
     for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
       if (sprime) sprime[ra + rr] = vs[rr];  // s', for a solve-only launch's identity
@@ -715,7 +740,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
       if (nq == 0 || tt_est >= T(0.5) * ss0) {
         explicit_t = false;
         tt = tt_est;
-        if (fused) tp = bc[2] / rT - acc_p;
+        if (fused) tp = sp_dot / rT - acc_p;
         if (rank == 0) {
           T* coef = static_cast<T*>(a.t_coef);
           for (int j = threadIdx.x; j < nq; j += blockDim.x) coef[j] = c1[j];
@@ -1017,6 +1042,8 @@ extern "C" int sgs_ls_step(const sgs_ls_args* a, void* stream) {
   SGS_REQUIRE(!a->do_finalize || a->col_fin == 0 || a->s_partials, "ls_step: s_partials missing");
   SGS_REQUIRE(!(a->do_finalize && a->do_solve) || a->col_sol == a->col_fin + 1,
               "ls_step: fused solve must target the next column");
+  SGS_REQUIRE(!a->p_lag || (a->do_finalize && a->do_solve && a->p_partials),
+              "ls_step: p_lag needs a fused finalize + solve with p partials");
   cudaStream_t s = as_stream(stream);
   if (a->fine_dtype == SGS_F64) return launch_ls<double>(a, s);
   if (a->fine_dtype == SGS_F32) return launch_ls<float>(a, s);

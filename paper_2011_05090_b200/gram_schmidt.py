@@ -277,7 +277,8 @@ class RgsState:
 
     # ---- kernels ---------------------------------------------------------------
     def _ls(self, *, fin: int | None = None, s_parts=None, s_nparts=0, s_scale=1.0,
-            sol: int | None = None, p_parts=None, p_nparts=0, p_scale=1.0) -> None:
+            sol: int | None = None, p_parts=None, p_nparts=0, p_scale=1.0,
+            lag: bool = False) -> None:
         a = self.__dict__.get("_ls_args")
         if a is None:
             a = self._ls_args = _lib.LsArgs()  # reused: the library copies it at launch
@@ -292,6 +293,7 @@ class RgsState:
         a.p_partials = p_parts
         a.p_nparts = p_nparts
         a.p_scale = p_scale
+        a.p_lag = 1 if lag else 0
         a.bf_ucrs = self.breakdown_factor * self.policy.u_crs
         a.S, a.P, a.R = self._S.data_ptr(), self._P.data_ptr(), self._R.data_ptr()
         a.Qs, a.Rinv, a.alpha = self._Qs.data_ptr(), self._Rinv.data_ptr(), self._alpha.data_ptr()
@@ -336,19 +338,29 @@ class RgsState:
              w_ptr, w_code, self._rc.data_ptr(), 1 if normalize_prev else 0,
              self._R.data_ptr(), self._cap, self.status.ptr, stream_ptr())
 
-    def _column(self, i: int, w_ptr: int, w_code: int, normalize_prev: bool, sketch: bool):
+    def _column(self, i: int, w_ptr: int, w_code: int, normalize_prev: bool, sketch: bool,
+                w_div: int | None = None, combine: bool = True):
         """Step 3 (and step 4 when ``sketch``): q'_i = w - Q r into Q[:, i] and the
-        partial sketches of q'_i.  Returns (pointer, nparts, scale) or None."""
+        partial sketches of q'_i.  Returns (pointer, nparts, scale) or None.
+        ``w_div`` (device fp64 scalar, fused SRHT path only): the column is
+        cast(w / w_div).  ``combine=False`` leaves the partials unsummed (the
+        caller combines them, e.g. with another sketch in one all-reduce)."""
         kvec = getattr(self, "_kvec_s", None)
+        if w_div is not None and not self.fused:
+            raise ValueError("w_div needs the fused SRHT column kernel")
         if self.fused:
             d = self._theta_dev
             call("sgs_rgs_update_srht", self._Q.data_ptr(), self.ccode, self.ldq, self.n_local,
-                 i, w_ptr, w_code, self._rc.data_ptr(), 1 if normalize_prev else 0,
+                 i, w_ptr, w_code, w_div, self._rc.data_ptr(), 1 if normalize_prev else 0,
                  self._R.data_ptr(), self._cap, 1 if sketch else 0, self.row0,
                  self.theta.log2_block, d["bits"].data_ptr() + (self.row0 // 32) * 4,
                  d["samples"].data_ptr(), self.k, self._parts_s.data_ptr(), self.status.ptr,
                  stream_ptr())
-            return self._combine(self._parts_s, self.nparts_q, kvec) if sketch else None
+            if not sketch:
+                return None
+            if not combine:
+                return self._parts_s.data_ptr(), self.nparts_q, self.theta.scale
+            return self._combine(self._parts_s, self.nparts_q, kvec)
         if self.theta.is_dense:
             d = self._theta_dev
             call("sgs_rgs_update_dense", self._Q.data_ptr(), self.ccode, self.ldq, self.n_local,
@@ -356,10 +368,18 @@ class RgsState:
                  self._R.data_ptr(), self._cap, 1 if sketch else 0,
                  d["thetaT"].data_ptr() + self.row0 * d["ldt"] * 8, d["ldt"], self.k,
                  self._parts_s.data_ptr(), self.status.ptr, stream_ptr())
-            return self._combine(self._parts_s, self.nparts_q, kvec) if sketch else None
+            if not sketch:
+                return None
+            if not combine:
+                return self._parts_s.data_ptr(), self.nparts_q, self.theta.scale
+            return self._combine(self._parts_s, self.nparts_q, kvec)
         self._update(i, w_ptr, w_code, normalize_prev)
         if not sketch:
             return None
+        if not combine:
+            self.theta.partials_into(self._qcol_ptr(i), self.ccode, self.ldq, 1, self._parts_s,
+                                     n_local=self.n_local, row0=self.row0, status=self.status)
+            return self._parts_s.data_ptr(), self.nparts, self.theta.scale
         return self._sketch_parts(self._qcol_ptr(i), self.ccode, self.ldq, self._parts_s, kvec)
 
     # ---- certification sketches ------------------------------------------------------

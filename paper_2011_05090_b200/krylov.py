@@ -408,15 +408,27 @@ class _ArnoldiEngine:
     normalisation q_i = q'_i / r_ii together with the previous step's Givens
     update), the SpMV (1/alpha folded in), the SRHT of w, the LS solve, the
     fused column kernel (update + sketch of q'_{i+1}) and the LS finalize.
-    Otherwise the generic path (separate SpMV, sketch and normalisation)."""
+    Otherwise the generic path (separate SpMV, sketch and normalisation).
+
+    ``lagged``: the one-synchronisation RGS-Arnoldi of PAPER.md:260-261.  The
+    matvec runs on the unnormalised q'_c right after its column kernel, and
+    one LS launch finalizes column c (r_cc = ||s'_c||) and solves column c+1
+    from p_{c+1} = (Theta A q'_c) / r_cc.  A step is then the column kernel
+    (w = A q'_c / r_cc formed on the fly, q_c normalised in its stream), the
+    SpMV, the SRHT of w and that LS launch, plus the Givens update; sharded,
+    the two k-vectors share one all-reduce."""
 
     def __init__(self, A: SparseMatrix, theta, policy, solver, m: int,
                  breakdown_factor: float = BREAKDOWN_FACTOR, phi=None, M=None,
-                 dist: _Dist | None = None):
+                 dist: _Dist | None = None, lagged: bool = False):
         self.A = A
         self.M = M
         self.m = m
         self.dist = dist
+        self.lagged = bool(lagged)
+        if self.lagged and phi is not None:
+            raise NotImplementedError("certification sketches (phi) are not formed by the "
+                                      "one-synchronisation Arnoldi")
         shard = {} if dist is None else {"comm": dist.comm, "row0": dist.row0,
                                          "n_local": dist.n_loc}
         self.state = RgsState(theta, policy, solver, phi=phi, capacity=m + 2,
@@ -435,6 +447,11 @@ class _ArnoldiEngine:
         self.hist = torch.zeros(m + 1, dtype=torch.float64, device=dev)
         self.norm_flag = torch.full((1,), -1, dtype=torch.int32, device=dev)
         self._owed = None  # step whose Givens update rides on the next step's head
+        if self.lagged:
+            self._kv2 = (torch.empty(2 * st.k, dtype=torch.float64, device=dev)
+                         if dist is not None else None)
+            if not self.fused:
+                self._wdiv = torch.empty(self.n_loc, dtype=torch.float64, device=dev)
 
     def _matvec(self, i: int, out: torch.Tensor, alpha, status) -> None:
         """out = (A M^{-1} q_i) / alpha over this rank's rows."""
@@ -446,13 +463,84 @@ class _ArnoldiEngine:
             xf = self.dist.full(st._Q[i, :self.n_loc])
             self.dist.block.spmv_into(xf.data_ptr(), st.ccode, out, alpha=alpha, status=status)
 
-    def start(self, b_dev: torch.Tensor, b_norm_ptr) -> None:
+    # ---- one-synchronisation (lagged) steps -----------------------------------------
+    def _lag_tail(self, c: int, s_raw, alpha) -> None:
+        """w = A M^{-1} q'_c (/ alpha) from the unnormalised column c, its sketch
+        p', and the LS launch finalizing c and solving c + 1 (p = p' / r_cc).
+        ``s_raw``: raw partials of s'_c (None for c = 0: s'_0 = p_0)."""
+        st, ws = self.state, self.ws
+        if self.dist is None:
+            _eff_matvec_into(self.A, self.M, ws, st._qcol_ptr(c), st.ccode, ws.w, alpha=alpha,
+                             status=st.status)
+        else:
+            xf = self.dist.full(st._Q[c, :self.n_loc])
+            self.dist.block.spmv_into(xf.data_ptr(), st.ccode, ws.w, alpha=alpha, status=st.status)
+        st.theta.partials_into(ws.w.data_ptr(), _lib.SGS_F64, self.n_loc, 1, st._parts_p,
+                               n_local=self.n_loc, row0=st.row0, status=st.status)
+        p_raw = (st._parts_p.data_ptr(), st.nparts, st.theta.scale)
+        if self.dist is not None:  # one all-reduce of [s'; p'] (2k)
+            k, kv = st.k, self._kv2
+            srcs = [(p_raw, kv[k:])] if s_raw is None else [(s_raw, kv[:k]), (p_raw, kv[k:])]
+            for (ptr, npart, _), dst in srcs:
+                call("sgs_partials_reduce", ptr, npart, k, 1, 1.0, dst.data_ptr(), _lib.SGS_F64,
+                     k, st.status.ptr, stream_ptr())
+            self.dist.comm.allreduce_(kv if s_raw is not None else kv[k:])
+            if s_raw is not None:
+                s_raw = (kv.data_ptr(), 1, st.theta.scale)
+            p_raw = (kv[k:].data_ptr(), 1, st.theta.scale)
+        s_ptr, s_np, s_sc = s_raw if s_raw is not None else (None, 0, 1.0)
+        st._ls(fin=c, s_parts=s_ptr, s_nparts=s_np, s_scale=s_sc, sol=c + 1, p_parts=p_raw[0],
+               p_nparts=p_raw[1], p_scale=p_raw[2], lag=True)
+
+    def _start_lagged(self, bn: torch.Tensor, alpha) -> None:
+        st, n = self.state, self.n_loc
+        pp, pn, ps = st._sketch_parts(bn.data_ptr(), _lib.SGS_F64, n, st._parts_p,
+                                      getattr(st, "_kvec_p", None))
+        call("sgs_partials_reduce", pp, pn, st.k, 1, ps, st._P.data_ptr(), st.fcode, st.k,
+             st.status.ptr, stream_ptr())
+        st._column(0, bn.data_ptr(), _lib.SGS_F64, False, False)
+        if self.m >= 1:
+            self._lag_tail(0, None, alpha)
+        else:
+            st._ls(fin=0)
+        st.m = 1
+
+    def _step_lagged(self, i: int, alpha, tol) -> None:
+        """Column i + 1 (its predecessor launch finalized column i and solved i + 1)."""
+        st, ws = self.state, self.ws
+        c = i + 1
+        rii = st._R.data_ptr() + (i * st._cap + i) * 8
+        if self.fused:
+            s_raw = st._column(c, ws.w.data_ptr(), _lib.SGS_F64, True, True, w_div=rii,
+                               combine=False)
+        else:
+            call("sgs_cast_div", ws.w.data_ptr(), _lib.SGS_F64, self._wdiv.data_ptr(),
+                 _lib.SGS_F64, rii, self.n_loc, stream_ptr())
+            s_raw = st._column(c, self._wdiv.data_ptr(), _lib.SGS_F64, True, True, combine=False)
+        if c < self.m:
+            self._lag_tail(c, s_raw, alpha)
+        else:  # last column: finalize only
+            if self.dist is not None:
+                k, kv = st.k, self._kv2
+                call("sgs_partials_reduce", s_raw[0], s_raw[1], k, 1, 1.0, kv.data_ptr(),
+                     _lib.SGS_F64, k, st.status.ptr, stream_ptr())
+                self.dist.comm.allreduce_(kv[:k])
+                s_raw = (kv.data_ptr(), 1, st.theta.scale)
+            st._ls(fin=c, s_parts=s_raw[0], s_nparts=s_raw[1], s_scale=s_raw[2])
+        st.m = c + 1
+        if tol is not None or alpha is not None:
+            self._givens(i, tol)
+
+    def start(self, b_dev: torch.Tensor, b_norm_ptr, alpha=None) -> None:
         """Push b (this rank's rows; divided by ||b|| when b_norm_ptr is given)
-        as column 0."""
+        as column 0 (lagged: and run the first matvec, with ``alpha``)."""
         st, n = self.state, self.n_loc
         bn = self.ws.v
         call("sgs_cast_div", b_dev.data_ptr(), _lib.SGS_F64, bn.data_ptr(), _lib.SGS_F64,
              b_norm_ptr, n, stream_ptr())
+        if self.lagged:
+            self._start_lagged(bn, alpha)
+            return
         if not self.fused:
             st._push_async(bn)
             return
@@ -468,6 +556,9 @@ class _ArnoldiEngine:
         st.m = 1
 
     def step(self, i: int, alpha: torch.Tensor | None, tol: float | None) -> None:
+        if self.lagged:
+            self._step_lagged(i, alpha, tol)
+            return
         st = self.state
         A, ws = self.A, self.ws
         if self.fused:
@@ -529,6 +620,16 @@ class _ArnoldiEngine:
             self._givens(self._owed, tol)
             self._owed = None
         out = st._sync_status()
+        if self.lagged:
+            # every committed column but the newest was normalised by its
+            # successor's column kernel; a breakdown in the finalize of column
+            # ncols means that kernel ran for the newest committed one too
+            nc = out["ncols"]
+            covered = (out["code"] in (_lib.ST_BREAKDOWN, _lib.ST_NONFINITE)
+                       and out["column"] == nc + 1)
+            if nc > 0 and not covered:
+                st._normalize(nc - 1, guarded=False)
+            return out
         # fused path: columns are normalised by the step heads; the newest
         # committed one is still q'/r_ii unless a head (run after a stop, or a
         # breakdown that left the previous column newest) already covered it
@@ -550,17 +651,18 @@ def _make_dist(comm, A: SparseMatrix, theta, M) -> _Dist | None:
 
 def arnoldi(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, theta=None,
             policy: PrecisionPolicy = MIXED32_64, solver: LsqSolver = HOUSEHOLDER_QR,
-            phi=None, *, comm=None) -> ArnoldiDecomposition:
+            phi=None, *, comm=None, lagged: bool = False) -> ArnoldiDecomposition:
     """m-step RGS-Arnoldi (krylov.py:176-199); fewer columns on a lucky
     breakdown.  With ``comm`` the rows are sharded across the ranks (b is the
     full vector on every rank; Q holds this rank's rows, H and R are
-    replicated)."""
+    replicated).  ``lagged``: the one-synchronisation variant of
+    PAPER.md:260-261 (see _ArnoldiEngine)."""
     _check_variant(variant)
     if theta is None:
         raise ValueError("the randomized variant needs a sketch operator")
     _lib.require_cuda()
     dist = _make_dist(comm, A, theta, None)
-    eng = _ArnoldiEngine(A, theta, policy, solver, m, phi=phi, dist=dist)
+    eng = _ArnoldiEngine(A, theta, policy, solver, m, phi=phi, dist=dist, lagged=lagged)
     st = eng.state
     b_dev = _to_device_f64(b, A.n, st.device)
     eng.start(b_dev if dist is None else dist.local(b_dev).contiguous(), None)
@@ -578,12 +680,13 @@ def arnoldi(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, thet
 def gmres(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, theta=None,
           policy: PrecisionPolicy = MIXED32_64, solver: LsqSolver = HOUSEHOLDER_QR,
           preconditioner=None, tol: float | None = None, phi=None, *,
-          comm=None) -> GmresResult:
+          comm=None, lagged: bool = False) -> GmresResult:
     """Single-cycle RGS-GMRES(m) with progressive Givens rotations (krylov.py:229-319),
     right-preconditioned by an ILU(0) ``preconditioner`` when given.  With
     ``comm`` (distributed.TorchComm) the operator rows and every n-vector are
     sharded across the ranks (one tile-aligned row block each); b is the full
-    vector on every rank and so is the returned x."""
+    vector on every rank and so is the returned x.  ``lagged``: Arnoldi by the
+    one-synchronisation RGS of PAPER.md:260-261 (see _ArnoldiEngine)."""
     _check_variant(variant)
     M = _as_preconditioner(preconditioner)
     if theta is None:
@@ -605,12 +708,12 @@ def gmres(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, theta=
                                                              device=device)
         return GmresResult(x=x0, residual_history=np.zeros(0), final_residual=0.0,
                            iterations=0, converged=True, breakdown=False)
-    eng = _ArnoldiEngine(A, theta, policy, solver, m, phi=phi, M=M, dist=dist)
+    eng = _ArnoldiEngine(A, theta, policy, solver, m, phi=phi, M=M, dist=dist, lagged=lagged)
     st = eng.state
     alpha = _operator_norm_estimate(A, eng.ws, M=M, dist=dist)
     if float(alpha) <= 0.0:
         raise np.linalg.LinAlgError("operator norm estimate is zero")
-    eng.start(b_loc, ws0.nrm.data_ptr())
+    eng.start(b_loc, ws0.nrm.data_ptr(), alpha)
     s1 = eng.run(alpha=alpha, tol=tol)
     code = s1["code"]
     if code == _lib.ST_RANK:
@@ -665,12 +768,13 @@ class RestartedResult:
 def gmres_restarted(A: SparseMatrix, b, theta, policy: PrecisionPolicy = MIXED32_64,
                     restart: int = 300, max_iters: int = 3000, tol: float = 1e-8,
                     solver: LsqSolver = HOUSEHOLDER_QR, preconditioner=None, *,
-                    comm=None) -> RestartedResult:
+                    comm=None, lagged: bool = False) -> RestartedResult:
     """Restarted RGMRES(restart) for BASELINE config 3 (the reference is
     single-cycle, krylov.py:236-241; the wrapper is shared verbatim with the
     oracle): each cycle runs gmres(A, r, min(restart, max_iters - its), tol =
     tol * ||b|| / ||r||), then x += dx and r = b - A x in binary64; stop at
-    ||r|| / ||b|| <= tol or its >= max_iters.  ``comm``: row-sharded, as gmres."""
+    ||r|| / ||b|| <= tol or its >= max_iters.  ``comm``: row-sharded, as gmres;
+    ``lagged``: one-synchronisation Arnoldi, as gmres."""
     _lib.require_cuda()
     device = torch.device("cuda", torch.cuda.current_device())
     return_numpy = not (isinstance(b, torch.Tensor) and b.is_cuda)
@@ -697,7 +801,8 @@ def gmres_restarted(A: SparseMatrix, b, theta, policy: PrecisionPolicy = MIXED32
         if b_norm == 0.0 or r_norm / b_norm <= tol or its >= max_iters:
             break
         res = gmres(A, r, m=min(restart, max_iters - its), theta=theta, policy=policy,
-                    solver=solver, tol=tol * b_norm / r_norm, preconditioner=M, comm=comm)
+                    solver=solver, tol=tol * b_norm / r_norm, preconditioner=M, comm=comm,
+                    lagged=lagged)
         cycles.append(res.iterations)
         its += res.iterations
         x += res.x
