@@ -48,33 +48,109 @@ int sm_count() {
 
 // y = (A x) / alpha with, when xdiv != NULL, x = cast(q / xdiv[0]) formed on the
 // fly from a not yet normalised basis column (the rounding the next column
-// kernel applies when it normalises q in place).  Thread per row.
+// kernel applies when it normalises q in place).
+// Staged CSR SpMV: one CTA per kSpRows consecutive rows.  Their nonzeros are
+// contiguous, so one elected thread copies the CTA's column indices and values
+// into shared memory with two TMA bulk copies (evict-first: the CSR stream is
+// read once per step and must not push x or the sketch state out of L2), issued
+// BEFORE the dependency wait - the matrix does not depend on the predecessor,
+// so resident CTAs stream it while the previous kernel drains.  Then thread per
+// row, one fma chain per row in storage order, reading the row's entries from
+// shared memory instead of strided global loads.  A CTA whose
+// range exceeds the buffer, or whose 16-byte-rounded copy would run past the
+// arrays' end, takes the global path (same arithmetic).
+constexpr int kSpRows = 512;
+constexpr int kSpThreads = 256;
+constexpr int kSpCap = kSpRows * 7 + 8;  // staged entries per CTA (7-point stencils fit)
+
+__device__ __forceinline__ uint32_t sp_smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
 template <typename TX>
-__global__ void __launch_bounds__(256)
-csr_spmv_kernel(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                const double* __restrict__ vals, const TX* __restrict__ x,
-                const double* __restrict__ xdiv, const double* __restrict__ alpha,
-                double* __restrict__ y, const sgs_status* st, unsigned long long* tl) {
+__device__ __forceinline__ double sp_xval(const TX* __restrict__ x, int c, const double* xdiv,
+                                          double dv) {
+  const TX xr = __ldg(x + c);
+  if (xdiv == nullptr) return (double)xr;
+  if constexpr (sizeof(TX) == 4) return (double)__double2float_rn((double)xr / dv);
+  else return (double)xr / dv;
+}
+
+template <typename TX>
+__global__ void __launch_bounds__(kSpThreads)
+csr_spmv_staged_kernel(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                       const double* __restrict__ vals, const TX* __restrict__ x,
+                       const double* __restrict__ xdiv, const double* __restrict__ alpha,
+                       double* __restrict__ y, const sgs_status* st, unsigned long long* tl,
+                       int allow_stage) {
+  __shared__ __align__(16) double svals[kSpCap + 2];
+  __shared__ __align__(16) int32_t sci[kSpCap + 4];
+  __shared__ __align__(8) uint64_t mbar;
+  const int64_t r0 = (int64_t)blockIdx.x * kSpRows;
+  const int64_t r1 = min(n, r0 + kSpRows);
+  const int b = __ldg(rp + r0), e = __ldg(rp + r1), nnz = __ldg(rp + n);
+  // 16-byte aligned source ranges covering [b, e)
+  const int b_ci = b & ~3, e_ci = (e + 3) & ~3;
+  const int b_v = b & ~1, e_v = (e + 1) & ~1;
+  const bool staged = allow_stage && (e_ci - b_ci) <= kSpCap + 4 && (e_v - b_v) <= kSpCap + 2 &&
+                      e_ci <= nnz && e_v <= nnz && e > b;
+  int rb[2], re[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t r = r0 + threadIdx.x + h * kSpThreads;
+    rb[h] = r < r1 ? __ldg(rp + r) : 0;
+    re[h] = r < r1 ? __ldg(rp + r + 1) : 0;
+  }
+  if (staged && threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sp_smem_u32(&mbar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    const uint32_t bci = (uint32_t)(e_ci - b_ci) * 4u, bv = (uint32_t)(e_v - b_v) * 8u;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sp_smem_u32(&mbar)),
+                 "r"(bci + bv) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(sp_smem_u32(sci)), "l"(ci + b_ci), "r"(bci),
+        "r"(sp_smem_u32(&mbar)), "l"(pol) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(sp_smem_u32(svals)), "l"(vals + b_v), "r"(bv),
+        "r"(sp_smem_u32(&mbar)), "l"(pol) : "memory");
+  }
+  __syncthreads();
   pdl_enter();
-  if (status_stopped(st)) return;
   if (tl && threadIdx.x == 0) atomicMin(tl + 9, gtimer());
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < n) {
-    const int b = __ldg(rp + r), e = __ldg(rp + r + 1);
-    double acc = 0.0;
-    if (xdiv) {
-      const double dv = __ldg(xdiv);
-      for (int q = b; q < e; ++q) {
-        const TX xr = __ldg(x + __ldg(ci + q));
-        TX xn;
-        if constexpr (sizeof(TX) == 4) xn = __double2float_rn((double)xr / dv);
-        else xn = (TX)((double)xr / dv);
-        acc = fma(__ldg(vals + q), (double)xn, acc);
-      }
-    } else {
-      for (int q = b; q < e; ++q) acc = fma(__ldg(vals + q), (double)__ldg(x + __ldg(ci + q)), acc);
+  if (status_stopped(st)) {
+    if (staged) {  // drain the copies before the shared memory goes away
+      asm volatile(
+          "{\n\t.reg .pred p;\nW0_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+          "@!p bra W0_%=;\n}" ::"r"(sp_smem_u32(&mbar)) : "memory");
     }
-    y[r] = alpha ? acc / __ldg(alpha) : acc;
+    return;
+  }
+  const double dv = xdiv ? __ldg(xdiv) : 1.0;
+  const double ia = alpha ? __ldg(alpha) : 1.0;
+  if (staged) {
+    asm volatile(
+        "{\n\t.reg .pred p;\nW1_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+        "@!p bra W1_%=;\n}" ::"r"(sp_smem_u32(&mbar)) : "memory");
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t r = r0 + threadIdx.x + h * kSpThreads;
+    if (r >= r1) continue;
+    double acc = 0.0;
+    if (staged) {
+      const int32_t* pc = sci + (rb[h] - b_ci);
+      const double* pv = svals + (rb[h] - b_v);
+      const int len = re[h] - rb[h];
+#pragma unroll 8
+      for (int q = 0; q < len; ++q) acc = fma(pv[q], sp_xval(x, pc[q], xdiv, dv), acc);
+    } else {
+      for (int q = rb[h]; q < re[h]; ++q) acc = fma(__ldg(vals + q), sp_xval(x, __ldg(ci + q), xdiv, dv), acc);
+    }
+    y[r] = alpha ? acc / ia : acc;
   }
   if (tl) {
     __syncthreads();
@@ -315,17 +391,19 @@ extern "C" int sgs_csr_spmv(int64_t n, const int32_t* row_ptr, const int32_t* co
                             const double* vals, const void* x, int x_dtype, const double* xdiv,
                             const double* alpha, double* y, const sgs_status* st, void* stream) {
   SGS_REQUIRE(n >= 1 && row_ptr && col_idx && vals && x && y, "spmv: bad args");
+  // staging needs 16-byte aligned arrays (torch allocations are); else global loads
+  const int stage = ((uintptr_t)col_idx & 15) == 0 && ((uintptr_t)vals & 15) == 0;
   cudaStream_t s = as_stream(stream);
-  const unsigned blocks = (unsigned)((n + 255) / 256);
+  const unsigned blocks = (unsigned)((n + kSpRows - 1) / kSpRows);
   if (x_dtype == SGS_F32)
-    return check_ex(launch_ex(csr_spmv_kernel<float>, dim3(blocks), dim3(256), 0, s, 1, n, row_ptr,
-                              col_idx, vals, static_cast<const float*>(x), xdiv, alpha, y, st,
-                              debug_timeline_row()),
-                    "csr_spmv_kernel");
-  return check_ex(launch_ex(csr_spmv_kernel<double>, dim3(blocks), dim3(256), 0, s, 1, n, row_ptr,
-                            col_idx, vals, static_cast<const double*>(x), xdiv, alpha, y, st,
-                            debug_timeline_row()),
-                  "csr_spmv_kernel");
+    return check_ex(launch_ex(csr_spmv_staged_kernel<float>, dim3(blocks), dim3(kSpThreads), 0, s,
+                              1, n, row_ptr, col_idx, vals, static_cast<const float*>(x), xdiv,
+                              alpha, y, st, debug_timeline_row(), stage),
+                    "csr_spmv_staged_kernel");
+  return check_ex(launch_ex(csr_spmv_staged_kernel<double>, dim3(blocks), dim3(kSpThreads), 0, s,
+                            1, n, row_ptr, col_idx, vals, static_cast<const double*>(x), xdiv,
+                            alpha, y, st, debug_timeline_row(), stage),
+                  "csr_spmv_staged_kernel");
 }
 
 extern "C" int64_t sgs_norm2_work_elems(int64_t n) { (void)n; return kNormBlocks; }
