@@ -209,6 +209,10 @@ typedef struct sgs_ls_args {
   int p_lag;             /* finalize + solve with p_partials: they hold p' = Theta A q'_fin of the
                             one-synchronisation Arnoldi, p = p' / r_fin,fin
                             (stored to P[:, col_sol]); the solve runs after the one exchange */
+  int giv_on;            /* with do_finalize, col_fin >= 1: also the progressive Givens update of
+                            GMRES step col_fin - 1 (as sgs_givens_step, same arithmetic) */
+  double* giv_cs; double* giv_sn; double* giv_g; double* giv_T; long long giv_ldt;
+  double* giv_hist; double giv_tol;  /* giv_tol < 0: no stop test */
 } sgs_ls_args;
 
 int64_t sgs_ls_scratch_elems(int k, int cap);

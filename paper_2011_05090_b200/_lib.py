@@ -42,6 +42,9 @@ class LsArgs(ctypes.Structure):
         ("r_crs", c_void_p), ("st", c_void_p), ("trace", c_void_p), ("cache_cols", c_int),
         ("timeline", c_void_p), ("t_pend", c_void_p), ("t_coef", c_void_p),
         ("p_lag", c_int),
+        ("giv_on", c_int), ("giv_cs", c_void_p), ("giv_sn", c_void_p), ("giv_g", c_void_p),
+        ("giv_T", c_void_p), ("giv_ldt", ctypes.c_longlong), ("giv_hist", c_void_p),
+        ("giv_tol", c_double),
     ]
 
 

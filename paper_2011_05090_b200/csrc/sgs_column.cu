@@ -68,44 +68,50 @@ static long col_pf_bytes() {
   return b;
 }
 
+// Ring depth: two CTAs per SM (<= 64 registers, __launch_bounds__ below), with
+// 4 x 16 KB stages each for fp32 and 3 x 32 KB for fp64.  Two CTAs per SM
+// matter for grids of a few waves (c3: 512 tiles): measured at c3 fp64, two
+// CTAs x 3 stages 2095 Arnoldi steps/s against one CTA x 6 stages 2024 and
+// one CTA x 4 stages 1996.  Large k shrinks the ring to fit shared memory.
 template <typename TQ> struct ColCfg;
 template <> struct ColCfg<float> { static constexpr int kStages = 4; };
 template <> struct ColCfg<double> { static constexpr int kStages = 3; };
+constexpr int kColMaxStages = 6;
 
 template <typename TQ>
 __host__ __device__ constexpr size_t col_stage_bytes() { return (size_t)kColT * sizeof(TQ); }
 
 template <typename TQ>
-__host__ __device__ constexpr size_t col_ring_bytes() {
+__host__ __device__ constexpr size_t col_ring_bytes(int stages) {
   // the FWHT buffer of the epilogue aliases the ring (used after the stream)
-  return col_stage_bytes<TQ>() * ColCfg<TQ>::kStages > (size_t)(kColT + kColT / 8 + 8) * 8
-             ? col_stage_bytes<TQ>() * ColCfg<TQ>::kStages
+  return col_stage_bytes<TQ>() * stages > (size_t)(kColT + kColT / 8 + 8) * 8
+             ? col_stage_bytes<TQ>() * stages
              : (size_t)(kColT + kColT / 8 + 8) * 8;
 }
 
 template <typename TQ, typename TW>
-__global__ void __launch_bounds__(kColThreads)
+__global__ void __launch_bounds__(kColThreads, 2)
 rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
                   const TW* __restrict__ w, const double* __restrict__ w_div,
                   const TQ* __restrict__ rc, int normalize_prev,
                   const double* __restrict__ R, int64_t ldr, int do_sketch, int64_t row0,
                   int log2_block, const uint32_t* __restrict__ sign_bits,
                   const int32_t* __restrict__ samples, int k, double* __restrict__ partials,
-                  const sgs_status* st, unsigned long long* tl, int pf_cols) {
+                  const sgs_status* st, unsigned long long* tl, int pf_cols, int nstages) {
   cg::cluster_group cl = cg::this_cluster();
   if (tl && threadIdx.x == 0) atomicMin(tl + (int64_t)i * 16 + 0, gtimer());
   constexpr int V = VecT<TQ>::N;                  // rows per vector (4 fp32, 2 fp64)
   constexpr int NH = kColT / (kColThreads * V);   // vectors per thread (2 fp32, 4 fp64)
   constexpr int LV = (V == 4) ? 2 : 1;            // log2 V
   constexpr int HB = kColLogT - ((NH == 2) ? 1 : 2);  // first element bit carried by h
-  constexpr int S = ColCfg<TQ>::kStages;
+  const int S = nstages;  // ring depth (<= kColMaxStages)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   TQ* ring = reinterpret_cast<TQ*>(smem_raw);                        // S x 4096
   double* z = reinterpret_cast<double*>(smem_raw);                   // aliases the ring
-  double* part = reinterpret_cast<double*>(smem_raw + col_ring_bytes<TQ>());  // k
+  double* part = reinterpret_cast<double*>(smem_raw + col_ring_bytes<TQ>(S));  // k
   int32_t* smp = reinterpret_cast<int32_t*>(part + k);               // k
   TQ* rs = reinterpret_cast<TQ*>(smp + k + (k & 1));                 // i coefficients
-  __shared__ uint64_t mbar[S];
+  __shared__ uint64_t mbar[kColMaxStages];
 
   const int tid = threadIdx.x;
   const int64_t lr0 = (int64_t)blockIdx.x * kColT;  // first local row of the tile
@@ -180,9 +186,10 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
 #pragma unroll
     for (int v = 0; v < V; ++v) acc[hh][v] = TQ(0);
   if (active) {
+    int s = 0;
+    uint32_t phase = 0u;  // (j / S) & 1, kept incrementally (S is a runtime depth)
     for (int j = 0; j < nplain; ++j) {
-      const int s = j % S;
-      mbar_wait(&mbar[s], (uint32_t)((j / S) & 1));
+      mbar_wait(&mbar[s], phase);
       const TQ c = rs[j];
       const TQ* buf = ring + (size_t)s * kColT;
 #pragma unroll
@@ -197,6 +204,10 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tma_load_1d(ring + (size_t)s * kColT, Q + (int64_t)(j + S) * ldq + lr0, bytes, &mbar[s],
                     policy);
+      }
+      if (++s == S) {
+        s = 0;
+        phase ^= 1u;
       }
     }
     if (i > 0 && normalize_prev) {
@@ -588,9 +599,22 @@ extern "C" int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n,
   cudaStream_t s = as_stream(stream);
   const int64_t nctas = column_ctas(n);
   const int esz = q_dtype == SGS_F32 ? 4 : 8;
-  const size_t ring = q_dtype == SGS_F32 ? col_ring_bytes<float>() : col_ring_bytes<double>();
-  const size_t smem = ring + (size_t)k * sizeof(double) + (size_t)(k + 1) * sizeof(int32_t) + 8 +
+  const size_t rest = (size_t)k * sizeof(double) + (size_t)(k + 1) * sizeof(int32_t) + 8 +
                       (size_t)(i > 0 ? i : 1) * esz;
+  int nst = q_dtype == SGS_F32 ? ColCfg<float>::kStages : ColCfg<double>::kStages;
+  auto ring_of = [&](int st_) {
+    return q_dtype == SGS_F32 ? col_ring_bytes<float>(st_) : col_ring_bytes<double>(st_);
+  };
+  {
+    static int env_st = -1;  // SGS_COL_STAGES: experiment override of the ring depth
+    if (env_st < 0) {
+      const char* e = getenv("SGS_COL_STAGES");
+      env_st = e ? std::max(2, std::min(kColMaxStages, atoi(e))) : 0;
+    }
+    if (env_st > 0) nst = env_st;
+  }
+  while (nst > 2 && ring_of(nst) + rest > 227 * 1024) --nst;  // large k / i: shallower ring
+  const size_t smem = ring_of(nst) + rest;
   SGS_REQUIRE(smem <= 227 * 1024, "update_srht: i=%d k=%d needs %zu bytes of shared memory", i,
               k, smem);
   // L2 prefetch of the columns behind the ring prologue, spread over the tiles
@@ -606,7 +630,8 @@ extern "C" int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n,
     err = launch_ex(kern, dim3((unsigned)nctas), dim3(kColThreads), smem, s, kColCluster,     \
                     static_cast<TQ*>(Q), ldq, n, i, static_cast<const TW*>(w), w_div,        \
                     static_cast<const TQ*>(r_crs), normalize_prev, R, ldr, do_sketch, row0,  \
-                    log2_block, sign_bits, samples, k, partials, st, debug_timeline(), pf);   \
+                    log2_block, sign_bits, samples, k, partials, st, debug_timeline(), pf,    \
+                    nst);                                                                     \
   } while (0)
   if (q_dtype == SGS_F32 && w_dtype == SGS_F32) SGS_COL(float, float);
   else if (q_dtype == SGS_F32 && w_dtype == SGS_F64) SGS_COL(float, double);

@@ -439,6 +439,44 @@ __device__ __noinline__ void ls_reduce_parts(const double* parts, int nparts, in
   }
   __syncthreads();
 }
+// Two partial sets (s' and p' of a one-synchronisation launch) in one pass,
+// all loads of a row in flight together; each chain sums in ls_reduce_parts'
+// order, so the results are bit-identical to two separate calls.
+template <typename T>
+__device__ __noinline__ void ls_reduce_parts2(const double* pa, int na, double sa, T* va,
+                                              const double* pb, int nb, double sb, T* vb,
+                                              int k, int ra, int nr, double* red) {
+  const int g = threadIdx.x >> 6, rl = threadIdx.x & 63;  // 8 groups x 64 rows
+  const int nmax = max(na, nb);
+  for (int r0 = 0; r0 < nr; r0 += 64) {
+    double acc_a = 0.0, acc_b = 0.0;
+    const int rr = r0 + rl;
+    if (rr < nr) {
+      const double* p = pa + ra + rr;
+      const double* q = pb + ra + rr;
+#pragma unroll 8
+      for (int j = g; j < nmax; j += kCanonG) {
+        if (j < na) acc_a += __ldcg(p + (int64_t)j * k);
+        if (j < nb) acc_b += __ldcg(q + (int64_t)j * k);
+      }
+    }
+    __syncthreads();
+    red[g * 64 + rl] = acc_a;
+    red[(kCanonG + g) * 64 + rl] = acc_b;
+    __syncthreads();
+    if (threadIdx.x < 128) {
+      const int h = threadIdx.x >> 6, o = threadIdx.x & 63;
+      if (r0 + o < nr) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < kCanonG; ++q) t += red[(h * kCanonG + q) * 64 + o];
+        if (h == 0) va[r0 + o] = from_double<T>(sa * t);
+        else vb[r0 + o] = from_double<T>(sb * t);
+      }
+    }
+  }
+  __syncthreads();
+}
 
 // Cluster sum of one scalar per CTA from slots[q*stride] (ascending q).
 template <typename T>
@@ -500,6 +538,42 @@ __device__ __forceinline__ void ls_deferred_column(const T* coef, int pend, int 
     if (pend < ncache) sq[(int64_t)pend * RM + rr] = tv;
   }
   __syncthreads();
+}
+
+// The gi earlier Givens rotations applied to h = rc[0..gi] by one warp (see
+// ls_step_kernel): outputs to Tc[0..gi), the carry to Tc[gi].  The warp stages
+// up to 320 rotations and h entries in buf (3 x 320 doubles of shared memory)
+// with all loads in flight, lane 0 runs the dependent chain from there (its
+// operand loads do not depend on the carry), and the warp stores the outputs.
+__device__ __noinline__ void ls_givens_chain(const double* rc, const double* cs, const double* sn,
+                                             double* Tc, int gi, double* buf) {
+  constexpr int kB = 320;
+  const int lane = threadIdx.x & 31;
+  double* bc = buf;
+  double* bs = buf + kB;
+  double* bh = buf + 2 * kB;
+  double carry = rc[0];
+  for (int j0 = 0; j0 < gi; j0 += kB) {
+    const int nb = min(kB, gi - j0);
+    for (int j = lane; j < nb; j += 32) {
+      bc[j] = cs[j0 + j];
+      bs[j] = sn[j0 + j];
+      bh[j] = rc[j0 + j + 1];
+    }
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll 8
+      for (int j = 0; j < nb; ++j) {
+        const double c = bc[j], s_ = bs[j], hn = bh[j];
+        bc[j] = __dadd_rn(__dmul_rn(c, carry), __dmul_rn(s_, hn));
+        carry = __dadd_rn(__dmul_rn(-s_, carry), __dmul_rn(c, hn));
+      }
+    }
+    __syncwarp();
+    for (int j = lane; j < nb; j += 32) Tc[j0 + j] = bc[j];
+    __syncwarp();
+  }
+  if (lane == 0) Tc[gi] = carry;
 }
 
 template <typename T>
@@ -568,6 +642,19 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   if (a.timeline && rank == 0 && threadIdx.x == 0) a.timeline[6] = gtimer();
   const int64_t code0 = *reinterpret_cast<volatile const int64_t*>(&a.st->code);
   double dmax = a.st->diag_max, dmin = a.st->diag_min;
+  // Progressive Givens update of GMRES step gi = col_fin - 1 (krylov.py:282-301),
+  // folded into this launch (one-synchronisation Arnoldi): H[:, gi] = R[:gi+2,
+  // col_fin].  Its first gi entries are the r of the previous launch's solve,
+  // so the chain of the gi earlier rotations runs here, before the wait, on the
+  // last warp of rank 0 (which sits out the cache fill below); only the new
+  // rotation needs r_ii.  The warp loads 32 rotations at a time and every lane
+  // runs the same chain from shuffled operands (same operations as
+  // givens_update).  The carry waits in T[gi, gi] for thread 0 (bar.syncs
+  // between), which overwrites it with the new rotation.
+  const int gi = (a.giv_on && a.do_finalize) ? a.col_fin - 1 : -1;
+  const bool giv_warp = gi >= 0 && rank == 0 && code0 == 0 && (threadIdx.x >> 5) == (int)(blockDim.x >> 5) - 1;
+  if (giv_warp) ls_givens_chain(R + (int64_t)a.col_fin * cap, a.giv_cs, a.giv_sn,
+                                 a.giv_T + (int64_t)gi * a.giv_ldt, gi, dred);
   // The previous finalize may have deferred its T column: form it now, while
   // the predecessor kernel streams (same arithmetic as the explicit path:
   // t = s - T[:, :pend] c2, rows of this CTA, from the shared-memory cache).
@@ -579,8 +666,9 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   const int last_fast = a.t_pend ? *reinterpret_cast<volatile const int*>(a.t_pend + 1) : -1;
   const int ncols_t = a.do_finalize ? a.col_fin : a.col_sol;  // columns of T in use
   const int ncache = min(ncols_t, a.cache_cols);
-  {  // warp per column, 4 columns x 3 row groups of loads in flight per lane
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (!giv_warp) {  // warp per column, 4 columns x 3 row groups of loads in flight per lane
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = (blockDim.x >> 5) - ((gi >= 0 && rank == 0 && code0 == 0) ? 1 : 0);
     for (int rb0 = 0; rb0 < nr; rb0 += 96)
       for (int j0 = wid * 4; j0 < ncache; j0 += nw * 4) {
         T v[4][3];
@@ -650,10 +738,13 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     const int nq = i;
     if (i == 0) {
       for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vs[rr] = P[ra + rr];  // s'_1 = p_1
+      if (lag) ls_reduce_parts<T>(a.p_partials, a.p_nparts, k, ra, nr, a.p_scale, vp, dred);
+    } else if (lag) {  // s' and p' together
+      ls_reduce_parts2<T>(a.s_partials, a.s_nparts, a.s_scale, vs, a.p_partials, a.p_nparts,
+                          a.p_scale, vp, k, ra, nr, dred);
     } else {
       ls_reduce_parts<T>(a.s_partials, a.s_nparts, k, ra, nr, a.s_scale, vs, dred);
     }
-    if (lag) ls_reduce_parts<T>(a.p_partials, a.p_nparts, k, ra, nr, a.p_scale, vp, dred);  // p'
     __syncthreads();
     SGS_TR(3);
     // ---- exchange #1: ||s'||^2, ||p_i||^2, T^T s' --------------------------------
@@ -833,6 +924,30 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
       a.st->diag_min = dmin;
       a.st->ncols = i + 1;
       a.st->r_ii = r_ii;
+      if (gi >= 0) {  // the new rotation (same operations as givens_update)
+        const double beta = R[0];
+        if (gi == 0) a.giv_g[0] = beta;
+        double* Tc = a.giv_T + (int64_t)gi * a.giv_ldt;
+        const double hi = Tc[gi], hn = r_ii;
+        const double rr = hypot(hi, hn);
+        double c, sv;
+        if (rr == 0.0) { c = 1.0; sv = 0.0; }
+        else { c = hi / rr; sv = hn / rr; }
+        a.giv_cs[gi] = c;
+        a.giv_sn[gi] = sv;
+        Tc[gi] = rr;
+        Tc[gi + 1] = 0.0;
+        const double gg = a.giv_g[gi];
+        a.giv_g[gi + 1] = __dmul_rn(-sv, gg);
+        a.giv_g[gi] = __dmul_rn(c, gg);
+        const double est = fabs(a.giv_g[gi + 1]) / beta;
+        a.giv_hist[gi] = est;
+        a.st->iters = gi + 1;
+        if (a.giv_tol >= 0.0 && est <= a.giv_tol) {  // later launches see it and return
+          a.st->code = SGS_ST_CONVERGED;
+          a.st->column = gi + 1;
+        }
+      }
     }
     __syncthreads();
     SGS_TR(8);
@@ -1044,6 +1159,9 @@ extern "C" int sgs_ls_step(const sgs_ls_args* a, void* stream) {
               "ls_step: fused solve must target the next column");
   SGS_REQUIRE(!a->p_lag || (a->do_finalize && a->do_solve && a->p_partials),
               "ls_step: p_lag needs a fused finalize + solve with p partials");
+  SGS_REQUIRE(!a->giv_on || (a->do_finalize && a->col_fin >= 1 && a->giv_cs && a->giv_sn &&
+                             a->giv_g && a->giv_T && a->giv_hist && a->giv_ldt >= a->col_fin + 1),
+              "ls_step: giv_on needs a finalize of column >= 1 and the Givens arrays");
   cudaStream_t s = as_stream(stream);
   if (a->fine_dtype == SGS_F64) return launch_ls<double>(a, s);
   if (a->fine_dtype == SGS_F32) return launch_ls<float>(a, s);

@@ -278,7 +278,7 @@ class RgsState:
     # ---- kernels ---------------------------------------------------------------
     def _ls(self, *, fin: int | None = None, s_parts=None, s_nparts=0, s_scale=1.0,
             sol: int | None = None, p_parts=None, p_nparts=0, p_scale=1.0,
-            lag: bool = False) -> None:
+            lag: bool = False, giv=None) -> None:
         a = self.__dict__.get("_ls_args")
         if a is None:
             a = self._ls_args = _lib.LsArgs()  # reused: the library copies it at launch
@@ -294,6 +294,14 @@ class RgsState:
         a.p_nparts = p_nparts
         a.p_scale = p_scale
         a.p_lag = 1 if lag else 0
+        if giv is None:
+            a.giv_on = 0
+        else:  # (cs, sn, g, T, hist, tol) device tensors of the GMRES driver
+            cs, sn, g, T, hist, tol = giv
+            a.giv_on = 1
+            a.giv_cs, a.giv_sn, a.giv_g = cs.data_ptr(), sn.data_ptr(), g.data_ptr()
+            a.giv_T, a.giv_ldt, a.giv_hist = T.data_ptr(), T.shape[1], hist.data_ptr()
+            a.giv_tol = -1.0 if tol is None else float(tol)
         a.bf_ucrs = self.breakdown_factor * self.policy.u_crs
         a.S, a.P, a.R = self._S.data_ptr(), self._P.data_ptr(), self._R.data_ptr()
         a.Qs, a.Rinv, a.alpha = self._Qs.data_ptr(), self._Rinv.data_ptr(), self._alpha.data_ptr()

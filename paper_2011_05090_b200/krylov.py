@@ -415,8 +415,8 @@ class _ArnoldiEngine:
     one LS launch finalizes column c (r_cc = ||s'_c||) and solves column c+1
     from p_{c+1} = (Theta A q'_c) / r_cc.  A step is then the column kernel
     (w = A q'_c / r_cc formed on the fly, q_c normalised in its stream), the
-    SpMV, the SRHT of w and that LS launch, plus the Givens update; sharded,
-    the two k-vectors share one all-reduce."""
+    SpMV, the SRHT of w and that LS launch, which also applies the Givens
+    update of step c - 1; sharded, the two k-vectors share one all-reduce."""
 
     def __init__(self, A: SparseMatrix, theta, policy, solver, m: int,
                  breakdown_factor: float = BREAKDOWN_FACTOR, phi=None, M=None,
@@ -464,7 +464,13 @@ class _ArnoldiEngine:
             self.dist.block.spmv_into(xf.data_ptr(), st.ccode, out, alpha=alpha, status=status)
 
     # ---- one-synchronisation (lagged) steps -----------------------------------------
-    def _lag_tail(self, c: int, s_raw, alpha) -> None:
+    def _giv(self, c: int, alpha, tol):
+        """Givens arrays for the LS launch finalizing column c (step c - 1)."""
+        if c < 1 or (tol is None and alpha is None):
+            return None
+        return (self.cs, self.sn, self.g, self.T, self.hist, tol)
+
+    def _lag_tail(self, c: int, s_raw, alpha, tol=None) -> None:
         """w = A M^{-1} q'_c (/ alpha) from the unnormalised column c, its sketch
         p', and the LS launch finalizing c and solving c + 1 (p = p' / r_cc).
         ``s_raw``: raw partials of s'_c (None for c = 0: s'_0 = p_0)."""
@@ -490,7 +496,7 @@ class _ArnoldiEngine:
             p_raw = (kv[k:].data_ptr(), 1, st.theta.scale)
         s_ptr, s_np, s_sc = s_raw if s_raw is not None else (None, 0, 1.0)
         st._ls(fin=c, s_parts=s_ptr, s_nparts=s_np, s_scale=s_sc, sol=c + 1, p_parts=p_raw[0],
-               p_nparts=p_raw[1], p_scale=p_raw[2], lag=True)
+               p_nparts=p_raw[1], p_scale=p_raw[2], lag=True, giv=self._giv(c, alpha, tol))
 
     def _start_lagged(self, bn: torch.Tensor, alpha) -> None:
         st, n = self.state, self.n_loc
@@ -518,7 +524,7 @@ class _ArnoldiEngine:
                  _lib.SGS_F64, rii, self.n_loc, stream_ptr())
             s_raw = st._column(c, self._wdiv.data_ptr(), _lib.SGS_F64, True, True, combine=False)
         if c < self.m:
-            self._lag_tail(c, s_raw, alpha)
+            self._lag_tail(c, s_raw, alpha, tol)
         else:  # last column: finalize only
             if self.dist is not None:
                 k, kv = st.k, self._kv2
@@ -526,10 +532,9 @@ class _ArnoldiEngine:
                      _lib.SGS_F64, k, st.status.ptr, stream_ptr())
                 self.dist.comm.allreduce_(kv[:k])
                 s_raw = (kv.data_ptr(), 1, st.theta.scale)
-            st._ls(fin=c, s_parts=s_raw[0], s_nparts=s_raw[1], s_scale=s_raw[2])
-        st.m = c + 1
-        if tol is not None or alpha is not None:
-            self._givens(i, tol)
+            st._ls(fin=c, s_parts=s_raw[0], s_nparts=s_raw[1], s_scale=s_raw[2],
+                   giv=self._giv(c, alpha, tol))
+        st.m = c + 1  # the Givens update of step i ran in that LS launch
 
     def start(self, b_dev: torch.Tensor, b_norm_ptr, alpha=None) -> None:
         """Push b (this rank's rows; divided by ||b|| when b_norm_ptr is given)
