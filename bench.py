@@ -266,10 +266,10 @@ def run_qr(args, cfg_name):
         evs = []
         orig = gsm.RgsState._column
 
-        def timed_column(self, i, w_ptr, w_code, normalize_prev, sketch):
+        def timed_column(self, i, w_ptr, w_code, normalize_prev, sketch, **kw_):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            out = orig(self, i, w_ptr, w_code, normalize_prev, sketch)
+            out = orig(self, i, w_ptr, w_code, normalize_prev, sketch, **kw_)
             b.record()
             evs.append((i, a, b))
             return out
@@ -286,6 +286,9 @@ def run_qr(args, cfg_name):
             # the timed unit is the update kernel + the dense sketch GEMV of q'
             # (Theta streamed once per column, q' re-read from L2)
             tot_b += sum(k * n_loc * 8 + n_loc * bq for i, _, _ in evs if i > 0)
+        elif cfg["kind"] == "rademacher":
+            # update kernel + packed-sign sketch of q' (1 bit per entry, q' re-read)
+            tot_b += sum(k * n_loc // 8 + n_loc * bq for i, _, _ in evs if i > 0)
         ach = tot_b / (tot_ms / 1e3) / 1e9
         traffic, traffic_note = None, None
         try:
@@ -298,7 +301,11 @@ def run_qr(args, cfg_name):
         except Exception:
             pass
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": traffic, "traffic_note": traffic_note, "kernel": "rgs_column_kernel (update + SRHT epilogue)" if cfg["kind"] != "gaussian" else "dense_ring_kernel (Q + Theta^T through a TMA bulk-copy ring)",
+                "frac": round(ach / peak, 4), "traffic": traffic, "traffic_note": traffic_note,
+                "kernel": {"gaussian": "dense_ring_kernel (Q + Theta^T through a TMA bulk-copy ring)",
+                           "rademacher": "rgs_update_kernel + rademacher_partials_kernel "
+                                         "(device-generated packed signs)"}.get(
+                    cfg["kind"], "rgs_column_kernel (update + SRHT epilogue)"),
                 "peak_source": peak_kind,
                 "share_of_step": round(tot_ms / ms, 4),
                 "launches": len(evs), "avg_launch_us": round(1e3 * tot_ms / len(evs), 2)}

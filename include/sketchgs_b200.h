@@ -102,6 +102,20 @@ int sgs_dense_partials(const double* thetaT, int64_t ldt, int k,
                        int64_t n, double* partials, const sgs_status* st,
                        void* stream);
 
+/* Rademacher sketch generated on the device (SketchKind.RADEMACHER,
+ * sketch.py:153-158): column j of the unscaled +-1 matrix is numpy
+ * Philox(key = (seed << 64) | (col0 + j)).integers(0, 2, size=k), reproduced
+ * bit for bit (Philox4x64-10, top bit of each 32-bit draw) into row j of an
+ * n x ceil(k/32) uint32 array (bit r % 32 of word r / 32 set = +1). */
+int sgs_rademacher_bits(uint64_t seed, int64_t col0, int64_t n, int k, uint32_t* bits,
+                        void* stream);
+/* Partials of Theta^T' X from the packed signs: the sgs_dense_partials
+ * chunking (sgs_dense_nparts(n) parts) and per-output chains, so bit-identical
+ * to it on the materialised matrix. */
+int sgs_rademacher_partials(const uint32_t* bits, int k, const void* X, int x_dtype,
+                            int64_t ldx, int ncols, int64_t n, double* partials,
+                            const sgs_status* st, void* stream);
+
 /* Y[:, c] = cast(scale * sum_p partials[c][p][:]) in fixed p order. */
 int sgs_partials_reduce(const double* partials, int nparts, int k, int ncols,
                         double scale, void* Y, int y_dtype, int64_t ldy,

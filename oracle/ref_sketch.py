@@ -43,6 +43,41 @@ def fwht_ref(v):
     return cols.reshape(shape)
 
 
+# numpy's Philox is Random123 Philox4x64-10 (numpy/random/src/philox/philox.h):
+# multipliers, Weyl key increments, and the counter incremented before each
+# block of four 64-bit outputs.
+_PH_M = (0xD2E7470EE14C6C93, 0xCA5A826395121157)
+_PH_W = (0x9E3779B97F4A7C15, 0xBB67AE8584CAA73B)
+_M64 = (1 << 64) - 1
+
+
+def philox4x64_10(ctr, key):
+    c, k = list(ctr), list(key)
+    for r in range(10):
+        if r:
+            k = [(k[0] + _PH_W[0]) & _M64, (k[1] + _PH_W[1]) & _M64]
+        p0, p1 = _PH_M[0] * c[0], _PH_M[1] * c[2]
+        c = [(p1 >> 64) ^ c[1] ^ k[0], p1 & _M64, (p0 >> 64) ^ c[3] ^ k[1], p0 & _M64]
+    return c
+
+
+def rademacher_column_bits(seed: int, j: int, k: int) -> np.ndarray:
+    """Philox(key=(seed << 64) | j).integers(0, 2, size=k) (sketch.py:153-158)
+    restated from the bit generator: next_uint32 returns the low then the high
+    half of each 64-bit output, and the bounded draw over {0, 1} (Lemire,
+    numpy's default for Generator.integers) is the top bit of one uint32.  This
+    is the algorithm the device generator sgs_rademacher_bits implements;
+    pinned against numpy by tests/test_oracle_golden.py."""
+    key = [int(j) & _M64, int(seed) & _M64]
+    out, ctr = [], 0
+    while len(out) < k:
+        ctr += 1
+        for v in philox4x64_10([ctr, 0, 0, 0], key):
+            out.append((v & 0xFFFFFFFF) >> 31)
+            out.append(v >> 63)
+    return np.asarray(out[:k], dtype=np.int64)
+
+
 def block_seed(seed: int, j: int) -> int:
     return int(seed) * 1_000_003 + int(j)
 

@@ -64,6 +64,9 @@ _SIGS = {
     "sgs_dense_column_nparts": (c_int, [c_int64, c_int]),
     "sgs_dense_partials": (c_int, [c_void_p, c_int64, c_int, c_void_p, c_int, c_int64, c_int,
                                    c_int64, c_void_p, c_void_p, c_void_p]),
+    "sgs_rademacher_bits": (c_int, [c_uint64, c_int64, c_int64, c_int, c_void_p, c_void_p]),
+    "sgs_rademacher_partials": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int64, c_int,
+                                        c_int64, c_void_p, c_void_p, c_void_p]),
     "sgs_partials_reduce": (c_int, [c_void_p, c_int, c_int, c_int, c_double, c_void_p, c_int,
                                     c_int64, c_void_p, c_void_p]),
     "sgs_partials_reduce_div": (c_int, [c_void_p, c_int, c_int, c_int, c_double, c_void_p,

@@ -477,6 +477,9 @@ extern "C" int sgs_srht_partials(const void* X, int x_dtype, int64_t ldx, int nc
 }
 
 extern "C" int sgs_dense_nparts(int64_t n) { return n < 1 ? 0 : dense_nparts_host(n); }
+namespace sgs {
+int dense_nparts_of(int64_t n) { return dense_nparts_host(n); }
+}  // namespace sgs
 
 template <typename TX>
 static int launch_dense(const double* thetaT, int64_t ldt, int k, const void* X, int64_t ldx,

@@ -204,7 +204,7 @@ class RgsState:
                       and self.row0 % 4096 == 0)
         if self.fused:
             self.nparts_q = int(_lib.load().sgs_column_nparts(self.n_local))
-        elif self.theta.is_dense:  # the dense column kernel's own row chunks
+        elif self.theta.is_gaussian:  # the dense column kernel's own row chunks
             self.nparts_q = int(_lib.load().sgs_dense_column_nparts(self.n_local, self.k))
         else:
             self.nparts_q = self.nparts
@@ -369,7 +369,7 @@ class RgsState:
             if not combine:
                 return self._parts_s.data_ptr(), self.nparts_q, self.theta.scale
             return self._combine(self._parts_s, self.nparts_q, kvec)
-        if self.theta.is_dense:
+        if self.theta.is_gaussian:
             d = self._theta_dev
             call("sgs_rgs_update_dense", self._Q.data_ptr(), self.ccode, self.ldq, self.n_local,
                  i, w_ptr, w_code, self._rc.data_ptr(), 1 if normalize_prev else 0,

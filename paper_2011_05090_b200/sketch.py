@@ -14,9 +14,11 @@ Kinds:
   constructor does (numpy Philox keyed ``(seed << 64) | stream`` with streams
   0x5149 / 0xFA7E, ``sketch.py:116-145``), then uploaded once: signs as a
   packed bitmask, samples as int32.  Applied by one tile-FWHT kernel.
-* ``RADEMACHER`` - the reference's +-1/sqrt(k) kind, materialised from the
-  same per-column Philox streams (``sketch.py:153-166``) and applied by the
-  dense kernel.
+* ``RADEMACHER`` - the reference's +-1/sqrt(k) kind.  Its per-column Philox
+  streams (``sketch.py:153-166``) are regenerated on the device bit for bit
+  (``sgs_rademacher_bits``: numpy's Philox4x64-10, top bit of each 32-bit
+  draw) and kept packed, 1 bit per entry; applied by
+  ``sgs_rademacher_partials`` with the dense kernels' chunking and chains.
 * ``GAUSSIAN`` (absent from the reference; BASELINE config 0) - Theta_ij
   = g_ij / sqrt(k), g ~ N(0, 1) from ``Philox((seed << 64) | 0x6A55)`` drawn as
   an (n, k) array (Theta column-major), applied by the dense kernel.
@@ -143,17 +145,18 @@ class SketchOperator:
 
     # ---- host construction of dense kinds --------------------------------------
     def _dense_host(self) -> np.ndarray:
-        """Unscaled Theta^T (n x k): N(0,1) or +-1 entries."""
-        if self.kind is SketchKind.GAUSSIAN:
-            return _philox(self.seed, _GAUSSIAN_STREAM).standard_normal((self.n, self.k))
-        out = np.empty((self.n, self.k))
-        for j in range(self.n):  # column j of Theta from its own stream (sketch.py:153-158)
-            out[j] = 2.0 * _philox(self.seed, j).integers(0, 2, size=self.k) - 1.0
-        return out
+        """Unscaled Theta^T (n x k) of the Gaussian kind: N(0,1) entries."""
+        return _philox(self.seed, _GAUSSIAN_STREAM).standard_normal((self.n, self.k))
 
     @property
     def is_dense(self) -> bool:
+        """Applied by the dense chunking (Gaussian fp64 stream or Rademacher bits)."""
         return self.kind in (SketchKind.GAUSSIAN, SketchKind.RADEMACHER)
+
+    @property
+    def is_gaussian(self) -> bool:
+        """Dense fp64 Theta^T in HBM (the fused dense column kernel)."""
+        return self.kind is SketchKind.GAUSSIAN
 
     # ---- device resources -------------------------------------------------------
     def device_data(self, device=None) -> dict:
@@ -165,7 +168,14 @@ class SketchOperator:
         d = self._dev.get(key)
         if d is not None:
             return d
-        if self.is_dense:
+        if self.kind is SketchKind.RADEMACHER:
+            kw = (self.k + 31) // 32
+            bits = torch.empty((self.n, kw), dtype=torch.int32, device=dev)
+            with torch.cuda.device(dev):
+                call("sgs_rademacher_bits", self.seed & (2**64 - 1), 0, self.n, self.k,
+                     bits.data_ptr(), stream_ptr())
+            d = {"rbits": bits, "kw": kw}
+        elif self.is_dense:
             ldt = self.k + (self.k & 1)
             host = self._dense_host()
             t = torch.zeros((self.n, ldt), dtype=torch.float64, device=dev)
@@ -202,6 +212,12 @@ class SketchOperator:
         xp = X if isinstance(X, int) else X.data_ptr()
         sp = stream_ptr(stream)
         st = status.ptr if status is not None else None
+        if self.kind is SketchKind.RADEMACHER:
+            np_ = self.nparts(n_local)
+            bp = d["rbits"].data_ptr() + row0 * d["kw"] * 4
+            call("sgs_rademacher_partials", bp, self.k, xp, x_dtype, ldx, ncols, n_local,
+                 out.data_ptr(), st, sp)
+            return np_
         if self.is_dense:
             np_ = self.nparts(n_local)
             thetaT = d["thetaT"]

@@ -33,6 +33,10 @@ CONFIGS = {
     # BASELINE.json configs[0..4]
     "c0": dict(kind="gaussian", n=100_000, m=300, k=600, sigma_min=1e-8, policy="f64",
                breakdown_factor=10.0),
+    # c0 shapes with the reference's own Rademacher sketch, generated on the
+    # device from its Philox streams (not a BASELINE config)
+    "c0r": dict(kind="rademacher", n=100_000, m=300, k=600, sigma_min=1e-8, policy="f64",
+                breakdown_factor=10.0),
     "c1": dict(kind="psrht", n=1_000_000, m=500, k=1500, sigma_min=1e-10, policy="mixed",
                breakdown_factor=0.0),
     "c2": dict(kind="block_srht", n=1 << 23, m=1000, k=2000, sigma_min=1e-6, policy="f64",

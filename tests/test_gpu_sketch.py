@@ -122,3 +122,25 @@ def test_large_psrht_linearity_and_norm(cuda):
     assert 0.9 < ratio < 1.1
     # bit-identical rerun
     assert torch.equal(th.apply(x), yx)
+
+
+@pytest.mark.parametrize("k,n,seed", [(64, 3000, 5), (601, 2000, 11), (1500, 700, 3)])
+def test_device_rademacher_bits_match_reference_streams(cuda, k, n, seed):
+    """sgs_rademacher_bits reproduces the reference's per-column streams
+    Philox((seed << 64) | j).integers(0, 2, size=k) (sketch.py:153-158) bit for bit."""
+    from oracle.ref_sketch import _gen
+    th = sg.make_sketch(sg.SketchKind.RADEMACHER, k, n, seed)
+    words = th.device_data()["rbits"].cpu().numpy().view(np.uint32)
+    bits = np.unpackbits(words.view(np.uint8), axis=1, bitorder="little")[:, :k]
+    ref = np.stack([_gen(seed, j).integers(0, 2, size=k) for j in range(n)])
+    assert np.array_equal(bits, ref)
+    # packed-sign partials == the dense fp64 definition, bit for bit on exact inputs
+    rng = np.random.default_rng(1)
+    X = rng.integers(-8, 8, size=(n, 3)).astype(np.float64)
+    Y = th.apply_block(X)
+    assert np.array_equal(Y, th.scale * ((2.0 * ref.T - 1.0) @ X))  # exact integer sums
+    Xr = rng.standard_normal((n, 2))
+    assert np.allclose(th.apply_block(Xr), (2.0 * ref.T - 1.0) @ Xr / np.sqrt(k), rtol=1e-13,
+                       atol=1e-13)
+    y0 = th.apply(Xr[:, 0])
+    assert np.array_equal(y0, th.apply_block(Xr)[:, 0])  # apply_block == apply

@@ -158,3 +158,11 @@ def test_sizing_helpers_match_reference():
         sg.eps_star_for_dim(1, 1e-3)
     with pytest.raises(ValueError):
         sg.EmbeddingParams(1.5, 0.1, 3)
+
+
+def test_rademacher_philox_restatement_matches_numpy():
+    """The device generator's algorithm (oracle.rademacher_column_bits) is numpy's
+    Philox(key=(seed << 64) | j).integers(0, 2, size=k) bit for bit."""
+    from oracle.ref_sketch import _gen, rademacher_column_bits
+    for seed, j, k in ((0, 0, 1), (5, 3, 20), (5, 49, 33), (7, 2**40 + 5, 600), (123, 99999, 1500)):
+        assert np.array_equal(rademacher_column_bits(seed, j, k), _gen(seed, j).integers(0, 2, size=k))
