@@ -116,6 +116,17 @@ int sgs_rademacher_partials(const uint32_t* bits, int k, const void* X, int x_dt
                             int64_t ldx, int ncols, int64_t n, double* partials,
                             const sgs_status* st, void* stream);
 
+/* ---- Matrix Market ingest (io.read_matrix_market, io.py:24-70) -----------
+ * Host-side, native: real/integer/double coordinate files, general or
+ * symmetric storage, square; SGS_EINVAL with the reference's message in
+ * sgs_last_error() otherwise (the Python layer raises MatrixMarketError).
+ * Entries come back 0-based in file order (CSR assembly, duplicate summing and
+ * the symmetric mirror are SparseMatrix.from_coo's). */
+int sgs_mm_read_header(const char* path, int64_t* nrows, int64_t* ncols, int64_t* nnz,
+                       int* symmetric);
+int sgs_mm_read_entries(const char* path, int64_t nnz, int64_t* rows, int64_t* cols,
+                        double* vals);
+
 /* Y[:, c] = cast(scale * sum_p partials[c][p][:]) in fixed p order. */
 int sgs_partials_reduce(const double* partials, int nparts, int k, int ncols,
                         double scale, void* Y, int y_dtype, int64_t ldy,

@@ -16,6 +16,7 @@ from .gram_schmidt import (BREAKDOWN_FACTOR, HOUSEHOLDER_QR, BreakdownError, GsV
                            loss_of_orthogonality, rgs_factorize)
 from .krylov import (ArnoldiDecomposition, GmresResult, Ilu0Preconditioner, RestartedResult,
                      SparseMatrix, arnoldi, gmres, gmres_restarted, ilu0)
+from .mmio import MatrixMarketError, read_matrix_market, write_matrix_market
 from .certification import (CertificationParams, CertificationResult, EmbeddingParams,
                             certify_factorization, epsilon_of, eps_star_for_dim,
                             make_certification_sketch, omega_bar, omega_bar_sharpness,
@@ -33,5 +34,5 @@ __all__ = [
     "gmres_restarted", "CertificationParams", "CertificationResult", "EmbeddingParams",
     "certify_factorization", "epsilon_of", "eps_star_for_dim", "make_certification_sketch",
     "omega_bar", "omega_bar_sharpness", "required_sketch_dim", "rounding_sketch_trial",
-    "vector_certificate_dim",
+    "vector_certificate_dim", "MatrixMarketError", "read_matrix_market", "write_matrix_market",
 ]

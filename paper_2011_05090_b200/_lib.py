@@ -64,6 +64,9 @@ _SIGS = {
     "sgs_dense_column_nparts": (c_int, [c_int64, c_int]),
     "sgs_dense_partials": (c_int, [c_void_p, c_int64, c_int, c_void_p, c_int, c_int64, c_int,
                                    c_int64, c_void_p, c_void_p, c_void_p]),
+    "sgs_mm_read_header": (c_int, [ctypes.c_char_p, POINTER(c_int64), POINTER(c_int64),
+                                   POINTER(c_int64), POINTER(c_int)]),
+    "sgs_mm_read_entries": (c_int, [ctypes.c_char_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "sgs_rademacher_bits": (c_int, [c_uint64, c_int64, c_int64, c_int, c_void_p, c_void_p]),
     "sgs_rademacher_partials": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int64, c_int,
                                         c_int64, c_void_p, c_void_p, c_void_p]),
