@@ -757,10 +757,12 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     if (defer && fused) block_sum2(l0, l2, red);
     else l0 = block_sum(l0, red);
     if (threadIdx.x == 0) { myA[0] = l0; myA[1] = bc[6]; myA[2] = l2; }  // bc[6]: ||p_i||^2
+    SGS_TR(14);
     if (nq > 0) {
       if (lag) ls_coldot<T, 2>(TS, nr, 0, nq, vs, vp, myA + 8, myA + 8 + cap);  // + T^T p'
       else ls_coldot<T, 1>(TS, nr, 0, nq, vs, nullptr, myA + 8, nullptr);
     }
+    SGS_TR(15);  // thread 0's share of the column dots done
     xsync();
     SGS_TR(4);
     if (threadIdx.x < 3) bc[threadIdx.x] = ls_slot_sum(XA + threadIdx.x, sA, CL);

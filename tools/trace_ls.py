@@ -40,4 +40,7 @@ for dec, rows in enumerate(np.array_split(tr[1:-1], 5)):
     d["pre:deferred"] = cyc(11, 12)
     d["pre:coldot"] = cyc(12, 13)
     d["pre:gather+matvec"] = cyc(13, 1)
+    d["exch1:norms"] = cyc(3, 14)
+    d["exch1:coldot"] = cyc(14, 15)
+    d["exch1:xsync"] = cyc(15, 4)
 print(json.dumps(out, indent=1))
