@@ -547,10 +547,14 @@ def run_gmres_sharded(args, comm):
     th.device_data()
     out = {}
     clocks = Clocks(local)
-    for pname in ("f64", "mixed"):
-        pol = sg.policy_from_name(pname)
+    # standard RGS-Arnoldi, then the one-synchronisation variant (one [s'; p']
+    # all-reduce per step instead of two k-vector all-reduces)
+    for pname in ("f64", "mixed", "f64_lagged", "mixed_lagged"):
+        pol = sg.policy_from_name(pname.split("_")[0])
+        lag = pname.endswith("_lagged")
         solve = lambda: sg.gmres_restarted(A, b, th, pol, cfg["restart"],  # noqa: E731
-                                           cfg["max_iters"], cfg["tol"], comm=comm)
+                                           cfg["max_iters"], cfg["tol"], comm=comm,
+                                           lagged=lag)
         for _ in range(args.warmup):
             solve()
         torch.cuda.synchronize()

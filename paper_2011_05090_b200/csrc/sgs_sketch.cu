@@ -43,9 +43,6 @@ srht_partials_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local,
                      int64_t ntiles, double* __restrict__ partials,
                      const sgs_status* st, unsigned long long* tl) {
   cg::cluster_group cl = cg::this_cluster();
-  pdl_enter();
-  if (status_stopped(st)) return;  // uniform across the cluster: nobody writes st here
-  if (tl && threadIdx.x == 0) atomicMin(tl + 12, gtimer());
   constexpr int T = 1 << LOGT;
   extern __shared__ double smem[];
   double* z = smem;                       // pidx(T) entries
@@ -55,13 +52,28 @@ srht_partials_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local,
   const int col = blockIdx.y;
   const int ngroups = gridDim.x / kSrhtCluster;
   const TX* x = X + (int64_t)col * ldx;
-
-  for (int j = threadIdx.x; j < k; j += blockDim.x) part[j] = 0.0;
-
   const int64_t t0 = (int64_t)blockIdx.x * tiles_per_cta;
   const int64_t t1 = min(t0 + tiles_per_cta, ntiles);
   const int64_t bmask = (int64_t(1) << log2_block) - 1;
+  const bool stage_sgn = LOGT == 12 && blockDim.x == kSrhtThreads;
+  // Before the dependency wait (the operator does not depend on the
+  // predecessor, only x does): clear the k-vector, load the first tile's
+  // sample rows and sign words.
+  for (int j = threadIdx.x; j < k; j += blockDim.x) part[j] = 0.0;
   int64_t cur_blk = -1;
+  if (t0 < t1) {
+    cur_blk = (row0 + t0 * T) >> log2_block;
+    const int32_t* sb = samples + cur_blk * (int64_t)k;
+    for (int j = threadIdx.x; j < k; j += blockDim.x) smp[j] = __ldg(sb + j);
+    if (stage_sgn && threadIdx.x < T / 32) {
+      const int64_t lw = t0 * T + 32 * (int64_t)threadIdx.x;
+      sgn[threadIdx.x] = lw < n_local ? __ldg(sign_bits + (lw >> 5)) : ~0u;
+    }
+  }
+  pdl_enter();
+  if (status_stopped(st)) return;  // uniform across the cluster: nobody writes st here
+  if (tl && threadIdx.x == 0) atomicMin(tl + 12, gtimer());
+
   for (int64_t t = t0; t < t1; ++t) {
     const int64_t lr0 = t * T;            // first local row of the tile
     const int64_t g0 = row0 + lr0;        // first global row
@@ -82,8 +94,9 @@ srht_partials_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local,
       // radix-8 pass runs in registers (same butterflies, same order).
       constexpr int Q = 8;
       // the tile's 128 sign words once into shared memory (lr0 is a multiple
-      // of 4096, so word w of the tile covers rows lr0 + 32 w .. + 31)
-      if (threadIdx.x < T / 32) {
+      // of 4096, so word w of the tile covers rows lr0 + 32 w .. + 31); the
+      // first tile's were loaded before the wait
+      if (t != t0 && threadIdx.x < T / 32) {
         const int64_t lw = lr0 + 32 * (int64_t)threadIdx.x;
         sgn[threadIdx.x] = lw < n_local ? __ldg(sign_bits + (lw >> 5)) : ~0u;
       }

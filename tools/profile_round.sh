@@ -24,4 +24,17 @@ timeout 300 python bench.py --config c3 --steps 1 --warmup 0 --no-cpu --no-e2e >
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
   --log-file "$OUT/c3_launches.csv" python bench.py --config c3 --steps 1 --warmup 0 --no-cpu --no-e2e \
   > "$OUT/ncu_c3.log" 2>&1
+# c3 one-synchronisation (lagged) cycle: launch list, then the staged SpMV and
+# the lagged LS launch in full
+L="python tools/timeline_gmres_lagged.py mixed"
+timeout 300 $L > "$OUT/c3_lagged_plain.log" 2>&1 || { echo "c3 lagged failed"; exit 1; }
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
+  --log-file "$OUT/c3_lagged_launches.csv" $L > "$OUT/ncu_c3_lagged.log" 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on \
+  -k regex:"csr_spmv_staged|ls_step|srht_partials" -s 1200 -c 3 -o "$OUT/c3_lagged_full" -f $L \
+  >> "$OUT/ncu_c3_lagged.log" 2>&1
+# device Rademacher sketch (c0r): bit generation and the packed-sign partials
+timeout 300 python tools/rad_probe.py > "$OUT/rad_plain.log" 2>&1 || { echo "rad failed"; exit 1; }
+timeout 600 ncu --set full --clock-control none --import-source on \
+  -k regex:"rademacher" -c 3 -o "$OUT/rad_full" -f python tools/rad_probe.py > "$OUT/ncu_rad.log" 2>&1
 echo done

@@ -1,7 +1,9 @@
+# Round bench + profiling pass (run under gpurun on one GPU):
+#   gpurun --timeout 3000 -- 'bash tools/round_bench.sh gpurun_out/r01c'
 set -u
-O=gpurun_out/r01b
+O=${1:-gpurun_out/r01c}
 mkdir -p $O
-for c in c1 c0 c2 c3; do
+for c in c1 c0 c0r c2 c3; do
   timeout 900 python bench.py --config $c > $O/bench_$c.json 2> $O/bench_$c.err || echo "bench $c failed"
   tail -1 $O/bench_$c.json | cut -c1-300
 done
