@@ -16,8 +16,9 @@ from paper_2011_05090_b200.workloads import CONFIGS, convdiff3d, make_w_device, 
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("lagged", [False, True])
 @pytest.mark.parametrize("policy", ["f64", "mixed"])
-def test_c3_rgmres_iterations_match_oracle(cuda, policy):
+def test_c3_rgmres_iterations_match_oracle(cuda, policy, lagged):
     ref = json.load(open(os.path.join(GOLDEN, "c3_oracle_128.json")))[policy]
     cfg = CONFIGS["c3"]
     N = cfg["grid"]
@@ -26,7 +27,7 @@ def test_c3_rgmres_iterations_match_oracle(cuda, policy):
     b = torch.from_numpy(rhs_gaussian(A.n, 0)).cuda()
     th = sg.make_sketch(sg.SketchKind.PSRHT, cfg["k"], A.n, 0)
     res = sg.gmres_restarted(A, b, th, sg.policy_from_name(policy), cfg["restart"],
-                             cfg["max_iters"], cfg["tol"])
+                             cfg["max_iters"], cfg["tol"], lagged=lagged)
     its = ref["iterations"]
     assert abs(res.iterations - its) <= round(0.02 * its), (res.iterations, its)
     assert res.final_residual <= cfg["tol"]
@@ -60,3 +61,29 @@ def test_c1_size_factorization_properties(cuda):
     st2.factorize_columns(W, W.shape[1], m)
     g = st2.device_factors()
     assert torch.equal(f.Q, g.Q) and torch.equal(f.R, g.R) and torch.equal(f.S, g.S)
+
+
+def test_c0_shape_device_rademacher_factorization(cuda):
+    """c0 shapes (n = 1e5, k = 600, fp64) with the reference's Rademacher
+    sketch generated on the device: W = QR to fp64 roundoff, S = Theta Q
+    nearly orthonormal (the sketch of the fp64 basis), streaming == batch."""
+    cfg = CONFIGS["c0r"]
+    n, m, k = cfg["n"], 120, cfg["k"]
+    W = make_w_device(n, m, 1e-4, 0, torch.float64, "cuda")
+    th = sg.make_sketch(sg.SketchKind.RADEMACHER, k, n, 0)
+    st = sg.RgsState(th, sg.UNIFIED64, capacity=m + 1)
+    st.factorize_columns(W, W.shape[1], m)
+    f = st.device_factors()
+    Wm = W[:, :n].t()
+    assert float(torch.linalg.norm(Wm - f.Q @ f.R) / torch.linalg.norm(Wm)) < 1e-14
+    eye = torch.eye(m, dtype=torch.float64, device="cuda")
+    assert float(torch.linalg.norm(eye - f.S.t() @ f.S, 2)) < 1e-12
+    cols = [0, m // 2, m - 1]
+    SQ = th.apply_block(f.Q[:, cols])
+    assert float(torch.linalg.norm(SQ - f.S[:, cols]) / torch.linalg.norm(f.S[:, cols])) < 1e-13
+    # streaming pushes give the batch factorisation bit for bit
+    st2 = sg.RgsState(th, sg.UNIFIED64, capacity=m + 1)
+    for j in range(12):
+        st2.push(Wm[:, j])
+    assert torch.equal(st2.device_factors().R, f.R[:12, :12])
+    assert torch.equal(st2.device_factors().Q, f.Q[:, :12])

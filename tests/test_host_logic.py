@@ -140,3 +140,27 @@ def test_srht_rows_limit_is_explicit():
     from paper_2011_05090_b200.sketch import MAX_SRHT_ROWS
     with pytest.raises(ValueError, match="k <= 8192"):
         sg.make_sketch(sg.SketchKind.PSRHT, MAX_SRHT_ROWS + 1, 1 << 20, 0)
+
+
+def test_oracle_lagged_gmres_restatement_cpu():
+    """The one-synchronisation restatement against the
+    reference's standard RGS-GMRES in the oracle: same Krylov space, so the
+    same iteration count to +-2 % and x to the stated tolerances."""
+    import numpy as np
+    from oracle import OracleSketch, csr_matvec, oracle_gmres, oracle_gmres_lagged
+    from paper_2011_05090_b200.workloads import convdiff3d, rhs_gaussian
+    N = 10
+    rp, ci, va = convdiff3d(N)
+    n = N ** 3
+    mv = lambda x: csr_matvec(rp, ci, va, n, x)  # noqa: E731
+    b = rhs_gaussian(n, 0)
+    th = OracleSketch("psrht", 120, n, 0)
+    for pol, tol in (("f64", 1e-9), ("mixed", 1e-6)):
+        a = oracle_gmres(mv, n, b, 80, th, pol, tol=tol)
+        lg = oracle_gmres_lagged(mv, n, b, 80, th, pol, tol=tol)
+        assert abs(a["iterations"] - lg["iterations"]) <= max(1, round(0.02 * a["iterations"]))
+        assert lg["final_residual"] <= 10 * a["final_residual"]
+    dec = oracle_gmres_lagged(mv, n, b, 25, th, "f64", scale_by_norm=False)
+    Q, H = dec["Q"], dec["H"]
+    AQ = np.column_stack([mv(Q[:, j]) for j in range(25)])
+    assert np.linalg.norm(AQ - Q @ H) <= 1e-12 * np.linalg.norm(AQ)
