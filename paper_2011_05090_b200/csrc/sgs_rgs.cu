@@ -418,22 +418,45 @@ __device__ __noinline__ void ls_gather(const T* part, int64_t stride, int CL, in
 template <typename T>
 __device__ __noinline__ void ls_reduce_parts(const double* parts, int nparts, int k, int ra,
                                              int nr, double scale, T* v, double* red) {
-  const int g = threadIdx.x >> 6, rl = threadIdx.x & 63;  // 8 groups x 64 rows
-  for (int r0 = 0; r0 < nr; r0 += 64) {
-    double acc = 0.0;
-    const int rr = r0 + rl;
-    if (rr < nr) {
-      const double* p = parts + ra + rr;
-#pragma unroll 4
-      for (int q = g; q < nparts; q += kCanonG) acc += __ldcg(p + (int64_t)q * k);
+  // 8 groups x 64 threads; a thread carries the chains of two rows (rl and
+  // rl + 64) and issues 8 terms of each before adding them, so a reduction
+  // over many parts (296 from the dense column kernel) takes a few L2 round
+  // trips instead of one per 4 terms.  Each chain still adds its parts in
+  // ascending order from 0.0 and the 8 chains are summed in group order: the
+  // canonical partial sum (canon_sum), bit for bit.
+  const int g = threadIdx.x >> 6, rl = threadIdx.x & 63;
+  for (int r0 = 0; r0 < nr; r0 += 128) {
+    const int rr0 = r0 + rl, rr1 = r0 + 64 + rl;
+    const bool ok0 = rr0 < nr, ok1 = rr1 < nr;
+    const double* p0 = parts + ra + (ok0 ? rr0 : 0);
+    const double* p1 = parts + ra + (ok1 ? rr1 : 0);
+    double acc0 = 0.0, acc1 = 0.0;
+    int q = g;
+    for (; q + 7 * kCanonG < nparts; q += 8 * kCanonG) {
+      double a[8], b[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        a[u] = ok0 ? __ldcg(p0 + (int64_t)(q + u * kCanonG) * k) : 0.0;
+        b[u] = ok1 ? __ldcg(p1 + (int64_t)(q + u * kCanonG) * k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        acc0 += a[u];
+        acc1 += b[u];
+      }
+    }
+    for (; q < nparts; q += kCanonG) {
+      if (ok0) acc0 += __ldcg(p0 + (int64_t)q * k);
+      if (ok1) acc1 += __ldcg(p1 + (int64_t)q * k);
     }
     __syncthreads();
-    red[g * 64 + rl] = acc;
+    red[g * 128 + rl] = acc0;
+    red[g * 128 + 64 + rl] = acc1;
     __syncthreads();
-    if (threadIdx.x < 64 && r0 + threadIdx.x < nr) {
+    if (threadIdx.x < 128 && r0 + (int)threadIdx.x < nr) {
       double t = 0.0;
 #pragma unroll
-      for (int q = 0; q < kCanonG; ++q) t += red[q * 64 + threadIdx.x];
+      for (int c = 0; c < kCanonG; ++c) t += red[c * 128 + threadIdx.x];
       v[r0 + threadIdx.x] = from_double<T>(scale * t);
     }
   }
