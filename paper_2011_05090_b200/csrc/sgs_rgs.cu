@@ -400,16 +400,18 @@ __device__ __noinline__ void ls_matvec(const T* __restrict__ M, int64_t ldm, int
 // c[j] = (sum_{q<CL} part[q*stride + j]) / div[j]  (ascending q), j in [j0, j1).
 template <typename T>
 __device__ __noinline__ void ls_gather(const T* part, int64_t stride, int CL, int j0, int j1,
-                                       const T* div, T* c) {
+                                       const T* div, T* c, T* div_keep = nullptr) {
   for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {  // CL <= 16: all loads in flight
     T v[kLsMaxCluster];
+    const T dj = div ? __ldcg(div + j) : T(1);
 #pragma unroll
     for (int q = 0; q < kLsMaxCluster; ++q)
       v[q] = q < CL ? __ldcg(part + (int64_t)q * stride + j) : T(0);
     T s = T(0);
 #pragma unroll
     for (int q = 0; q < kLsMaxCluster; ++q) if (q < CL) s += v[q];
-    c[j] = div ? s / __ldcg(div + j) : s;
+    c[j] = div ? s / dj : s;
+    if (div_keep) div_keep[j] = dj;  // a later phase reuses the divisor from shared memory
   }
 }
 
@@ -789,7 +791,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     xsync();
     SGS_TR(4);
     if (threadIdx.x < 3) bc[threadIdx.x] = ls_slot_sum(XA + threadIdx.x, sA, CL);
-    if (nq > 0) ls_gather<T>(XA + 8, sA, CL, 0, nq, AL, c1);  // T^T s' / alpha
+    if (nq > 0) ls_gather<T>(XA + 8, sA, CL, 0, nq, AL, c1, to);  // T^T s' / alpha; to = alpha
     if (lag && nq > 0) ls_gather<T>(XA + 8 + cap, sA, CL, 0, nq, AL, zc);  // T^T p' / alpha
     __syncthreads();
     const double r_ii = (double)sqrt(bc[0]);
@@ -831,7 +833,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     for (int j = threadIdx.x; j < nq; j += blockDim.x) {
       const T cj = c1[j] / rT;       // (Qs^T s)_j
       c1[j] = cj;
-      c2[j] = cj / __ldcg(AL + j);   // coefficient on the unnormalised column T_j
+      c2[j] = cj / to[j];            // coefficient on the unnormalised column T_j (to = alpha)
     }
     __syncthreads();
     // Fast path: Q_s = T diag(1/alpha) is orthonormal, so ||t||^2 = ||s||^2 -
@@ -849,8 +851,8 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
         acc_c = fma(c1[j], c1[j], acc_c);
         if (fused) acc_p = fma(c1[j], zc[j], acc_p);
       }
-      acc_c = block_sum(acc_c, red);
-      if (fused) acc_p = block_sum(acc_p, red);
+      if (fused) block_sum2(acc_c, acc_p, red);  // one barrier pair, block_sum's order
+      else acc_c = block_sum(acc_c, red);
       const T ss0 = bc[0] / (rT * rT);
       const T tt_est = ss0 - acc_c;
       if (nq == 0 || tt_est >= T(0.5) * ss0) {
