@@ -59,11 +59,12 @@ __device__ __forceinline__ void l2_prefetch(const void* src, uint32_t bytes) {
 
 // L2 prefetch budget (bytes) of the SRHT column kernel's pre-wait prologue:
 // about what one LS launch's latency lets HBM move (SGS_COL_PF_MB overrides;
-// measured at c1.  The dense ring kernel measured slower with it at c0.)
+// measured at c1: 48 MB 5777, 64 MB 5820, 72 MB 5831, 80 MB 5841, 88 MB 5818,
+// 96 MB 5807 columns/s.  The dense ring kernel measured slower with it at c0.)
 static long col_pf_bytes() {
   static const long b = [] {
     const char* e = getenv("SGS_COL_PF_MB");
-    return (e ? atol(e) : 64L) << 20;
+    return (e ? atol(e) : 80L) << 20;
   }();
   return b;
 }
