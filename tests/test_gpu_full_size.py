@@ -87,3 +87,66 @@ def test_c0_shape_device_rademacher_factorization(cuda):
         st2.push(Wm[:, j])
     assert torch.equal(st2.device_factors().R, f.R[:12, :12])
     assert torch.equal(st2.device_factors().Q, f.Q[:, :12])
+
+
+def _metrics_dev(W, f):
+    """factor_metrics (oracle/metrics.py) on the GPU in fp64: ||I - S^T S||_2,
+    ||I - Q^T Q||_2, ||W - QR||_F / ||W||_F."""
+    Q, R, S = f.Q.double(), f.R.double(), f.S.double()
+    Wd = W.double()
+    eye = torch.eye(Q.shape[1], dtype=torch.float64, device=Q.device)
+    return {"orth_S_2": float(torch.linalg.matrix_norm(eye - S.t() @ S, ord=2)),
+            "orth_Q_2": float(torch.linalg.matrix_norm(eye - Q.t() @ Q, ord=2)),
+            "relres_F": float(torch.linalg.norm(Wd - Q @ R) / torch.linalg.norm(Wd))}
+
+
+def _golden_fullsize():
+    return np.load(os.path.join(GOLDEN, "fullsize.npz"))
+
+
+def test_c0_full_size_metrics_within_10x_of_oracle(cuda):
+    """BASELINE c0 at full size (n = 1e5, m = 300, k = 600 Gaussian, fp64,
+    sigma_min = 1e-8): the 2-norm metrics within 10x of the oracle's
+    (tests/golden/fullsize.npz, oracle/make_fullsize_golden.py)."""
+    from paper_2011_05090_b200.workloads import make_w
+    g = _golden_fullsize()
+    n, m, k = 100_000, 300, 600
+    W = torch.from_numpy(make_w(n, m, 1e-8, 0)).cuda()
+    th = sg.make_sketch(sg.SketchKind.GAUSSIAN, k, n, 0)
+    f, _ = sg.rgs_factorize(W, th, sg.UNIFIED64, device_factors=True)
+    ours = _metrics_dev(W, f)
+    for key, v in ours.items():
+        assert v <= 10.0 * max(float(g[f"c0_{key}"]), 1e-15), (key, v, float(g[f"c0_{key}"]))
+
+
+def test_c0_twin_full_size_q_r_s_within_1e10(cuda):
+    """c0's well-conditioned twin (sigma_min = 1e-2) at full size: R, S and
+    sampled rows of Q within 1e-10 of the oracle (the north_star fp64 gate)."""
+    from paper_2011_05090_b200.workloads import make_w
+    g = _golden_fullsize()
+    n, m, k = 100_000, 300, 600
+    W = torch.from_numpy(make_w(n, m, 1e-2, 0)).cuda()
+    th = sg.make_sketch(sg.SketchKind.GAUSSIAN, k, n, 0)
+    f, _ = sg.rgs_factorize(W, th, sg.UNIFIED64, device_factors=True)
+    rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))  # noqa: E731
+    assert rel(f.R.cpu().numpy(), g["c0twin_R"]) <= 1e-10
+    assert rel(f.S.cpu().numpy(), g["c0twin_S"]) <= 1e-10
+    rows = torch.from_numpy(g["c0twin_rows"]).cuda()
+    assert rel(f.Q[rows].cpu().numpy(), g["c0twin_Qrows"]) <= 1e-10
+
+
+def test_c1_full_size_metrics_within_10x_of_oracle(cuda):
+    """BASELINE c1 at full size (n = 1e6, m = 500, k = 1500 P-SRHT,
+    MIXED32_64, breakdown_factor 0, W fp32): the 2-norm metrics within 10x of
+    the oracle's, and diag(R) close to the oracle's."""
+    from paper_2011_05090_b200.workloads import make_w
+    g = _golden_fullsize()
+    n, m, k = 1_000_000, 500, 1500
+    W = torch.from_numpy(make_w(n, m, 1e-10, 0, dtype=np.float32)).cuda()
+    th = sg.make_sketch(sg.SketchKind.PSRHT, k, n, 0)
+    f, _ = sg.rgs_factorize(W, th, sg.MIXED32_64, breakdown_factor=0.0, device_factors=True)
+    ours = _metrics_dev(W, f)
+    for key, v in ours.items():
+        assert v <= 10.0 * max(float(g[f"c1_{key}"]), 1e-15), (key, v, float(g[f"c1_{key}"]))
+    d = torch.diagonal(f.R).cpu().numpy()
+    assert np.linalg.norm(d - g["c1_Rdiag"]) <= 1e-3 * np.linalg.norm(g["c1_Rdiag"])
