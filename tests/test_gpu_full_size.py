@@ -150,3 +150,24 @@ def test_c1_full_size_metrics_within_10x_of_oracle(cuda):
         assert v <= 10.0 * max(float(g[f"c1_{key}"]), 1e-15), (key, v, float(g[f"c1_{key}"]))
     d = torch.diagonal(f.R).cpu().numpy()
     assert np.linalg.norm(d - g["c1_Rdiag"]) <= 1e-3 * np.linalg.norm(g["c1_Rdiag"])
+
+
+def test_c2_shape_q_r_s_vs_oracle(cuda):
+    """BASELINE c2's shape (n = 2^23, k = 2000 block-SRHT over 8 seeded 2^20-row
+    blocks, fp64, breakdown_factor 0) with 200 of its 1000 columns (the oracle
+    host cannot hold the full W): R, S and sampled rows of Q within 1e-10 of the
+    oracle (tests/golden/c2m200.npz, oracle/make_c2_golden.py), metrics within 10x."""
+    from paper_2011_05090_b200.workloads import make_w
+    g = np.load(os.path.join(GOLDEN, "c2m200.npz"))
+    n, m, k = 1 << 23, 200, 2000
+    W = torch.from_numpy(make_w(n, m, 1e-6, 0)).cuda()
+    th = sg.make_sketch(sg.SketchKind.BLOCK_SRHT, k, n, 0, block_log2=20)
+    f, _ = sg.rgs_factorize(W, th, sg.UNIFIED64, breakdown_factor=0.0, device_factors=True)
+    rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))  # noqa: E731
+    assert rel(f.R.cpu().numpy(), g["c2_R"]) <= 1e-10
+    assert rel(f.S.cpu().numpy(), g["c2_S"]) <= 1e-10
+    rows = torch.from_numpy(g["c2_rows"]).cuda()
+    assert rel(f.Q[rows].cpu().numpy(), g["c2_Qrows"]) <= 1e-10
+    ours = _metrics_dev(W, f)
+    for key, v in ours.items():
+        assert v <= 10.0 * max(float(g[f"c2_{key}"]), 1e-15), (key, v, float(g[f"c2_{key}"]))

@@ -25,4 +25,19 @@ for name, n, m, k, smin, kind, pol, bf, dt in (
         out[name]["rel_R"] = rel(f.R.cpu().numpy(), g["c0twin_R"])
         out[name]["rel_S"] = rel(f.S.cpu().numpy(), g["c0twin_S"])
         out[name]["rel_Qrows"] = rel(f.Q[rows].cpu().numpy(), g["c0twin_Qrows"])
+gp = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
+                  "c2m200.npz")
+if os.path.exists(gp):  # c2's shape, 200 columns (oracle/make_c2_golden.py)
+    g2 = np.load(gp)
+    n, m, k = 1 << 23, 200, 2000
+    W = torch.from_numpy(make_w(n, m, 1e-6, 0)).cuda()
+    th = sg.make_sketch(sg.SketchKind.BLOCK_SRHT, k, n, 0, block_log2=20)
+    f, _ = sg.rgs_factorize(W, th, sg.UNIFIED64, breakdown_factor=0.0, device_factors=True)
+    ours = _metrics_dev(W, f)
+    rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))  # noqa: E731
+    rows = torch.from_numpy(g2["c2_rows"]).cuda()
+    out["c2m200"] = {key: {"gpu": v, "oracle": float(g2[f"c2_{key}"])} for key, v in ours.items()}
+    out["c2m200"].update(rel_R=rel(f.R.cpu().numpy(), g2["c2_R"]),
+                         rel_S=rel(f.S.cpu().numpy(), g2["c2_S"]),
+                         rel_Qrows=rel(f.Q[rows].cpu().numpy(), g2["c2_Qrows"]))
 print(json.dumps(out, indent=1))
