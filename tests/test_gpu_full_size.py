@@ -171,3 +171,22 @@ def test_c2_shape_q_r_s_vs_oracle(cuda):
     ours = _metrics_dev(W, f)
     for key, v in ours.items():
         assert v <= 10.0 * max(float(g[f"c2_{key}"]), 1e-15), (key, v, float(g[f"c2_{key}"]))
+
+
+def test_c4_shape_metrics_vs_oracle(cuda):
+    """BASELINE c4's shape on one GPU (n = 2^25, k = 3000 block-SRHT over 32
+    seeded 2^20-row blocks, W fp32, MIXED32_64, breakdown_factor 0) with 64 of
+    its 1500 columns (c4 itself needs 4 GPUs): the 2-norm metrics within 10x of
+    the oracle's (tests/golden/c4m64.npz, oracle/make_c4_golden.py) and R close
+    to the oracle's at the fp32 level."""
+    from paper_2011_05090_b200.workloads import make_w
+    g = np.load(os.path.join(GOLDEN, "c4m64.npz"))
+    n, m, k = 1 << 25, 64, 3000
+    W = torch.from_numpy(make_w(n, m, 1e-10, 0, dtype=np.float32)).cuda()
+    th = sg.make_sketch(sg.SketchKind.BLOCK_SRHT, k, n, 0, block_log2=20)
+    f, _ = sg.rgs_factorize(W, th, sg.MIXED32_64, breakdown_factor=0.0, device_factors=True)
+    ours = _metrics_dev(W, f)
+    for key, v in ours.items():
+        assert v <= 10.0 * max(float(g[f"c4_{key}"]), 1e-15), (key, v, float(g[f"c4_{key}"]))
+    R = f.R.cpu().numpy()
+    assert np.linalg.norm(R - g["c4_R"]) <= 1e-5 * np.linalg.norm(g["c4_R"])

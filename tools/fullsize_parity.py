@@ -40,4 +40,16 @@ if os.path.exists(gp):  # c2's shape, 200 columns (oracle/make_c2_golden.py)
     out["c2m200"].update(rel_R=rel(f.R.cpu().numpy(), g2["c2_R"]),
                          rel_S=rel(f.S.cpu().numpy(), g2["c2_S"]),
                          rel_Qrows=rel(f.Q[rows].cpu().numpy(), g2["c2_Qrows"]))
+g4p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
+                   "c4m64.npz")
+if os.path.exists(g4p):  # c4's shape, 64 columns (oracle/make_c4_golden.py)
+    g4 = np.load(g4p)
+    n, m, k = 1 << 25, 64, 3000
+    W = torch.from_numpy(make_w(n, m, 1e-10, 0, dtype=np.float32)).cuda()
+    th = sg.make_sketch(sg.SketchKind.BLOCK_SRHT, k, n, 0, block_log2=20)
+    f, _ = sg.rgs_factorize(W, th, sg.MIXED32_64, breakdown_factor=0.0, device_factors=True)
+    ours = _metrics_dev(W, f)
+    out["c4m64"] = {key: {"gpu": v, "oracle": float(g4[f"c4_{key}"])} for key, v in ours.items()}
+    R = f.R.cpu().numpy()
+    out["c4m64"]["rel_R"] = float(np.linalg.norm(R - g4["c4_R"]) / np.linalg.norm(g4["c4_R"]))
 print(json.dumps(out, indent=1))
