@@ -31,7 +31,7 @@ timeout 300 $L > "$OUT/c3_lagged_plain.log" 2>&1 || { echo "c3 lagged failed"; e
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
   --log-file "$OUT/c3_lagged_launches.csv" $L > "$OUT/ncu_c3_lagged.log" 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:"csr_spmv_staged|ls_step|srht_partials" -s 1200 -c 3 -o "$OUT/c3_lagged_full" -f $L \
+  -k regex:"csr_spmv_staged|ls_step|srht_partials" -s 300 -c 3 -o "$OUT/c3_lagged_full" -f $L \
   >> "$OUT/ncu_c3_lagged.log" 2>&1
 # device Rademacher sketch (c0r): bit generation and the packed-sign partials
 timeout 300 python tools/rad_probe.py > "$OUT/rad_plain.log" 2>&1 || { echo "rad failed"; exit 1; }
