@@ -28,6 +28,10 @@ def _free_port():
 CASES = {
     "psrht_mixed": dict(kind="psrht", n=3 * 4096 * 4 + 1000, m=40, k=200, pol="mixed", blog=None),
     "block_f64": dict(kind="block_srht", n=4 * 8192, m=30, k=160, pol="f64", blog=13),
+    # device-generated Rademacher signs: the shard reads its rows of the packed
+    # sign array (row0 need not be tile-aligned for the dense chunking)
+    "rademacher_f64": dict(kind="rademacher", n=6001, m=24, k=120, pol="f64", blog=None),
+    "gaussian_mixed": dict(kind="gaussian", n=7003, m=20, k=100, pol="mixed", blog=None),
 }
 
 
