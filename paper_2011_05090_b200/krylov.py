@@ -13,6 +13,7 @@ runs on the host, x = (||b|| / alpha) Q y on the device.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -30,6 +31,7 @@ __all__ = ["SparseMatrix", "Ilu0Preconditioner", "ilu0", "arnoldi", "gmres", "gm
            "ArnoldiDecomposition", "GmresResult", "RestartedResult"]
 
 _POLL = 8  # Arnoldi steps between status polls
+_HALO = os.environ.get("SGS_HALO", "1") != "0"  # row-sharded SpMV: halo window (else all-gather)
 
 
 @dataclass
@@ -125,7 +127,9 @@ class _RowBlock:
     """A contiguous row block of a SparseMatrix on the device; its SpMV takes
     the full input vector and writes the block's rows."""
 
-    def __init__(self, A: SparseMatrix, row0: int, n_rows: int, device=None):
+    def __init__(self, A: SparseMatrix, row0: int, n_rows: int, device=None, col0: int = 0):
+        """``col0``: the input vector starts at global column col0 (a halo
+        window); column indices are stored relative to it."""
         _lib.require_cuda()
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None \
             else torch.device(device)
@@ -133,7 +137,8 @@ class _RowBlock:
         rp = np.asarray(A.row_ptr[row0:row0 + n_rows + 1], dtype=np.int64) - lo
         self.n, self.n_rows, self.row0 = A.n, n_rows, row0
         self.rp = torch.from_numpy(rp.astype(np.int32)).to(dev)
-        self.ci = torch.from_numpy(np.asarray(A.col_idx[lo:hi], dtype=np.int32)).to(dev)
+        ci = np.asarray(A.col_idx[lo:hi], dtype=np.int64) - int(col0)
+        self.ci = torch.from_numpy(ci.astype(np.int32)).to(dev)
         self.va = torch.from_numpy(np.asarray(A.values[lo:hi], dtype=np.float64)).to(dev)
 
     def spmv_into(self, x_ptr: int, x_code: int, y: torch.Tensor, alpha=None, status=None):
@@ -330,8 +335,12 @@ class _Dist:
     operator rows [row0, row0 + n_loc) and the same rows of every n-vector
     (shard_rows, aligned to the sketch's tiles).  The RGS state is sharded as
     in RgsState(comm=...): one k-vector all-reduce per sketch, replicated LS
-    and Givens.  The SpMV all-gathers its input vector; norms all-reduce
-    their squares."""
+    and Givens.  Norms all-reduce their squares.  The SpMV input is a halo
+    window: the columns this rank's rows touch form [wlo, whi), and each
+    step receives only the other ranks' rows inside it by point-to-point
+    messages (for c3's stencil one 128 x 128 plane per neighbour instead of
+    the whole vector); a window wider than half the vector falls back to the
+    all-gather."""
 
     def __init__(self, comm, A: SparseMatrix, align: int, device):
         from .workloads import shard_rows
@@ -344,6 +353,65 @@ class _Dist:
         self.block = A.row_block(self.row0, self.n_loc, device)
         self.device = device
         self._full = {}
+        self._win = {}
+        self._plan_halo(A)
+
+    def _plan_halo(self, A: SparseMatrix) -> None:
+        import torch.distributed as tdist
+        lo, hi = int(A.row_ptr[self.row0]), int(A.row_ptr[self.row0 + self.n_loc])
+        cols = np.asarray(A.col_idx[lo:hi])
+        wlo = min(int(cols.min()) if cols.size else self.row0, self.row0)
+        whi = max(int(cols.max()) + 1 if cols.size else 0, self.row0 + self.n_loc)
+        world, me = self.comm.world, self.comm.rank
+        win = torch.tensor([wlo, whi], dtype=torch.int64, device=self.device)
+        allw = [torch.empty_like(win) for _ in range(world)]
+        tdist.all_gather(allw, win, group=self.comm.group)
+        allw = [tuple(int(v) for v in t.cpu()) for t in allw]
+        rows = [sum(self.counts[:r]) for r in range(world)]  # first row of each rank
+        self.recvs, self.sends = [], []
+        for q in range(world):
+            if q == me:
+                continue
+            q0, q1 = rows[q], rows[q] + self.counts[q]
+            a, b = max(wlo, q0), min(whi, q1)
+            if a < b:
+                self.recvs.append((q, a, b))       # rows [a, b) of rank q into the window
+            r0_, r1_ = allw[q]
+            a, b = max(r0_, self.row0), min(r1_, self.row0 + self.n_loc)
+            if a < b:
+                self.sends.append((q, a, b))       # my rows [a, b) to rank q
+        # the halo path when the window is small; every rank decides identically
+        # (each rank's choice only affects its own receives and the matching sends)
+        widths = [w[1] - w[0] for w in allw]
+        self.halo = _HALO and max(widths) <= self.n // 2
+        self.wlo, self.whi = wlo, whi
+        if self.halo:
+            self.wblock = _RowBlock(A, self.row0, self.n_loc, self.device, col0=wlo)
+
+    def window(self, x_local: torch.Tensor):
+        """(input vector, row block) for this rank's SpMV: the halo window of
+        x (or the all-gathered x when the window is wide)."""
+        if not self.halo:
+            return self.full(x_local), self.block
+        import torch.distributed as tdist
+        buf = self._win.get(x_local.dtype)
+        if buf is None:
+            buf = self._win[x_local.dtype] = torch.empty(self.whi - self.wlo,
+                                                          dtype=x_local.dtype,
+                                                          device=self.device)
+        o = self.row0 - self.wlo
+        buf[o:o + self.n_loc].copy_(x_local)
+        ops = []
+        for q, a, b in self.recvs:
+            ops.append(tdist.P2POp(tdist.irecv, buf[a - self.wlo:b - self.wlo], q,
+                                   group=self.comm.group))
+        for q, a, b in self.sends:
+            ops.append(tdist.P2POp(tdist.isend, x_local[a - self.row0:b - self.row0], q,
+                                   group=self.comm.group))
+        if ops:
+            for req in tdist.batch_isend_irecv(ops):
+                req.wait()
+        return buf, self.wblock
 
     def full(self, x_local: torch.Tensor) -> torch.Tensor:
         buf = self._full.get(x_local.dtype)
@@ -392,7 +460,8 @@ def _operator_norm_estimate(A: SparseMatrix, ws: _Workspace, iters: int = 20,
         if dist is None:
             _eff_matvec_into(A, M, ws, ws.v.data_ptr(), _lib.SGS_F64, ws.w)
         else:
-            dist.block.spmv_into(dist.full(ws.v).data_ptr(), _lib.SGS_F64, ws.w)
+            xw, blk = dist.window(ws.v)
+            blk.spmv_into(xw.data_ptr(), _lib.SGS_F64, ws.w)
         ws.norm(ws.w, 1)
         if dist is not None:
             dist.norm_(ws.nrm, 1)
@@ -460,8 +529,8 @@ class _ArnoldiEngine:
             _eff_matvec_into(self.A, self.M, self.ws, st._qcol_ptr(i), st.ccode, out,
                              alpha=alpha, status=status)
         else:
-            xf = self.dist.full(st._Q[i, :self.n_loc])
-            self.dist.block.spmv_into(xf.data_ptr(), st.ccode, out, alpha=alpha, status=status)
+            xw, blk = self.dist.window(st._Q[i, :self.n_loc])
+            blk.spmv_into(xw.data_ptr(), st.ccode, out, alpha=alpha, status=status)
 
     # ---- one-synchronisation (lagged) steps -----------------------------------------
     def _giv(self, c: int, alpha, tol):
@@ -479,8 +548,8 @@ class _ArnoldiEngine:
             _eff_matvec_into(self.A, self.M, ws, st._qcol_ptr(c), st.ccode, ws.w, alpha=alpha,
                              status=st.status)
         else:
-            xf = self.dist.full(st._Q[c, :self.n_loc])
-            self.dist.block.spmv_into(xf.data_ptr(), st.ccode, ws.w, alpha=alpha, status=st.status)
+            xw, blk = self.dist.window(st._Q[c, :self.n_loc])
+            blk.spmv_into(xw.data_ptr(), st.ccode, ws.w, alpha=alpha, status=st.status)
         st.theta.partials_into(ws.w.data_ptr(), _lib.SGS_F64, self.n_loc, 1, st._parts_p,
                                n_local=self.n_loc, row0=st.row0, status=st.status)
         p_raw = (st._parts_p.data_ptr(), st.nparts, st.theta.scale)

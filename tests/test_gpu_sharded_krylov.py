@@ -48,6 +48,18 @@ def _worker(rank, world, port, out):
     rr = sg.gmres_restarted(A, b, th, sg.UNIFIED64, restart=25, max_iters=200, tol=1e-8,
                             comm=comm)
     dec = sg.arnoldi(A, b, 20, theta=th, policy=sg.UNIFIED64, comm=comm)
+    # the halo window (default) and the all-gather give the SpMV the same x:
+    # bit-identical solves
+    import paper_2011_05090_b200.krylov as kr
+    assert kr._HALO
+    kr._HALO = False
+    g64 = sg.gmres(A, b, m=60, theta=th, policy=sg.UNIFIED64, tol=1e-9, comm=comm)
+    glg = sg.gmres(A, b, m=40, theta=th, policy=sg.MIXED32_64, tol=1e-6, comm=comm, lagged=True)
+    kr._HALO = True
+    hlg = sg.gmres(A, b, m=40, theta=th, policy=sg.MIXED32_64, tol=1e-6, comm=comm, lagged=True)
+    assert np.array_equal(g64.x, r64.x) and np.array_equal(g64.residual_history,
+                                                          r64.residual_history)
+    assert np.array_equal(glg.x, hlg.x)
     out[rank] = (r64.x, r64.iterations, r64.residual_history, r64.final_residual,
                  rmx.iterations, rmx.final_residual, rr.x, rr.iterations, rr.cycles,
                  dec.Q, dec.H)
