@@ -514,9 +514,9 @@ def run_gmres(args):
     cpu = None
     if not args.no_cpu:
         threads = os.cpu_count() or 1
-        v, dt = cpu_gmres_sample(12, threads)
+        v, dt = cpu_gmres_sample(40, threads)
         cpu = {"value": v, "unit": "steps/s", "cores": threads, "kind": "port",
-               "sample": f"12 Arnoldi steps of c3 at full size (n={n}, k={cfg['k']}, fp64), "
+               "sample": f"40 Arnoldi steps of c3 at full size (n={n}, k={cfg['k']}, fp64), "
                          f"oracle port, {dt:.1f} s"}
     print(json.dumps({"metric": "RGMRES Arnoldi steps/s", "value": out["f64"]["steps_per_s"],
                       "unit": "steps/s", "n_gpus": 1, "steps": args.steps,
@@ -601,7 +601,8 @@ def main():
     ap.add_argument("--columns", type=int, default=None,
                     help="override the config's column count (functional runs; the workload "
                          "name records it)")
-    ap.add_argument("--cpu-cols", type=int, default=24)
+    ap.add_argument("--cpu-cols", type=int, default=96,
+                    help="columns of the CPU baseline sample (about 10-30 s of host work at c1)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
