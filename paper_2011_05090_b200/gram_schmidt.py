@@ -630,6 +630,12 @@ class RgsState:
         # cross-stream waits in the kernel chain.
         late, late_chunk = self._e2e_late
         bounds, c0, sz = [0], 0, 2
+        if self.theta.is_gaussian:
+            # the dense P = Theta W GEMM reads all of Theta and fills 64-column
+            # tiles per launch: sketch whole tiles (a chunk of 8 columns would
+            # cost as much as 64)
+            bounds = list(range(0, m, 64)) + [m]
+            c0 = m
         while c0 < m:
             c0 = min(m, c0 + min(sz, chunk if c0 < late else late_chunk))
             bounds.append(c0)
