@@ -289,15 +289,16 @@ dense_gemv_kernel(const double* __restrict__ thetaT, int64_t ldt, int k,
   }
 }
 
-// split-K GEMM tile: 128 sketch rows (j) x 64 columns (c), 256 threads each
-// owning 8 (j) x 4 (c) outputs; per output the chain is the ascending-row FMA
+// split-K GEMM tile: 128 sketch rows (j) x 64 columns (c), 128 threads each
+// owning 8 (j) x 8 (c) outputs; per output the chain is the ascending-row FMA
 // of dense_gemv_kernel over the same row chunk, so P = Theta W is
 // bit-identical to per-column sketches.  Operands stream through a
 // kGBS-stage cp.async pipeline of kGBR-row stages (16-byte copies for the
 // rows of Theta^T, element copies for the column-major W, whose part
-// boundaries are not aligned); W is kept transposed in shared memory, padded
-// against bank conflicts.
-constexpr int kGBJ = 128, kGBC = 64, kGBR = 16, kGBS = 3, kGBP = kGBR + 1;
+// boundaries are not aligned).  Both operands sit row-major in shared memory
+// (j resp. c contiguous), so a row's 8 + 8 operands are four 16-byte loads
+// each for 64 FMAs.
+constexpr int kGBJ = 128, kGBC = 64, kGBR = 16, kGBS = 3, kGBT = 128;
 
 __device__ __forceinline__ uint32_t smem_u32a(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -316,13 +317,30 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// W rows padded by 16 bytes: the element copies of a column's 16 rows land in
+// different banks
+template <typename TX> __host__ __device__ constexpr int gemm_bpad() { return kGBC + 16 / (int)sizeof(TX); }
+
 template <typename TX>
-constexpr size_t dense_gemm_smem() {
-  return (size_t)kGBS * kGBR * kGBJ * sizeof(double) + (size_t)kGBS * kGBC * kGBP * sizeof(TX);
+__host__ __device__ constexpr size_t dense_gemm_smem() {
+  return (size_t)kGBS * kGBR * kGBJ * sizeof(double) +
+         (size_t)kGBS * kGBR * gemm_bpad<TX>() * sizeof(TX);
 }
 
 template <typename TX>
-__global__ void __launch_bounds__(256)
+__device__ __forceinline__ void load4(const TX* p, double (&v)[4]) {
+  if constexpr (sizeof(TX) == 8) {
+    const double2 a = *reinterpret_cast<const double2*>(p);
+    const double2 b = *reinterpret_cast<const double2*>(p + 2);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  } else {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  }
+}
+
+template <typename TX>
+__global__ void __launch_bounds__(kGBT, 2)
 dense_gemm_kernel(const double* __restrict__ thetaT, int64_t ldt, int k,
                   const TX* __restrict__ X, int64_t ldx, int ncols, int64_t n,
                   double* __restrict__ partials, const sgs_status* st) {
@@ -330,19 +348,20 @@ dense_gemm_kernel(const double* __restrict__ thetaT, int64_t ldt, int k,
   if (status_stopped(st)) return;
   extern __shared__ __align__(16) unsigned char gsm_raw[];
   double (*As)[kGBR][kGBJ] = reinterpret_cast<double (*)[kGBR][kGBJ]>(gsm_raw);
-  TX (*Bt)[kGBC][kGBP] = reinterpret_cast<TX (*)[kGBC][kGBP]>(
+  constexpr int BP = gemm_bpad<TX>();
+  TX (*Bs)[kGBR][BP] = reinterpret_cast<TX (*)[kGBR][BP]>(
       gsm_raw + (size_t)kGBS * kGBR * kGBJ * sizeof(double));
   const int jt = blockIdx.x * kGBJ, ct = blockIdx.y * kGBC;
   const int p = blockIdx.z, nparts = gridDim.z;
   const int64_t r0 = chunk_begin(n, nparts, p), r1 = chunk_begin(n, nparts, p + 1);
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 8 threads
   // thread outputs: j = jt + tx*4 + {0..3} and jt + 64 + tx*4 + {0..3};
-  //                 c = ct + ty*2 + {0,1} and ct + 32 + ty*2 + {0,1}
-  double acc[8][4];
+  //                 c = ct + ty*4 + {0..3} and ct + 32 + ty*4 + {0..3}
+  double acc[8][8];
 #pragma unroll
   for (int a = 0; a < 8; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
   const int nst = (int)((r1 - r0 + kGBR - 1) / kGBR);
   auto issue = [&](int sidx) {
     if (sidx < nst) {
@@ -350,21 +369,21 @@ dense_gemm_kernel(const double* __restrict__ thetaT, int64_t ldt, int k,
       const int64_t rs = r0 + (int64_t)sidx * kGBR;
       // Theta^T: kGBR rows x kGBJ doubles, 16-byte chunks (ldt even, zero padded)
 #pragma unroll
-      for (int u = 0; u < kGBR * kGBJ / 2 / 256; ++u) {
-        const int e = threadIdx.x + u * 256;
+      for (int u = 0; u < kGBR * kGBJ / 2 / kGBT; ++u) {
+        const int e = threadIdx.x + u * kGBT;
         const int rr = e / (kGBJ / 2), jj = 2 * (e % (kGBJ / 2));
         const bool ok = rs + rr < r1 && jt + jj < ldt;
         const double* src = ok ? thetaT + (rs + rr) * ldt + jt + jj : thetaT;
         cp_async_el<16>(&As[buf][rr][jj], src, ok);
       }
-      // W: kGBC columns x kGBR rows, one element per copy, stored transposed
+      // W: kGBR rows x kGBC columns, one element per copy (column-major source)
 #pragma unroll
-      for (int u = 0; u < kGBR * kGBC / 256; ++u) {
-        const int e = threadIdx.x + u * 256;
+      for (int u = 0; u < kGBR * kGBC / kGBT; ++u) {
+        const int e = threadIdx.x + u * kGBT;
         const int cc = e / kGBR, rr = e % kGBR;
         const bool ok = rs + rr < r1 && ct + cc < ncols;
         const TX* src = ok ? X + (int64_t)(ct + cc) * ldx + rs + rr : X;
-        cp_async_el<sizeof(TX)>(&Bt[buf][cc][rr], src, ok);
+        cp_async_el<sizeof(TX)>(&Bs[buf][rr][cc], src, ok);
       }
     }
     cp_async_commit();  // one group per stage slot, even when empty
@@ -378,15 +397,22 @@ dense_gemm_kernel(const double* __restrict__ thetaT, int64_t ldt, int k,
     const int buf = sidx % kGBS;
     const int nrow = (int)min((int64_t)kGBR, r1 - (r0 + (int64_t)sidx * kGBR));
     for (int rr = 0; rr < nrow; ++rr) {  // ascending rows: the GEMV's chain
-      const double4 a0 = *reinterpret_cast<const double4*>(&As[buf][rr][tx * 4]);
-      const double4 a1 = *reinterpret_cast<const double4*>(&As[buf][rr][64 + tx * 4]);
-      const double av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const double bv[4] = {(double)Bt[buf][ty * 2][rr], (double)Bt[buf][ty * 2 + 1][rr],
-                            (double)Bt[buf][32 + ty * 2][rr], (double)Bt[buf][33 + ty * 2][rr]};
+      double av[8], bv[8];
+      {
+        double t0[4], t1[4];
+        load4<double>(&As[buf][rr][tx * 4], t0);
+        load4<double>(&As[buf][rr][64 + tx * 4], t1);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) { av[q] = t0[q]; av[4 + q] = t1[q]; }
+        load4<TX>(&Bs[buf][rr][ty * 4], t0);
+        load4<TX>(&Bs[buf][rr][32 + ty * 4], t1);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) { bv[q] = t0[q]; bv[4 + q] = t1[q]; }
+      }
 #pragma unroll
       for (int a = 0; a < 8; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+        for (int b = 0; b < 8; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
     }
   }
   cp_async_wait<0>();
@@ -394,8 +420,8 @@ dense_gemm_kernel(const double* __restrict__ thetaT, int64_t ldt, int k,
   for (int a = 0; a < 8; ++a) {
     const int j = jt + (a < 4 ? tx * 4 + a : 64 + tx * 4 + a - 4);
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int c = ct + (b < 2 ? ty * 2 + b : 32 + ty * 2 + b - 2);
+    for (int b = 0; b < 8; ++b) {
+      const int c = ct + (b < 4 ? ty * 4 + b : 32 + ty * 4 + b - 4);
       if (j < k && c < ncols) partials[((int64_t)c * nparts + p) * k + j] = acc[a][b];
     }
   }
@@ -524,7 +550,7 @@ static int launch_dense(const double* thetaT, int64_t ldt, int k, const void* X,
   constexpr size_t smem = dense_gemm_smem<TX>();
   cudaFuncSetAttribute(dense_gemm_kernel<TX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
-  return check_ex(launch_ex(dense_gemm_kernel<TX>, grid, dim3(256), smem, s, 1, thetaT, ldt, k,
+  return check_ex(launch_ex(dense_gemm_kernel<TX>, grid, dim3(kGBT), smem, s, 1, thetaT, ldt, k,
                             x, ldx, ncols, n, partials, st), "dense_gemm_kernel");
 }
 
