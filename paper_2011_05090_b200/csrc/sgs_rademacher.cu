@@ -74,23 +74,27 @@ constexpr int kRdThreads = 256;
 constexpr int kRdSub = 256;                 // chunk rows staged per pass
 constexpr int kRdWpb = kRdThreads / 32;     // sign words per row block
 
-template <typename TX>
+// CB columns per CTA (8 for batches such as P = Theta W): the staged sign
+// word and its bit are shared by the CB chains of a sketch row.
+template <typename TX, int CB>
 __global__ void __launch_bounds__(kRdThreads)
 rademacher_partials_kernel(const uint32_t* __restrict__ bits, int kw, int k,
-                           const TX* __restrict__ X, int64_t ldx, int64_t n, int nparts,
-                           double* __restrict__ partials, const sgs_status* st) {
+                           const TX* __restrict__ X, int64_t ldx, int64_t n, int ncols,
+                           int nparts, double* __restrict__ partials, const sgs_status* st) {
   __shared__ uint32_t sb[kRdSub * kRdWpb];
-  __shared__ double sx[kRdSub];
+  __shared__ double sx[CB][kRdSub];
   pdl_enter();
   if (status_stopped(st)) return;
-  const int p = blockIdx.x, c = blockIdx.z;
+  const int p = blockIdx.x, c0 = blockIdx.z * CB;
+  const int nc = min(CB, ncols - c0);
   const int w0 = blockIdx.y * kRdWpb;
   const int nwb = min(kRdWpb, kw - w0);
   const int r = blockIdx.y * kRdThreads + threadIdx.x;
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t r0 = (n * p) / nparts, r1 = (n * (p + 1)) / nparts;
-  const TX* x = X + (int64_t)c * ldx;
-  double acc = 0.0;
+  double acc[CB];
+#pragma unroll
+  for (int c = 0; c < CB; ++c) acc[c] = 0.0;
   for (int64_t j0 = r0; j0 < r1; j0 += kRdSub) {
     const int nj = (int)min((int64_t)kRdSub, r1 - j0);
     __syncthreads();
@@ -99,18 +103,26 @@ rademacher_partials_kernel(const uint32_t* __restrict__ bits, int kw, int k,
       if (threadIdx.x < nj && q < nwb)
         sb[threadIdx.x * kRdWpb + q] = __ldg(bits + (j0 + threadIdx.x) * kw + w0 + q);
     }
-    if (threadIdx.x < nj) sx[threadIdx.x] = (double)x[j0 + threadIdx.x];
+#pragma unroll
+    for (int c = 0; c < CB; ++c)
+      if (threadIdx.x < nj && c < nc) sx[c][threadIdx.x] = (double)X[(int64_t)(c0 + c) * ldx + j0 + threadIdx.x];
     __syncthreads();
     if (wl < nwb) {
-#pragma unroll 8
+#pragma unroll 4
       for (int jj = 0; jj < nj; ++jj) {
         const uint32_t wd = sb[jj * kRdWpb + wl];
         const unsigned long long neg = (unsigned long long)((~wd >> lane) & 1u) << 63;
-        acc += __longlong_as_double(__double_as_longlong(sx[jj]) ^ neg);
+#pragma unroll
+        for (int c = 0; c < CB; ++c)  // (+-1) x: flip x's sign bit, one DADD per entry
+          acc[c] += __longlong_as_double(__double_as_longlong(sx[c][jj]) ^ neg);
       }
     }
   }
-  if (r < k) partials[((int64_t)c * nparts + p) * k + r] = acc;
+  if (r < k) {
+#pragma unroll
+    for (int c = 0; c < CB; ++c)
+      if (c < nc) partials[((int64_t)(c0 + c) * nparts + p) * k + r] = acc[c];
+  }
 }
 
 int dense_nparts_of(int64_t n);  // sgs_sketch.cu: the dense chunking
@@ -128,9 +140,16 @@ template <typename TX>
 static int launch_rd(const uint32_t* bits, int kw, int k, const void* X, int64_t ldx, int ncols,
                      int64_t n, double* partials, const sgs_status* st, cudaStream_t s) {
   const int np = dense_nparts_of(n);
-  dim3 grid(np, (k + kRdThreads - 1) / kRdThreads, ncols);
-  return check_ex(launch_ex(rademacher_partials_kernel<TX>, grid, dim3(kRdThreads), 0, s, 1, bits,
-                            kw, k, static_cast<const TX*>(X), ldx, n, np, partials, st),
+  const int ky = (k + kRdThreads - 1) / kRdThreads;
+  if (ncols == 1)
+    return check_ex(launch_ex(rademacher_partials_kernel<TX, 1>, dim3(np, ky, 1), dim3(kRdThreads),
+                              0, s, 1, bits, kw, k, static_cast<const TX*>(X), ldx, n, ncols, np,
+                              partials, st),
+                    "rademacher_partials_kernel");
+  constexpr int CB = 8;
+  return check_ex(launch_ex(rademacher_partials_kernel<TX, CB>,
+                            dim3(np, ky, (ncols + CB - 1) / CB), dim3(kRdThreads), 0, s, 1, bits,
+                            kw, k, static_cast<const TX*>(X), ldx, n, ncols, np, partials, st),
                   "rademacher_partials_kernel");
 }
 
