@@ -166,3 +166,17 @@ def test_rademacher_philox_restatement_matches_numpy():
     from oracle.ref_sketch import _gen, rademacher_column_bits
     for seed, j, k in ((0, 0, 1), (5, 3, 20), (5, 49, 33), (7, 2**40 + 5, 600), (123, 99999, 1500)):
         assert np.array_equal(rademacher_column_bits(seed, j, k), _gen(seed, j).integers(0, 2, size=k))
+
+
+def test_problem_generators_match_reference():
+    """oracle.ref_io restates the reference's generators (io.py:84-141) bit for
+    bit: tests/golden/io_gen.npz, and test_io.py's W[99, 49] golden value."""
+    from oracle.ref_io import laplacian_2d, random_sparse, synthetic_matrix
+    g = golden("io_gen.npz")
+    W = synthetic_matrix(100, 50)
+    assert np.array_equal(W, g["synth"])
+    assert W[99, 49] == 0.43473583367982266 or abs(W[99, 49] - 0.43473583367982266) <= 1e-15
+    for name, (n, rp, ci, v) in (("lap6", laplacian_2d(6)), ("rs30", random_sparse(30, 3, 9)),
+                                 ("rs200", random_sparse(200, 8, 4))):
+        assert np.array_equal(rp, g[f"{name}_rp"]) and np.array_equal(ci, g[f"{name}_ci"])
+        assert np.array_equal(v, g[f"{name}_v"])
