@@ -172,13 +172,17 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
         wv[hh][v] = (rows[hh] + v < n) ? cvt<TQ>((double)__ldcs(w + rows[hh] + v) / d) : TQ(0);
   }
   if (tl && threadIdx.x == 0) atomicMin(tl + (int64_t)i * 16 + 1, gtimer());
+  // the first coefficients and the status in one round trip (both are the
+  // predecessor LS launch's outputs)
+  const TQ rc0 = tid < i ? rc[tid] : TQ(0);
   if (status_stopped(st)) {  // uniform over the grid; drain the prologue before leaving
     if (tid == 0 && active)
       for (int j = 0; j < S && j < nplain; ++j) mbar_wait(&mbar[j], 0u);
     __syncthreads();
     return;
   }
-  for (int j = tid; j < i; j += blockDim.x) rs[j] = rc[j];
+  if (tid < i) rs[tid] = rc0;
+  for (int j = tid + blockDim.x; j < i; j += blockDim.x) rs[j] = rc[j];
   __syncthreads();
 
   TQ acc[NH][V];
