@@ -95,18 +95,35 @@ def update_alg_bytes(n, i, bq, bw):
 
 
 # ---------------------------------------------------------------------------
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def _oracle_problem(cfg, n_cols, threads):
+    from oracle import OracleSketch
+    from paper_2011_05090_b200.workloads import make_w
+    n, k = cfg["n"], cfg["k"]
+    W = make_w(n, n_cols, cfg["sigma_min"], 0,
+               dtype=np.float32 if cfg["policy"] == "mixed" else np.float64, threads=threads)
+    th = OracleSketch(cfg["kind"], k, n, 0, threads=threads,
+                      **({"block_log2": cfg["block_log2"]} if "block_log2" in cfg else {}))
+    return W, th
+
+
 def cpu_sample(cfg, n_cols, threads):
     """Time the oracle port (the reference's algorithm, reference numerics) on
     the first n_cols columns of a config-shaped problem."""
     from threadpoolctl import threadpool_limits
-    from oracle import OracleRgs, OracleSketch
-    from paper_2011_05090_b200.workloads import make_w
-    n, k = cfg["n"], cfg["k"]
-    W = make_w(n, n_cols, cfg["sigma_min"], 0,
-               dtype=np.float32 if cfg["policy"] == "mixed" else np.float64)
-    th = OracleSketch(cfg["kind"], k, n, 0, **({"block_log2": cfg["block_log2"]}
-                                               if "block_log2" in cfg else {}))
-    with threadpool_limits(limits=threads):
+    from oracle import OracleRgs
+    W, th = _oracle_problem(cfg, n_cols, threads)
+    with threadpool_limits(limits=threads, user_api="blas"):
         st = OracleRgs(th, cfg["policy"], cfg["breakdown_factor"], capacity=n_cols)
         t0 = time.perf_counter()
         for j in range(n_cols):
@@ -115,53 +132,156 @@ def cpu_sample(cfg, n_cols, threads):
     return n_cols / dt, dt
 
 
-# ---------------------------------------------------------------------------
+def cpu_baseline_block(cfg_name, cfg, all_cols, one_cols):
+    """cpu_baseline of the GPU arm: the oracle port on the first columns of the
+    config's problem with every host thread, and (BASELINE.md section 3,
+    SURVEY 8(d)) with one BLAS thread ("1 core")."""
+    threads = os.cpu_count() or 1
+    v, dt = cpu_sample(cfg, all_cols, threads)
+    v1, dt1 = cpu_sample(cfg, one_cols, 1)
+    return {"value": v, "unit": "columns/s", "cores": threads, "kind": "port",
+            "cpu_model": cpu_model(),
+            "sample": f"first {all_cols} columns of {cfg_name} (n={cfg['n']}, k={cfg['k']} "
+                      f"{cfg['kind']}, {cfg['policy']}), oracle port of sketchgs, "
+                      f"{threads} threads, {dt:.1f} s (early columns: the full run is the "
+                      f"reference arm, bench.py --impl reference)",
+            "one_core": {"value": v1, "unit": "columns/s", "cores": 1,
+                         "sample": f"first {one_cols} columns, OPENBLAS 1 thread, {dt1:.1f} s"}}
+
+
+def qr_config(cfg_name, cfg, n, m, k, world, suffix=""):
+    """The `config` object of an RGS-QR bench line (both arms emit exactly this)."""
+    return {"workload": cfg_name + suffix, "n": n, "m": m, "k": k, "sketch": cfg["kind"],
+            "policy": cfg["policy"], "breakdown_factor": cfg["breakdown_factor"],
+            "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+            "l2": "inputs larger than L2 (W, Q >> 126 MB)"}
+
+
+# full factorisations the reference arm can time within a few minutes on the
+# GPU box's host (c1: ~2.5 min on 16 threads); larger configs time a prefix
+REF_FULL = {"c0", "c0r", "c1"}
+
+
 def run_reference(args, cfg_name):
+    """The reference arm: the oracle port of sketchgs (pinned bit for bit to the
+    reference by tests/test_oracle_golden.py) on the host cores, same config,
+    metric and unit as our arm.  For c0/c1 the K timed steps are K consecutive
+    segments of ONE full factorisation of the config's W (value = m / total
+    time: late columns cost more, so a prefix would flatter the CPU); warm-up
+    steps push columns into a throwaway state.  Generation of W and Theta is
+    excluded."""
     import torch  # noqa: F401  (keeps the import cost out of the timed region)
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    if cfg_name == "c3":
+        return run_reference_gmres(args)
+    from threadpoolctl import threadpool_limits
+    from oracle import OracleRgs
     from paper_2011_05090_b200.workloads import CONFIGS
     cfg = CONFIGS[cfg_name]
     threads = os.cpu_count() or 1
-    ncols = args.cpu_cols
-    vals = []
-    for _ in range(args.warmup):
-        cpu_sample(cfg, max(2, ncols // 4), threads)
-    for _ in range(args.steps):
-        v, _ = cpu_sample(cfg, ncols, threads)
-        vals.append(v)
-    v = statistics.mean(vals)
-    sample = (f"first {ncols} columns of a {cfg_name}-shaped RGS-QR (n={cfg['n']}, k={cfg['k']} "
-              f"{cfg['kind']}, {cfg['policy']}), oracle port of sketchgs, numpy/OpenBLAS")
+    world = max(1, args.gpus)
+    m = args.columns if args.columns is not None else cfg["m"]
+    full = cfg_name in REF_FULL or args.columns is not None
+    m_run = m if full else min(m, args.cpu_cols)
+    t_gen = time.perf_counter()
+    W, th = _oracle_problem(cfg, m_run if full else m_run, threads)
+    t_gen = time.perf_counter() - t_gen
+    K = max(1, min(args.steps, m_run))
+    bounds = [(m_run * s) // K for s in range(K + 1)]
+    times = []
+    with threadpool_limits(limits=threads, user_api="blas"):
+        warm = OracleRgs(th, cfg["policy"], cfg["breakdown_factor"], capacity=max(1, args.warmup))
+        for j in range(min(args.warmup, m_run)):
+            warm.push(W[:, j])
+        del warm
+        st = OracleRgs(th, cfg["policy"], cfg["breakdown_factor"], capacity=m_run)
+        for s in range(K):
+            t0 = time.perf_counter()
+            for j in range(bounds[s], bounds[s + 1]):
+                st.push(W[:, j])
+            times.append(time.perf_counter() - t0)
+    total = sum(times)
+    v = m_run / total
+    what = (f"one full {cfg_name} factorisation ({m_run} columns) in {K} consecutive segments"
+            if full else f"first {m_run} of {m} columns of {cfg_name} in {K} segments "
+                         f"(the full run exceeds the bench budget)")
+    sample = (f"{what}, oracle port of sketchgs (numpy/OpenBLAS, {threads} threads), "
+              f"{total:.1f} s timed, W/Theta generation {t_gen:.1f} s excluded")
     print(json.dumps({
         "impl": "reference", "metric": "RGS-QR columns/s", "value": v, "unit": "columns/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * ncols / v, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32/f64" if cfg["policy"] == "mixed" else "f64",
-        "data": "synthetic", "config": {"workload": cfg_name, **_cfg_public(cfg)},
+        "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * total / K, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32 (Q, update) / f64 (sketch, LS)" if cfg["policy"] == "mixed" else "f64",
+        "data": "synthetic (W = G diag(sigma) V^T, seeded numpy Philox)",
+        "config": qr_config(cfg_name, cfg, cfg["n"], m, cfg["k"], world,
+                            "" if args.columns is None else f"-m{m}"),
+        "columns_timed": m_run, "segment_s": [round(t, 3) for t in times],
         "cpu_baseline": {"value": v, "unit": "columns/s", "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": v, "unit": "columns/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
-def _cfg_public(cfg):
-    return {k: v for k, v in cfg.items()}
+def run_reference_gmres(args):
+    """Reference arm of c3: the oracle port's RGS-Arnoldi steps on the full
+    128^3 operator (SpMV, two P-SRHT applies and the Householder LS per step,
+    reference numerics).  A whole 549-iteration solve takes ~10 min on the
+    host, so each timed step is a bounded run of consecutive Arnoldi steps of
+    the first cycle."""
+    from threadpoolctl import threadpool_limits
+    from oracle import OracleRgs, OracleSketch, csr_matvec
+    from paper_2011_05090_b200.workloads import CONFIGS, convdiff3d, rhs_gaussian
+    cfg = CONFIGS["c3"]
+    threads = os.cpu_count() or 1
+    N = cfg["grid"]
+    rp, ci, va = convdiff3d(N, (cfg["beta"],) * 3)
+    n = N ** 3
+    b = rhs_gaussian(n, 0)
+    th = OracleSketch("psrht", cfg["k"], n, 0)
+    K = max(1, args.steps)
+    per = max(1, 60 // K)
+    times = []
+    with threadpool_limits(limits=threads, user_api="blas"):
+        st = OracleRgs(th, "f64", capacity=K * per + args.warmup + 2)
+        st.push(b / np.linalg.norm(b))
+        i = 0
+        for _ in range(args.warmup):
+            st.push(csr_matvec(rp, ci, va, n, st.Q[:, i].astype(np.float64)))
+            i += 1
+        for _ in range(K):
+            t0 = time.perf_counter()
+            for _ in range(per):
+                st.push(csr_matvec(rp, ci, va, n, st.Q[:, i].astype(np.float64)))
+                i += 1
+            times.append(time.perf_counter() - t0)
+    total = sum(times)
+    v = K * per / total
+    print(json.dumps({
+        "impl": "reference", "metric": "RGMRES Arnoldi steps/s", "value": v, "unit": "steps/s",
+        "n_gpus": max(1, args.gpus), "steps": K, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * total / K, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "c3", **cfg, "l2": "inputs larger than L2 (basis, CSR >> 126 MB)"},
+        "cpu_baseline": {"value": v, "unit": "steps/s", "cores": threads, "kind": "port",
+                         "cpu_model": cpu_model(),
+                         "sample": f"Arnoldi steps {args.warmup + 1}..{i} of the first cycle "
+                                   f"({per} per timed step), fp64 basis, oracle port"},
+        "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
 
 
 # ---------------------------------------------------------------------------
-def run_qr(args, cfg_name):
+def run_qr(args, cfg_name, comm):
+    """One config's bench line (a dict on rank 0, None elsewhere)."""
     import torch
     import paper_2011_05090_b200 as sg
     from paper_2011_05090_b200 import _lib
-    from paper_2011_05090_b200.distributed import init_from_env
     from paper_2011_05090_b200.workloads import CONFIGS, make_w_device, shard_rows
 
-    # SGS_DIST_BACKEND=gloo runs several ranks on one GPU: a functional check of
-    # the sharded path only, never a timing
-    comm = init_from_env(os.environ.get("SGS_DIST_BACKEND", "nccl"))
     rank = comm.rank if comm else 0
     world = comm.world if comm else 1
     local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
@@ -171,11 +291,8 @@ def run_qr(args, cfg_name):
     n, m, k = cfg["n"], cfg["m"], cfg["k"]
     if cfg_name == "c4" and world < 4 and args.columns is None:
         # W and Q are 201 GB each in fp32 (BASELINE configs[4]: 4 and 8 GPUs only)
-        if rank == 0:
-            print(json.dumps({"metric": "RGS-QR columns/s", "impl": "ours", "n_gpus": world,
-                              "unavailable": "c4 needs >= 4 GPUs (W and Q are 201 GB each)"}),
-                  flush=True)
-        return
+        return {"metric": "RGS-QR columns/s", "impl": "ours", "n_gpus": world,
+                "unavailable": "c4 needs >= 4 GPUs (W and Q are 201 GB each)"}
     if args.columns is not None:  # functional runs of a config's shapes with fewer columns
         m = args.columns
     pol = sg.policy_from_name(cfg["policy"])
@@ -205,10 +322,16 @@ def run_qr(args, cfg_name):
         return gstate
 
     # the timed steps replay one CUDA graph of the whole factorisation (every
-    # kernel re-runs; the graph only removes host launch overhead)
+    # kernel re-runs; the graph only removes host launch overhead).  A sharded
+    # state captures its NCCL all-reduces too, after one eager factorisation
+    # has brought the communicator up (gloo is host-side: no graph).
     graph = None
     graph_launches = 0
-    if not args.no_graph and comm is None:
+    if not args.no_graph and (comm is None or comm.capturable):
+        if comm is not None:
+            step()
+            torch.distributed.barrier()
+            gstate.m = 0
         lcg = _lib.launch_count()
         graph = gstate.capture_factorization(Wt, ldw, m)
         graph_launches = _lib.launch_count() - lcg
@@ -362,28 +485,22 @@ def run_qr(args, cfg_name):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        v, dt = cpu_sample(cfg, args.cpu_cols, threads)
-        cpu = {"value": v, "unit": "columns/s", "cores": threads, "kind": "port",
-               "sample": f"first {args.cpu_cols} columns of a {cfg_name}-shaped problem "
-                         f"(n={n}, k={k} {cfg['kind']}, {cfg['policy']}), oracle port, "
-                         f"{dt:.1f} s"}
+        cpu = cpu_baseline_block(cfg_name, cfg, args.cpu_cols, max(8, args.cpu_cols // 4))
     if rank == 0:
-        print(json.dumps({
+        return {
             "metric": "RGS-QR columns/s", "value": value, "unit": "columns/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak" if weak else "strong",
             "vs_baseline": None,
             "dtype": "f32 (Q, update) / f64 (sketch, LS)" if cfg["policy"] == "mixed" else "f64",
             "data": "synthetic (W = G diag(sigma) V^T generated on device, seeded)",
-            "config": {"workload": cfg_name + ("-weak" if weak else "")
-                                   + (f"-m{m}" if args.columns is not None else ""), "n": n, "m": m, "k": k,
-                       "sketch": cfg["kind"], "policy": cfg["policy"], "breakdown_factor": bf,
-                       "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+            "config": {**qr_config(cfg_name, cfg, n, m, k, world,
+                                   ("-weak" if weak else "")
+                                   + (f"-m{m}" if args.columns is not None else "")),
                        **({"weak": f"n = {world} x {n_per_gpu} rows (~{n_per_gpu} per GPU); "
                                    f"value counts column shards: {world} per column"}
-                          if weak else {}),
-                       "l2": "inputs larger than L2 (W, Q >> 126 MB)"},
+                          if weak else {})},
+            "graph": graph is not None,
             "hbm_gbs_whole_step": round(hbm_gbs, 1),
             "hbm_frac_whole_step": round(hbm_gbs / (peak * world), 4),
             # BASELINE.json quotes the nominal ~8 TB/s; the roofline uses the measured peak
@@ -392,9 +509,8 @@ def run_qr(args, cfg_name):
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             **({"e2e_note": e2e_note} if e2e_note else {}), "gpu_launches": launches,
             "clocks": clk,
-        }), flush=True)
-    if comm:
-        torch.distributed.destroy_process_group()
+        }
+    return None
 
 
 def cpu_gmres_sample(n_steps, threads):
@@ -604,7 +720,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c1")
+    ap.add_argument("--config", default=None,
+                    help="c0|c0r|c1|c2|c3|c4; default c1 at N = 1, c2 (strong) at N > 1")
     ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
                     help="N > 1 on c1: weak (1e6 rows per GPU, default) or strong (n = 1e6 split)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -616,14 +733,43 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="N >= 4: skip the c4 line")
     args = ap.parse_args()
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.config is None:
+        # N = 1: BASELINE configs[1] (the metric's config); N > 1: configs[2],
+        # the row-sharded c2, strong-scaled with the same Theta at every N
+        args.config = "c2" if max(world_env, args.gpus) > 1 else "c1"
     if args.impl == "reference":
-        run_reference(args, args.config if args.config != "c3" else "c1")
+        run_reference(args, args.config)
         return
     if args.config == "c3":
         run_gmres(args)
         return
-    run_qr(args, args.config)
+    from paper_2011_05090_b200.distributed import init_from_env
+    # SGS_DIST_BACKEND=gloo runs several ranks on one GPU: a functional check of
+    # the sharded path only, never a timing
+    comm = init_from_env(os.environ.get("SGS_DIST_BACKEND", "nccl"))
+    line = run_qr(args, args.config, comm)
+    world = comm.world if comm else 1
+    if args.config == "c2" and world >= 4 and not args.no_c4 and args.columns is None:
+        # BASELINE configs[4] exists only at 4 and 8 GPUs: its line rides along
+        # with c2's (fewer timed steps; W and Q are 201 GB each)
+        import copy
+        import torch
+        torch.cuda.empty_cache()
+        a4 = copy.copy(args)
+        a4.steps, a4.warmup, a4.no_e2e, a4.no_cpu = min(args.steps, 3), min(args.warmup, 3), True, True
+        l4 = run_qr(a4, "c4", comm)
+        if line is not None and l4 is not None:
+            line["results"] = {"c4": {k_: l4.get(k_) for k_ in (
+                "value", "unit", "ms_per_step", "steps", "warmup", "config", "hbm_gbs_whole_step",
+                "hbm_frac_whole_step", "roofline", "gpu_launches", "graph", "unavailable")}}
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if comm:
+        import torch
+        torch.distributed.destroy_process_group()
 
 
 if __name__ == "__main__":

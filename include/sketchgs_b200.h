@@ -49,7 +49,8 @@ extern "C" {
 #define SGS_ST_BREAKDOWN 1   /* reference: gram_schmidt.BreakdownError (gram_schmidt.py:323-326) */
 #define SGS_ST_RANK 2        /* reference: np.linalg.LinAlgError (gram_schmidt.py:186-189) */
 #define SGS_ST_CONVERGED 3   /* reference: gmres early exit est <= tol (krylov.py:300-301) */
-#define SGS_ST_NONFINITE 4   /* non-finite sketched norm */
+/* (no code 4: a NaN r_ii flows through as in the reference, which has no
+   non-finite guard - gram_schmidt.py:322-326 only compares r_ii <= tol) */
 
 /* Device-resident status block (64 bytes, 8-byte aligned). */
 typedef struct sgs_status {

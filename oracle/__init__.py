@@ -24,5 +24,5 @@ from .ref_rgs import OracleRgs, householder_lsq, oracle_certificates, oracle_rgs
 from .ref_krylov import (OracleIlu0, csr_matvec, oracle_arnoldi, oracle_gmres, oracle_gmres_lagged,
                          oracle_gmres_restarted,
                          power_norm_estimate)
-from .metrics import factor_metrics, rel_diff
+from .metrics import factor_metrics, factor_metrics_blocked, rel_diff
 from .ref_cert import oracle_certify, oracle_epsilon_of, oracle_omega_bar

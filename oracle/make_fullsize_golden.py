@@ -11,7 +11,9 @@ the north_star gates need, small enough to commit (tests/golden/fullsize.npz):
   * c1 (n=1e6, m=500, k=1500 P-SRHT, MIXED32_64, breakdown_factor=0): the
     metrics and diag(R).
 W comes from paper_2011_05090_b200.workloads.make_w (numpy Philox, the same
-generator the GPU tests call).  Usage: python oracle/make_fullsize_golden.py
+generator the GPU tests call; bit-identical for any thread count).  The
+metrics come from oracle.factor_metrics_blocked, the function the GPU tests
+apply to their own factors.  Usage: python oracle/make_fullsize_golden.py
 """
 
 import os
@@ -23,7 +25,7 @@ import numpy as np
 ROOT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..")
 sys.path.insert(0, ROOT)
 
-from oracle import OracleSketch, factor_metrics, oracle_rgs_factorize  # noqa: E402
+from oracle import OracleSketch, factor_metrics_blocked, oracle_rgs_factorize  # noqa: E402
 from paper_2011_05090_b200.workloads import make_w  # noqa: E402
 
 QROWS = np.arange(0, 100_000, 997)
@@ -35,7 +37,7 @@ def main():
     n, m, k = 100_000, 300, 600
     W = make_w(n, m, 1e-8, 0)
     ref = oracle_rgs_factorize(W, OracleSketch("gaussian", k, n, 0), "f64")
-    met = factor_metrics(W, ref["Q"], ref["R"], ref["S"])
+    met = factor_metrics_blocked(W, ref["Q"], ref["R"], ref["S"])
     for key, v in met.items():
         d[f"c0_{key}"] = v
     print("c0", met, round(time.time() - t0, 1), "s", flush=True)
@@ -44,7 +46,7 @@ def main():
     ref = oracle_rgs_factorize(W, OracleSketch("gaussian", k, n, 0), "f64")
     d["c0twin_R"], d["c0twin_S"] = ref["R"], ref["S"]
     d["c0twin_Qrows"], d["c0twin_rows"] = ref["Q"][QROWS], QROWS
-    met = factor_metrics(W, ref["Q"], ref["R"], ref["S"])
+    met = factor_metrics_blocked(W, ref["Q"], ref["R"], ref["S"])
     for key, v in met.items():
         d[f"c0twin_{key}"] = v
     print("c0 twin", met, round(time.time() - t0, 1), "s", flush=True)
@@ -53,7 +55,7 @@ def main():
     n, m, k = 1_000_000, 500, 1500
     W = make_w(n, m, 1e-10, 0, dtype=np.float32)
     ref = oracle_rgs_factorize(W, OracleSketch("psrht", k, n, 0), "mixed", breakdown_factor=0.0)
-    met = factor_metrics(W, ref["Q"], ref["R"], ref["S"])
+    met = factor_metrics_blocked(W, ref["Q"], ref["R"], ref["S"])
     for key, v in met.items():
         d[f"c1_{key}"] = v
     d["c1_Rdiag"] = np.diag(ref["R"]).copy()

@@ -159,15 +159,22 @@ class OracleRgs:
 
 
 def oracle_rgs_factorize(W, theta, policy: str = "mixed", breakdown_factor: float = 10.0,
-                         phi=None):
-    """Returns dict Q, R, S, P (+ S_phi, P_phi) (gram_schmidt.py:350-375)."""
+                         phi=None, capacity: int = 16, progress=None):
+    """Returns dict Q, R, S, P (+ S_phi, P_phi) (gram_schmidt.py:350-375).
+
+    `capacity` only sizes the first allocation (the reference starts at 16 and
+    doubles, which changes storage, not arithmetic); the full-size golden runs
+    preallocate m columns so the doubling copy of a 67 GB Q never happens.
+    `progress(j)` is called after column j (logging of long runs)."""
     W = np.asarray(W)
     n, m = W.shape
     if not (theta.k >= m and n >= m >= 1):
         raise ValueError("need k >= m and n >= m >= 1")
-    st = OracleRgs(theta, policy, breakdown_factor, capacity=16, phi=phi)
+    st = OracleRgs(theta, policy, breakdown_factor, capacity=capacity, phi=phi)
     for j in range(m):
         st.push(W[:, j])
+        if progress is not None:
+            progress(j)
     out = {"Q": st.Q.copy(), "R": st.R.copy(), "S": st.S.copy(), "P": st.P.copy()}
     if phi is not None:
         out["S_phi"] = st._S_phi[:, :st.m].copy()

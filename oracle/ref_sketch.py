@@ -85,8 +85,13 @@ def block_seed(seed: int, j: int) -> int:
 class OracleSketch:
     """Duck-typed k x n operator (.k, .n, .apply, .apply_block) on the host."""
 
-    def __init__(self, kind: str, k: int, n: int, seed: int, block_log2: int = 20):
+    def __init__(self, kind: str, k: int, n: int, seed: int, block_log2: int = 20,
+                 threads: int = 1):
         self.kind, self.k, self.n, self.seed = kind, int(k), int(n), int(seed)
+        # block-SRHT only: transform the blocks on `threads` host threads (numpy
+        # releases the GIL); the block sums are still added in block order, so
+        # the result is bit-identical to threads=1
+        self.threads = int(threads)
         if kind == "psrht":
             self.s, self.signs, self.samples = psrht_setup(k, n, seed)
         elif kind == "block_srht":
@@ -119,8 +124,15 @@ class OracleSketch:
             return self._psrht(self.s, self.signs, self.samples, x)
         if self.kind == "block_srht":
             acc = np.zeros(self.k)
-            for j, (s, sg, sm) in enumerate(self.blocks):
-                acc += self._psrht(s, sg, sm, x[j * self.bs:(j + 1) * self.bs])
+            one = lambda j: self._psrht(*self.blocks[j], x[j * self.bs:(j + 1) * self.bs])  # noqa: E731
+            if self.threads > 1:
+                from concurrent.futures import ThreadPoolExecutor
+                with ThreadPoolExecutor(min(self.threads, len(self.blocks))) as ex:
+                    parts = list(ex.map(one, range(len(self.blocks))))
+            else:
+                parts = map(one, range(len(self.blocks)))
+            for y in parts:
+                acc += y
             return acc / math.sqrt(len(self.blocks))
         return (1.0 / math.sqrt(self.k)) * (self.D @ x)   # sketch.py:174-175
 

@@ -13,7 +13,7 @@ from .precision import (MIXED32_64, U_BINARY32, U_BINARY64, UNIFIED32, UNIFIED64
 from .sketch import SketchKind, SketchOperator, as_device_sketch, block_seed, fwht, make_sketch
 from .gram_schmidt import (BREAKDOWN_FACTOR, HOUSEHOLDER_QR, BreakdownError, GsVariant,
                            LsqSolver, QrFactors, RgsState, StabilityCertificate, certificates,
-                           loss_of_orthogonality, rgs_factorize)
+                           loss_of_orthogonality, rgs_factorize, sketched_lsq)
 from .krylov import (ArnoldiDecomposition, GmresResult, Ilu0Preconditioner, RestartedResult,
                      SparseMatrix, arnoldi, gmres, gmres_restarted, ilu0)
 from .mmio import MatrixMarketError, read_matrix_market, write_matrix_market
@@ -29,7 +29,7 @@ __all__ = [
     "policy_from_name", "SketchKind", "SketchOperator", "as_device_sketch", "block_seed", "fwht",
     "make_sketch", "BREAKDOWN_FACTOR", "HOUSEHOLDER_QR", "BreakdownError", "GsVariant",
     "LsqSolver", "QrFactors", "RgsState", "StabilityCertificate", "certificates",
-    "loss_of_orthogonality", "rgs_factorize", "ArnoldiDecomposition", "GmresResult",
+    "loss_of_orthogonality", "rgs_factorize", "sketched_lsq", "ArnoldiDecomposition", "GmresResult",
     "RestartedResult", "SparseMatrix", "Ilu0Preconditioner", "ilu0", "arnoldi", "gmres",
     "gmres_restarted", "CertificationParams", "CertificationResult", "EmbeddingParams",
     "certify_factorization", "epsilon_of", "eps_star_for_dim", "make_certification_sketch",

@@ -24,7 +24,6 @@ ST_OK = 0
 ST_BREAKDOWN = 1
 ST_RANK = 2
 ST_CONVERGED = 3
-ST_NONFINITE = 4
 
 
 class LsArgs(ctypes.Structure):

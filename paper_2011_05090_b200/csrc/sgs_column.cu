@@ -185,11 +185,23 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
   for (int j = tid + blockDim.x; j < i; j += blockDim.x) rs[j] = rc[j];
   __syncthreads();
 
-  TQ acc[NH][V];
+  // Q_{i-1} r in the coarse dtype, two-level for fp32 (kAccBlock, sgs_common.cuh)
+  TQ acc[NH][V], tot[NH][V];
 #pragma unroll
   for (int hh = 0; hh < NH; ++hh)
 #pragma unroll
-    for (int v = 0; v < V; ++v) acc[hh][v] = TQ(0);
+    for (int v = 0; v < V; ++v) acc[hh][v] = tot[hh][v] = TQ(0);
+  auto fold = [&](int j) {
+    if (two_level<TQ>() && ((j + 1) & (kAccBlock - 1)) == 0) {
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh)
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          tot[hh][v] += acc[hh][v];
+          acc[hh][v] = TQ(0);
+        }
+    }
+  };
   if (active) {
     int s = 0;
     uint32_t phase = 0u;  // (j / S) & 1, kept incrementally (S is a runtime depth)
@@ -204,6 +216,7 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
 #pragma unroll
         for (int v = 0; v < V; ++v) acc[hh][v] = fma(q[v], c, acc[hh][v]);
       }
+      fold(j);
       __syncthreads();  // everybody has read stage s
       if (tid == 0 && j + S < nplain) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -241,6 +254,7 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
             }
         }
       }
+      fold(j);
     }
   }
   double xs[NH * V];  // d o q' of this thread's rows, element order (h, v)
@@ -249,7 +263,8 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
     for (int hh = 0; hh < NH; ++hh) {
       TQ out[V];
 #pragma unroll
-      for (int v = 0; v < V; ++v) out[v] = (rows[hh] + v < n) ? wv[hh][v] - acc[hh][v] : TQ(0);
+      for (int v = 0; v < V; ++v)
+        out[v] = (rows[hh] + v < n) ? wv[hh][v] - (tot[hh][v] + acc[hh][v]) : TQ(0);
       TQ* dst = Q + (int64_t)i * ldq + rows[hh];
       if (rows[hh] + V <= n) vstore(dst, out);
       else
@@ -408,9 +423,18 @@ dense_ring_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
   }
   for (int j = tid; j < i; j += T) rs[j] = rc[j];
   __syncthreads();
-  TQ acc[kDcMaxRPT];
+  TQ acc[kDcMaxRPT], tot[kDcMaxRPT];  // two-level sum of Q r, as rgs_column_kernel
 #pragma unroll
-  for (int u = 0; u < kDcMaxRPT; ++u) acc[u] = TQ(0);
+  for (int u = 0; u < kDcMaxRPT; ++u) acc[u] = tot[u] = TQ(0);
+  auto fold = [&](int j) {
+    if (two_level<TQ>() && ((j + 1) & (kAccBlock - 1)) == 0) {
+#pragma unroll
+      for (int u = 0; u < kDcMaxRPT; ++u) {
+        tot[u] += acc[u];
+        acc[u] = TQ(0);
+      }
+    }
+  };
   const int kp = (k + 1) >> 1;
   double2 acc2[QP];
 #pragma unroll
@@ -421,15 +445,19 @@ dense_ring_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
       const int lr = tid + u * T;
       if (lr >= nr) continue;
       const int64_t r = r0 + lr;
-      TQ a = acc[u];
+      TQ a = acc[u], tt = tot[u];
       if (i > 0 && normalize_prev) {
         const int jj = i - 1;
         TQ* cp = Q + (int64_t)jj * ldq + r;
         const TQ qn = cvt<TQ>((double)*cp / R[(int64_t)jj * ldr + jj]);
         *cp = qn;
         a = fma(qn, rs[jj], a);
+        if (two_level<TQ>() && ((jj + 1) & (kAccBlock - 1)) == 0) {
+          tt += a;
+          a = TQ(0);
+        }
       }
-      const TQ out = wv[u] - a;
+      const TQ out = wv[u] - (tt + a);
       Q[(int64_t)i * ldq + r] = out;
       xq[lr] = (double)out;
     }
@@ -459,6 +487,7 @@ dense_ring_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
           const int lr = tid + u * T;
           if (lr < nr) acc[u] = fma(col[lr], c, acc[u]);
         }
+        fold(j);
       }
     } else {
       const int rr0 = (t - n1) * Rr, rr1 = min(nr, rr0 + Rr);

@@ -27,7 +27,9 @@ namespace sgs {
 constexpr int kUpdThreads = 256;
 constexpr int kUpdUnroll = 8;
 
-// Q[:, i] = cast(w) - Q[:, :i] @ rc   (coarse arithmetic, FMA chain over j)
+// Q[:, i] = cast(w) - Q[:, :i] @ rc   (coarse arithmetic: fma chains over blocks
+// of kAccBlock columns, block sums added in order - the two-level sum of the
+// fused column kernel, sgs_column.cu)
 template <typename TQ, typename TW>
 __global__ void __launch_bounds__(kUpdThreads)
 rgs_update_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* __restrict__ w,
@@ -43,9 +45,18 @@ rgs_update_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
   const int64_t row0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * V;
   if (row0 >= n) return;
   const bool full = row0 + V <= n;
-  TQ acc[V];
+  TQ acc[V], tot[V];
 #pragma unroll
-  for (int v = 0; v < V; ++v) acc[v] = TQ(0);
+  for (int v = 0; v < V; ++v) acc[v] = tot[v] = TQ(0);
+  auto fold = [&](int j) {
+    if (two_level<TQ>() && ((j + 1) & (kAccBlock - 1)) == 0) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        tot[v] += acc[v];
+        acc[v] = TQ(0);
+      }
+    }
+  };
   const int nplain = normalize_prev ? i - 1 : i;
   if (full) {
     int j = 0;
@@ -58,6 +69,7 @@ rgs_update_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
         const TQ c = rs[j + u];
 #pragma unroll
         for (int v = 0; v < V; ++v) acc[v] = fma(q[u][v], c, acc[v]);
+        fold(j + u);
       }
     }
     for (; j < nplain; ++j) {
@@ -66,6 +78,7 @@ rgs_update_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
       const TQ c = rs[j];
 #pragma unroll
       for (int v = 0; v < V; ++v) acc[v] = fma(q[v], c, acc[v]);
+      fold(j);
     }
     if (normalize_prev) {
       const int j = i - 1;
@@ -79,16 +92,18 @@ rgs_update_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
       const TQ c = rs[j];
 #pragma unroll
       for (int v = 0; v < V; ++v) acc[v] = fma(q[v], c, acc[v]);
+      fold(j);
     }
     TQ out[V];
 #pragma unroll
-    for (int v = 0; v < V; ++v) out[v] = cvt<TQ>(__ldcs(w + row0 + v)) - acc[v];
+    for (int v = 0; v < V; ++v) out[v] = cvt<TQ>(__ldcs(w + row0 + v)) - (tot[v] + acc[v]);
     vstore(Q + (int64_t)i * ldq + row0, out);
   } else {
     const int nv = (int)(n - row0);
     for (int j = 0; j < nplain; ++j) {
       const TQ c = rs[j];
       for (int v = 0; v < nv; ++v) acc[v] = fma(Q[(int64_t)j * ldq + row0 + v], c, acc[v]);
+      fold(j);
     }
     if (normalize_prev) {
       const int j = i - 1;
@@ -100,8 +115,10 @@ rgs_update_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
         *p = q;
         acc[v] = fma(q, c, acc[v]);
       }
+      fold(j);
     }
-    for (int v = 0; v < nv; ++v) Q[(int64_t)i * ldq + row0 + v] = cvt<TQ>(w[row0 + v]) - acc[v];
+    for (int v = 0; v < nv; ++v)
+      Q[(int64_t)i * ldq + row0 + v] = cvt<TQ>(w[row0 + v]) - (tot[v] + acc[v]);
   }
 }
 

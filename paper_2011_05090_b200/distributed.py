@@ -25,6 +25,9 @@ class TorchComm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        # NCCL collectives are stream-ordered device work and can be captured
+        # in a CUDA graph with the kernels around them; gloo runs on the host
+        self.capturable = dist.get_backend(group) == "nccl"
 
     def allreduce_(self, t: torch.Tensor) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)

@@ -41,7 +41,7 @@ from .sketch import SketchOperator, as_device_sketch
 __all__ = [
     "GsVariant", "LsqSolver", "HOUSEHOLDER_QR", "QrFactors", "StabilityCertificate",
     "BreakdownError", "RgsState", "rgs_factorize", "certificates", "loss_of_orthogonality",
-    "BREAKDOWN_FACTOR",
+    "BREAKDOWN_FACTOR", "sketched_lsq",
 ]
 
 BREAKDOWN_FACTOR = 10.0
@@ -438,7 +438,7 @@ class RgsState:
 
     def _raise_status(self, st: dict) -> None:
         code = st["code"]
-        if code in (_lib.ST_BREAKDOWN, _lib.ST_NONFINITE):
+        if code == _lib.ST_BREAKDOWN:
             raise BreakdownError(st["column"], st["r_ii"], st["tol"])
         if code == _lib.ST_RANK:
             raise np.linalg.LinAlgError("sketched basis numerically rank deficient")
@@ -743,8 +743,13 @@ class RgsState:
         g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
+        # a sharded state captures its collectives too (NCCL all-reduces are
+        # stream-ordered and capturable once the communicator is up; the
+        # process group's watchdog thread keeps querying its events, hence a
+        # thread-local capture mode)
+        mode = "global" if self.comm is None else "thread_local"
         with torch.cuda.stream(side):
-            with torch.cuda.graph(g, stream=side):
+            with torch.cuda.graph(g, stream=side, capture_error_mode=mode):
                 self._enqueue_factorization(Wcm, ldw, m)
         torch.cuda.current_stream().wait_stream(side)
         return g
@@ -758,21 +763,28 @@ _LS_DEFER = os.environ.get("SGS_LS_DEFER", "1") != "0"
 
 
 def _pinned_buffer(shape, dtype):
-    """Pinned host buffer (tensor, numpy view) for returned factors.  A buffer
-    whose numpy view is no longer referenced by a previous result is reused;
-    page-locking gigabytes on every call would dominate the end-to-end time."""
-    import sys
+    """Pinned host buffer (tensor, numpy view) for returned factors.
+
+    Page-locking gigabytes on every call would dominate the end-to-end time, so
+    buffers are pooled.  Ownership is explicit: each hand-out creates a fresh
+    numpy array over the buffer and the pool keeps only a weak reference to
+    it.  The buffer is reused once that array - and every view of it (views
+    hold their base) - has been garbage collected; while a caller holds any of
+    them, a new buffer is allocated.  (A raw data pointer is not ownership:
+    copy the array to keep data past the result's lifetime.)"""
+    import weakref
     for ent in _PINNED_POOL:
-        t, arr = ent
-        # references: the pool tuple, the loop variable, getrefcount's argument
-        if tuple(t.shape) == tuple(shape) and t.dtype == dtype and sys.getrefcount(arr) <= 3:
-            return ent
+        t, ref = ent
+        if tuple(t.shape) == tuple(shape) and t.dtype == dtype and ref() is None:
+            arr = t.numpy()
+            ent[1] = weakref.ref(arr)
+            return t, arr
     t = torch.empty(shape, dtype=dtype, pin_memory=True)
-    ent = (t, t.numpy())
-    _PINNED_POOL.append(ent)
+    arr = t.numpy()  # arr.base is t: the array keeps the pinned storage alive
+    _PINNED_POOL.append([t, weakref.ref(arr)])
     if len(_PINNED_POOL) > 12:  # Q, R, S, P of three live results
         _PINNED_POOL.pop(0)
-    return ent
+    return t, arr
 
 
 def _is_pinned(a: np.ndarray) -> bool:
@@ -858,6 +870,66 @@ def rgs_factorize(W, theta, policy: PrecisionPolicy = MIXED32_64,
     factors = state.factors(device=device_factors)
     cert = certificates(factors) if with_certificate else None
     return factors, cert
+
+
+def sketched_lsq(S_prev, p, solver: LsqSolver = HOUSEHOLDER_QR):
+    """min_y ||S_prev y - p||_2 on the device (reference gram_schmidt.py:193-205,
+    the "householder" branch; tests/test_gram_schmidt.py:96-114).
+
+    Runs the least-squares kernel of the factorizer (``sgs_ls_step``): each
+    column s_j is appended as RGS appends s'_j - normalised by r_jj = ||s_j||
+    into the QR of the sketched basis - and p is solved against it, so
+    y_j = r_j / r_jj.  That QR is NOT a Householder chain: it is the parallel
+    selective-reorthogonalisation Gram-Schmidt QR documented in DESIGN.md
+    section 3 (an orthogonal factor T, column norms alpha, explicit R_S^-1),
+    backward stable for the well-conditioned bases RGS keeps.
+    The reference's rank test (min|diag R| < 1e-8 max(max|diag R|, 1),
+    gram_schmidt.py:186-189) runs on the column-normalised basis and raises
+    ``np.linalg.LinAlgError``; a zero column (r_jj = 0) raises it too (the
+    reference's Householder step gives it a zero diagonal).  numpy in -> numpy
+    out, CUDA tensor in -> CUDA tensor out."""
+    if solver.method != "householder":
+        raise NotImplementedError("the device least-squares kernel is the QR solver "
+                                  "(HOUSEHOLDER_QR)")
+    _lib.require_cuda()
+    on_dev = isinstance(S_prev, torch.Tensor) and S_prev.is_cuda
+    S = S_prev if isinstance(S_prev, torch.Tensor) else torch.from_numpy(np.asarray(S_prev))
+    if S.ndim == 1:
+        S = S.reshape(-1, 1)
+    if S.ndim != 2:
+        raise ValueError("S_prev must be a k x i matrix")
+    k, i = S.shape
+    fdt = torch.float32 if S.dtype == torch.float32 else torch.float64
+    dev = S.device if on_dev else torch.device("cuda", torch.cuda.current_device())
+    pv = p if isinstance(p, torch.Tensor) else torch.from_numpy(np.asarray(p, dtype=np.float64))
+    if tuple(pv.shape) != (k,):
+        raise ValueError("right-hand side length mismatch")
+    if i == 0:
+        out = torch.zeros(0, dtype=fdt, device=dev)
+        return out if on_dev else out.cpu().numpy()
+    if i >= k:
+        raise ValueError("cannot append more columns than rows")
+    cols = S.to(device=dev, dtype=torch.float64).t().contiguous()  # (i, k): row j = s_j
+    pd = pv.to(device=dev, dtype=torch.float64).contiguous()
+    st = RgsState.__new__(RgsState)  # the LS half of a state: no basis Q
+    st.device, st.k, st.phi, st._cap = dev, k, None, 0
+    st.policy = UNIFIED64 if fdt == torch.float64 else MIXED32_64
+    st.breakdown_factor = 0.0  # tol = 0: only an exactly zero column "breaks down"
+    st.cdt = st.fdt = fdt
+    st.ccode = st.fcode = _lib.dtype_code(fdt)
+    st.ldq = 32
+    with torch.cuda.device(dev):
+        st.status = _lib.Status(dev)
+        st._alloc(i + 2)
+        for j in range(i):
+            st._ls(fin=j, s_parts=cols[j].data_ptr(), s_nparts=1, s_scale=1.0)
+        st._ls(sol=i, p_parts=pd.data_ptr(), p_nparts=1, p_scale=1.0)
+        res = st.status.read()
+    if res["code"] in (_lib.ST_RANK, _lib.ST_BREAKDOWN):
+        raise np.linalg.LinAlgError("sketched basis numerically rank deficient")
+    R = st._R  # column c of R is row c of the tensor
+    y = (R[i, :i] / torch.diagonal(R)[:i]).to(fdt)
+    return y if on_dev else y.cpu().numpy()
 
 
 def certificates(factors: QrFactors) -> StabilityCertificate:

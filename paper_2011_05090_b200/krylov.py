@@ -402,12 +402,14 @@ class _Dist:
         o = self.row0 - self.wlo
         buf[o:o + self.n_loc].copy_(x_local)
         ops = []
+        # q is a rank WITHIN comm.group (TorchComm.rank is dist.get_rank(group)):
+        # pass it as group_peer (P2POp's positional peer is a global rank)
         for q, a, b in self.recvs:
-            ops.append(tdist.P2POp(tdist.irecv, buf[a - self.wlo:b - self.wlo], q,
-                                   group=self.comm.group))
+            ops.append(tdist.P2POp(tdist.irecv, buf[a - self.wlo:b - self.wlo],
+                                   group=self.comm.group, group_peer=q))
         for q, a, b in self.sends:
-            ops.append(tdist.P2POp(tdist.isend, x_local[a - self.row0:b - self.row0], q,
-                                   group=self.comm.group))
+            ops.append(tdist.P2POp(tdist.isend, x_local[a - self.row0:b - self.row0],
+                                   group=self.comm.group, group_peer=q))
         if ops:
             for req in tdist.batch_isend_irecv(ops):
                 req.wait()
@@ -699,7 +701,7 @@ class _ArnoldiEngine:
             # successor's column kernel; a breakdown in the finalize of column
             # ncols means that kernel ran for the newest committed one too
             nc = out["ncols"]
-            covered = (out["code"] in (_lib.ST_BREAKDOWN, _lib.ST_NONFINITE)
+            covered = (out["code"] == _lib.ST_BREAKDOWN
                        and out["column"] == nc + 1)
             if nc > 0 and not covered:
                 st._normalize(nc - 1, guarded=False)
@@ -741,7 +743,7 @@ def arnoldi(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, thet
     b_dev = _to_device_f64(b, A.n, st.device)
     eng.start(b_dev if dist is None else dist.local(b_dev).contiguous(), None)
     s0 = eng.run(alpha=None, tol=None)
-    breakdown = s0["code"] in (_lib.ST_BREAKDOWN, _lib.ST_NONFINITE)
+    breakdown = s0["code"] == _lib.ST_BREAKDOWN
     if s0["code"] == _lib.ST_RANK:
         raise np.linalg.LinAlgError("sketched basis numerically rank deficient")
     if s0["code"] and s0["ncols"] == 0:
@@ -794,7 +796,7 @@ def gmres(A: SparseMatrix, b, m: int, variant: GsVariant = GsVariant.RGS, theta=
         raise np.linalg.LinAlgError("sketched basis numerically rank deficient")
     if code and s1["ncols"] == 0:
         st._raise_status(s1)
-    breakdown = code in (_lib.ST_BREAKDOWN, _lib.ST_NONFINITE)
+    breakdown = code == _lib.ST_BREAKDOWN
     k = s1["iters"]
     hist = eng.hist[:k].cpu().numpy()
     x = torch.zeros(n_loc, dtype=torch.float64, device=device)

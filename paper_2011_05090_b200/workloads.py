@@ -24,6 +24,7 @@ CPU oracle, so parity compares identical inputs.
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 
@@ -63,23 +64,54 @@ def haar_and_sigma(m: int, sigma_min: float, seed: int):
 
 
 def make_w_rows(n: int, m: int, sigma_min: float, seed: int, r0: int, r1: int,
-                dtype=np.float64) -> np.ndarray:
-    """Rows [r0, r1) of W (row-major), generated blockwise."""
-    V, sigma = haar_and_sigma(m, sigma_min, seed)
-    M = sigma[:, None] * V.T  # diag(sigma) V^T
+                dtype=np.float64, threads: int | None = None) -> np.ndarray:
+    """Rows [r0, r1) of W (row-major), generated blockwise.
+
+    The product (G diag sigma) V^T is formed in fixed 2^22-element row chunks
+    (boundaries relative to the 2^20-row block) with single-threaded BLAS, so
+    the bits of W depend neither on the BLAS thread count nor on [r0, r1):
+    OpenBLAS dgemm results change with both.  Blocks are independent, so
+    `threads` Python threads generate them in parallel (numpy's generator and
+    BLAS release the GIL)."""
+    from threadpoolctl import threadpool_limits
     out = np.empty((r1 - r0, m), dtype=dtype)
     b0, b1 = r0 // ROW_BLOCK, (r1 - 1) // ROW_BLOCK
-    for b in range(b0, b1 + 1):
-        lo, hi = b * ROW_BLOCK, min((b + 1) * ROW_BLOCK, n)
-        G = _philox(seed, 0x10000 + b).standard_normal((hi - lo, m)) / math.sqrt(n)
-        blk = G @ M
-        a, c = max(lo, r0), min(hi, r1)
-        out[a - r0:c - r0] = blk[a - lo:c - lo]
+    step = max(1, (1 << 22) // m)
+    scale = math.sqrt(n)
+
+    with threadpool_limits(limits=1, user_api="blas"):
+        V, sigma = haar_and_sigma(m, sigma_min, seed)
+        M = sigma[:, None] * V.T  # diag(sigma) V^T
+
+        def one(b):
+            lo, hi = b * ROW_BLOCK, min((b + 1) * ROW_BLOCK, n)
+            a, c = max(lo, r0), min(hi, r1)
+            gen = _philox(seed, 0x10000 + b)
+            for c0 in range(lo, c, step):
+                c1 = min(c0 + step, hi)
+                G = gen.standard_normal((c1 - c0, m))  # the block's stream, in order
+                if c1 <= a:
+                    continue
+                G /= scale
+                blk = G @ M
+                x0, x1 = max(c0, a), min(c1, c)
+                out[x0 - r0:x1 - r0] = blk[x0 - c0:x1 - c0]
+
+        blocks = range(b0, b1 + 1) if r1 > r0 else range(0)
+        nt = min(len(blocks), threads if threads is not None else (os.cpu_count() or 1))
+        if nt > 1:
+            from concurrent.futures import ThreadPoolExecutor
+            with ThreadPoolExecutor(nt) as ex:
+                list(ex.map(one, blocks))
+        else:
+            for b in blocks:
+                one(b)
     return out
 
 
-def make_w(n: int, m: int, sigma_min: float, seed: int, dtype=np.float64) -> np.ndarray:
-    return make_w_rows(n, m, sigma_min, seed, 0, n, dtype)
+def make_w(n: int, m: int, sigma_min: float, seed: int, dtype=np.float64,
+           threads: int | None = None) -> np.ndarray:
+    return make_w_rows(n, m, sigma_min, seed, 0, n, dtype, threads)
 
 
 def make_w_device(n: int, m: int, sigma_min: float, seed: int, dtype, device,

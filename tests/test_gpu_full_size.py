@@ -90,14 +90,22 @@ def test_c0_shape_device_rademacher_factorization(cuda):
 
 
 def _metrics_dev(W, f):
-    """factor_metrics (oracle/metrics.py) on the GPU in fp64: ||I - S^T S||_2,
-    ||I - Q^T Q||_2, ||W - QR||_F / ||W||_F."""
-    Q, R, S = f.Q.double(), f.R.double(), f.S.double()
-    Wd = W.double()
-    eye = torch.eye(Q.shape[1], dtype=torch.float64, device=Q.device)
-    return {"orth_S_2": float(torch.linalg.matrix_norm(eye - S.t() @ S, ord=2)),
-            "orth_Q_2": float(torch.linalg.matrix_norm(eye - Q.t() @ Q, ord=2)),
-            "relres_F": float(torch.linalg.norm(Wd - Q @ R) / torch.linalg.norm(Wd))}
+    """The three 2-norm gates, by the SAME function that produced the oracle's
+    values in the golden files (oracle.factor_metrics_blocked, fp64)."""
+    from oracle import factor_metrics_blocked
+    return factor_metrics_blocked(W, f.Q, f.R, f.S, device="cuda")
+
+
+def _upload_colmajor(W):
+    """Host (n, m) -> a column-major CUDA copy, returned as its (n, m) view
+    (rgs_factorize uses column-major views in place: no second device copy of
+    a 67 GB W)."""
+    n, m = W.shape
+    Wd = torch.empty((m, n), dtype=torch.from_numpy(W[:1]).dtype, device="cuda")
+    step = 1 << 20
+    for r0 in range(0, n, step):
+        Wd[:, r0:r0 + step] = torch.from_numpy(W[r0:r0 + step]).cuda().t()
+    return Wd.t()
 
 
 def _golden_fullsize():
@@ -152,41 +160,49 @@ def test_c1_full_size_metrics_within_10x_of_oracle(cuda):
     assert np.linalg.norm(d - g["c1_Rdiag"]) <= 1e-3 * np.linalg.norm(g["c1_Rdiag"])
 
 
-def test_c2_shape_q_r_s_vs_oracle(cuda):
-    """BASELINE c2's shape (n = 2^23, k = 2000 block-SRHT over 8 seeded 2^20-row
-    blocks, fp64, breakdown_factor 0) with 200 of its 1000 columns (the oracle
-    host cannot hold the full W): R, S and sampled rows of Q within 1e-10 of the
-    oracle (tests/golden/c2m200.npz, oracle/make_c2_golden.py), metrics within 10x."""
+def test_c2_full_size_q_r_s_p_vs_oracle(cuda):
+    """BASELINE c2 at FULL size on one GPU (n = 2^23, m = 1000, k = 2000
+    block-SRHT over 8 seeded 2^20-row blocks, fp64, sigma_min = 1e-6,
+    breakdown_factor 0) against the oracle run on the GPU box's host
+    (tests/golden/c2full.npz, oracle/make_sharded_golden.py): R, S, P and 101
+    sampled rows of Q within 1e-10 (north_star fp64 gate), the three metrics
+    within 10x.  This covers the whole LS growth to i = 1000 at k = 2000
+    (reference _IncrementalHouseholderQR, gram_schmidt.py:148-190)."""
     from paper_2011_05090_b200.workloads import make_w
-    g = np.load(os.path.join(GOLDEN, "c2m200.npz"))
-    n, m, k = 1 << 23, 200, 2000
-    W = torch.from_numpy(make_w(n, m, 1e-6, 0)).cuda()
+    g = np.load(os.path.join(GOLDEN, "c2full.npz"))
+    n, m, k = (int(v) for v in g["meta"])
+    assert (n, m, k) == (1 << 23, 1000, 2000)
+    W = _upload_colmajor(make_w(n, m, 1e-6, 0))
     th = sg.make_sketch(sg.SketchKind.BLOCK_SRHT, k, n, 0, block_log2=20)
-    f, _ = sg.rgs_factorize(W, th, sg.UNIFIED64, breakdown_factor=0.0, device_factors=True)
+    f, _ = sg.rgs_factorize(W, th, sg.UNIFIED64, breakdown_factor=0.0, device_factors=True,
+                            with_certificate=False)
     rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))  # noqa: E731
-    assert rel(f.R.cpu().numpy(), g["c2_R"]) <= 1e-10
-    assert rel(f.S.cpu().numpy(), g["c2_S"]) <= 1e-10
-    rows = torch.from_numpy(g["c2_rows"]).cuda()
-    assert rel(f.Q[rows].cpu().numpy(), g["c2_Qrows"]) <= 1e-10
+    assert rel(f.R.cpu().numpy(), g["R"]) <= 1e-10
+    assert rel(f.S.cpu().numpy(), g["S"]) <= 1e-10
+    assert rel(f.P.cpu().numpy(), g["P"]) <= 1e-13
+    rows = torch.from_numpy(g["rows"]).cuda()
+    assert rel(f.Q[rows].cpu().numpy(), g["Qrows"]) <= 1e-10
     ours = _metrics_dev(W, f)
     for key, v in ours.items():
-        assert v <= 10.0 * max(float(g[f"c2_{key}"]), 1e-15), (key, v, float(g[f"c2_{key}"]))
+        assert v <= 10.0 * max(float(g[key]), 1e-15), (key, v, float(g[key]))
 
 
-def test_c4_shape_metrics_vs_oracle(cuda):
+def test_c4_shape_m400_metrics_vs_oracle(cuda):
     """BASELINE c4's shape on one GPU (n = 2^25, k = 3000 block-SRHT over 32
-    seeded 2^20-row blocks, W fp32, MIXED32_64, breakdown_factor 0) with 64 of
-    its 1500 columns (c4 itself needs 4 GPUs): the 2-norm metrics within 10x of
-    the oracle's (tests/golden/c4m64.npz, oracle/make_c4_golden.py) and R close
-    to the oracle's at the fp32 level."""
+    seeded 2^20-row blocks, W fp32, MIXED32_64, sigma_min = 1e-10,
+    breakdown_factor 0) with m = 400 columns (the full m = 1500 needs 4 GPUs;
+    400 is what one GPU's 180 GB and the oracle host hold together): the
+    2-norm metrics within 10x of the oracle's (tests/golden/c4m400.npz,
+    oracle/make_sharded_golden.py), R close at the fp32 level."""
     from paper_2011_05090_b200.workloads import make_w
-    g = np.load(os.path.join(GOLDEN, "c4m64.npz"))
-    n, m, k = 1 << 25, 64, 3000
-    W = torch.from_numpy(make_w(n, m, 1e-10, 0, dtype=np.float32)).cuda()
+    g = np.load(os.path.join(GOLDEN, "c4m400.npz"))
+    n, m, k = (int(v) for v in g["meta"])
+    W = _upload_colmajor(make_w(n, m, 1e-10, 0, dtype=np.float32))
     th = sg.make_sketch(sg.SketchKind.BLOCK_SRHT, k, n, 0, block_log2=20)
-    f, _ = sg.rgs_factorize(W, th, sg.MIXED32_64, breakdown_factor=0.0, device_factors=True)
+    f, _ = sg.rgs_factorize(W, th, sg.MIXED32_64, breakdown_factor=0.0, device_factors=True,
+                            with_certificate=False)
     ours = _metrics_dev(W, f)
     for key, v in ours.items():
-        assert v <= 10.0 * max(float(g[f"c4_{key}"]), 1e-15), (key, v, float(g[f"c4_{key}"]))
+        assert v <= 10.0 * max(float(g[key]), 1e-15), (key, v, float(g[key]))
     R = f.R.cpu().numpy()
-    assert np.linalg.norm(R - g["c4_R"]) <= 1e-5 * np.linalg.norm(g["c4_R"])
+    assert np.linalg.norm(R - g["R"]) <= 1e-4 * np.linalg.norm(g["R"])
