@@ -103,8 +103,6 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
   if (tl && threadIdx.x == 0) atomicMin(tl + (int64_t)i * 16 + 0, gtimer());
   constexpr int V = VecT<TQ>::N;                  // rows per vector (4 fp32, 2 fp64)
   constexpr int NH = kColT / (kColThreads * V);   // vectors per thread (2 fp32, 4 fp64)
-  constexpr int LV = (V == 4) ? 2 : 1;            // log2 V
-  constexpr int HB = kColLogT - ((NH == 2) ? 1 : 2);  // first element bit carried by h
   const int S = nstages;  // ring depth (<= kColMaxStages)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   TQ* ring = reinterpret_cast<TQ*>(smem_raw);                        // S x 4096
@@ -285,14 +283,16 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
   // ---- sketch epilogue (z aliases the drained ring) ----------------------------
   __syncthreads();
   if (active) {
-    fwht_reg<3>(xs);  // bits [0, LV) from v and [HB, 12) from h
+    // the stage order of the stand-alone tile kernel (srht_tile_kernel,
+    // sgs_sketch.cu): bits 6..11, then 0..5 - four radix-8 passes - so the
+    // partials equal sgs_srht_partials' of the same column bit for bit
 #pragma unroll
     for (int hh = 0; hh < NH; ++hh)
 #pragma unroll
       for (int v = 0; v < V; ++v) z[pidx(hh * (kColThreads * V) + tid * V + v)] = xs[hh * V + v];
     __syncthreads();
 #pragma unroll
-    for (int b0 = LV; b0 < HB; b0 += 3) {  // bits [LV, HB): three radix-8 passes
+    for (int b0 : {6, 9, 0, 3}) {
       fwht_pass<kColLogT, 3>(z, b0);
       __syncthreads();
     }

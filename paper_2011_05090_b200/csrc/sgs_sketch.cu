@@ -16,6 +16,8 @@
 #include "sgs_common.cuh"
 #include "sgs_fwht.cuh"
 
+#include <cstdlib>
+
 namespace cg = cooperative_groups;
 
 namespace sgs {
@@ -27,6 +29,16 @@ constexpr int kSrhtThreads = 512;
 constexpr int kSrhtMaxLogT = 12;   // 4096-row tiles (32 KB of fp64)
 constexpr int kSrhtTargetCTAs = 1024;  // one tile per CTA up to 1024 tiles (4M rows)
 constexpr int kSrhtCluster = 8;    // CTAs whose k-vector partials are combined through DSMEM
+
+// SGS_SRHT_LEGACY=1: the three-pass shared-memory transform for 4096-row tiles
+// too (A/B switch; the default is the two-phase register kernel below)
+static bool srht_legacy() {
+  static const bool v = [] {
+    const char* e = getenv("SGS_SRHT_LEGACY");
+    return e && atoi(e) != 0;
+  }();
+  return v;
+}
 
 // One CTA transforms `tiles_per_cta` consecutive tiles and accumulates the
 // signed sampled entries into a shared k-vector; the 8 CTAs of a cluster then
@@ -155,6 +167,122 @@ srht_partials_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local,
   cl.sync();  // keep shared memory alive until every CTA has read it
 }
 
+// 4096-row tiles, two-phase register FWHT (the production path for LOGT = 12).
+// One 64-thread CTA per tile unit.  Phase 1: thread t holds the 64 elements
+// t + 64 j of the tile (j = element bits 6..11, coalesced loads, signs applied
+// on load) and transforms bits 6..11 in registers; one exchange through
+// shared memory (padding e + e/64: both access patterns conflict-free) gives
+// it the elements 64 t + j (bits 0..5), transformed in registers as well.  So
+// the 12 stages cost one shared-memory round trip instead of three radix-8
+// passes, and the 64-bit adds (768 per thread per tile) are the bound.  The
+// stage order (bits 6..11, then 0..5) is also the one of the fused column
+// kernel's epilogue (sgs_column.cu), so with one tile per CTA both write the
+// same partials bit for bit.  The transformed tile goes back to shared memory
+// for the gather of the k sampled rows; the cluster of 8 CTAs sums its
+// k-vectors through DSMEM in rank order, one partial per cluster, as before.
+constexpr int kTileThreads = 64;
+constexpr int kTileBuf = 4096 + 64;  // xidx(4096)
+__device__ __forceinline__ int xidx(int e) { return e + (e >> 6); }
+
+template <typename TX>
+__global__ void __launch_bounds__(kTileThreads)
+srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t row0,
+                 int log2_block, const uint32_t* __restrict__ sign_bits,
+                 const int32_t* __restrict__ samples, int k, int tiles_per_cta, int64_t ntiles,
+                 double* __restrict__ partials, const sgs_status* st, unsigned long long* tl) {
+  cg::cluster_group cl = cg::this_cluster();
+  constexpr int LOGT = 12, T = 1 << LOGT;
+  extern __shared__ double smem[];
+  double* buf = smem;                                  // xidx(T) entries
+  double* part = smem + kTileBuf;                      // k entries
+  int32_t* smp = reinterpret_cast<int32_t*>(part + k);  // k entries
+  const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+  const int col = blockIdx.y;
+  const int ngroups = gridDim.x / kSrhtCluster;
+  const TX* x = X + (int64_t)col * ldx;
+  const int64_t t0 = (int64_t)blockIdx.x * tiles_per_cta;
+  const int64_t t1 = min(t0 + tiles_per_cta, ntiles);
+  const int64_t bmask = (int64_t(1) << log2_block) - 1;
+  // the operator does not depend on the predecessor: k-vector and first
+  // sample set before the dependency wait
+  for (int j = t; j < k; j += kTileThreads) part[j] = 0.0;
+  int64_t cur_blk = -1;
+  if (t0 < t1) {
+    cur_blk = (row0 + t0 * T) >> log2_block;
+    const int32_t* sb = samples + cur_blk * (int64_t)k;
+    for (int j = t; j < k; j += kTileThreads) smp[j] = __ldg(sb + j);
+  }
+  pdl_enter();
+  if (status_stopped(st)) return;  // uniform across the cluster
+  if (tl && t == 0) atomicMin(tl + 12, gtimer());
+  for (int64_t ti = t0; ti < t1; ++ti) {
+    const int64_t lr0 = ti * T;
+    const int64_t g0 = row0 + lr0;
+    const int64_t blk = g0 >> log2_block;
+    const int64_t h = (g0 & bmask) >> LOGT;
+    double v[64];
+    if (lr0 + T <= n_local) {
+#pragma unroll
+      for (int j = 0; j < 64; ++j) v[j] = load_as_double(x + lr0 + t + 64 * j);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        const int64_t lr = lr0 + t + 64 * j;
+        v[j] = lr < n_local ? load_as_double(x + lr) : 0.0;
+      }
+    }
+    // sign word of element t + 64 j: (lr0 + 64 j + 32 w) / 32, warp-uniform
+    const uint32_t* sw = sign_bits + (lr0 >> 5) + w;
+#pragma unroll
+    for (int j = 0; j < 64; ++j) {
+      const bool in = lr0 + 64 * j + 32 * w < n_local;
+      const uint32_t word = in ? __ldg(sw + 2 * j) : ~0u;
+      if (((word >> lane) & 1u) == 0u) v[j] = -v[j];
+    }
+    fwht_reg<6>(v);                       // bits 6..11
+    __syncthreads();                      // previous tile's gather has read buf / smp
+    if (blk != cur_blk) {
+      const int32_t* sb = samples + blk * (int64_t)k;
+      for (int j = t; j < k; j += kTileThreads) smp[j] = __ldg(sb + j);
+      cur_blk = blk;
+    }
+#pragma unroll
+    for (int j = 0; j < 64; ++j) buf[xidx(t + 64 * j)] = v[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 64; ++j) v[j] = buf[xidx(64 * t + j)];
+    fwht_reg<6>(v);                       // bits 0..5
+    // thread t re-writes exactly the slots it read: no barrier in between
+#pragma unroll
+    for (int j = 0; j < 64; ++j) buf[xidx(64 * t + j)] = v[j];
+    __syncthreads();
+    for (int j = t; j < k; j += kTileThreads) {
+      const int32_t r = smp[j];
+      const double z = buf[xidx(r & (T - 1))];
+      const int64_t rh = (int64_t)(r >> LOGT);
+      part[j] += (__popcll(rh & h) & 1) ? -z : z;
+    }
+  }
+  cl.sync();  // all k-vectors of the cluster are final
+  const int rank = (int)cl.block_rank();
+  const int j0 = (int)(((int64_t)rank * k) / kSrhtCluster);
+  const int j1 = (int)(((int64_t)(rank + 1) * k) / kSrhtCluster);
+  double* out = partials + ((int64_t)col * ngroups + blockIdx.x / kSrhtCluster) * k;
+  for (int j = j0 + t; j < j1; j += kTileThreads) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < kSrhtCluster; ++q) s += cl.map_shared_rank(part, q)[j];
+    out[j] = s;
+  }
+  if (tl && t == 0) atomicMax(tl + 13, gtimer());
+  cl.sync();  // keep shared memory alive until every CTA has read it
+}
+
+template <typename TX>
+static size_t srht_tile_smem(int k) {
+  return (size_t)(kTileBuf + k) * sizeof(double) + (size_t)k * sizeof(int32_t);
+}
+
 static void srht_geometry(int64_t n_local, int log2_block, int* logt, int64_t* ntiles,
                           int* tpc, int* nctas) {
   const int lt = log2_block < kSrhtMaxLogT ? log2_block : kSrhtMaxLogT;
@@ -174,6 +302,20 @@ static int launch_srht_t(const void* X, int64_t ldx, int ncols, int64_t n_local,
                          int log2_block, const uint32_t* sign_bits, const int32_t* samples,
                          int k, double* partials, const sgs_status* st, cudaStream_t s,
                          int tpc, int64_t ntiles, int nctas) {
+  if constexpr (LOGT == 12) {
+    const size_t sm = srht_tile_smem<TX>(k);
+    if (sm <= 227 * 1024 && !srht_legacy()) {
+      auto kern = srht_tile_kernel<TX>;
+      if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
+      return check_ex(launch_ex(kern, dim3(nctas, ncols), dim3(kTileThreads), sm, s, kSrhtCluster,
+                                static_cast<const TX*>(X), ldx, n_local, row0, log2_block,
+                                sign_bits, samples, k, tpc, ntiles, partials, st,
+                                debug_timeline_row()),
+                      "srht_tile_kernel");
+    }
+  }
   constexpr int T = 1 << LOGT;
   const size_t smem = (size_t)(T + T / 8 + 8 + k) * sizeof(double) + (size_t)k * sizeof(int32_t) +
                       (size_t)(T / 32) * sizeof(uint32_t);

@@ -144,3 +144,34 @@ def test_device_rademacher_bits_match_reference_streams(cuda, k, n, seed):
                        atol=1e-13)
     y0 = th.apply(Xr[:, 0])
     assert np.array_equal(y0, th.apply_block(Xr)[:, 0])  # apply_block == apply
+
+
+@pytest.mark.parametrize("dt,n,kind", [(torch.float64, 1_000_000, "psrht"),
+                                       (torch.float32, 3 * 4096 + 100, "psrht"),
+                                       (torch.float64, 4 * 4096, "block_srht")])
+def test_column_kernel_sketch_equals_stand_alone_sketch(cuda, dt, n, kind):
+    """The fused column kernel's SRHT epilogue and the stand-alone tile kernel
+    run the same transform (stage order bits 6..11 then 0..5, one tile per
+    CTA, 8-CTA cluster sums): for column 0 (q'_0 = w) their partials are
+    bit-identical, so the S of a factorisation equals Theta applied to the
+    unnormalised basis exactly as apply() would compute it."""
+    from paper_2011_05090_b200 import _lib
+    kw = {"block_log2": 12} if kind == "block_srht" else {}
+    th = sg.make_sketch(sg.SketchKind(kind), 300, n, 7, **kw)
+    d = th.device_data(cuda)
+    code = _lib.dtype_code(dt)
+    w = torch.randn(n, dtype=torch.float64, device=cuda, generator=torch.Generator(cuda).manual_seed(1)).to(dt)
+    ldq = (n + 31) // 32 * 32
+    Q = torch.zeros((2, ldq), dtype=dt, device=cuda)
+    npc = int(_lib.load().sgs_column_nparts(n))
+    assert npc == th.nparts(n)
+    pc = torch.empty((npc, th.k), dtype=torch.float64, device=cuda)
+    ps = torch.empty_like(pc)
+    st = _lib.Status(cuda)
+    _lib.call("sgs_rgs_update_srht", Q.data_ptr(), code, ldq, n, 0, w.data_ptr(), code, None,
+              None, 0, None, 2, 1, 0, th.log2_block, d["bits"].data_ptr(),
+              d["samples"].data_ptr(), th.k, pc.data_ptr(), st.ptr, _lib.stream_ptr())
+    th.partials_into(w, code, n, 1, ps, status=st)
+    torch.cuda.synchronize()
+    assert torch.equal(Q[0, :n], w)
+    assert torch.equal(pc, ps)
