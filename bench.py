@@ -336,6 +336,8 @@ def run_qr(args, cfg_name, comm):
         graph = gstate.capture_factorization(Wt, ldw, m)
         graph_launches = _lib.launch_count() - lcg
 
+    graph_used = graph is not None
+
     def timed_step():
         if graph is not None:
             graph.replay()
@@ -500,7 +502,7 @@ def run_qr(args, cfg_name, comm):
                        **({"weak": f"n = {world} x {n_per_gpu} rows (~{n_per_gpu} per GPU); "
                                    f"value counts column shards: {world} per column"}
                           if weak else {})},
-            "graph": graph is not None,
+            "graph": graph_used,
             "hbm_gbs_whole_step": round(hbm_gbs, 1),
             "hbm_frac_whole_step": round(hbm_gbs / (peak * world), 4),
             # BASELINE.json quotes the nominal ~8 TB/s; the roofline uses the measured peak

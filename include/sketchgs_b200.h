@@ -89,11 +89,19 @@ int sgs_srht_partials(const void* X, int x_dtype, int64_t ldx, int ncols,
                       const uint32_t* sign_bits, const int32_t* samples, int k,
                       double* partials, const sgs_status* st, void* stream);
 
-/* Dense sketch (Gaussian / materialised Rademacher, absent from the
- * reference's SketchKind; duck-typed in through sketch.py:120-206):
- * partials of Theta^T' X over nparts fixed row chunks. ncols==1 is a GEMV,
- * ncols>1 a split-K GEMM; both accumulate each chunk in ascending row order,
- * so apply_block is bit-identical to apply. */
+/* Dense sketch (Gaussian, absent from the reference's SketchKind; duck-typed
+ * in through sketch.py:120-206; a column block sketched as the dense
+ * contraction sketch.py:186-198 does column by column): partials of
+ * Theta^T' X on the fp64 tensor cores (DMMA, mma.sync m8n8k4 f64).  The rows
+ * are split into sub-chunks, each a chain of 4-row DMMA steps in ascending
+ * order; 8 consecutive sub-chunks are summed in a thread-block cluster, so
+ * sgs_gaussian_nparts(n) (<= 37) partials per column.  ncols == 1 runs the
+ * same chains, so apply_block is bit-identical to apply.
+ * SGS_DENSE_LEGACY=1 selects the DFMA GEMV / split-K GEMM with
+ * sgs_dense_nparts(n) partials instead. */
+int sgs_gaussian_nparts(int64_t n);
+/* Row chunks of the packed-sign Rademacher partials (and of the legacy dense
+ * kernels): min(296, ceil(n / 32)). */
 int sgs_dense_nparts(int64_t n);
 /* Partial k-vectors per column written by sgs_rgs_update_dense (its own
  * 16-row-aligned chunking, about two chunks per SM). */
@@ -179,6 +187,16 @@ int sgs_rgs_update_dense(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
                          int normalize_prev, const double* R, int64_t ldr,
                          int do_sketch, const double* thetaT, int64_t ldt, int k,
                          double* partials, const sgs_status* st, void* stream);
+/* The same fused column step for the device-generated Rademacher sketch
+ * (SketchKind.RADEMACHER, sketch.py:153-166): q'_i = w - Q r streamed once,
+ * then Theta q' from the packed signs of sgs_rademacher_bits (1 bit per entry,
+ * n x ceil(k/32) words) - no second read of q', no fp64 Theta stream.  The
+ * chunking and partial count are sgs_dense_column_nparts(n, k). */
+int sgs_rgs_update_rademacher(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
+                              const void* w, int w_dtype, const void* r_crs,
+                              int normalize_prev, const double* R, int64_t ldr,
+                              int do_sketch, const uint32_t* rbits, int k,
+                              double* partials, const sgs_status* st, void* stream);
 
 /* Q[:, col] = cast_crs(Q[:, col] / R[col, col])   (gram_schmidt.py:329) */
 int sgs_normalize_column(void* Q, int q_dtype, int64_t ldq, int64_t n,

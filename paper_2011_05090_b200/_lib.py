@@ -60,6 +60,7 @@ _SIGS = {
     "sgs_srht_partials": (c_int, [c_void_p, c_int, c_int64, c_int, c_int64, c_int64, c_int,
                                   c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
     "sgs_dense_nparts": (c_int, [c_int64]),
+    "sgs_gaussian_nparts": (c_int, [c_int64]),
     "sgs_dense_column_nparts": (c_int, [c_int64, c_int]),
     "sgs_dense_partials": (c_int, [c_void_p, c_int64, c_int, c_void_p, c_int, c_int64, c_int,
                                    c_int64, c_void_p, c_void_p, c_void_p]),
@@ -83,6 +84,9 @@ _SIGS = {
     "sgs_rgs_update_dense": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_void_p, c_int,
                                      c_void_p, c_int, c_void_p, c_int64, c_int, c_void_p,
                                      c_int64, c_int, c_void_p, c_void_p, c_void_p]),
+    "sgs_rgs_update_rademacher": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_void_p,
+                                          c_int, c_void_p, c_int, c_void_p, c_int64, c_int,
+                                          c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
     "sgs_normalize_column": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_void_p,
                                      c_int64, c_void_p, c_void_p]),
     "sgs_gemv_f64": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_void_p, c_void_p,

@@ -353,13 +353,13 @@ __device__ __forceinline__ void tma_copy_1d(void* dst, const void* src, uint32_t
       "l"(policy) : "memory");
 }
 
-template <typename TQ, typename TW, int QP>
+template <typename TQ, typename TW, int QP, bool RAD>
 __global__ void __launch_bounds__(512)
 dense_ring_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* __restrict__ w,
                   const TQ* __restrict__ rc, int normalize_prev, const double* __restrict__ R,
                   int64_t ldr, int do_sketch, const double* __restrict__ thetaT, int64_t ldt,
                   int k, double* __restrict__ partials, int64_t chunk, int stage_bytes,
-                  const sgs_status* st) {
+                  const sgs_status* st, const uint32_t* __restrict__ rbits, int kw) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* ring = smem_raw;  // kDcStages x stage_bytes
   double* xq = reinterpret_cast<double*>(smem_raw + (size_t)kDcStages * stage_bytes);  // chunk
@@ -375,9 +375,11 @@ dense_ring_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
   const uint32_t segb = (uint32_t)(((size_t)nr * sizeof(TQ) + 15) / 16 * 16);
   const int G = max(1, stage_bytes / (int)segb);               // Q columns per stage
   const uint32_t rowb = (uint32_t)(ldt * sizeof(double));
-  const int Rr = max(1, stage_bytes / (int)rowb);               // Theta rows per stage
+  const int Rr = RAD ? 1 : max(1, stage_bytes / (int)rowb);     // Theta rows per stage
   const int n1 = (nplain + G - 1) / G;
-  const int n2 = do_sketch ? (nr + Rr - 1) / Rr : 0;
+  // the Rademacher variant streams only Q through the ring; its +-1 entries
+  // come packed (1 bit each, L2-resident) straight from global memory
+  const int n2 = (do_sketch && !RAD) ? (nr + Rr - 1) / Rr : 0;
   const int ntot = n1 + n2;
   uint64_t policy = 0;
   if (tid == 0) {
@@ -510,6 +512,26 @@ dense_ring_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
     if (t == n1 - 1) finish_update();
   }
   if (!do_sketch) return;
+  if constexpr (RAD) {
+    // Theta q' over the chunk's rows with the device-generated signs: per
+    // sketch row the chain in ascending row order, acc + (+-x) - i.e.
+    // fma(+-1, x, acc), the materialised Gaussian-path arithmetic exactly
+    // (finish_update ended with a block barrier: xq is complete)
+    for (int rr = 0; rr < nr; ++rr) {
+      const double xv = xq[rr];
+      const uint32_t* brow = rbits + (int64_t)(r0 + rr) * kw;
+#pragma unroll
+      for (int q = 0; q < QP; ++q) {
+        const int jj = tid + q * T;
+        if (2 * jj < k) {
+          const uint32_t word = __ldg(brow + ((2 * jj) >> 5));
+          const int b = (2 * jj) & 31;
+          acc2[q].x += ((word >> b) & 1u) ? xv : -xv;
+          acc2[q].y += ((word >> (b + 1)) & 1u) ? xv : -xv;
+        }
+      }
+    }
+  }
   double* outp = partials + (int64_t)p * k;
 #pragma unroll
   for (int q = 0; q < QP; ++q) {
@@ -539,18 +561,21 @@ static int dense_ring_threads(int k) {
   return threads;
 }
 
-template <typename TQ, typename TW>
+template <typename TQ, typename TW, bool RAD>
 static int launch_dense_ring(void* Q, int64_t ldq, int64_t n, int i, const void* w,
                              const void* r_crs, int normalize_prev, const double* R, int64_t ldr,
                              int do_sketch, const double* thetaT, int64_t ldt, int k,
-                             double* partials, const sgs_status* st, cudaStream_t s) {
+                             double* partials, const sgs_status* st, cudaStream_t s,
+                             const uint32_t* rbits = nullptr, int kw = 0) {
   const int threads = dense_ring_threads(k);
   const int kp = (k + 1) / 2;
   const int qp = (kp + threads - 1) / threads;
   int64_t chunk;
   int np;
   dense_ring_geom(n, threads, &chunk, &np);
-  const int stage_bytes = (int)std::max<int64_t>(kDcStageBytes, ((int64_t)ldt * 8 + 15) / 16 * 16);
+  const int stage_bytes =
+      RAD ? kDcStageBytes
+          : (int)std::max<int64_t>(kDcStageBytes, ((int64_t)ldt * 8 + 15) / 16 * 16);
   const size_t smem = (size_t)kDcStages * stage_bytes + (size_t)chunk * 8 +
                       (size_t)(i > 0 ? i : 1) * sizeof(TQ);
   if (smem > 227 * 1024) {
@@ -560,11 +585,11 @@ static int launch_dense_ring(void* Q, int64_t ldq, int64_t n, int i, const void*
   cudaError_t e;
 #define SGS_DR(QPV)                                                                              \
   do {                                                                                           \
-    auto kern = dense_ring_kernel<TQ, TW, QPV>;                                                  \
+    auto kern = dense_ring_kernel<TQ, TW, QPV, RAD>;                                             \
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
     e = launch_ex(kern, dim3(np), dim3(threads), smem, s, 1, static_cast<TQ*>(Q), ldq, n, i,     \
                   static_cast<const TW*>(w), static_cast<const TQ*>(r_crs), normalize_prev, R,   \
-                  ldr, do_sketch, thetaT, ldt, k, partials, chunk, stage_bytes, st);             \
+                  ldr, do_sketch, thetaT, ldt, k, partials, chunk, stage_bytes, st, rbits, kw);  \
   } while (0)
   if (qp <= 1) SGS_DR(1);
   else if (qp <= 2) SGS_DR(2);
@@ -601,13 +626,36 @@ extern "C" int sgs_rgs_update_dense(void* Q, int q_dtype, int64_t ldq, int64_t n
                              ((uintptr_t)thetaT & 15) == 0), "update_dense: sketch args");
   SGS_REQUIRE(((uintptr_t)Q & 15) == 0 && (ldq % 16) == 0, "update_dense: Q alignment");
   cudaStream_t s = as_stream(stream);
-#define SGS_DCL(TQ, TW)                                                                          return launch_dense_ring<TQ, TW>(Q, ldq, n, i, w, r_crs, normalize_prev, R, ldr, do_sketch,                                      thetaT, ldt, k, partials, st, s)
+#define SGS_DCL(TQ, TW)                                                                          return launch_dense_ring<TQ, TW, false>(Q, ldq, n, i, w, r_crs, normalize_prev, R, ldr, do_sketch,                                      thetaT, ldt, k, partials, st, s)
   if (q_dtype == SGS_F32 && w_dtype == SGS_F32) SGS_DCL(float, float);
   if (q_dtype == SGS_F32 && w_dtype == SGS_F64) SGS_DCL(float, double);
   if (q_dtype == SGS_F64 && w_dtype == SGS_F32) SGS_DCL(double, float);
   if (q_dtype == SGS_F64 && w_dtype == SGS_F64) SGS_DCL(double, double);
 #undef SGS_DCL
   set_error("update_dense: bad dtype");
+  return SGS_EINVAL;
+}
+
+extern "C" int sgs_rgs_update_rademacher(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
+                                         const void* w, int w_dtype, const void* r_crs,
+                                         int normalize_prev, const double* R, int64_t ldr,
+                                         int do_sketch, const uint32_t* rbits, int k,
+                                         double* partials, const sgs_status* st, void* stream) {
+  SGS_REQUIRE(Q && w && (i == 0 || r_crs) && n >= 1 && i >= 0, "update_rademacher: bad args");
+  SGS_REQUIRE(!normalize_prev || (i > 0 && R), "update_rademacher: normalize_prev needs R");
+  SGS_REQUIRE(!do_sketch || (rbits && partials && k >= 1), "update_rademacher: sketch args");
+  SGS_REQUIRE(((uintptr_t)Q & 15) == 0 && (ldq % 16) == 0, "update_rademacher: Q alignment");
+  cudaStream_t s = as_stream(stream);
+  const int kw = (k + 31) / 32;
+#define SGS_RCL(TQ, TW)                                                                        \
+  return launch_dense_ring<TQ, TW, true>(Q, ldq, n, i, w, r_crs, normalize_prev, R, ldr,       \
+                                         do_sketch, nullptr, 0, k, partials, st, s, rbits, kw)
+  if (q_dtype == SGS_F32 && w_dtype == SGS_F32) SGS_RCL(float, float);
+  if (q_dtype == SGS_F32 && w_dtype == SGS_F64) SGS_RCL(float, double);
+  if (q_dtype == SGS_F64 && w_dtype == SGS_F32) SGS_RCL(double, float);
+  if (q_dtype == SGS_F64 && w_dtype == SGS_F64) SGS_RCL(double, double);
+#undef SGS_RCL
+  set_error("update_rademacher: bad dtype");
   return SGS_EINVAL;
 }
 

@@ -184,13 +184,12 @@ constexpr int kTileThreads = 64;
 constexpr int kTileBuf = 4096 + 64;  // xidx(4096)
 __device__ __forceinline__ int xidx(int e) { return e + (e >> 6); }
 
-template <typename TX>
+template <typename TX, bool CLUSTERED>
 __global__ void __launch_bounds__(kTileThreads)
 srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t row0,
                  int log2_block, const uint32_t* __restrict__ sign_bits,
                  const int32_t* __restrict__ samples, int k, int tiles_per_cta, int64_t ntiles,
                  double* __restrict__ partials, const sgs_status* st, unsigned long long* tl) {
-  cg::cluster_group cl = cg::this_cluster();
   constexpr int LOGT = 12, T = 1 << LOGT;
   extern __shared__ double smem[];
   double* buf = smem;                                  // xidx(T) entries
@@ -198,7 +197,6 @@ srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t
   int32_t* smp = reinterpret_cast<int32_t*>(part + k);  // k entries
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
   const int col = blockIdx.y;
-  const int ngroups = gridDim.x / kSrhtCluster;
   const TX* x = X + (int64_t)col * ldx;
   const int64_t t0 = (int64_t)blockIdx.x * tiles_per_cta;
   const int64_t t1 = min(t0 + tiles_per_cta, ntiles);
@@ -263,19 +261,30 @@ srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t
       part[j] += (__popcll(rh & h) & 1) ? -z : z;
     }
   }
-  cl.sync();  // all k-vectors of the cluster are final
-  const int rank = (int)cl.block_rank();
-  const int j0 = (int)(((int64_t)rank * k) / kSrhtCluster);
-  const int j1 = (int)(((int64_t)(rank + 1) * k) / kSrhtCluster);
-  double* out = partials + ((int64_t)col * ngroups + blockIdx.x / kSrhtCluster) * k;
-  for (int j = j0 + t; j < j1; j += kTileThreads) {
-    double s = 0.0;
+  if constexpr (!CLUSTERED) {
+    // 8 tiles accumulated in tile order from 0.0: the cluster sum below, bit
+    // for bit ((0 + z0) + z1 ... = 0 + (0 + z0) + (0 + z1) ...)
+    __syncthreads();
+    double* out = partials + ((int64_t)col * gridDim.x + blockIdx.x) * k;
+    for (int j = t; j < k; j += kTileThreads) out[j] = part[j];
+    if (tl && t == 0) atomicMax(tl + 13, gtimer());
+  } else {
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();  // all k-vectors of the cluster are final
+    const int ngroups = gridDim.x / kSrhtCluster;
+    const int rank = (int)cl.block_rank();
+    const int j0 = (int)(((int64_t)rank * k) / kSrhtCluster);
+    const int j1 = (int)(((int64_t)(rank + 1) * k) / kSrhtCluster);
+    double* out = partials + ((int64_t)col * ngroups + blockIdx.x / kSrhtCluster) * k;
+    for (int j = j0 + t; j < j1; j += kTileThreads) {
+      double s = 0.0;
 #pragma unroll
-    for (int q = 0; q < kSrhtCluster; ++q) s += cl.map_shared_rank(part, q)[j];
-    out[j] = s;
+      for (int q = 0; q < kSrhtCluster; ++q) s += cl.map_shared_rank(part, q)[j];
+      out[j] = s;
+    }
+    if (tl && t == 0) atomicMax(tl + 13, gtimer());
+    cl.sync();  // keep shared memory alive until every CTA has read it
   }
-  if (tl && t == 0) atomicMax(tl + 13, gtimer());
-  cl.sync();  // keep shared memory alive until every CTA has read it
 }
 
 template <typename TX>
@@ -283,11 +292,22 @@ static size_t srht_tile_smem(int k) {
   return (size_t)(kTileBuf + k) * sizeof(double) + (size_t)k * sizeof(int32_t);
 }
 
+// Partition of a column into tiles and partials.  4096-row tiles (the tile
+// kernel): one partial per 8 consecutive tiles, *nctas = number of partials
+// (the fused column kernel's structure).  Smaller tiles (and SGS_SRHT_LEGACY):
+// tiles_per_cta tiles per CTA, one partial per 8-CTA cluster.
 static void srht_geometry(int64_t n_local, int log2_block, int* logt, int64_t* ntiles,
                           int* tpc, int* nctas) {
   const int lt = log2_block < kSrhtMaxLogT ? log2_block : kSrhtMaxLogT;
   const int64_t T = int64_t(1) << lt;
   const int64_t nt = (n_local + T - 1) / T;
+  if (lt == 12 && !srht_legacy()) {
+    *logt = lt;
+    *ntiles = nt;
+    *tpc = 1;
+    *nctas = (int)((nt + kSrhtCluster - 1) / kSrhtCluster);
+    return;
+  }
   const int64_t per = (nt + kSrhtTargetCTAs - 1) / kSrhtTargetCTAs;
   *logt = lt;
   *ntiles = nt;
@@ -303,16 +323,22 @@ static int launch_srht_t(const void* X, int64_t ldx, int ncols, int64_t n_local,
                          int k, double* partials, const sgs_status* st, cudaStream_t s,
                          int tpc, int64_t ntiles, int nctas) {
   if constexpr (LOGT == 12) {
-    const size_t sm = srht_tile_smem<TX>(k);
-    if (sm <= 227 * 1024 && !srht_legacy()) {
-      auto kern = srht_tile_kernel<TX>;
+    if (!srht_legacy()) {
+      // one partial per 8 consecutive tiles (nctas = partials here): few
+      // columns -> one tile per CTA and a DSMEM cluster sum (parallelism);
+      // batches -> one CTA runs its 8 tiles in order (no per-tile prologue
+      // or cluster exchange).  Both give the same bits.
+      const size_t sm = srht_tile_smem<TX>(k);
+      const bool batch = (int64_t)nctas * ncols >= 4 * (int64_t)sm_count();
+      auto kern = batch ? srht_tile_kernel<TX, false> : srht_tile_kernel<TX, true>;
       if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                            cudaSharedmemCarveoutMaxShared);
-      return check_ex(launch_ex(kern, dim3(nctas, ncols), dim3(kTileThreads), sm, s, kSrhtCluster,
+      const dim3 grid(batch ? nctas : nctas * kSrhtCluster, ncols);
+      return check_ex(launch_ex(kern, grid, dim3(kTileThreads), sm, s, batch ? 1 : kSrhtCluster,
                                 static_cast<const TX*>(X), ldx, n_local, row0, log2_block,
-                                sign_bits, samples, k, tpc, ntiles, partials, st,
-                                debug_timeline_row()),
+                                sign_bits, samples, k, batch ? kSrhtCluster : 1, ntiles, partials,
+                                st, debug_timeline_row()),
                       "srht_tile_kernel");
     }
   }
@@ -632,7 +658,7 @@ extern "C" int sgs_srht_nparts(int64_t n_local, int log2_block) {
   int64_t nt;
   if (n_local < 1 || log2_block < 0 || log2_block > 40) return 0;
   srht_geometry(n_local, log2_block, &lt, &nt, &tpc, &nc);
-  return nc / kSrhtCluster;
+  return (lt == 12 && !srht_legacy()) ? nc : nc / kSrhtCluster;
 }
 
 extern "C" int sgs_srht_partials(const void* X, int x_dtype, int64_t ldx, int ncols,
@@ -661,6 +687,185 @@ extern "C" int sgs_dense_nparts(int64_t n) { return n < 1 ? 0 : dense_nparts_hos
 namespace sgs {
 int dense_nparts_of(int64_t n) { return dense_nparts_host(n); }
 }  // namespace sgs
+
+// ---------------------------------------------------------------------------
+// Gaussian P = Theta W on the fp64 tensor cores (mma.sync m8n8k4 f64: the DMMA
+// SASS op).  The contraction over the n rows is split into nsub sub-chunks
+// (chunk_begin over gaussian_nsub(n) <= 296 of them, a multiple of 8); each
+// CTA owns one sub-chunk and a (j, c) output tile, and its per-output chain
+// is a sequence of DMMAs over ascending 4-row k-steps (the chunk's last step
+// zero-padded).  The 8 CTAs of a cluster are 8 consecutive sub-chunks: they
+// sum their tiles through distributed shared memory in rank order, so one
+// partial per 8 sub-chunks goes to HBM (c0: 37 x k per column instead of
+// 296 x k).  apply() (one column) runs the same kernel with an 8-column tile:
+// every output element is the same chain of the same operands, so
+// apply_block is bit-identical to apply whatever the tile shape.
+//
+// Fragments (PTX m8n8k4 .f64, lane l): A[l/4][l%4] = Theta^T[r + l%4][j + l/4],
+// B[l%4][l/4] = W[r + l%4][c + l/4], D[l/4][2 (l%4) + {0,1}].
+constexpr int kMmaStageRows = 16;
+constexpr int kMmaStages = 3;
+constexpr int kMmaMaxSub = 296;
+
+static int gaussian_nsub(int64_t n) {
+  int64_t p = (n + 31) / 32;
+  p = (p + kSrhtCluster - 1) / kSrhtCluster * kSrhtCluster;
+  if (p > kMmaMaxSub) p = kMmaMaxSub;
+  return (int)p;
+}
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1]) : "d"(a), "d"(b));
+}
+
+template <int WJ, int WC, int TJ, int TC>
+struct MmaTile {
+  static constexpr int kThreads = 32 * WJ * WC;
+  static constexpr int kJ = WJ * TJ * 8;     // Theta rows (j) per CTA
+  static constexpr int kC = WC * TC * 8;     // columns (c) per CTA
+  static constexpr int kAS = kJ + 4;         // padded smem row strides: the 4 rows
+  static constexpr int kBS = kC + 4;         // of a k-step fall in distinct banks
+};
+
+template <typename TX, int WJ, int WC, int TJ, int TC>
+__global__ void __launch_bounds__(32 * WJ * WC)
+dense_mma_kernel(const double* __restrict__ thetaT, int64_t ldt, int k, const TX* __restrict__ X,
+                 int64_t ldx, int ncols, int64_t n, int nsub, double* __restrict__ partials,
+                 const sgs_status* st) {
+  using G = MmaTile<WJ, WC, TJ, TC>;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char mma_raw[];
+  double* As = reinterpret_cast<double*>(mma_raw);                              // S x 16 x kAS
+  TX* Bs = reinterpret_cast<TX*>(As + (size_t)kMmaStages * kMmaStageRows * G::kAS);  // S x 16 x kBS
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wj = warp % WJ, wc = warp / WJ;
+  const int p = blockIdx.x;                       // sub-chunk
+  const int jt = blockIdx.y * G::kJ, ct = blockIdx.z * G::kC;
+  const int64_t r0 = chunk_begin(n, nsub, p), r1 = chunk_begin(n, nsub, p + 1);
+  const int nst = (int)((r1 - r0 + kMmaStageRows - 1) / kMmaStageRows);
+  double acc[TJ][TC][2];
+#pragma unroll
+  for (int a = 0; a < TJ; ++a)
+#pragma unroll
+    for (int b = 0; b < TC; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  // X may be the predecessor kernel's output (a basis column, A q): wait first
+  pdl_enter();
+  const bool stop = status_stopped(st);  // uniform: the cluster still meets at its barriers
+  auto issue = [&](int sidx) {
+    if (sidx < nst) {
+      const int buf = sidx % kMmaStages;
+      const int64_t rs = r0 + (int64_t)sidx * kMmaStageRows;
+      double* Ab = As + (size_t)buf * kMmaStageRows * G::kAS;
+      TX* Bb = Bs + (size_t)buf * kMmaStageRows * G::kBS;
+      for (int e = tid; e < kMmaStageRows * G::kJ / 2; e += G::kThreads) {
+        const int rr = e / (G::kJ / 2), jj = 2 * (e % (G::kJ / 2));
+        const bool ok = rs + rr < r1 && jt + jj < ldt;
+        cp_async_el<16>(Ab + rr * G::kAS + jj, ok ? thetaT + (rs + rr) * ldt + jt + jj : thetaT, ok);
+      }
+      for (int e = tid; e < kMmaStageRows * G::kC; e += G::kThreads) {
+        const int cc = e / kMmaStageRows, rr = e % kMmaStageRows;
+        const bool ok = rs + rr < r1 && ct + cc < ncols;
+        cp_async_el<sizeof(TX)>(Bb + rr * G::kBS + cc,
+                                ok ? X + (int64_t)(ct + cc) * ldx + rs + rr : X, ok);
+      }
+    }
+    cp_async_commit();
+  };
+  if (!stop) {
+#pragma unroll
+    for (int q = 0; q < kMmaStages - 1; ++q) issue(q);
+    for (int sidx = 0; sidx < nst; ++sidx) {
+      cp_async_wait<kMmaStages - 2>();
+      __syncthreads();
+      issue(sidx + kMmaStages - 1);
+      const int buf = sidx % kMmaStages;
+      const double* Ab = As + (size_t)buf * kMmaStageRows * G::kAS;
+      const TX* Bb = Bs + (size_t)buf * kMmaStageRows * G::kBS;
+#pragma unroll
+      for (int ks = 0; ks < kMmaStageRows / 4; ++ks) {  // ascending 4-row k-steps
+        const int rr = 4 * ks + (lane & 3);
+        double a[TJ], b[TC];
+#pragma unroll
+        for (int tj = 0; tj < TJ; ++tj) a[tj] = Ab[rr * G::kAS + (wj * TJ + tj) * 8 + (lane >> 2)];
+#pragma unroll
+        for (int tc = 0; tc < TC; ++tc)
+          b[tc] = (double)Bb[rr * G::kBS + (wc * TC + tc) * 8 + (lane >> 2)];
+#pragma unroll
+        for (int tj = 0; tj < TJ; ++tj)
+#pragma unroll
+          for (int tc = 0; tc < TC; ++tc) dmma(acc[tj][tc], a[tj], b[tc]);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();  // stage buffers free: the output tile aliases them
+  double* Ot = reinterpret_cast<double*>(mma_raw);  // kC x kJ, column c contiguous in j
+#pragma unroll
+  for (int tj = 0; tj < TJ; ++tj)
+#pragma unroll
+    for (int tc = 0; tc < TC; ++tc)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int jl = (wj * TJ + tj) * 8 + (lane >> 2);
+        const int cl_ = (wc * TC + tc) * 8 + 2 * (lane & 3) + h;
+        Ot[cl_ * G::kJ + jl] = acc[tj][tc][h];
+      }
+  cl.sync();
+  if (!stop) {
+    const int rank = (int)cl.block_rank();
+    constexpr int kOut = G::kJ * G::kC;
+    const int e0 = rank * kOut / kSrhtCluster, e1 = (rank + 1) * kOut / kSrhtCluster;
+    const int np2 = nsub / kSrhtCluster, p2 = p / kSrhtCluster;
+    for (int e = e0 + tid; e < e1; e += G::kThreads) {
+      const int cc = e / G::kJ, jj = e % G::kJ;
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < kSrhtCluster; ++q) s += cl.map_shared_rank(Ot, q)[e];
+      if (ct + cc < ncols && jt + jj < k)
+        partials[((int64_t)(ct + cc) * np2 + p2) * k + jt + jj] = s;
+    }
+  }
+  cl.sync();  // the tile stays readable until every CTA of the cluster is done
+}
+
+template <typename TX, int WJ, int WC, int TJ, int TC>
+static int launch_dense_mma_t(const double* thetaT, int64_t ldt, int k, const TX* X, int64_t ldx,
+                              int ncols, int64_t n, double* partials, const sgs_status* st,
+                              cudaStream_t s) {
+  using G = MmaTile<WJ, WC, TJ, TC>;
+  const int nsub = gaussian_nsub(n);
+  const size_t stage = (size_t)kMmaStageRows * G::kAS * sizeof(double) +
+                       (size_t)kMmaStageRows * G::kBS * sizeof(TX);
+  size_t smem = kMmaStages * stage;
+  const size_t otile = (size_t)G::kJ * G::kC * sizeof(double);
+  if (otile > smem) smem = otile;
+  auto kern = dense_mma_kernel<TX, WJ, WC, TJ, TC>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid(nsub, (k + G::kJ - 1) / G::kJ, (ncols + G::kC - 1) / G::kC);
+  return check_ex(launch_ex(kern, grid, dim3(G::kThreads), smem, s, kSrhtCluster, thetaT, ldt, k,
+                            X, ldx, ncols, n, nsub, partials, st),
+                  "dense_mma_kernel");
+}
+
+template <typename TX>
+static int launch_dense_mma(const double* thetaT, int64_t ldt, int k, const void* X, int64_t ldx,
+                            int ncols, int64_t n, double* partials, const sgs_status* st,
+                            cudaStream_t s) {
+  const TX* x = static_cast<const TX*>(X);
+  if (ncols <= 8)  // apply(): 256 (j) x 8 (c) tiles, 8 warps along j
+    return launch_dense_mma_t<TX, 8, 1, 4, 1>(thetaT, ldt, k, x, ldx, ncols, n, partials, st, s);
+  return launch_dense_mma_t<TX, 4, 2, 4, 4>(thetaT, ldt, k, x, ldx, ncols, n, partials, st, s);
+}
+
+// SGS_DENSE_LEGACY=1: the DFMA GEMV / split-K GEMM with 296 partials (A/B)
+static bool dense_legacy() {
+  static const bool v = [] {
+    const char* e = getenv("SGS_DENSE_LEGACY");
+    return e && atoi(e) != 0;
+  }();
+  return v;
+}
 
 template <typename TX>
 static int launch_dense(const double* thetaT, int64_t ldt, int k, const void* X, int64_t ldx,
@@ -705,8 +910,18 @@ extern "C" int sgs_dense_partials(const double* thetaT, int64_t ldt, int k, cons
   SGS_REQUIRE(((uintptr_t)thetaT & 15) == 0, "dense: thetaT must be 16-byte aligned");
   SGS_REQUIRE(x_dtype == SGS_F32 || x_dtype == SGS_F64, "dense: bad dtype");
   cudaStream_t s = as_stream(stream);
+  if (!dense_legacy()) {
+    if (x_dtype == SGS_F32)
+      return launch_dense_mma<float>(thetaT, ldt, k, X, ldx, ncols, n, partials, st, s);
+    return launch_dense_mma<double>(thetaT, ldt, k, X, ldx, ncols, n, partials, st, s);
+  }
   if (x_dtype == SGS_F32) return launch_dense<float>(thetaT, ldt, k, X, ldx, ncols, n, partials, st, s);
   return launch_dense<double>(thetaT, ldt, k, X, ldx, ncols, n, partials, st, s);
+}
+
+extern "C" int sgs_gaussian_nparts(int64_t n) {
+  if (n < 1) return 0;
+  return dense_legacy() ? dense_nparts_host(n) : gaussian_nsub(n) / kSrhtCluster;
 }
 
 static int partials_reduce_impl(const double* partials, int nparts, int k, int ncols,

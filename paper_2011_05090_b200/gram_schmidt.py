@@ -36,7 +36,7 @@ import torch
 from . import _lib
 from ._lib import call, stream_ptr
 from .precision import MIXED32_64, UNIFIED64, PrecisionPolicy
-from .sketch import SketchOperator, as_device_sketch
+from .sketch import SketchKind, SketchOperator, as_device_sketch
 
 __all__ = [
     "GsVariant", "LsqSolver", "HOUSEHOLDER_QR", "QrFactors", "StabilityCertificate",
@@ -204,7 +204,7 @@ class RgsState:
                       and self.row0 % 4096 == 0)
         if self.fused:
             self.nparts_q = int(_lib.load().sgs_column_nparts(self.n_local))
-        elif self.theta.is_gaussian:  # the dense column kernel's own row chunks
+        elif self.theta.is_dense:  # the dense column kernel's own row chunks (Gaussian, Rademacher)
             self.nparts_q = int(_lib.load().sgs_dense_column_nparts(self.n_local, self.k))
         else:
             self.nparts_q = self.nparts
@@ -307,7 +307,14 @@ class RgsState:
         a.Qs, a.Rinv, a.alpha = self._Qs.data_ptr(), self._Rinv.data_ptr(), self._alpha.data_ptr()
         a.scratch, a.r_crs, a.st = self._scratch.data_ptr(), self._rc.data_ptr(), self.status.ptr
         a.trace = self._trace_ptr(fin if fin is not None else sol)
-        if _LS_DEFER:
+        # The fast path publishes r from Pythagorean identities (||t||^2 =
+        # ||s||^2 - sum c1^2, t^T p = s^T p - sum c1_j z_j).  In fp64 they are
+        # as accurate as the explicit dots (c1-shaped mixed emulation: the
+        # same metrics to 1e-16), but with an fp32 LS (UNIFIED32) the t^T p
+        # identity cancels catastrophically once W is numerically rank
+        # deficient (numpy emulation of the acceptance problem: cond(Q) 2.5e7
+        # against 47 with explicit dots and 23 for the reference's Householder).
+        if _LS_DEFER and self.fdt != torch.float32:
             a.t_pend, a.t_coef = self._tpend.data_ptr(), self._tcoef.data_ptr()
         else:
             a.t_pend = a.t_coef = None
@@ -375,6 +382,19 @@ class RgsState:
                  i, w_ptr, w_code, self._rc.data_ptr(), 1 if normalize_prev else 0,
                  self._R.data_ptr(), self._cap, 1 if sketch else 0,
                  d["thetaT"].data_ptr() + self.row0 * d["ldt"] * 8, d["ldt"], self.k,
+                 self._parts_s.data_ptr(), self.status.ptr, stream_ptr())
+            if not sketch:
+                return None
+            if not combine:
+                return self._parts_s.data_ptr(), self.nparts_q, self.theta.scale
+            return self._combine(self._parts_s, self.nparts_q, kvec)
+        if self.theta.kind is SketchKind.RADEMACHER:
+            # fused: q' streamed once, Theta q' from the packed device signs
+            d = self._theta_dev
+            call("sgs_rgs_update_rademacher", self._Q.data_ptr(), self.ccode, self.ldq,
+                 self.n_local, i, w_ptr, w_code, self._rc.data_ptr(), 1 if normalize_prev else 0,
+                 self._R.data_ptr(), self._cap, 1 if sketch else 0,
+                 d["rbits"].data_ptr() + self.row0 * d["kw"] * 4, self.k,
                  self._parts_s.data_ptr(), self.status.ptr, stream_ptr())
             if not sketch:
                 return None
@@ -921,6 +941,7 @@ def sketched_lsq(S_prev, p, solver: LsqSolver = HOUSEHOLDER_QR):
     with torch.cuda.device(dev):
         st.status = _lib.Status(dev)
         st._alloc(i + 2)
+        st._P[0].copy_(cols[0])  # the first finalize takes s'_1 = p_1 (RGS step i == 0)
         for j in range(i):
             st._ls(fin=j, s_parts=cols[j].data_ptr(), s_nparts=1, s_scale=1.0)
         st._ls(sol=i, p_parts=pd.data_ptr(), p_nparts=1, p_scale=1.0)

@@ -191,6 +191,8 @@ class SketchOperator:
     def nparts(self, n_local: int | None = None) -> int:
         n_local = self.n if n_local is None else int(n_local)
         lib = _lib.load()
+        if self.kind is SketchKind.GAUSSIAN:
+            return int(lib.sgs_gaussian_nparts(n_local))
         if self.is_dense:
             return int(lib.sgs_dense_nparts(n_local))
         return int(lib.sgs_srht_nparts(n_local, self.log2_block))

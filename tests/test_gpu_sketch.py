@@ -175,3 +175,37 @@ def test_column_kernel_sketch_equals_stand_alone_sketch(cuda, dt, n, kind):
     torch.cuda.synchronize()
     assert torch.equal(Q[0, :n], w)
     assert torch.equal(pc, ps)
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_batched_tile_sketch_equals_per_column(cuda, dt):
+    """Batches of many columns run the SRHT tile kernel one CTA per 8 tiles
+    (tiles in order, no cluster); single columns run one tile per CTA with a
+    DSMEM cluster sum.  Same partial structure and order: apply_block over 24
+    columns of c1's shape equals 24 apply() calls bit for bit."""
+    n, k, m = 1_000_000, 1500, 24
+    th = sg.make_sketch(sg.SketchKind.PSRHT, k, n, 2)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    X = torch.randn((m, n), dtype=torch.float64, device="cuda", generator=g).to(dt)
+    Y = th.apply_block(X.t())
+    for j in range(m):
+        assert torch.equal(Y[:, j], th.apply(X[j]))
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_gaussian_dmma_batch_equals_per_column(cuda, dt):
+    """The Gaussian P = Theta W on the fp64 tensor cores: the 128 x 64 tile
+    variant (batches) and the 256 x 8 variant (apply) run the same ascending
+    4-row DMMA chains per output - DMMA evaluates its four products as a
+    sequential fma chain (tools/dmma_probe.py) - so apply_block equals apply
+    bit for bit, and both match the oracle's fp64 GEMV to rounding."""
+    n, k, m = 100_000, 600, 20
+    th = sg.make_sketch(sg.SketchKind.GAUSSIAN, k, n, 3)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    X = torch.randn((m, n), dtype=torch.float64, device="cuda", generator=g).to(dt)
+    Y = th.apply_block(X.t())
+    for j in range(m):
+        assert torch.equal(Y[:, j], th.apply(X[j]))
+    orc = OracleSketch("gaussian", k, n, 3)
+    ref = orc.apply(X[0].double().cpu().numpy())
+    assert _relnorm(Y[:, 0].cpu().numpy(), ref) <= 1e-14

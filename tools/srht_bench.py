@@ -64,4 +64,14 @@ x = torch.randn((1, n), dtype=torch.float32, device="cuda", generator=g)
 ms = timed(th, x, _lib.SGS_F32, n, 1, 1, reps=50)
 out["c4_col_us"] = round(1e3 * ms, 2)
 out["c4_gbs"] = round(n * 4 / ms / 1e6, 1)
+del x
+# c0: Gaussian P = Theta W, 300 fp64 columns of 1e5 rows, k = 600 (DMMA, or
+# the DFMA GEMM with SGS_DENSE_LEGACY=1)
+n, m, k = 100_000, 300, 600
+th = sg.make_sketch(sg.SketchKind.GAUSSIAN, k, n, 0)
+W = torch.randn((m, n), dtype=torch.float64, device="cuda", generator=g)
+ms = timed(th, W, _lib.SGS_F64, n, m, m)
+out["c0_pbatch_ms"] = round(ms, 4)
+out["c0_pbatch_tflops"] = round(2.0 * k * n * m / ms / 1e9, 2)
+out["dense_legacy"] = os.environ.get("SGS_DENSE_LEGACY", "0")
 print(json.dumps(out), flush=True)
