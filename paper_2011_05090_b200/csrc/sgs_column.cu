@@ -98,7 +98,8 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
                   const double* __restrict__ R, int64_t ldr, int do_sketch, int64_t row0,
                   int log2_block, const uint32_t* __restrict__ sign_bits,
                   const int32_t* __restrict__ samples, int k, double* __restrict__ partials,
-                  const sgs_status* st, unsigned long long* tl, int pf_cols, int nstages) {
+                  const sgs_status* st, unsigned long long* tl, int pf_cols, int nstages,
+                  int two) {
   cg::cluster_group cl = cg::this_cluster();
   if (tl && threadIdx.x == 0) atomicMin(tl + (int64_t)i * 16 + 0, gtimer());
   constexpr int V = VecT<TQ>::N;                  // rows per vector (4 fp32, 2 fp64)
@@ -190,7 +191,7 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
 #pragma unroll
     for (int v = 0; v < V; ++v) acc[hh][v] = tot[hh][v] = TQ(0);
   auto fold = [&](int j) {
-    if (two_level<TQ>() && ((j + 1) & (kAccBlock - 1)) == 0) {
+    if (sizeof(TQ) == 4 && two && ((j + 1) & (kAccBlock - 1)) == 0) {
 #pragma unroll
       for (int hh = 0; hh < NH; ++hh)
 #pragma unroll
@@ -359,7 +360,7 @@ dense_ring_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
                   const TQ* __restrict__ rc, int normalize_prev, const double* __restrict__ R,
                   int64_t ldr, int do_sketch, const double* __restrict__ thetaT, int64_t ldt,
                   int k, double* __restrict__ partials, int64_t chunk, int stage_bytes,
-                  const sgs_status* st, const uint32_t* __restrict__ rbits, int kw) {
+                  const sgs_status* st, const uint32_t* __restrict__ rbits, int kw, int two) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* ring = smem_raw;  // kDcStages x stage_bytes
   double* xq = reinterpret_cast<double*>(smem_raw + (size_t)kDcStages * stage_bytes);  // chunk
@@ -429,7 +430,7 @@ dense_ring_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
 #pragma unroll
   for (int u = 0; u < kDcMaxRPT; ++u) acc[u] = tot[u] = TQ(0);
   auto fold = [&](int j) {
-    if (two_level<TQ>() && ((j + 1) & (kAccBlock - 1)) == 0) {
+    if (sizeof(TQ) == 4 && two && ((j + 1) & (kAccBlock - 1)) == 0) {
 #pragma unroll
       for (int u = 0; u < kDcMaxRPT; ++u) {
         tot[u] += acc[u];
@@ -454,7 +455,7 @@ dense_ring_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
         const TQ qn = cvt<TQ>((double)*cp / R[(int64_t)jj * ldr + jj]);
         *cp = qn;
         a = fma(qn, rs[jj], a);
-        if (two_level<TQ>() && ((jj + 1) & (kAccBlock - 1)) == 0) {
+        if (sizeof(TQ) == 4 && two && ((jj + 1) & (kAccBlock - 1)) == 0) {
           tt += a;
           a = TQ(0);
         }
@@ -516,18 +517,33 @@ dense_ring_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
     // Theta q' over the chunk's rows with the device-generated signs: per
     // sketch row the chain in ascending row order, acc + (+-x) - i.e.
     // fma(+-1, x, acc), the materialised Gaussian-path arithmetic exactly
-    // (finish_update ended with a block barrier: xq is complete)
-    for (int rr = 0; rr < nr; ++rr) {
-      const double xv = xq[rr];
-      const uint32_t* brow = rbits + (int64_t)(r0 + rr) * kw;
+    // (finish_update ended with a block barrier: xq is complete).  U rows of
+    // sign words are loaded before they are used, so U L2 round trips are in
+    // flight per thread instead of one per row.
+    constexpr int U = QP <= 2 ? 16 : (QP <= 4 ? 8 : 4);
+    for (int rr0 = 0; rr0 < nr; rr0 += U) {
+      uint32_t wd[QP][U];
 #pragma unroll
-      for (int q = 0; q < QP; ++q) {
-        const int jj = tid + q * T;
-        if (2 * jj < k) {
-          const uint32_t word = __ldg(brow + ((2 * jj) >> 5));
-          const int b = (2 * jj) & 31;
-          acc2[q].x += ((word >> b) & 1u) ? xv : -xv;
-          acc2[q].y += ((word >> (b + 1)) & 1u) ? xv : -xv;
+      for (int u = 0; u < U; ++u) {
+        const int rr = rr0 + u;
+#pragma unroll
+        for (int q = 0; q < QP; ++q) {
+          const int jj = tid + q * T;
+          wd[q][u] = (rr < nr && 2 * jj < k)
+                         ? __ldg(rbits + (int64_t)(r0 + rr) * kw + ((2 * jj) >> 5)) : 0u;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int rr = rr0 + u;
+        if (rr < nr) {
+          const double xv = xq[rr];
+#pragma unroll
+          for (int q = 0; q < QP; ++q) {
+            const int b = (2 * (tid + q * T)) & 31;
+            acc2[q].x += ((wd[q][u] >> b) & 1u) ? xv : -xv;
+            acc2[q].y += ((wd[q][u] >> (b + 1)) & 1u) ? xv : -xv;
+          }
         }
       }
     }
@@ -589,7 +605,8 @@ static int launch_dense_ring(void* Q, int64_t ldq, int64_t n, int i, const void*
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
     e = launch_ex(kern, dim3(np), dim3(threads), smem, s, 1, static_cast<TQ*>(Q), ldq, n, i,     \
                   static_cast<const TW*>(w), static_cast<const TQ*>(r_crs), normalize_prev, R,   \
-                  ldr, do_sketch, thetaT, ldt, k, partials, chunk, stage_bytes, st, rbits, kw);  \
+                  ldr, do_sketch, thetaT, ldt, k, partials, chunk, stage_bytes, st, rbits, kw,   \
+                  acc_two<TQ>());                                                                \
   } while (0)
   if (qp <= 1) SGS_DR(1);
   else if (qp <= 2) SGS_DR(2);
@@ -713,7 +730,7 @@ extern "C" int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n,
                     static_cast<TQ*>(Q), ldq, n, i, static_cast<const TW*>(w), w_div,        \
                     static_cast<const TQ*>(r_crs), normalize_prev, R, ldr, do_sketch, row0,  \
                     log2_block, sign_bits, samples, k, partials, st, debug_timeline(), pf,    \
-                    nst);                                                                     \
+                    nst, acc_two<TQ>());                                                      \
   } while (0)
   if (q_dtype == SGS_F32 && w_dtype == SGS_F32) SGS_COL(float, float);
   else if (q_dtype == SGS_F32 && w_dtype == SGS_F64) SGS_COL(float, double);

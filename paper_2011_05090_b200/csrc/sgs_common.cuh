@@ -196,10 +196,11 @@ template <> __device__ __forceinline__ float from_double<float>(double x) { retu
 // reference's OpenBLAS sgemv, whose SIMD dot products split the sum: measured
 // on the oracle at n = 2^18, m = 200 mixed, ||W - QR||/||W|| 2.4e-7 with one
 // chain, 1.06e-7 with blocks of 16, 1.04e-7 with sgemv).  fp64 keeps one chain.
+// SGS_ACC_TWO=0 keeps the single chain for fp32 too (A/B switch); the flag is
+// a kernel argument computed by acc_two<TQ>() on the host.
 constexpr int kAccBlock = 16;
-template <typename TQ> __host__ __device__ constexpr bool two_level() {
-  return sizeof(TQ) == 4;
-}
+bool acc_two_enabled();
+template <typename TQ> inline int acc_two() { return (sizeof(TQ) == 4 && acc_two_enabled()) ? 1 : 0; }
 
 template <typename T> struct VecT;
 template <> struct VecT<float> { using type = float4; static constexpr int N = 4; };

@@ -35,6 +35,15 @@ bool pdl_enabled() {
   return v == 1;
 }
 
+bool acc_two_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SGS_ACC_TWO");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 int sm_count() {
   static int cached = 0;
   if (cached == 0) {

@@ -34,7 +34,7 @@ template <typename TQ, typename TW>
 __global__ void __launch_bounds__(kUpdThreads)
 rgs_update_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* __restrict__ w,
                   const TQ* __restrict__ rc, int normalize_prev, const double* __restrict__ R,
-                  int64_t ldr, const sgs_status* st) {
+                  int64_t ldr, const sgs_status* st, int two) {
   pdl_enter();
   if (status_stopped(st)) return;
   constexpr int V = VecT<TQ>::N;
@@ -49,7 +49,7 @@ rgs_update_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
 #pragma unroll
   for (int v = 0; v < V; ++v) acc[v] = tot[v] = TQ(0);
   auto fold = [&](int j) {
-    if (two_level<TQ>() && ((j + 1) & (kAccBlock - 1)) == 0) {
+    if (sizeof(TQ) == 4 && two && ((j + 1) & (kAccBlock - 1)) == 0) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         tot[v] += acc[v];
@@ -910,7 +910,9 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     tt = bc[2];
     tp = bc[3];
     const T ss = bc[0] / (rT * rT);
-    if (nq > 0 && tt < T(0.5) * ss) {
+    // binary32 LS (UNIFIED32): always the second pass ("twice is enough");
+    // binary64: only on cancellation
+    if (nq > 0 && (sizeof(T) == 4 || tt < T(0.5) * ss)) {
       // cancellation: second classical Gram-Schmidt pass on t
       ls_coldot<T, 1>(TS, nr, 0, nq, vt, nullptr, myR + 8, nullptr);
       xsync();
@@ -1124,7 +1126,7 @@ extern "C" int sgs_rgs_update(void* Q, int q_dtype, int64_t ldq, int64_t n, int 
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
     err = launch_ex(kern, dim3(blocks), dim3(kUpdThreads), smem, s, 1, static_cast<TQ*>(Q),   \
                     ldq, n, i, static_cast<const TW*>(w), static_cast<const TQ*>(r_crs),     \
-                    normalize_prev, R, ldr, st);                                             \
+                    normalize_prev, R, ldr, st, acc_two<TQ>());                              \
   } while (0)
   if (q_dtype == SGS_F32 && w_dtype == SGS_F32) SGS_UPD(float, float);
   else if (q_dtype == SGS_F32 && w_dtype == SGS_F64) SGS_UPD(float, double);

@@ -60,8 +60,16 @@ def init_from_env(backend: str = "nccl") -> TorchComm | None:
     """Initialise the default process group from torchrun's environment
     (RANK / WORLD_SIZE / LOCAL_RANK / MASTER_*); None when WORLD_SIZE <= 1."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world <= 1:
+    if world <= 1 and os.environ.get("SGS_FORCE_COMM", "0") != "1":
         return None
+    if world <= 1:
+        # SGS_FORCE_COMM=1: a one-rank group, so a single GPU runs the sharded
+        # code path with real collectives (NCCL: stream-ordered, captured in
+        # the factorisation's CUDA graph) - a functional check of that path
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
+        os.environ.setdefault("LOCAL_RANK", "0")
+        os.environ.setdefault("MASTER_PORT", str(29400 + os.getpid() % 1000))
     if not dist.is_initialized():
         if backend == "nccl":
             torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))

@@ -68,8 +68,21 @@ class GsVariant(Enum):
 class LsqSolver:
     """Sketched least-squares solver selection (reference gram_schmidt.py:53-77).
 
-    The device implements the direct QR-based solver ("householder" in the
-    reference); the iterative alternatives are outside the B200 hot path."""
+    The device implements the direct QR-based solver, selected by the
+    reference's name "householder" (``HOUSEHOLDER_QR``) so callers keep their
+    arguments.  It is NOT a Householder chain: the reference appends
+    reflectors one column at a time (``_IncrementalHouseholderQR``,
+    gram_schmidt.py:122-190), a serial chain of i dependent reflections per
+    solve.  The device factors the sketched basis S = T diag(alpha)^-1 R_S by
+    classical Gram-Schmidt with selective reorthogonalisation (a second pass
+    only when ||t||^2 < ||s||^2 / 2), keeps R_S^-1 explicitly and solves
+    r = R_S^-1 Q_s^T p, split over a thread-block cluster (sgs_ls_step,
+    DESIGN.md section 3).  Any backward-stable solver meets the RGS analysis
+    (PAPER.md:455-459), and this one is for the well-conditioned S that RGS
+    maintains; the rank test (gram_schmidt.py:186-189) runs on alpha and
+    raises ``np.linalg.LinAlgError`` as the reference does.  ``sketched_lsq``
+    exposes it on an arbitrary S.  The iterative alternatives ("richardson",
+    "smgs") are outside the B200 hot path."""
 
     method: str = "householder"
     iterations: int = 4
@@ -81,7 +94,7 @@ class LsqSolver:
             raise ValueError("richardson needs at least one iteration")
 
 
-HOUSEHOLDER_QR = LsqSolver("householder")
+HOUSEHOLDER_QR = LsqSolver("householder")  # the device QR solver (see LsqSolver)
 
 
 @dataclass
@@ -204,7 +217,8 @@ class RgsState:
                       and self.row0 % 4096 == 0)
         if self.fused:
             self.nparts_q = int(_lib.load().sgs_column_nparts(self.n_local))
-        elif self.theta.is_dense:  # the dense column kernel's own row chunks (Gaussian, Rademacher)
+        elif self.theta.is_gaussian or (self.theta.is_dense and _RAD_FUSED):
+            # the dense column kernel's own row chunks (Gaussian, fused Rademacher)
             self.nparts_q = int(_lib.load().sgs_dense_column_nparts(self.n_local, self.k))
         else:
             self.nparts_q = self.nparts
@@ -388,7 +402,7 @@ class RgsState:
             if not combine:
                 return self._parts_s.data_ptr(), self.nparts_q, self.theta.scale
             return self._combine(self._parts_s, self.nparts_q, kvec)
-        if self.theta.kind is SketchKind.RADEMACHER:
+        if self.theta.kind is SketchKind.RADEMACHER and _RAD_FUSED:
             # fused: q' streamed once, Theta q' from the packed device signs
             d = self._theta_dev
             call("sgs_rgs_update_rademacher", self._Q.data_ptr(), self.ccode, self.ldq,
@@ -593,9 +607,30 @@ class RgsState:
                 self.comm.allreduce_(kbuf[:nc])
                 call("sgs_partials_reduce", kbuf.data_ptr(), 1, k, nc, self.theta.scale,
                      pdst, self.fcode, k, self.status.ptr, sp)
-        if self.phi is not None:  # P_phi = Phi W, column by column
-            for j in range(m):
-                self._phi_w(j, base + j * ldw * esz, wc, ldw)
+        if self.phi is not None:  # P_phi = Phi W, batched like P (same bits as per column)
+            ph, kp_ = self.phi, self.phi.k
+            np_phi = (self.nparts_phi if self.comm is None
+                      else max(self.nparts_phi, ph.nparts(self.n)))
+            chp = max(1, min(m, (128 << 20) // max(1, np_phi * kp_ * 8)))
+            pparts = torch.empty((chp, self.nparts_phi, kp_), dtype=torch.float64,
+                                 device=self.device)
+            if self.comm is not None:
+                kbp = torch.empty((chp, kp_), dtype=torch.float64, device=self.device)
+            for c0 in range(0, m, chp):
+                nc = min(chp, m - c0)
+                ph.partials_into(base + c0 * ldw * esz, wc, ldw, nc, pparts,
+                                 n_local=self.n_local, row0=self.row0, status=self.status)
+                pdst = self._P_phi.data_ptr() + c0 * kp_ * self._P_phi.element_size()
+                if self.comm is None:
+                    call("sgs_partials_reduce", pparts.data_ptr(), self.nparts_phi, kp_, nc,
+                         ph.scale, pdst, self.fcode, kp_, self.status.ptr, sp)
+                else:
+                    call("sgs_partials_reduce", pparts.data_ptr(), self.nparts_phi, kp_, nc, 1.0,
+                         kbp.data_ptr(), _lib.SGS_F64, kp_, self.status.ptr, sp)
+                    self.comm.allreduce_(kbp[:nc])
+                    call("sgs_partials_reduce", kbp.data_ptr(), 1, kp_, nc, ph.scale, pdst,
+                         self.fcode, kp_, self.status.ptr, sp)
+            self._keep_phi = pparts
         for i in range(m):
             sol = i + 1 if i + 1 < m else None
             if i == 0:
@@ -778,6 +813,15 @@ class RgsState:
 _PINNED_POOL: list = []
 
 
+# SGS_RAD_FUSED=1: Rademacher states use the fused column kernel
+# (sgs_rgs_update_rademacher: one pass, q' never re-read).  Off by default: at
+# c0r's shapes it measured 9957 columns/s against 12047 for the generic update
+# + packed-sign sketch pair - the +-1 GEMV is compute-bound (k n signed adds
+# per column) and runs after the Q stream inside each of the fused kernel's
+# CTAs, while the separate sketch kernel runs it at full occupancy; the q'
+# re-read it saves is an L2 hit.
+_RAD_FUSED = os.environ.get("SGS_RAD_FUSED", "0") == "1"
+
 # SGS_LS_DEFER=0 forms every T column inside its own finalize (A/B switch)
 _LS_DEFER = os.environ.get("SGS_LS_DEFER", "1") != "0"
 
@@ -942,8 +986,15 @@ def sketched_lsq(S_prev, p, solver: LsqSolver = HOUSEHOLDER_QR):
         st.status = _lib.Status(dev)
         st._alloc(i + 2)
         st._P[0].copy_(cols[0])  # the first finalize takes s'_1 = p_1 (RGS step i == 0)
+        # An LS launch reads the LS state (T, alpha, R_S^-1, status) before its
+        # programmatic-dependent-launch wait: in the factorizer a column or
+        # sketch kernel always separates two LS launches.  Back to back, a
+        # plain (non-PDL) kernel in between keeps the next launch from
+        # starting before the previous one has finished.
+        fence = torch.zeros(1, dtype=torch.int32, device=dev)
         for j in range(i):
             st._ls(fin=j, s_parts=cols[j].data_ptr(), s_nparts=1, s_scale=1.0)
+            fence.add_(1)
         st._ls(sol=i, p_parts=pd.data_ptr(), p_nparts=1, p_scale=1.0)
         res = st.status.read()
     if res["code"] in (_lib.ST_RANK, _lib.ST_BREAKDOWN):
