@@ -99,3 +99,58 @@ def test_two_rank_sharded_rgs_matches_unsharded():
     assert rel(Q, ref["Q"]) < 1e-12
     assert rel(out[0][3], ref["R"]) < 1e-12
     assert rel(out[0][4], ref["S"]) < 1e-12
+
+
+class _StubBlock:
+    """Stands in for the device row block (the halo test moves vectors only)."""
+
+    def __init__(self, *a, **kw):
+        pass
+
+
+def _halo_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # a subgroup that excludes global rank 0: group ranks 0, 1, 2 are global
+    # ranks 1, 2, 3, so a peer passed as a global rank would reach the wrong
+    # process (advisor finding on krylov.py's halo P2POps)
+    grp = dist.new_group([1, 2, 3])
+    if rank != 0:
+        from paper_2011_05090_b200 import krylov
+        krylov._RowBlock = _StubBlock
+        n = 6144
+        # 1-D three-point stencil: each shard's rows touch one row of each neighbour
+        rp = np.zeros(n + 1, dtype=np.int64)
+        cols = []
+        for i in range(n):
+            row = [j for j in (i - 1, i, i + 1) if 0 <= j < n]
+            cols += row
+            rp[i + 1] = len(cols)
+        A = krylov.SparseMatrix(n=n, row_ptr=rp, col_idx=np.asarray(cols, dtype=np.int64),
+                                values=np.ones(len(cols)))
+        comm = TorchComm(grp)
+        d = krylov._Dist(comm, A, 1024, "cpu")
+        x = torch.arange(n, dtype=torch.float64) * 0.5 + 1.0
+        buf, _ = d.window(x[d.row0:d.row0 + d.n_loc].clone())
+        full = d.full(x[d.row0:d.row0 + d.n_loc].clone())
+        out[rank] = (d.halo, d.wlo, d.whi, buf.numpy().copy(),
+                     bool(torch.equal(full, x)), comm.rank)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_halo_exchange_in_a_subgroup():
+    world = 4
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_halo_worker, args=(world, port, out), nprocs=world, join=True)
+    x = np.arange(6144, dtype=np.float64) * 0.5 + 1.0
+    for g in (1, 2, 3):
+        halo, wlo, whi, buf, full_ok, grank = out[g]
+        assert grank == g - 1
+        assert halo, "the 3-point stencil's windows are narrow: halo path expected"
+        assert np.array_equal(buf, x[wlo:whi]), g
+        assert full_ok
+    assert (out[1][1], out[1][2]) == (0, 2049)
+    assert (out[2][1], out[2][2]) == (2047, 4097)
