@@ -80,6 +80,21 @@ class Clocks:
                 "reasons": sorted(reasons)}
 
 
+def _traffic(cfg_name):
+    """(DRAM bytes of one launch of the dominant kernel from the committed ncu
+    --set full capture, note) for a config, or (None, None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as fh:
+            tj = json.load(fh).get(cfg_name)
+    except (OSError, ValueError):
+        tj = None
+    if not tj:
+        return None, None
+    return tj["dram_bytes"], (f"ncu --set full, {tj['kernel']} at column {tj['column']}: "
+                              f"{tj['dram_bytes']:.4g} B DRAM vs {tj['alg_bytes']:.4g} B "
+                              f"algorithmic ({tj['source']})")
+
+
 def qr_alg_bytes(n, m, bq, bw, k=0, gaussian=False):
     """n b_Q m(m+1)/2 + 2 n b_W m (+ (m+1) k n 8 for Gaussian)."""
     b = n * bq * m * (m + 1) / 2 + 2 * n * bw * m
@@ -416,15 +431,7 @@ def run_qr(args, cfg_name, comm):
             tot_b += sum(k * n_loc // 8 + n_loc * bq for i, _, _ in evs if i > 0)
         ach = tot_b / (tot_ms / 1e3) / 1e9
         traffic, traffic_note = None, None
-        try:
-            with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
-                tj = json.load(fh)
-            if tj.get("config") == cfg_name:
-                traffic = tj["dram_bytes"]
-                traffic_note = (f"ncu --set full, column {tj['column']}: {tj['dram_bytes']:.4g} B "
-                                f"DRAM vs {tj['alg_bytes']:.4g} B algorithmic ({tj['source']})")
-        except Exception:
-            pass
+        traffic, traffic_note = _traffic(cfg_name)
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "frac_nominal_8tbs": round(ach / 8000.0, 4),
                 "traffic": traffic, "traffic_note": traffic_note,
@@ -616,7 +623,7 @@ def run_gmres(args):
     f64_ms = out["f64"]["ms_per_solve"]
     roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
             "frac": round(ach / peak, 4), "frac_nominal_8tbs": round(ach / 8000.0, 4),
-            "traffic": None,
+            "traffic": _traffic("c3")[0], "traffic_note": _traffic("c3")[1],
             "kernel": "rgs_column_kernel (Q stream + SRHT epilogue), fp64 basis",
             "peak_source": peak_kind, "share_of_step": round(tot_ms / f64_ms, 4),
             "launches": len(evs), "avg_launch_us": round(1e3 * tot_ms / len(evs), 2),

@@ -88,6 +88,18 @@ int sgs_srht_partials(const void* X, int x_dtype, int64_t ldx, int ncols,
                       int64_t n_local, int64_t row0, int log2_block,
                       const uint32_t* sign_bits, const int32_t* samples, int k,
                       double* partials, const sgs_status* st, void* stream);
+/* Two SRHT-kind sketches of the same columns in one pass (the P batch of
+ * rgs_factorize with a certification sketch Phi: P = Theta W and
+ * P_phi = Phi W, gram_schmidt.py:303-305 per column).  Both need 4096-row
+ * tiles (log2 blocks >= 12); each partials array equals sgs_srht_partials'
+ * of its sketch bit for bit.  W is read from HBM once; the second transform
+ * re-reads each tile from L1/L2. */
+int sgs_srht_partials_pair(const void* X, int x_dtype, int64_t ldx, int ncols,
+                           int64_t n_local, int64_t row0, int log2_block,
+                           const uint32_t* sign_bits, const int32_t* samples, int k,
+                           double* partials, int log2_block2, const uint32_t* sign_bits2,
+                           const int32_t* samples2, int k2, double* partials2,
+                           const sgs_status* st, void* stream);
 
 /* Dense sketch (Gaussian, absent from the reference's SketchKind; duck-typed
  * in through sketch.py:120-206; a column block sketched as the dense
@@ -178,6 +190,20 @@ int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
                         int do_sketch, int64_t row0, int log2_block,
                         const uint32_t* sign_bits, const int32_t* samples, int k,
                         double* partials, const sgs_status* st, void* stream);
+/* sgs_rgs_update_srht with the certification sketch Phi of q' in the same
+ * epilogue (reference RgsState.push, gram_schmidt.py:333-335: S_phi gets
+ * Phi q'_i / r_ii).  Phi must be a P-SRHT / block-SRHT with log2 block >= 12
+ * (4096-row tiles); phi_partials receives sgs_column_nparts(n) kphi-vectors,
+ * bit-identical to sgs_srht_partials of Q[:, i] with Phi.  do_sketch must be
+ * set.  phi_partials == NULL is sgs_rgs_update_srht. */
+int sgs_rgs_update_srht_phi(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
+                            const void* w, int w_dtype, const double* w_div /* nullable */,
+                            const void* r_crs, int normalize_prev, const double* R, int64_t ldr,
+                            int do_sketch, int64_t row0, int log2_block,
+                            const uint32_t* sign_bits, const int32_t* samples, int k,
+                            double* partials, const uint32_t* phi_sign_bits,
+                            const int32_t* phi_samples, int kphi, int phi_log2_block,
+                            double* phi_partials, const sgs_status* st, void* stream);
 
 /* Fused column kernel for dense sketches: sgs_rgs_update over the row chunks
  * of sgs_dense_partials, q' kept in shared memory, then (do_sketch != 0) the

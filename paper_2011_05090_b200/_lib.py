@@ -81,6 +81,14 @@ _SIGS = {
     "sgs_rgs_update_srht": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_void_p, c_int,
                                     c_void_p, c_void_p, c_int, c_void_p, c_int64, c_int, c_int64, c_int,
                                     c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
+    "sgs_srht_partials_pair": (c_int, [c_void_p, c_int, c_int64, c_int, c_int64, c_int64, c_int,
+                                       c_void_p, c_void_p, c_int, c_void_p, c_int, c_void_p,
+                                       c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
+    "sgs_rgs_update_srht_phi": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_void_p, c_int,
+                                        c_void_p, c_void_p, c_int, c_void_p, c_int64, c_int,
+                                        c_int64, c_int, c_void_p, c_void_p, c_int, c_void_p,
+                                        c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p,
+                                        c_void_p]),
     "sgs_rgs_update_dense": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_void_p, c_int,
                                      c_void_p, c_int, c_void_p, c_int64, c_int, c_void_p,
                                      c_int64, c_int, c_void_p, c_void_p, c_void_p]),
@@ -153,6 +161,11 @@ def load(path: str = LIB_PATH):
 
 def lib():
     return load()
+
+
+def srht_legacy() -> bool:
+    """SGS_SRHT_LEGACY=1: the library's three-pass SRHT kernel (no pair kernel)."""
+    return os.environ.get("SGS_SRHT_LEGACY", "0") not in ("", "0")
 
 
 def require_cuda():

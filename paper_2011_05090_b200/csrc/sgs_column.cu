@@ -90,7 +90,18 @@ __host__ __device__ constexpr size_t col_ring_bytes(int stages) {
              : (size_t)(kColT + kColT / 8 + 8) * 8;
 }
 
-template <typename TQ, typename TW>
+// Certification sketch Phi (gram_schmidt.py:333-335) in the same epilogue when
+// it is a P-SRHT / block-SRHT with 4096-row tiles: the tile of q' is still in
+// registers, so Phi q' costs a second transform and gather, no re-read of q'.
+struct ColPhi {
+  const uint32_t* sign_bits;  // Phi's sign bitmask, offset to this shard's first row
+  const int32_t* samples;     // (nblocks, kphi) block-local sample rows
+  int k;
+  int log2_block;
+  double* partials;           // one kphi-vector per 8-CTA cluster
+};
+
+template <typename TQ, typename TW, bool PHI>
 __global__ void __launch_bounds__(kColThreads, 2)
 rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
                   const TW* __restrict__ w, const double* __restrict__ w_div,
@@ -99,7 +110,7 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
                   int log2_block, const uint32_t* __restrict__ sign_bits,
                   const int32_t* __restrict__ samples, int k, double* __restrict__ partials,
                   const sgs_status* st, unsigned long long* tl, int pf_cols, int nstages,
-                  int two) {
+                  int two, ColPhi phi) {
   cg::cluster_group cl = cg::this_cluster();
   if (tl && threadIdx.x == 0) atomicMin(tl + (int64_t)i * 16 + 0, gtimer());
   constexpr int V = VecT<TQ>::N;                  // rows per vector (4 fp32, 2 fp64)
@@ -110,7 +121,10 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
   double* z = reinterpret_cast<double*>(smem_raw);                   // aliases the ring
   double* part = reinterpret_cast<double*>(smem_raw + col_ring_bytes<TQ>(S));  // k
   int32_t* smp = reinterpret_cast<int32_t*>(part + k);               // k
-  TQ* rs = reinterpret_cast<TQ*>(smp + k + (k & 1));                 // i coefficients
+  double* part2 = reinterpret_cast<double*>(smp + k + (k & 1));      // PHI: phi.k
+  int32_t* smp2 = reinterpret_cast<int32_t*>(part2 + (PHI ? phi.k : 0));  // PHI: phi.k
+  TQ* rs = PHI ? reinterpret_cast<TQ*>(smp2 + phi.k + (phi.k & 1))
+               : reinterpret_cast<TQ*>(smp + k + (k & 1));           // i coefficients
   __shared__ uint64_t mbar[kColMaxStages];
 
   const int tid = threadIdx.x;
@@ -133,6 +147,10 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
   if (do_sketch && active) {
     const int32_t* sb = samples + blk * (int64_t)k;
     for (int j = tid; j < k; j += blockDim.x) smp[j] = __ldg(sb + j);
+    if constexpr (PHI) {
+      const int32_t* sb2 = phi.samples + (g0 >> phi.log2_block) * (int64_t)phi.k;
+      for (int j = tid; j < phi.k; j += blockDim.x) smp2[j] = __ldg(sb2 + j);
+    }
   }
   __syncthreads();
   // Columns 0..i-2 of Q were finalised by the column kernel before the
@@ -306,6 +324,40 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
   } else {
     for (int j = tid; j < k; j += blockDim.x) part[j] = 0.0;
   }
+  if constexpr (PHI) {
+    // Phi q': the same tile from registers with Phi's signs (x = xs * s_theta,
+    // so the flip is s_theta XOR s_phi), the same four passes, Phi's samples
+    if (active) {
+      __syncthreads();  // every thread has gathered Theta's rows from z
+      const int64_t hp = (g0 & ((int64_t(1) << phi.log2_block) - 1)) >> kColLogT;
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh) {
+        const uint32_t wt = (rows[hh] < n) ? __ldg(sign_bits + (rows[hh] >> 5)) : 0u;
+        const uint32_t wp = (rows[hh] < n) ? __ldg(phi.sign_bits + (rows[hh] >> 5)) : 0u;
+        const uint32_t flip = wt ^ wp;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const double x = xs[hh * V + v];
+          z[pidx(hh * (kColThreads * V) + tid * V + v)] =
+              ((flip >> ((rows[hh] + v) & 31)) & 1u) ? -x : x;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int b0 : {6, 9, 0, 3}) {
+        fwht_pass<kColLogT, 3>(z, b0);
+        __syncthreads();
+      }
+      for (int j = tid; j < phi.k; j += blockDim.x) {
+        const int32_t r = smp2[j];
+        const double v = z[pidx(r & (kColT - 1))];
+        const int64_t rh = (int64_t)(r >> kColLogT);
+        part2[j] = (__popcll(rh & hp) & 1) ? -v : v;
+      }
+    } else {
+      for (int j = tid; j < phi.k; j += blockDim.x) part2[j] = 0.0;
+    }
+  }
   cl.sync();
   const int rank = (int)cl.block_rank();
   const int j0 = (int)(((int64_t)rank * k) / kColCluster);
@@ -316,6 +368,17 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
 #pragma unroll
     for (int q = 0; q < kColCluster; ++q) s += cl.map_shared_rank(part, q)[j];
     outp[j] = s;
+  }
+  if constexpr (PHI) {
+    const int p0 = (int)(((int64_t)rank * phi.k) / kColCluster);
+    const int p1 = (int)(((int64_t)(rank + 1) * phi.k) / kColCluster);
+    double* outq = phi.partials + (int64_t)(blockIdx.x / kColCluster) * phi.k;
+    for (int j = p0 + tid; j < p1; j += blockDim.x) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < kColCluster; ++q) s += cl.map_shared_rank(part2, q)[j];
+      outq[j] = s;
+    }
   }
   cl.sync();
   if (tl && threadIdx.x == 0) atomicMax(tl + (int64_t)i * 16 + 2, gtimer());
@@ -680,13 +743,19 @@ extern "C" int sgs_column_nparts(int64_t n_local) {
   return n_local < 1 ? 0 : (int)(column_ctas(n_local) / kColCluster);
 }
 
-extern "C" int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
-                                   const void* w, int w_dtype, const double* w_div,
-                                   const void* r_crs, int normalize_prev, const double* R,
-                                   int64_t ldr, int do_sketch, int64_t row0, int log2_block,
-                                   const uint32_t* sign_bits, const int32_t* samples, int k,
-                                   double* partials, const sgs_status* st, void* stream) {
+static int update_srht_impl(void* Q, int q_dtype, int64_t ldq, int64_t n, int i, const void* w,
+                             int w_dtype, const double* w_div, const void* r_crs,
+                             int normalize_prev, const double* R, int64_t ldr, int do_sketch,
+                             int64_t row0, int log2_block, const uint32_t* sign_bits,
+                             const int32_t* samples, int k, double* partials,
+                             const uint32_t* phi_sign_bits, const int32_t* phi_samples, int kphi,
+                             int phi_log2_block, double* phi_partials,
+                             const sgs_status* st, void* stream) {
   SGS_REQUIRE(Q && w, "update_srht: null pointer");
+  const bool use_phi = phi_partials != nullptr;
+  SGS_REQUIRE(!use_phi || (do_sketch && phi_sign_bits && phi_samples && kphi >= 1 &&
+                           kphi <= 8192 && phi_log2_block >= kColLogT),
+              "update_srht: certification sketch arguments (P-SRHT, 4096-row tiles)");
   SGS_REQUIRE(i >= 0 && n >= 1 && ldq >= n && (ldq % 4) == 0, "update_srht: bad sizes");
   SGS_REQUIRE(i == 0 || r_crs, "update_srht: r_crs required for i > 0");
   SGS_REQUIRE(!normalize_prev || (i > 0 && R), "update_srht: normalize_prev needs R, i > 0");
@@ -699,6 +768,7 @@ extern "C" int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n,
   const int64_t nctas = column_ctas(n);
   const int esz = q_dtype == SGS_F32 ? 4 : 8;
   const size_t rest = (size_t)k * sizeof(double) + (size_t)(k + 1) * sizeof(int32_t) + 8 +
+                      (use_phi ? (size_t)kphi * sizeof(double) + (size_t)(kphi + 1) * 4 : 0) +
                       (size_t)(i > 0 ? i : 1) * esz;
   int nst = q_dtype == SGS_F32 ? ColCfg<float>::kStages : ColCfg<double>::kStages;
   auto ring_of = [&](int st_) {
@@ -722,15 +792,16 @@ extern "C" int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n,
                                   : (int)std::min<int64_t>(kColThreads - 32,
                                                            col_pf_bytes() / (nctas * kColT * esz));
   cudaError_t err = cudaSuccess;
+  const ColPhi phi{phi_sign_bits, phi_samples, use_phi ? kphi : 0, phi_log2_block, phi_partials};
 #define SGS_COL(TQ, TW)                                                                       \
   do {                                                                                        \
-    auto kern = rgs_column_kernel<TQ, TW>;                                                    \
+    auto kern = use_phi ? rgs_column_kernel<TQ, TW, true> : rgs_column_kernel<TQ, TW, false>; \
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
     err = launch_ex(kern, dim3((unsigned)nctas), dim3(kColThreads), smem, s, kColCluster,     \
                     static_cast<TQ*>(Q), ldq, n, i, static_cast<const TW*>(w), w_div,        \
                     static_cast<const TQ*>(r_crs), normalize_prev, R, ldr, do_sketch, row0,  \
                     log2_block, sign_bits, samples, k, partials, st, debug_timeline(), pf,    \
-                    nst, acc_two<TQ>());                                                      \
+                    nst, acc_two<TQ>(), phi);                                                 \
   } while (0)
   if (q_dtype == SGS_F32 && w_dtype == SGS_F32) SGS_COL(float, float);
   else if (q_dtype == SGS_F32 && w_dtype == SGS_F64) SGS_COL(float, double);
@@ -742,4 +813,30 @@ extern "C" int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n,
   }
 #undef SGS_COL
   return check_ex(err, "rgs_column_kernel");
+}
+
+extern "C" int sgs_rgs_update_srht_phi(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
+                                       const void* w, int w_dtype, const double* w_div,
+                                       const void* r_crs, int normalize_prev, const double* R,
+                                       int64_t ldr, int do_sketch, int64_t row0, int log2_block,
+                                       const uint32_t* sign_bits, const int32_t* samples, int k,
+                                       double* partials, const uint32_t* phi_sign_bits,
+                                       const int32_t* phi_samples, int kphi, int phi_log2_block,
+                                       double* phi_partials, const sgs_status* st,
+                                       void* stream) {
+  return update_srht_impl(Q, q_dtype, ldq, n, i, w, w_dtype, w_div, r_crs, normalize_prev, R, ldr,
+                          do_sketch, row0, log2_block, sign_bits, samples, k, partials,
+                          phi_sign_bits, phi_samples, kphi, phi_log2_block, phi_partials, st,
+                          stream);
+}
+
+extern "C" int sgs_rgs_update_srht(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
+                                   const void* w, int w_dtype, const double* w_div,
+                                   const void* r_crs, int normalize_prev, const double* R,
+                                   int64_t ldr, int do_sketch, int64_t row0, int log2_block,
+                                   const uint32_t* sign_bits, const int32_t* samples, int k,
+                                   double* partials, const sgs_status* st, void* stream) {
+  return sgs_rgs_update_srht_phi(Q, q_dtype, ldq, n, i, w, w_dtype, w_div, r_crs, normalize_prev,
+                                 R, ldr, do_sketch, row0, log2_block, sign_bits, samples, k,
+                                 partials, nullptr, nullptr, 0, 0, nullptr, st, stream);
 }

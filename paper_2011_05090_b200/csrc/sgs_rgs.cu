@@ -464,9 +464,20 @@ __device__ __noinline__ void ls_reduce_parts(const double* parts, int nparts, in
         acc1 += b[u];
       }
     }
-    for (; q < nparts; q += kCanonG) {
-      if (ok0) acc0 += __ldcg(p0 + (int64_t)q * k);
-      if (ok1) acc1 += __ldcg(p1 + (int64_t)q * k);
+    {  // the < 8 remaining terms of each chain: all loads in flight, then added in order
+      double a[8], b[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool in = q + u * kCanonG < nparts;
+        a[u] = (ok0 && in) ? __ldcg(p0 + (int64_t)(q + u * kCanonG) * k) : 0.0;
+        b[u] = (ok1 && in) ? __ldcg(p1 + (int64_t)(q + u * kCanonG) * k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (q + u * kCanonG < nparts) {
+          acc0 += a[u];
+          acc1 += b[u];
+        }
     }
     __syncthreads();
     red[g * 128 + rl] = acc0;
@@ -496,10 +507,20 @@ __device__ __noinline__ void ls_reduce_parts2(const double* pa, int na, double s
     if (rr < nr) {
       const double* p = pa + ra + rr;
       const double* q = pb + ra + rr;
-#pragma unroll 8
-      for (int j = g; j < nmax; j += kCanonG) {
-        if (j < na) acc_a += __ldcg(p + (int64_t)j * k);
-        if (j < nb) acc_b += __ldcg(q + (int64_t)j * k);
+      for (int j0 = g; j0 < nmax; j0 += 8 * kCanonG) {  // 8 terms per chain in flight
+        double x[8], y[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int j = j0 + u * kCanonG;
+          x[u] = j < na ? __ldcg(p + (int64_t)j * k) : 0.0;
+          y[u] = j < nb ? __ldcg(q + (int64_t)j * k) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int j = j0 + u * kCanonG;
+          if (j < na) acc_a += x[u];
+          if (j < nb) acc_b += y[u];
+        }
       }
     }
     __syncthreads();
@@ -625,8 +646,8 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   const int CL = (int)cl.num_blocks();
 #define xsync() cl.sync()
   const int k = a.k, cap = a.cap;
-  const int ra = (int)(((int64_t)rank * k) / CL);
-  const int rb = (int)(((int64_t)(rank + 1) * k) / CL);
+  const int ra = (rank * k) / CL;  // k <= 65536, CL <= 16: int32 arithmetic
+  const int rb = ((rank + 1) * k) / CL;
   const int nr = rb - ra;
   const int RM = (k + CL - 1) / CL;
   const bool fused = a.do_finalize && a.do_solve;
@@ -670,8 +691,8 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     if (trc) trc[ix] = clock64(); \
   } while (0)
   auto slice = [&](int n, int& o0, int& o1) {
-    o0 = (int)(((int64_t)rank * n) / CL);
-    o1 = (int)(((int64_t)(rank + 1) * n) / CL);
+    o0 = (rank * n) / CL;  // n <= 8192
+    o1 = ((rank + 1) * n) / CL;
   };
 
   // ---- before the dependency wait -------------------------------------------------
@@ -811,6 +832,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     if (nq > 0) ls_gather<T>(XA + 8, sA, CL, 0, nq, AL, c1, to);  // T^T s' / alpha; to = alpha
     if (lag && nq > 0) ls_gather<T>(XA + 8 + cap, sA, CL, 0, nq, AL, zc);  // T^T p' / alpha
     __syncthreads();
+    SGS_TR(5);
     const double r_ii = (double)sqrt(bc[0]);
     const double tol = a.bf_ucrs * (double)sqrt(bc[1]);
     if (r_ii <= tol) {  // NaN compares false and propagates, as in numpy (gram_schmidt.py:325)
@@ -853,6 +875,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
       c2[j] = cj / to[j];            // coefficient on the unnormalised column T_j (to = alpha)
     }
     __syncthreads();
+    SGS_TR(6);
     // Fast path: Q_s = T diag(1/alpha) is orthonormal, so ||t||^2 = ||s||^2 -
     // sum_j c1_j^2 and t^T p = s^T p - sum_j c1_j zc_j (zc = Q_s^T p from before
     // the wait).  Every CTA evaluates them from identical gathered values in

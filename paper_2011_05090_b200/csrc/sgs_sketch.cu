@@ -184,40 +184,62 @@ constexpr int kTileThreads = 64;
 constexpr int kTileBuf = 4096 + 64;  // xidx(4096)
 __device__ __forceinline__ int xidx(int e) { return e + (e >> 6); }
 
-template <typename TX, bool CLUSTERED>
+// A second SRHT-kind sketch with the same tile structure (the certification
+// sketch Phi of the P batch, gram_schmidt.py:304-305): each tile is
+// transformed a second time with Phi's signs and samples after Theta's gather,
+// its values re-read from L1/L2 (not HBM) by the thread that just loaded them.
+struct SrhtSecond {
+  const uint32_t* sign_bits;
+  const int32_t* samples;
+  int k;
+  int log2_block;
+  double* partials;
+};
+
+template <typename TX, bool CLUSTERED, bool PAIR>
 __global__ void __launch_bounds__(kTileThreads)
 srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t row0,
                  int log2_block, const uint32_t* __restrict__ sign_bits,
                  const int32_t* __restrict__ samples, int k, int tiles_per_cta, int64_t ntiles,
-                 double* __restrict__ partials, const sgs_status* st, unsigned long long* tl) {
+                 double* __restrict__ partials, const sgs_status* st, unsigned long long* tl,
+                 SrhtSecond b2) {
   constexpr int LOGT = 12, T = 1 << LOGT;
   extern __shared__ double smem[];
   double* buf = smem;                                  // xidx(T) entries
   double* part = smem + kTileBuf;                      // k entries
   int32_t* smp = reinterpret_cast<int32_t*>(part + k);  // k entries
+  double* part2 = reinterpret_cast<double*>(smp + k + (k & 1));  // PAIR: b2.k
+  int32_t* smp2 = reinterpret_cast<int32_t*>(part2 + (PAIR ? b2.k : 0));
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
   const int col = blockIdx.y;
   const TX* x = X + (int64_t)col * ldx;
   const int64_t t0 = (int64_t)blockIdx.x * tiles_per_cta;
   const int64_t t1 = min(t0 + tiles_per_cta, ntiles);
-  const int64_t bmask = (int64_t(1) << log2_block) - 1;
   // the operator does not depend on the predecessor: k-vector and first
   // sample set before the dependency wait
   for (int j = t; j < k; j += kTileThreads) part[j] = 0.0;
-  int64_t cur_blk = -1;
+  if constexpr (PAIR)
+    for (int j = t; j < b2.k; j += kTileThreads) part2[j] = 0.0;
+  int64_t cur_blk = -1, cur_blk2 = -1;
   if (t0 < t1) {
     cur_blk = (row0 + t0 * T) >> log2_block;
     const int32_t* sb = samples + cur_blk * (int64_t)k;
     for (int j = t; j < k; j += kTileThreads) smp[j] = __ldg(sb + j);
+    if constexpr (PAIR) {
+      cur_blk2 = (row0 + t0 * T) >> b2.log2_block;
+      const int32_t* sb2 = b2.samples + cur_blk2 * (int64_t)b2.k;
+      for (int j = t; j < b2.k; j += kTileThreads) smp2[j] = __ldg(sb2 + j);
+    }
   }
   pdl_enter();
   if (status_stopped(st)) return;  // uniform across the cluster
   if (tl && t == 0) atomicMin(tl + 12, gtimer());
-  for (int64_t ti = t0; ti < t1; ++ti) {
-    const int64_t lr0 = ti * T;
+  // one sketch of the tile at lr0: load (signs on load), bits 6..11 in
+  // registers, one exchange, bits 0..5, gather the sampled rows into acc
+  auto tile = [&](int64_t lr0, const uint32_t* __restrict__ bits, int lb, const int32_t* sm,
+                  int kk, double* acc) {
     const int64_t g0 = row0 + lr0;
-    const int64_t blk = g0 >> log2_block;
-    const int64_t h = (g0 & bmask) >> LOGT;
+    const int64_t h = (g0 & ((int64_t(1) << lb) - 1)) >> LOGT;
     double v[64];
     if (lr0 + T <= n_local) {
 #pragma unroll
@@ -230,7 +252,7 @@ srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t
       }
     }
     // sign word of element t + 64 j: (lr0 + 64 j + 32 w) / 32, warp-uniform
-    const uint32_t* sw = sign_bits + (lr0 >> 5) + w;
+    const uint32_t* sw = bits + (lr0 >> 5) + w;
 #pragma unroll
     for (int j = 0; j < 64; ++j) {
       const bool in = lr0 + 64 * j + 32 * w < n_local;
@@ -238,12 +260,7 @@ srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t
       if (((word >> lane) & 1u) == 0u) v[j] = -v[j];
     }
     fwht_reg<6>(v);                       // bits 6..11
-    __syncthreads();                      // previous tile's gather has read buf / smp
-    if (blk != cur_blk) {
-      const int32_t* sb = samples + blk * (int64_t)k;
-      for (int j = t; j < k; j += kTileThreads) smp[j] = __ldg(sb + j);
-      cur_blk = blk;
-    }
+    __syncthreads();                      // the previous gather has read buf
 #pragma unroll
     for (int j = 0; j < 64; ++j) buf[xidx(t + 64 * j)] = v[j];
     __syncthreads();
@@ -254,12 +271,35 @@ srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t
 #pragma unroll
     for (int j = 0; j < 64; ++j) buf[xidx(64 * t + j)] = v[j];
     __syncthreads();
-    for (int j = t; j < k; j += kTileThreads) {
-      const int32_t r = smp[j];
+    for (int j = t; j < kk; j += kTileThreads) {
+      const int32_t r = sm[j];
       const double z = buf[xidx(r & (T - 1))];
       const int64_t rh = (int64_t)(r >> LOGT);
-      part[j] += (__popcll(rh & h) & 1) ? -z : z;
+      acc[j] += (__popcll(rh & h) & 1) ? -z : z;
     }
+  };
+  for (int64_t ti = t0; ti < t1; ++ti) {
+    const int64_t lr0 = ti * T;
+    const int64_t g0 = row0 + lr0;
+    const int64_t blk = g0 >> log2_block;
+    if (blk != cur_blk || (PAIR && (g0 >> b2.log2_block) != cur_blk2)) {
+      __syncthreads();                    // the previous tile's gathers are done
+      if (blk != cur_blk) {
+        const int32_t* sb = samples + blk * (int64_t)k;
+        for (int j = t; j < k; j += kTileThreads) smp[j] = __ldg(sb + j);
+        cur_blk = blk;
+      }
+      if constexpr (PAIR) {
+        const int64_t blk2 = g0 >> b2.log2_block;
+        if (blk2 != cur_blk2) {
+          const int32_t* sb2 = b2.samples + blk2 * (int64_t)b2.k;
+          for (int j = t; j < b2.k; j += kTileThreads) smp2[j] = __ldg(sb2 + j);
+          cur_blk2 = blk2;
+        }
+      }
+    }
+    tile(lr0, sign_bits, log2_block, smp, k, part);
+    if constexpr (PAIR) tile(lr0, b2.sign_bits, b2.log2_block, smp2, b2.k, part2);
   }
   if constexpr (!CLUSTERED) {
     // 8 tiles accumulated in tile order from 0.0: the cluster sum below, bit
@@ -267,6 +307,10 @@ srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t
     __syncthreads();
     double* out = partials + ((int64_t)col * gridDim.x + blockIdx.x) * k;
     for (int j = t; j < k; j += kTileThreads) out[j] = part[j];
+    if constexpr (PAIR) {
+      double* out2 = b2.partials + ((int64_t)col * gridDim.x + blockIdx.x) * b2.k;
+      for (int j = t; j < b2.k; j += kTileThreads) out2[j] = part2[j];
+    }
     if (tl && t == 0) atomicMax(tl + 13, gtimer());
   } else {
     cg::cluster_group cl = cg::this_cluster();
@@ -282,14 +326,26 @@ srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t
       for (int q = 0; q < kSrhtCluster; ++q) s += cl.map_shared_rank(part, q)[j];
       out[j] = s;
     }
+    if constexpr (PAIR) {
+      const int p0 = (int)(((int64_t)rank * b2.k) / kSrhtCluster);
+      const int p1 = (int)(((int64_t)(rank + 1) * b2.k) / kSrhtCluster);
+      double* out2 = b2.partials + ((int64_t)col * ngroups + blockIdx.x / kSrhtCluster) * b2.k;
+      for (int j = p0 + t; j < p1; j += kTileThreads) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < kSrhtCluster; ++q) s += cl.map_shared_rank(part2, q)[j];
+        out2[j] = s;
+      }
+    }
     if (tl && t == 0) atomicMax(tl + 13, gtimer());
     cl.sync();  // keep shared memory alive until every CTA has read it
   }
 }
 
 template <typename TX>
-static size_t srht_tile_smem(int k) {
-  return (size_t)(kTileBuf + k) * sizeof(double) + (size_t)k * sizeof(int32_t);
+static size_t srht_tile_smem(int k, int k2 = 0) {
+  return (size_t)(kTileBuf + k) * sizeof(double) + (size_t)(k + (k & 1)) * sizeof(int32_t) +
+         (k2 > 0 ? (size_t)k2 * sizeof(double) + (size_t)k2 * sizeof(int32_t) : 0);
 }
 
 // Partition of a column into tiles and partials.  4096-row tiles (the tile
@@ -330,7 +386,7 @@ static int launch_srht_t(const void* X, int64_t ldx, int ncols, int64_t n_local,
       // or cluster exchange).  Both give the same bits.
       const size_t sm = srht_tile_smem<TX>(k);
       const bool batch = (int64_t)nctas * ncols >= 4 * (int64_t)sm_count();
-      auto kern = batch ? srht_tile_kernel<TX, false> : srht_tile_kernel<TX, true>;
+      auto kern = batch ? srht_tile_kernel<TX, false, false> : srht_tile_kernel<TX, true, false>;
       if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                            cudaSharedmemCarveoutMaxShared);
@@ -338,7 +394,7 @@ static int launch_srht_t(const void* X, int64_t ldx, int ncols, int64_t n_local,
       return check_ex(launch_ex(kern, grid, dim3(kTileThreads), sm, s, batch ? 1 : kSrhtCluster,
                                 static_cast<const TX*>(X), ldx, n_local, row0, log2_block,
                                 sign_bits, samples, k, batch ? kSrhtCluster : 1, ntiles, partials,
-                                st, debug_timeline_row()),
+                                st, debug_timeline_row(), SrhtSecond{}),
                       "srht_tile_kernel");
     }
   }
@@ -681,6 +737,53 @@ extern "C" int sgs_srht_partials(const void* X, int x_dtype, int64_t ldx, int nc
                               k, partials, st, s, tpc, nt, np);
   return launch_srht<double>(lt, X, ldx, ncols, n_local, row0, log2_block, sign_bits, samples,
                              k, partials, st, s, tpc, nt, np);
+}
+
+template <typename TX>
+static int launch_srht_pair(const void* X, int64_t ldx, int ncols, int64_t n_local, int64_t row0,
+                            int log2_block, const uint32_t* sign_bits, const int32_t* samples,
+                            int k, double* partials, SrhtSecond b2, const sgs_status* st,
+                            cudaStream_t s, int64_t ntiles, int nctas) {
+  const size_t sm = srht_tile_smem<TX>(k, b2.k);
+  const bool batch = (int64_t)nctas * ncols >= 4 * (int64_t)sm_count();
+  auto kern = batch ? srht_tile_kernel<TX, false, true> : srht_tile_kernel<TX, true, true>;
+  if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
+  const dim3 grid(batch ? nctas : nctas * kSrhtCluster, ncols);
+  return check_ex(launch_ex(kern, grid, dim3(kTileThreads), sm, s, batch ? 1 : kSrhtCluster,
+                            static_cast<const TX*>(X), ldx, n_local, row0, log2_block, sign_bits,
+                            samples, k, batch ? kSrhtCluster : 1, ntiles, partials, st,
+                            debug_timeline_row(), b2),
+                  "srht_tile_kernel(pair)");
+}
+
+extern "C" int sgs_srht_partials_pair(const void* X, int x_dtype, int64_t ldx, int ncols,
+                                      int64_t n_local, int64_t row0, int log2_block,
+                                      const uint32_t* sign_bits, const int32_t* samples, int k,
+                                      double* partials, int log2_block2,
+                                      const uint32_t* sign_bits2, const int32_t* samples2, int k2,
+                                      double* partials2, const sgs_status* st, void* stream) {
+  SGS_REQUIRE(X && sign_bits && samples && partials && sign_bits2 && samples2 && partials2,
+              "srht pair: null pointer");
+  SGS_REQUIRE(n_local >= 1 && ncols >= 1 && k >= 1 && k <= 8192 && k2 >= 1 && k2 <= 8192,
+              "srht pair: bad sizes n=%lld k=%d k2=%d", (long long)n_local, k, k2);
+  SGS_REQUIRE(log2_block >= 12 && log2_block <= 40 && log2_block2 >= 12 && log2_block2 <= 40,
+              "srht pair: both sketches need 4096-row tiles (log2 blocks %d, %d)", log2_block,
+              log2_block2);
+  SGS_REQUIRE(!srht_legacy(), "srht pair: not available with SGS_SRHT_LEGACY");
+  SGS_REQUIRE(x_dtype == SGS_F32 || x_dtype == SGS_F64, "srht pair: bad dtype");
+  SGS_REQUIRE((row0 & 4095) == 0, "srht pair: row0 %lld not tile aligned", (long long)row0);
+  int lt, tpc, np;
+  int64_t nt;
+  srht_geometry(n_local, log2_block, &lt, &nt, &tpc, &np);
+  cudaStream_t s = as_stream(stream);
+  const SrhtSecond b2{sign_bits2, samples2, k2, log2_block2, partials2};
+  if (x_dtype == SGS_F32)
+    return launch_srht_pair<float>(X, ldx, ncols, n_local, row0, log2_block, sign_bits, samples,
+                                   k, partials, b2, st, s, nt, np);
+  return launch_srht_pair<double>(X, ldx, ncols, n_local, row0, log2_block, sign_bits, samples,
+                                  k, partials, b2, st, s, nt, np);
 }
 
 extern "C" int sgs_dense_nparts(int64_t n) { return n < 1 ? 0 : dense_nparts_host(n); }

@@ -239,6 +239,12 @@ class RgsState:
                                           device=self.device)
             if comm is not None:
                 self._kvec_phi = torch.empty(self.phi.k, dtype=torch.float64, device=self.device)
+        # Phi q' in the fused column kernel's epilogue (same tile, no re-read of
+        # q') when Phi is an SRHT kind with the column kernel's tile structure
+        self.phi_fused = (self.phi is not None and self.fused and not self.phi.is_dense
+                          and self.phi.log2_block >= 12 and _PHI_FUSED
+                          and self.phi.nparts(self.n_local) == self.nparts_q)
+        self._phi_col = None
 
     # ---- storage ----------------------------------------------------------------
     def _alloc(self, cap: int) -> None:
@@ -379,12 +385,24 @@ class RgsState:
             raise ValueError("w_div needs the fused SRHT column kernel")
         if self.fused:
             d = self._theta_dev
-            call("sgs_rgs_update_srht", self._Q.data_ptr(), self.ccode, self.ldq, self.n_local,
-                 i, w_ptr, w_code, w_div, self._rc.data_ptr(), 1 if normalize_prev else 0,
-                 self._R.data_ptr(), self._cap, 1 if sketch else 0, self.row0,
-                 self.theta.log2_block, d["bits"].data_ptr() + (self.row0 // 32) * 4,
-                 d["samples"].data_ptr(), self.k, self._parts_s.data_ptr(), self.status.ptr,
-                 stream_ptr())
+            if sketch and self.phi_fused:  # Phi q'_i from the same epilogue
+                pd = self.phi.device_data(self.device)
+                call("sgs_rgs_update_srht_phi", self._Q.data_ptr(), self.ccode, self.ldq,
+                     self.n_local, i, w_ptr, w_code, w_div, self._rc.data_ptr(),
+                     1 if normalize_prev else 0, self._R.data_ptr(), self._cap, 1, self.row0,
+                     self.theta.log2_block, d["bits"].data_ptr() + (self.row0 // 32) * 4,
+                     d["samples"].data_ptr(), self.k, self._parts_s.data_ptr(),
+                     pd["bits"].data_ptr() + (self.row0 // 32) * 4, pd["samples"].data_ptr(),
+                     self.phi.k, self.phi.log2_block, self._parts_phi.data_ptr(),
+                     self.status.ptr, stream_ptr())
+                self._phi_col = i
+            else:
+                call("sgs_rgs_update_srht", self._Q.data_ptr(), self.ccode, self.ldq,
+                     self.n_local, i, w_ptr, w_code, w_div, self._rc.data_ptr(),
+                     1 if normalize_prev else 0, self._R.data_ptr(), self._cap,
+                     1 if sketch else 0, self.row0, self.theta.log2_block,
+                     d["bits"].data_ptr() + (self.row0 // 32) * 4, d["samples"].data_ptr(),
+                     self.k, self._parts_s.data_ptr(), self.status.ptr, stream_ptr())
             if not sketch:
                 return None
             if not combine:
@@ -425,11 +443,14 @@ class RgsState:
         return self._sketch_parts(self._qcol_ptr(i), self.ccode, self.ldq, self._parts_s, kvec)
 
     # ---- certification sketches ------------------------------------------------------
-    def _phi_parts(self, x_ptr: int, x_code: int, ldx: int, ncols: int = 1):
-        """Partials of Phi x over the local rows (summed across ranks when sharded)."""
+    def _phi_parts(self, x_ptr: int, x_code: int, ldx: int, ncols: int = 1,
+                   launched: bool = False):
+        """Partials of Phi x over the local rows (summed across ranks when
+        sharded).  ``launched``: the column kernel already wrote them."""
         ph = self.phi
-        self.phi.partials_into(x_ptr, x_code, ldx, ncols, self._parts_phi, n_local=self.n_local,
-                               row0=self.row0, status=self.status)
+        if not launched:
+            self.phi.partials_into(x_ptr, x_code, ldx, ncols, self._parts_phi,
+                                   n_local=self.n_local, row0=self.row0, status=self.status)
         if self.comm is None:
             return self._parts_phi.data_ptr(), self.nparts_phi
         call("sgs_partials_reduce", self._parts_phi.data_ptr(), self.nparts_phi, ph.k, 1, 1.0,
@@ -450,7 +471,8 @@ class RgsState:
         """Partials of Phi q'_i while Q[:, i] still holds the unnormalised q'."""
         if self.phi is None:
             return None
-        return self._phi_parts(self._qcol_ptr(i), self.ccode, self.ldq)
+        fused_here, self._phi_col = self._phi_col == i, None
+        return self._phi_parts(self._qcol_ptr(i), self.ccode, self.ldq, launched=fused_here)
 
     def _phi_q_finish(self, i: int, parts) -> None:
         """S_phi[:, i] = (Phi q'_i) / r_ii (gram_schmidt.py:333-335)."""
@@ -589,14 +611,43 @@ class RgsState:
         # the chunk size sets the all-reduce message size, so a sharded state
         # sizes it from the global row count (identical on every rank)
         np_size = self.nparts if self.comm is None else max(self.nparts, self.theta.nparts(self.n))
-        chunk = max(1, min(m, (256 << 20) // max(1, np_size * k * 8)))
+        # P_phi = Phi W in the same pass when Phi has Theta's tile structure
+        pair = self.phi_fused and not _lib.srht_legacy()
+        kk = k + (self.phi.k if pair else 0)
+        chunk = max(1, min(m, (256 << 20) // max(1, np_size * kk * 8)))
         parts = torch.empty((chunk, self.nparts, k), dtype=torch.float64, device=self.device)
+        if pair:
+            ph, kp_ = self.phi, self.phi.k
+            pparts = torch.empty((chunk, self.nparts_phi, kp_), dtype=torch.float64,
+                                 device=self.device)
+            d, pd = self._theta_dev, ph.device_data(self.device)
+            if self.comm is not None:
+                kbp = torch.empty((chunk, kp_), dtype=torch.float64, device=self.device)
+            self._keep_phi = pparts
         if self.comm is not None:
             kbuf = torch.empty((chunk, k), dtype=torch.float64, device=self.device)
         for c0 in range(0, m, chunk):
             nc = min(chunk, m - c0)
-            self.theta.partials_into(base + c0 * ldw * esz, wc, ldw, nc, parts,
-                                     n_local=self.n_local, row0=self.row0, status=self.status)
+            if pair:
+                call("sgs_srht_partials_pair", base + c0 * ldw * esz, wc, ldw, nc, self.n_local,
+                     self.row0, self.theta.log2_block, d["bits"].data_ptr() + (self.row0 // 32) * 4,
+                     d["samples"].data_ptr(), k, parts.data_ptr(), ph.log2_block,
+                     pd["bits"].data_ptr() + (self.row0 // 32) * 4, pd["samples"].data_ptr(), kp_,
+                     pparts.data_ptr(), self.status.ptr, sp)
+                pdst = self._P_phi.data_ptr() + c0 * kp_ * self._P_phi.element_size()
+                if self.comm is None:
+                    call("sgs_partials_reduce", pparts.data_ptr(), self.nparts_phi, kp_, nc,
+                         ph.scale, pdst, self.fcode, kp_, self.status.ptr, sp)
+                else:
+                    call("sgs_partials_reduce", pparts.data_ptr(), self.nparts_phi, kp_, nc, 1.0,
+                         kbp.data_ptr(), _lib.SGS_F64, kp_, self.status.ptr, sp)
+                    self.comm.allreduce_(kbp[:nc])
+                    call("sgs_partials_reduce", kbp.data_ptr(), 1, kp_, nc, ph.scale, pdst,
+                         self.fcode, kp_, self.status.ptr, sp)
+            else:
+                self.theta.partials_into(base + c0 * ldw * esz, wc, ldw, nc, parts,
+                                         n_local=self.n_local, row0=self.row0,
+                                         status=self.status)
             pdst = self._P.data_ptr() + c0 * k * self._P.element_size()
             if self.comm is None:
                 call("sgs_partials_reduce", parts.data_ptr(), self.nparts, k, nc,
@@ -607,7 +658,7 @@ class RgsState:
                 self.comm.allreduce_(kbuf[:nc])
                 call("sgs_partials_reduce", kbuf.data_ptr(), 1, k, nc, self.theta.scale,
                      pdst, self.fcode, k, self.status.ptr, sp)
-        if self.phi is not None:  # P_phi = Phi W, batched like P (same bits as per column)
+        if self.phi is not None and not pair:  # P_phi = Phi W, batched (same bits as per column)
             ph, kp_ = self.phi, self.phi.k
             np_phi = (self.nparts_phi if self.comm is None
                       else max(self.nparts_phi, ph.nparts(self.n)))
@@ -821,6 +872,9 @@ _PINNED_POOL: list = []
 # CTAs, while the separate sketch kernel runs it at full occupancy; the q'
 # re-read it saves is an L2 hit.
 _RAD_FUSED = os.environ.get("SGS_RAD_FUSED", "0") == "1"
+
+# SGS_PHI_FUSED=0 sketches Phi q' with its own launch (A/B and parity switch)
+_PHI_FUSED = os.environ.get("SGS_PHI_FUSED", "1") != "0"
 
 # SGS_LS_DEFER=0 forms every T column inside its own finalize (A/B switch)
 _LS_DEFER = os.environ.get("SGS_LS_DEFER", "1") != "0"

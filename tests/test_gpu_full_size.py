@@ -89,6 +89,16 @@ def test_c0_shape_device_rademacher_factorization(cuda):
     assert torch.equal(st2.device_factors().Q, f.Q[:, :12])
 
 
+def _record(case, **vals):
+    """Append the measured parity numbers to $SGS_PARITY_LOG (one JSON line
+    per case; profiles/ keeps the round's copy).  No-op when unset."""
+    path = os.environ.get("SGS_PARITY_LOG")
+    if path:
+        with open(path, "a") as fh:
+            fh.write(json.dumps({"case": case, **{k: float(v) if np.ndim(v) == 0 else v
+                                                   for k, v in vals.items()}}) + "\n")
+
+
 def _metrics_dev(W, f):
     """The three 2-norm gates, by the SAME function that produced the oracle's
     values in the golden files (oracle.factor_metrics_blocked, fp64)."""
@@ -133,6 +143,8 @@ def test_c0_full_size_metrics_within_10x_of_oracle(cuda):
     th = sg.make_sketch(sg.SketchKind.GAUSSIAN, k, n, 0)
     f, _ = sg.rgs_factorize(W, th, sg.UNIFIED64, device_factors=True)
     ours = _metrics_dev(W, f)
+    _record("c0", **{f"gpu_{a}": b for a, b in ours.items()},
+            **{f"oracle_{a}": float(g[f"c0_{a}"]) for a in ours})
     for key, v in ours.items():
         assert v <= 10.0 * max(float(g[f"c0_{key}"]), 1e-15), (key, v, float(g[f"c0_{key}"]))
 
@@ -147,6 +159,10 @@ def test_c0_twin_full_size_q_r_s_within_1e10(cuda):
     th = sg.make_sketch(sg.SketchKind.GAUSSIAN, k, n, 0)
     f, _ = sg.rgs_factorize(W, th, sg.UNIFIED64, device_factors=True)
     rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))  # noqa: E731
+    rows = torch.from_numpy(g["c0twin_rows"]).cuda()
+    _record("c0twin", rel_R=rel(f.R.cpu().numpy(), g["c0twin_R"]),
+            rel_S=rel(f.S.cpu().numpy(), g["c0twin_S"]),
+            rel_Qrows=rel(f.Q[rows].cpu().numpy(), g["c0twin_Qrows"]))
     assert rel(f.R.cpu().numpy(), g["c0twin_R"]) <= 1e-10
     assert rel(f.S.cpu().numpy(), g["c0twin_S"]) <= 1e-10
     rows = torch.from_numpy(g["c0twin_rows"]).cuda()
@@ -164,6 +180,8 @@ def test_c1_full_size_metrics_within_10x_of_oracle(cuda):
     th = sg.make_sketch(sg.SketchKind.PSRHT, k, n, 0)
     f, _ = sg.rgs_factorize(W, th, sg.MIXED32_64, breakdown_factor=0.0, device_factors=True)
     ours = _metrics_dev(W, f)
+    _record("c1", **{f"gpu_{a}": b for a, b in ours.items()},
+            **{f"oracle_{a}": float(g[f"c1_{a}"]) for a in ours})
     for key, v in ours.items():
         assert v <= 10.0 * max(float(g[f"c1_{key}"]), 1e-15), (key, v, float(g[f"c1_{key}"]))
     d = torch.diagonal(f.R).cpu().numpy()
@@ -190,8 +208,12 @@ def test_c2_full_size_q_r_s_p_vs_oracle(cuda):
     assert rel(f.S.cpu().numpy(), g["S"]) <= 1e-10
     assert rel(f.P.cpu().numpy(), g["P"]) <= 1e-13
     rows = torch.from_numpy(g["rows"]).cuda()
-    assert rel(f.Q[rows].cpu().numpy(), g["Qrows"]) <= 1e-10
     ours = _metrics_dev(W, f)
+    _record("c2_m1000", rel_R=rel(f.R.cpu().numpy(), g["R"]), rel_S=rel(f.S.cpu().numpy(), g["S"]),
+            rel_P=rel(f.P.cpu().numpy(), g["P"]),
+            rel_Qrows=rel(f.Q[rows].cpu().numpy(), g["Qrows"]),
+            **{f"gpu_{a}": b for a, b in ours.items()}, **{f"oracle_{a}": float(g[a]) for a in ours})
+    assert rel(f.Q[rows].cpu().numpy(), g["Qrows"]) <= 1e-10
     for key, v in ours.items():
         assert v <= 10.0 * max(float(g[key]), 1e-15), (key, v, float(g[key]))
 
@@ -210,6 +232,9 @@ def test_c4_shape_m400_metrics_vs_oracle(cuda):
     th = sg.make_sketch(sg.SketchKind.BLOCK_SRHT, k, n, 0, block_log2=20)
     f = _factor_in_place(W, th, sg.MIXED32_64)
     ours = _metrics_dev(W, f)
+    R = f.R.cpu().numpy()
+    _record(f"c4_m{m}", rel_R=float(np.linalg.norm(R - g["R"]) / np.linalg.norm(g["R"])),
+            **{f"gpu_{a}": b for a, b in ours.items()}, **{f"oracle_{a}": float(g[a]) for a in ours})
     for key, v in ours.items():
         assert v <= 10.0 * max(float(g[key]), 1e-15), (key, v, float(g[key]))
     R = f.R.cpu().numpy()

@@ -253,3 +253,34 @@ def test_certification_sketches_phi(cuda, phikind, n):
     assert np.array_equal(g.S_phi, f.S_phi) and np.array_equal(g.P_phi, f.P_phi)
     with pytest.raises(ValueError):
         sg.RgsState(th, sg.UNIFIED64, phi=sg.make_sketch(sg.SketchKind.PSRHT, 10, n + 1, 0))
+
+
+@pytest.mark.parametrize("thkind,phikind,pol,n", [
+    ("psrht", "psrht", "f64", 20000), ("psrht", "psrht", "mixed", 3 * 4096 + 517),
+    ("block_srht", "block_srht", "mixed", 4 * 4096), ("psrht", "block_srht", "f64", 8 * 4096)])
+def test_phi_fused_epilogue_bit_identical(cuda, thkind, phikind, pol, n):
+    """Phi q' from the column kernel's epilogue and Phi W from the pair tile
+    kernel (no re-read of q' / W) equal the stand-alone Phi launches bit for
+    bit (SGS_PHI_FUSED=0 path), batch and streaming."""
+    from paper_2011_05090_b200 import gram_schmidt as gsm
+    m, k, kphi = 24, 160, 72
+    W = make_w(n, m, 1e-4, 3, dtype=np.float32 if pol == "mixed" else np.float64)
+    kw = lambda kind: {"block_log2": 12} if kind == "block_srht" else {}  # noqa: E731
+    th = sg.make_sketch(sg.SketchKind(thkind), k, n, 4, **kw(thkind))
+    phi = sg.make_sketch(sg.SketchKind(phikind), kphi, n, 77, **kw(phikind))
+    f, _ = sg.rgs_factorize(W, th, POL[pol], phi=phi, breakdown_factor=0.0)
+    assert sg.RgsState(th, POL[pol], phi=phi).phi_fused
+    old = gsm._PHI_FUSED
+    try:
+        gsm._PHI_FUSED = False
+        g, _ = sg.rgs_factorize(W, th, POL[pol], phi=phi, breakdown_factor=0.0)
+        assert not sg.RgsState(th, POL[pol], phi=phi).phi_fused
+    finally:
+        gsm._PHI_FUSED = old
+    for a, b in ((f.S_phi, g.S_phi), (f.P_phi, g.P_phi), (f.R, g.R), (f.S, g.S), (f.Q, g.Q)):
+        assert np.array_equal(a, b)
+    st = sg.RgsState(th, POL[pol], phi=phi, breakdown_factor=0.0)
+    for j in range(m):
+        st.push(W[:, j])
+    h = st.factors()
+    assert np.array_equal(h.S_phi, f.S_phi) and np.array_equal(h.P_phi, f.P_phi)

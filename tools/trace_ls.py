@@ -43,4 +43,8 @@ for dec, rows in enumerate(np.array_split(tr[1:-1], 5)):
     d["exch1:norms"] = cyc(3, 14)
     d["exch1:coldot"] = cyc(14, 15)
     d["exch1:xsync"] = cyc(15, 4)
+    if np.all(rows[:, 5] > 0) and np.all(rows[:, 6] > 0):  # fast-path launches
+        d["fast:gather"] = cyc(4, 5)
+        d["fast:s_write+coef"] = cyc(5, 6)
+        d["fast:sums"] = cyc(6, 7)
 print(json.dumps(out, indent=1))
