@@ -215,6 +215,7 @@ srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t
   const TX* x = X + (int64_t)col * ldx;
   const int64_t t0 = (int64_t)blockIdx.x * tiles_per_cta;
   const int64_t t1 = min(t0 + tiles_per_cta, ntiles);
+  const int64_t bmask = (int64_t(1) << log2_block) - 1;
   // the operator does not depend on the predecessor: k-vector and first
   // sample set before the dependency wait
   for (int j = t; j < k; j += kTileThreads) part[j] = 0.0;
@@ -278,7 +279,81 @@ srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t
       acc[j] += (__popcll(rh & h) & 1) ? -z : z;
     }
   };
-  for (int64_t ti = t0; ti < t1; ++ti) {
+  // Batches of fp32 columns (the c1 / c4 P = Theta W): the next tile's values
+  // and sign words are loaded while the current tile is transformed (64
+  // registers + a 2 x 128-word sign buffer in shared memory), so a CTA's 8
+  // tiles stream back to back instead of alternating HBM latency and math.
+  // Same operations in the same order: bit-identical partials.
+  constexpr bool PF = sizeof(TX) == 4 && !PAIR && !CLUSTERED;
+  if constexpr (PF) {
+    uint32_t* sgn = reinterpret_cast<uint32_t*>(smp + k + (k & 1));  // 2 x 128 words
+    auto load_raw = [&](int64_t lr0, TX (&r)[64]) {
+      if (lr0 + T <= n_local) {
+#pragma unroll
+        for (int j = 0; j < 64; ++j) r[j] = __ldg(x + lr0 + t + 64 * j);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 64; ++j) {
+          const int64_t lr = lr0 + t + 64 * j;
+          r[j] = lr < n_local ? __ldg(x + lr) : TX(0);
+        }
+      }
+    };
+    auto load_sgn = [&](int64_t lr0, uint32_t& s0, uint32_t& s1) {
+      const int64_t w0 = (lr0 >> 5) + t, w1 = w0 + 64;  // words t and t + 64 of the tile
+      s0 = (lr0 + 32 * (int64_t)t < n_local) ? __ldg(sign_bits + w0) : ~0u;
+      s1 = (lr0 + 32 * (int64_t)(t + 64) < n_local) ? __ldg(sign_bits + w1) : ~0u;
+    };
+    TX nx[64];
+    uint32_t ns0 = 0u, ns1 = 0u;
+    if (t0 < t1) {
+      load_raw(t0 * T, nx);
+      load_sgn(t0 * T, ns0, ns1);
+    }
+    for (int64_t ti = t0; ti < t1; ++ti) {
+      const int64_t lr0 = ti * T;
+      const int64_t g0 = row0 + lr0;
+      const int64_t blk = g0 >> log2_block;
+      const int64_t h = (g0 & bmask) >> LOGT;
+      uint32_t* sg = sgn + 128 * (int)((ti - t0) & 1);
+      sg[t] = ns0;
+      sg[t + 64] = ns1;
+      double v[64];
+#pragma unroll
+      for (int j = 0; j < 64; ++j) v[j] = (double)nx[j];
+      if (ti + 1 < t1) {  // in flight while this tile is transformed
+        load_raw(lr0 + T, nx);
+        load_sgn(lr0 + T, ns0, ns1);
+      }
+      __syncthreads();  // sg visible; the previous tile's gather is done with buf / smp
+      if (blk != cur_blk) {
+        const int32_t* sb = samples + blk * (int64_t)k;
+        for (int j = t; j < k; j += kTileThreads) smp[j] = __ldg(sb + j);
+        cur_blk = blk;
+      }
+      // sign word of element t + 64 j: word 2 j + w of the tile
+#pragma unroll
+      for (int j = 0; j < 64; ++j)
+        if (((sg[2 * j + w] >> lane) & 1u) == 0u) v[j] = -v[j];
+      fwht_reg<6>(v);                       // bits 6..11
+#pragma unroll
+      for (int j = 0; j < 64; ++j) buf[xidx(t + 64 * j)] = v[j];
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 64; ++j) v[j] = buf[xidx(64 * t + j)];
+      fwht_reg<6>(v);                       // bits 0..5
+#pragma unroll
+      for (int j = 0; j < 64; ++j) buf[xidx(64 * t + j)] = v[j];
+      __syncthreads();
+      for (int j = t; j < k; j += kTileThreads) {
+        const int32_t r = smp[j];
+        const double z = buf[xidx(r & (T - 1))];
+        const int64_t rh = (int64_t)(r >> LOGT);
+        part[j] += (__popcll(rh & h) & 1) ? -z : z;
+      }
+    }
+  }
+  for (int64_t ti = t0; ti < (PF ? t0 : t1); ++ti) {
     const int64_t lr0 = ti * T;
     const int64_t g0 = row0 + lr0;
     const int64_t blk = g0 >> log2_block;
@@ -345,7 +420,8 @@ srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t
 template <typename TX>
 static size_t srht_tile_smem(int k, int k2 = 0) {
   return (size_t)(kTileBuf + k) * sizeof(double) + (size_t)(k + (k & 1)) * sizeof(int32_t) +
-         (k2 > 0 ? (size_t)k2 * sizeof(double) + (size_t)k2 * sizeof(int32_t) : 0);
+         (k2 > 0 ? (size_t)k2 * sizeof(double) + (size_t)k2 * sizeof(int32_t) : 0) +
+         256 * sizeof(uint32_t);  // the prefetch path's sign buffer
 }
 
 // Partition of a column into tiles and partials.  4096-row tiles (the tile

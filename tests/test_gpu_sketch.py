@@ -193,6 +193,21 @@ def test_batched_tile_sketch_equals_per_column(cuda, dt):
 
 
 @pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_batched_block_srht_equals_per_column(cuda, dt):
+    """Batch mode with a block-SRHT of 4096-row blocks: every tile of a CTA's
+    eight switches sample rows (and the fp32 path prefetches the next tile's
+    values and sign words while transforming the current one); a ragged last
+    block-row is zero padded.  apply_block equals apply bit for bit."""
+    n, k, m = 64 * 4096, 700, 80
+    th = sg.make_sketch(sg.SketchKind.BLOCK_SRHT, k, n, 9, block_log2=12)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    X = torch.randn((m, n), dtype=torch.float64, device="cuda", generator=g).to(dt)
+    Y = th.apply_block(X.t())
+    for j in range(0, m, 7):
+        assert torch.equal(Y[:, j], th.apply(X[j]))
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
 def test_gaussian_dmma_batch_equals_per_column(cuda, dt):
     """The Gaussian P = Theta W on the fp64 tensor cores: the 128 x 64 tile
     variant (batches) and the 256 x 8 variant (apply) run the same ascending
