@@ -10,6 +10,8 @@ from paper_2011_05090_b200.workloads import CONFIGS, make_w_device
 
 cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c1"]
 n, m, k = cfg["n"], cfg["m"], cfg["k"]
+if len(sys.argv) > 2:  # override n (e.g. grids that fit beside a resident LS cluster)
+    n = int(sys.argv[2])
 pol = sg.policy_from_name(cfg["policy"])
 th = sg.make_sketch(sg.SketchKind(cfg["kind"]), k, n, 0)
 W = make_w_device(n, m, cfg["sigma_min"], 0,
