@@ -88,6 +88,14 @@ int sgs_srht_partials(const void* X, int x_dtype, int64_t ldx, int ncols,
                       int64_t n_local, int64_t row0, int log2_block,
                       const uint32_t* sign_bits, const int32_t* samples, int k,
                       double* partials, const sgs_status* st, void* stream);
+/* sgs_srht_partials with the CTA geometry of 4096-row tiles chosen: 0 as
+ * sgs_srht_partials (by size), 1 one CTA per 8 consecutive tiles (a small
+ * grid: a following cluster launch can be resident alongside), 2 one tile
+ * per CTA with an 8-CTA cluster sum.  Bit-identical partials for all three. */
+int sgs_srht_partials_geom(const void* X, int x_dtype, int64_t ldx, int ncols,
+                           int64_t n_local, int64_t row0, int log2_block,
+                           const uint32_t* sign_bits, const int32_t* samples, int k,
+                           double* partials, int geom, const sgs_status* st, void* stream);
 /* Two SRHT-kind sketches of the same columns in one pass (the P batch of
  * rgs_factorize with a certification sketch Phi: P = Theta W and
  * P_phi = Phi W, gram_schmidt.py:303-305 per column).  Both need 4096-row

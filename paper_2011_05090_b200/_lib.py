@@ -15,7 +15,9 @@ from ctypes import POINTER, c_double, c_int, c_int64, c_uint64, c_void_p
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libsketchgs_b200.so")
+# SGS_LIB_CHECKED=1: the checked build (device-side bound checks, `make checked`)
+LIB_PATH = os.path.join(_HERE, "_lib", "libsketchgs_b200_checked.so"
+                        if os.environ.get("SGS_LIB_CHECKED", "0") == "1" else "libsketchgs_b200.so")
 
 SGS_F32 = 0
 SGS_F64 = 1
@@ -81,6 +83,9 @@ _SIGS = {
     "sgs_rgs_update_srht": (c_int, [c_void_p, c_int, c_int64, c_int64, c_int, c_void_p, c_int,
                                     c_void_p, c_void_p, c_int, c_void_p, c_int64, c_int, c_int64, c_int,
                                     c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
+    "sgs_srht_partials_geom": (c_int, [c_void_p, c_int, c_int64, c_int, c_int64, c_int64, c_int,
+                                       c_void_p, c_void_p, c_int, c_void_p, c_int, c_void_p,
+                                       c_void_p]),
     "sgs_srht_partials_pair": (c_int, [c_void_p, c_int, c_int64, c_int, c_int64, c_int64, c_int,
                                        c_void_p, c_void_p, c_int, c_void_p, c_int, c_void_p,
                                        c_void_p, c_int, c_void_p, c_void_p, c_void_p]),

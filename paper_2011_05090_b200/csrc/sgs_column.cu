@@ -126,6 +126,10 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
   TQ* rs = PHI ? reinterpret_cast<TQ*>(smp2 + phi.k + (phi.k & 1))
                : reinterpret_cast<TQ*>(smp + k + (k & 1));           // i coefficients
   __shared__ uint64_t mbar[kColMaxStages];
+  // the carve-up (ring | k partials | k samples | [phi] | i coefficients) fits
+  SGS_DCHECK(S >= 2 && S <= kColMaxStages && k >= 1);
+  SGS_DCHECK(dyn_smem_offset(rs + (i > 0 ? i : 1), smem_raw) <= dyn_smem_bytes());
+  SGS_DCHECK(col_ring_bytes<TQ>(S) >= (size_t)(kColT + kColT / 8 + 8) * 8);
 
   const int tid = threadIdx.x;
   const int64_t lr0 = (int64_t)blockIdx.x * kColT;  // first local row of the tile
@@ -317,6 +321,7 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
     }
     for (int j = tid; j < k; j += blockDim.x) {
       const int32_t r = smp[j];
+      SGS_DCHECK(r >= 0 && (int64_t)r < (int64_t(1) << log2_block));  // block-local sample row
       const double v = z[pidx(r & (kColT - 1))];
       const int64_t rh = (int64_t)(r >> kColLogT);
       part[j] = (__popcll(rh & h) & 1) ? -v : v;
@@ -430,6 +435,8 @@ dense_ring_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
   TQ* rs = reinterpret_cast<TQ*>(xq + chunk);                                           // i
   // full[s]: the stage's bytes landed; empty[s]: every warp has read it
   __shared__ uint64_t full[kDcStages], empty[kDcStages];
+  SGS_DCHECK(dyn_smem_offset(rs + (i > 0 ? i : 1), smem_raw) <= dyn_smem_bytes());
+  SGS_DCHECK((int64_t)chunk <= (int64_t)kDcMaxRPT * blockDim.x);
   const int tid = threadIdx.x, T = blockDim.x;
   const int nwarps = T >> 5;
   const int p = blockIdx.x;

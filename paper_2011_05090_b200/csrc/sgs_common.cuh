@@ -39,6 +39,39 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 constexpr int kMaxSMs = 148;
 int sm_count();
 
+// ---- device-side checks (the checked build) ------------------------------------
+// `make checked` compiles the library with -DSGS_DEVICE_CHECKS into
+// _lib/libsketchgs_b200_checked.so (SGS_LIB_CHECKED=1 loads it): every
+// SGS_DCHECK then tests an index / shared-memory bound inside the kernels and
+// traps with its location on a violation - the stand-in for compute-sanitizer
+// memcheck, which this GPU pool does not run.  Compiled out otherwise.
+#ifdef SGS_DEVICE_CHECKS
+#define SGS_DCHECK(cond)                                                              \
+  do {                                                                                \
+    if (!(cond)) {                                                                    \
+      printf("SGS_DCHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,  \
+             (int)blockIdx.x, (int)threadIdx.x, #cond);                               \
+      __trap();                                                                       \
+    }                                                                                 \
+  } while (0)
+#else
+#define SGS_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
+// bytes of dynamic shared memory this launch was given
+__device__ __forceinline__ uint32_t dyn_smem_bytes() {
+  uint32_t v;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(v));
+  return v;
+}
+// byte offset of p from the start of the dynamic shared memory window
+__device__ __forceinline__ uint32_t dyn_smem_offset(const void* p, const void* base) {
+  return (uint32_t)(reinterpret_cast<const unsigned char*>(p) -
+                    reinterpret_cast<const unsigned char*>(base));
+}
+
 // ---- device helpers ---------------------------------------------------------
 // Kernels handed a status block return early once a code is set, so a host
 // that enqueued ahead of a breakdown/convergence turns the tail into no-ops.

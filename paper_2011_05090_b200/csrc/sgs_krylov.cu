@@ -103,6 +103,7 @@ csr_spmv_staged_kernel(int64_t n, const int32_t* __restrict__ rp, const int32_t*
   const int b_v = b & ~1, e_v = (e + 1) & ~1;
   const bool staged = allow_stage && (e_ci - b_ci) <= kSpCap + 4 && (e_v - b_v) <= kSpCap + 2 &&
                       e_ci <= nnz && e_v <= nnz && e > b;
+  SGS_DCHECK(b >= 0 && b <= e && e <= nnz);
   int rb[2], re[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {

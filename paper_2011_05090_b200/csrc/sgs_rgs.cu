@@ -657,6 +657,11 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LsSmem<T> L(smem_raw, RM, cap);
+  // fixed arrays + the cache of ncache columns of T fit; the row slice fits RM
+  SGS_DCHECK(CL >= 1 && CL <= kLsMaxCluster && nr >= 0 && nr <= RM);
+  SGS_DCHECK(L.bytes + (size_t)a.cache_cols * RM * sizeof(T) <= dyn_smem_bytes());
+  SGS_DCHECK(!a.do_finalize || (a.col_fin >= 0 && a.col_fin < cap));
+  SGS_DCHECK(!a.do_solve || (a.col_sol >= 1 && a.col_sol < cap));
   T* vs = L.vs;    // RM   s' -> s (own rows)
   T* vt = L.vt;    // RM   t
   T* vp = L.vp;    // RM   p

@@ -211,6 +211,7 @@ srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t
   double* part2 = reinterpret_cast<double*>(smp + k + (k & 1));  // PAIR: b2.k
   int32_t* smp2 = reinterpret_cast<int32_t*>(part2 + (PAIR ? b2.k : 0));
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+  SGS_DCHECK(dyn_smem_offset(smp2 + (PAIR ? b2.k : 0) + 256, smem) <= dyn_smem_bytes());
   const int col = blockIdx.y;
   const TX* x = X + (int64_t)col * ldx;
   const int64_t t0 = (int64_t)blockIdx.x * tiles_per_cta;
@@ -274,6 +275,7 @@ srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t
     __syncthreads();
     for (int j = t; j < kk; j += kTileThreads) {
       const int32_t r = sm[j];
+      SGS_DCHECK(r >= 0 && (int64_t)r < (int64_t(1) << lb));
       const double z = buf[xidx(r & (T - 1))];
       const int64_t rh = (int64_t)(r >> LOGT);
       acc[j] += (__popcll(rh & h) & 1) ? -z : z;
@@ -347,6 +349,7 @@ srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t
       __syncthreads();
       for (int j = t; j < k; j += kTileThreads) {
         const int32_t r = smp[j];
+        SGS_DCHECK(r >= 0 && (int64_t)r < (int64_t(1) << log2_block));
         const double z = buf[xidx(r & (T - 1))];
         const int64_t rh = (int64_t)(r >> LOGT);
         part[j] += (__popcll(rh & h) & 1) ? -z : z;
@@ -453,7 +456,7 @@ template <typename TX, int LOGT>
 static int launch_srht_t(const void* X, int64_t ldx, int ncols, int64_t n_local, int64_t row0,
                          int log2_block, const uint32_t* sign_bits, const int32_t* samples,
                          int k, double* partials, const sgs_status* st, cudaStream_t s,
-                         int tpc, int64_t ntiles, int nctas) {
+                         int tpc, int64_t ntiles, int nctas, int geom) {
   if constexpr (LOGT == 12) {
     if (!srht_legacy()) {
       // one partial per 8 consecutive tiles (nctas = partials here): few
@@ -461,7 +464,10 @@ static int launch_srht_t(const void* X, int64_t ldx, int ncols, int64_t n_local,
       // batches -> one CTA runs its 8 tiles in order (no per-tile prologue
       // or cluster exchange).  Both give the same bits.
       const size_t sm = srht_tile_smem<TX>(k);
-      const bool batch = (int64_t)nctas * ncols >= 4 * (int64_t)sm_count();
+      // geom 1: one CTA per 8 tiles even for one column - a grid of ntiles/8
+      // CTAs leaves most SMs free, so a following LS cluster launch finds a
+      // GPC and runs its pre-wait part alongside (RGMRES's sketch of w)
+      const bool batch = geom == 1 || (geom == 0 && (int64_t)nctas * ncols >= 4 * (int64_t)sm_count());
       auto kern = batch ? srht_tile_kernel<TX, false, false> : srht_tile_kernel<TX, true, false>;
       if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -497,11 +503,11 @@ template <typename TX>
 static int launch_srht(int logt, const void* X, int64_t ldx, int ncols, int64_t n_local,
                        int64_t row0, int log2_block, const uint32_t* sign_bits,
                        const int32_t* samples, int k, double* partials, const sgs_status* st,
-                       cudaStream_t s, int tpc, int64_t ntiles, int nctas) {
+                       cudaStream_t s, int tpc, int64_t ntiles, int nctas, int geom) {
 #define SGS_SRHT_CASE(L)                                                                   \
   case L:                                                                                  \
     return launch_srht_t<TX, L>(X, ldx, ncols, n_local, row0, log2_block, sign_bits,       \
-                                samples, k, partials, st, s, tpc, ntiles, nctas);
+                                samples, k, partials, st, s, tpc, ntiles, nctas, geom);
   switch (logt) {
     SGS_SRHT_CASE(0) SGS_SRHT_CASE(1) SGS_SRHT_CASE(2) SGS_SRHT_CASE(3) SGS_SRHT_CASE(4)
     SGS_SRHT_CASE(5) SGS_SRHT_CASE(6) SGS_SRHT_CASE(7) SGS_SRHT_CASE(8) SGS_SRHT_CASE(9)
@@ -793,10 +799,26 @@ extern "C" int sgs_srht_nparts(int64_t n_local, int log2_block) {
   return (lt == 12 && !srht_legacy()) ? nc : nc / kSrhtCluster;
 }
 
+extern "C" int sgs_srht_partials_geom(const void* X, int x_dtype, int64_t ldx, int ncols,
+                                      int64_t n_local, int64_t row0, int log2_block,
+                                      const uint32_t* sign_bits, const int32_t* samples, int k,
+                                      double* partials, int geom, const sgs_status* st,
+                                      void* stream);
+
 extern "C" int sgs_srht_partials(const void* X, int x_dtype, int64_t ldx, int ncols,
                                  int64_t n_local, int64_t row0, int log2_block,
                                  const uint32_t* sign_bits, const int32_t* samples, int k,
                                  double* partials, const sgs_status* st, void* stream) {
+  return sgs_srht_partials_geom(X, x_dtype, ldx, ncols, n_local, row0, log2_block, sign_bits,
+                                samples, k, partials, 0, st, stream);
+}
+
+extern "C" int sgs_srht_partials_geom(const void* X, int x_dtype, int64_t ldx, int ncols,
+                                      int64_t n_local, int64_t row0, int log2_block,
+                                      const uint32_t* sign_bits, const int32_t* samples, int k,
+                                      double* partials, int geom, const sgs_status* st,
+                                      void* stream) {
+  SGS_REQUIRE(geom >= 0 && geom <= 2, "srht: bad geometry %d", geom);
   SGS_REQUIRE(X && sign_bits && samples && partials, "srht: null pointer");
   SGS_REQUIRE(n_local >= 1 && ncols >= 1 && k >= 1 && k <= 8192, "srht: bad sizes n=%lld k=%d",
               (long long)n_local, k);
@@ -810,9 +832,9 @@ extern "C" int sgs_srht_partials(const void* X, int x_dtype, int64_t ldx, int nc
   cudaStream_t s = as_stream(stream);
   if (x_dtype == SGS_F32)
     return launch_srht<float>(lt, X, ldx, ncols, n_local, row0, log2_block, sign_bits, samples,
-                              k, partials, st, s, tpc, nt, np);
+                              k, partials, st, s, tpc, nt, np, geom);
   return launch_srht<double>(lt, X, ldx, ncols, n_local, row0, log2_block, sign_bits, samples,
-                             k, partials, st, s, tpc, nt, np);
+                             k, partials, st, s, tpc, nt, np, geom);
 }
 
 template <typename TX>
@@ -915,6 +937,7 @@ dense_mma_kernel(const double* __restrict__ thetaT, int64_t ldt, int k, const TX
   using G = MmaTile<WJ, WC, TJ, TC>;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char mma_raw[];
+  SGS_DCHECK((size_t)G::kJ * G::kC * sizeof(double) <= dyn_smem_bytes());
   double* As = reinterpret_cast<double*>(mma_raw);                              // S x 16 x kAS
   TX* Bs = reinterpret_cast<TX*>(As + (size_t)kMmaStages * kMmaStageRows * G::kAS);  // S x 16 x kBS
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

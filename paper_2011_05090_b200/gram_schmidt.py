@@ -362,10 +362,11 @@ class RgsState:
         return kvec.data_ptr(), 1, self.theta.scale
 
     def _sketch_parts(self, x_ptr: int, x_code: int, ldx: int, out: torch.Tensor,
-                      kvec: torch.Tensor | None):
+                      kvec: torch.Tensor | None, small_grid: bool = False):
         """Partials of one local column via the stand-alone sketch kernel."""
+        kw = {"small_grid": True} if small_grid and not self.theta.is_dense else {}
         self.theta.partials_into(x_ptr, x_code, ldx, 1, out, n_local=self.n_local,
-                                 row0=self.row0, status=self.status)
+                                 row0=self.row0, status=self.status, **kw)
         return self._combine(out, self.nparts, kvec)
 
     def _update(self, i: int, w_ptr: int, w_code: int, normalize_prev: bool) -> None:

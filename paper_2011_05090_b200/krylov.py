@@ -27,6 +27,13 @@ from .gram_schmidt import (BREAKDOWN_FACTOR, HOUSEHOLDER_QR, GsVariant, LazyFact
                            QrFactors, RgsState)
 from .precision import MIXED32_64, PrecisionPolicy
 
+# SGS_W_SMALL_GRID=1: sketch w = A q with one CTA per 8 tiles (64 CTAs at c3)
+# instead of one tile per CTA (same partials): the LS cluster that follows
+# then launches beside it and overlaps its pre-wait part (srht -> LS gap
+# 8.6 -> 0.8 us), but one fp64 column on 64 CTAs takes 46 us instead of 9
+# (c3 fp32 basis, one-sync: 3686 -> 3310 steps/s).  Off by default.
+_W_SMALL_GRID = os.environ.get("SGS_W_SMALL_GRID", "0") == "1"
+
 __all__ = ["SparseMatrix", "Ilu0Preconditioner", "ilu0", "arnoldi", "gmres", "gmres_restarted",
            "ArnoldiDecomposition", "GmresResult", "RestartedResult"]
 
@@ -553,7 +560,8 @@ class _ArnoldiEngine:
             xw, blk = self.dist.window(st._Q[c, :self.n_loc])
             blk.spmv_into(xw.data_ptr(), st.ccode, ws.w, alpha=alpha, status=st.status)
         st.theta.partials_into(ws.w.data_ptr(), _lib.SGS_F64, self.n_loc, 1, st._parts_p,
-                               n_local=self.n_loc, row0=st.row0, status=st.status)
+                               n_local=self.n_loc, row0=st.row0, status=st.status,
+                               small_grid=_W_SMALL_GRID)
         p_raw = (st._parts_p.data_ptr(), st.nparts, st.theta.scale)
         if self.dist is not None:  # one all-reduce of [s'; p'] (2k)
             k, kv = st.k, self._kv2
@@ -651,7 +659,8 @@ class _ArnoldiEngine:
                  stream_ptr())
             self._matvec(i, ws.w, alpha, st.status)
             pp, pn, ps = st._sketch_parts(ws.w.data_ptr(), _lib.SGS_F64, self.n_loc,
-                                          st._parts_p, getattr(st, "_kvec_p", None))
+                                          st._parts_p, getattr(st, "_kvec_p", None),
+                                          small_grid=_W_SMALL_GRID)
             st._phi_w(i + 1, ws.w.data_ptr(), _lib.SGS_F64, self.n_loc)
             st._ls(sol=i + 1, p_parts=pp, p_nparts=pn, p_scale=ps)
             sp, sn, ss = st._column(i + 1, ws.w.data_ptr(), _lib.SGS_F64, False, True)

@@ -205,7 +205,7 @@ class SketchOperator:
 
     def partials_into(self, X: torch.Tensor | int, x_dtype: int, ldx: int, ncols: int,
                       out: torch.Tensor, *, n_local: int | None = None, row0: int = 0,
-                      status=None, stream=None) -> int:
+                      status=None, stream=None, small_grid: bool = False) -> int:
         """Launch the partial sketches of ncols columns of X (device pointer or
         tensor, column-major with leading dimension ldx) into ``out``.  Returns
         the number of parts per column."""
@@ -231,8 +231,10 @@ class SketchOperator:
         if row0 % 32:
             raise ValueError("shard row offset must be a multiple of 32")
         bp = d["bits"].data_ptr() + (row0 // 32) * 4
-        call("sgs_srht_partials", xp, x_dtype, ldx, ncols, n_local, row0, self.log2_block,
-             bp, d["samples"].data_ptr(), self.k, out.data_ptr(), st, sp)
+        # small_grid: one CTA per 8 tiles (same partials) so that a cluster
+        # launch queued behind finds free SMs (sgs_srht_partials_geom)
+        call("sgs_srht_partials_geom", xp, x_dtype, ldx, ncols, n_local, row0, self.log2_block,
+             bp, d["samples"].data_ptr(), self.k, out.data_ptr(), 1 if small_grid else 0, st, sp)
         return np_
 
     # ---- reference-facing application ------------------------------------------

@@ -54,4 +54,6 @@ M = sg.ilu0(A)
 r = sg.gmres(A, b, m=30, theta=th, policy=sg.UNIFIED64, tol=1e-8, preconditioner=M)
 print("ilu gmres", r.iterations, flush=True)
 torch.cuda.synchronize()
+from paper_2011_05090_b200 import _lib  # noqa: E402
+print("LIBRARY", _lib.LIB_PATH, flush=True)
 print("SANITIZE_WORKLOAD_DONE", flush=True)
