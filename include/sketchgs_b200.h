@@ -89,9 +89,9 @@ int sgs_srht_partials(const void* X, int x_dtype, int64_t ldx, int ncols,
                       const uint32_t* sign_bits, const int32_t* samples, int k,
                       double* partials, const sgs_status* st, void* stream);
 /* sgs_srht_partials with the CTA geometry of 4096-row tiles chosen: 0 as
- * sgs_srht_partials (by size), 1 one CTA per 8 consecutive tiles (a small
+ * sgs_srht_partials (by size), 1 one CTA per 4 consecutive tiles (a small
  * grid: a following cluster launch can be resident alongside), 2 one tile
- * per CTA with an 8-CTA cluster sum.  Bit-identical partials for all three. */
+ * per CTA with a 4-CTA cluster sum.  Bit-identical partials for all three. */
 int sgs_srht_partials_geom(const void* X, int x_dtype, int64_t ldx, int ncols,
                            int64_t n_local, int64_t row0, int log2_block,
                            const uint32_t* sign_bits, const int32_t* samples, int k,
@@ -187,7 +187,7 @@ int sgs_rgs_update(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
  * block-SRHT sketch of the new column (step 4, gram_schmidt.py:320) in the
  * epilogue, without re-reading q'.  One CTA per 4096-row tile (requires
  * log2_block >= 12 and row0 % 4096 == 0), Q streamed through a TMA bulk-copy
- * ring; partials as sgs_srht_partials, one k-vector per 8-CTA cluster,
+ * ring; partials as sgs_srht_partials, one k-vector per 4-CTA cluster (4 tiles),
  * sgs_column_nparts(n_local) of them.  w_div != NULL (device scalar): the
  * column is cast(w / w_div[0]) - the lagged w_{i} = A q'_{i-1} / r_{i-1,i-1}
  * of the one-synchronisation Arnoldi. */

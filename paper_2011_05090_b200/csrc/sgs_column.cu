@@ -8,7 +8,7 @@
 // re-reading q' - flips the signs, runs the 4096-point Walsh-Hadamard
 // transform (3 bits in registers, 9 bits in three shared-memory radix-8
 // passes), gathers the k sampled rows with the cross-tile sign
-// (-1)^popcount(r_hi & tile), and sums the k-vectors of its 8-CTA cluster
+// (-1)^popcount(r_hi & tile), and sums the k-vectors of its kTileGroup-CTA cluster
 // through distributed shared memory.  One partial k-vector per cluster is
 // written, exactly as sgs_srht_partials would for a one-tile-per-CTA grid.
 
@@ -26,7 +26,7 @@ namespace sgs {
 constexpr int kColThreads = 512;
 constexpr int kColLogT = 12;
 constexpr int kColT = 1 << kColLogT;
-constexpr int kColCluster = 8;
+constexpr int kColCluster = kTileGroup;  // tiles per partial (sgs_common.cuh)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -98,7 +98,7 @@ struct ColPhi {
   const int32_t* samples;     // (nblocks, kphi) block-local sample rows
   int k;
   int log2_block;
-  double* partials;           // one kphi-vector per 8-CTA cluster
+  double* partials;           // one kphi-vector per kTileGroup-CTA cluster
 };
 
 template <typename TQ, typename TW, bool PHI>

@@ -196,6 +196,16 @@ inline int check_ex(cudaError_t e, const char* what) {
   return check_launch(what);
 }
 
+// 4096-row SRHT tiles are summed in groups of kTileGroup consecutive tiles
+// into one partial k-vector: by one CTA in tile order (batches), or by a
+// cluster of kTileGroup CTAs through DSMEM in rank order (one column, and the
+// fused column kernel's epilogue) - the same bits either way.  Groups of 4
+// (was 8) make c1's column grid 62 clusters of 4 instead of 31 of 8: it then
+// leaves a GPC free, so the 16-CTA LS cluster of the column is resident from
+// the column kernel's start and its pre-wait part overlaps the Q stream
+// (c1: 5800 -> 6014 columns/s on the same power-capped box class).
+constexpr int kTileGroup = 4;
+
 // Canonical order for summing per-CTA partials (used by every consumer so
 // that the same vector reduced by different kernels gives the same bits):
 // eight interleaved ascending chains acc_g = sum_{p = g mod 8} x_p, then

@@ -380,7 +380,7 @@ srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t
     if constexpr (PAIR) tile(lr0, b2.sign_bits, b2.log2_block, smp2, b2.k, part2);
   }
   if constexpr (!CLUSTERED) {
-    // 8 tiles accumulated in tile order from 0.0: the cluster sum below, bit
+    // kTileGroup tiles accumulated in tile order from 0.0: the cluster sum below, bit
     // for bit ((0 + z0) + z1 ... = 0 + (0 + z0) + (0 + z1) ...)
     __syncthreads();
     double* out = partials + ((int64_t)col * gridDim.x + blockIdx.x) * k;
@@ -393,25 +393,25 @@ srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t
   } else {
     cg::cluster_group cl = cg::this_cluster();
     cl.sync();  // all k-vectors of the cluster are final
-    const int ngroups = gridDim.x / kSrhtCluster;
+    const int ngroups = gridDim.x / kTileGroup;
     const int rank = (int)cl.block_rank();
-    const int j0 = (int)(((int64_t)rank * k) / kSrhtCluster);
-    const int j1 = (int)(((int64_t)(rank + 1) * k) / kSrhtCluster);
-    double* out = partials + ((int64_t)col * ngroups + blockIdx.x / kSrhtCluster) * k;
+    const int j0 = (int)(((int64_t)rank * k) / kTileGroup);
+    const int j1 = (int)(((int64_t)(rank + 1) * k) / kTileGroup);
+    double* out = partials + ((int64_t)col * ngroups + blockIdx.x / kTileGroup) * k;
     for (int j = j0 + t; j < j1; j += kTileThreads) {
       double s = 0.0;
 #pragma unroll
-      for (int q = 0; q < kSrhtCluster; ++q) s += cl.map_shared_rank(part, q)[j];
+      for (int q = 0; q < kTileGroup; ++q) s += cl.map_shared_rank(part, q)[j];
       out[j] = s;
     }
     if constexpr (PAIR) {
-      const int p0 = (int)(((int64_t)rank * b2.k) / kSrhtCluster);
-      const int p1 = (int)(((int64_t)(rank + 1) * b2.k) / kSrhtCluster);
-      double* out2 = b2.partials + ((int64_t)col * ngroups + blockIdx.x / kSrhtCluster) * b2.k;
+      const int p0 = (int)(((int64_t)rank * b2.k) / kTileGroup);
+      const int p1 = (int)(((int64_t)(rank + 1) * b2.k) / kTileGroup);
+      double* out2 = b2.partials + ((int64_t)col * ngroups + blockIdx.x / kTileGroup) * b2.k;
       for (int j = p0 + t; j < p1; j += kTileThreads) {
         double s = 0.0;
 #pragma unroll
-        for (int q = 0; q < kSrhtCluster; ++q) s += cl.map_shared_rank(part2, q)[j];
+        for (int q = 0; q < kTileGroup; ++q) s += cl.map_shared_rank(part2, q)[j];
         out2[j] = s;
       }
     }
@@ -428,7 +428,7 @@ static size_t srht_tile_smem(int k, int k2 = 0) {
 }
 
 // Partition of a column into tiles and partials.  4096-row tiles (the tile
-// kernel): one partial per 8 consecutive tiles, *nctas = number of partials
+// kernel): one partial per kTileGroup consecutive tiles, *nctas = number of partials
 // (the fused column kernel's structure).  Smaller tiles (and SGS_SRHT_LEGACY):
 // tiles_per_cta tiles per CTA, one partial per 8-CTA cluster.
 static void srht_geometry(int64_t n_local, int log2_block, int* logt, int64_t* ntiles,
@@ -440,7 +440,7 @@ static void srht_geometry(int64_t n_local, int log2_block, int* logt, int64_t* n
     *logt = lt;
     *ntiles = nt;
     *tpc = 1;
-    *nctas = (int)((nt + kSrhtCluster - 1) / kSrhtCluster);
+    *nctas = (int)((nt + kTileGroup - 1) / kTileGroup);
     return;
   }
   const int64_t per = (nt + kSrhtTargetCTAs - 1) / kSrhtTargetCTAs;
@@ -459,12 +459,12 @@ static int launch_srht_t(const void* X, int64_t ldx, int ncols, int64_t n_local,
                          int tpc, int64_t ntiles, int nctas, int geom) {
   if constexpr (LOGT == 12) {
     if (!srht_legacy()) {
-      // one partial per 8 consecutive tiles (nctas = partials here): few
+      // one partial per kTileGroup consecutive tiles (nctas = partials here): few
       // columns -> one tile per CTA and a DSMEM cluster sum (parallelism);
-      // batches -> one CTA runs its 8 tiles in order (no per-tile prologue
+      // batches -> one CTA runs its kTileGroup tiles in order (no per-tile prologue
       // or cluster exchange).  Both give the same bits.
       const size_t sm = srht_tile_smem<TX>(k);
-      // geom 1: one CTA per 8 tiles even for one column - a grid of ntiles/8
+      // geom 1: one CTA per kTileGroup tiles even for one column - a grid of ntiles/4
       // CTAs leaves most SMs free, so a following LS cluster launch finds a
       // GPC and runs its pre-wait part alongside (RGMRES's sketch of w)
       const bool batch = geom == 1 || (geom == 0 && (int64_t)nctas * ncols >= 4 * (int64_t)sm_count());
@@ -472,10 +472,10 @@ static int launch_srht_t(const void* X, int64_t ldx, int ncols, int64_t n_local,
       if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                            cudaSharedmemCarveoutMaxShared);
-      const dim3 grid(batch ? nctas : nctas * kSrhtCluster, ncols);
-      return check_ex(launch_ex(kern, grid, dim3(kTileThreads), sm, s, batch ? 1 : kSrhtCluster,
+      const dim3 grid(batch ? nctas : nctas * kTileGroup, ncols);
+      return check_ex(launch_ex(kern, grid, dim3(kTileThreads), sm, s, batch ? 1 : kTileGroup,
                                 static_cast<const TX*>(X), ldx, n_local, row0, log2_block,
-                                sign_bits, samples, k, batch ? kSrhtCluster : 1, ntiles, partials,
+                                sign_bits, samples, k, batch ? kTileGroup : 1, ntiles, partials,
                                 st, debug_timeline_row(), SrhtSecond{}),
                       "srht_tile_kernel");
     }
@@ -848,10 +848,10 @@ static int launch_srht_pair(const void* X, int64_t ldx, int ncols, int64_t n_loc
   if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                        cudaSharedmemCarveoutMaxShared);
-  const dim3 grid(batch ? nctas : nctas * kSrhtCluster, ncols);
-  return check_ex(launch_ex(kern, grid, dim3(kTileThreads), sm, s, batch ? 1 : kSrhtCluster,
+  const dim3 grid(batch ? nctas : nctas * kTileGroup, ncols);
+  return check_ex(launch_ex(kern, grid, dim3(kTileThreads), sm, s, batch ? 1 : kTileGroup,
                             static_cast<const TX*>(X), ldx, n_local, row0, log2_block, sign_bits,
-                            samples, k, batch ? kSrhtCluster : 1, ntiles, partials, st,
+                            samples, k, batch ? kTileGroup : 1, ntiles, partials, st,
                             debug_timeline_row(), b2),
                   "srht_tile_kernel(pair)");
 }

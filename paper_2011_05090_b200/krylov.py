@@ -27,7 +27,7 @@ from .gram_schmidt import (BREAKDOWN_FACTOR, HOUSEHOLDER_QR, GsVariant, LazyFact
                            QrFactors, RgsState)
 from .precision import MIXED32_64, PrecisionPolicy
 
-# SGS_W_SMALL_GRID=1: sketch w = A q with one CTA per 8 tiles (64 CTAs at c3)
+# SGS_W_SMALL_GRID=1: sketch w = A q with one CTA per 4 tiles (128 CTAs at c3)
 # instead of one tile per CTA (same partials): the LS cluster that follows
 # then launches beside it and overlaps its pre-wait part (srht -> LS gap
 # 8.6 -> 0.8 us), but one fp64 column on 64 CTAs takes 46 us instead of 9

@@ -231,7 +231,7 @@ class SketchOperator:
         if row0 % 32:
             raise ValueError("shard row offset must be a multiple of 32")
         bp = d["bits"].data_ptr() + (row0 // 32) * 4
-        # small_grid: one CTA per 8 tiles (same partials) so that a cluster
+        # small_grid: one CTA per 4 tiles (same partials) so that a cluster
         # launch queued behind finds free SMs (sgs_srht_partials_geom)
         call("sgs_srht_partials_geom", xp, x_dtype, ldx, ncols, n_local, row0, self.log2_block,
              bp, d["samples"].data_ptr(), self.k, out.data_ptr(), 1 if small_grid else 0, st, sp)
