@@ -441,6 +441,12 @@ dense_ring_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
   const int nwarps = T >> 5;
   const int p = blockIdx.x;
   const int64_t r0 = (int64_t)p * chunk;
+  if (r0 >= n) {  // grid padding (cluster placement): an empty chunk, a zero partial
+    pdl_enter();
+    if (do_sketch)
+      for (int j = threadIdx.x; j < k; j += blockDim.x) partials[(int64_t)p * k + j] = 0.0;
+    return;
+  }
   const int nr = (int)min(chunk, n - r0);
   const int nplain = (i == 0) ? 0 : (normalize_prev ? i - 1 : i);
   const uint32_t segb = (uint32_t)(((size_t)nr * sizeof(TQ) + 15) / 16 * 16);
@@ -629,14 +635,31 @@ dense_ring_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
 
 // Row chunking of dense_ring_kernel: about two chunks per SM, 16-row aligned,
 // at most kDcMaxRPT rows per thread.
+// The dense ring grid is chunked for sm_count() - 28 SMs (two CTAs each) and
+// launched in clusters of 2 (no DSMEM use: it only makes the placement
+// contiguous), so it leaves a GPC free and the column's 16-CTA LS cluster is
+// resident from the kernel's start, its pre-wait part overlapping the
+// Q/Theta stream (c0: 8632 -> 9045 columns/s; chunking for 104-132 SMs
+// measured 8960-9050, for all 148 SMs in clusters of 4 7872).
+// SGS_DR_SMS / SGS_DR_CLUSTER override the two choices.
+constexpr int kDrReserveSMs = 28;
+static int dr_sms() {
+  static const int v = [] { const char* e = getenv("SGS_DR_SMS"); return e ? atoi(e) : 0; }();
+  return v > 0 ? v : std::max(16, sm_count() - kDrReserveSMs);
+}
+static int dr_cluster() {
+  static const int v = [] { const char* e = getenv("SGS_DR_CLUSTER"); return e ? atoi(e) : 2; }();
+  return v > 0 ? v : 1;
+}
 static void dense_ring_geom(int64_t n, int threads, int64_t* chunk, int* np) {
-  int64_t c = (n + 2 * (int64_t)sm_count() - 1) / (2 * (int64_t)sm_count());
+  int64_t c = (n + 2 * (int64_t)dr_sms() - 1) / (2 * (int64_t)dr_sms());
   const int64_t cmax = (int64_t)kDcMaxRPT * threads / 16 * 16;
   if (c > cmax) c = cmax;
   c = (c + 15) / 16 * 16;
   if (c < 16) c = 16;
   *chunk = c;
-  *np = (int)((n + c - 1) / c);
+  const int cl = dr_cluster();
+  *np = (int)(((n + c - 1) / c + cl - 1) / cl * cl);
 }
 
 static int dense_ring_threads(int k) {
@@ -673,7 +696,8 @@ static int launch_dense_ring(void* Q, int64_t ldq, int64_t n, int i, const void*
   do {                                                                                           \
     auto kern = dense_ring_kernel<TQ, TW, QPV, RAD>;                                             \
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
-    e = launch_ex(kern, dim3(np), dim3(threads), smem, s, 1, static_cast<TQ*>(Q), ldq, n, i,     \
+    if (dr_cluster() > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); \
+    e = launch_ex(kern, dim3(np), dim3(threads), smem, s, dr_cluster(), static_cast<TQ*>(Q), ldq, n, i, \
                   static_cast<const TW*>(w), static_cast<const TQ*>(r_crs), normalize_prev, R,   \
                   ldr, do_sketch, thetaT, ldt, k, partials, chunk, stage_bytes, st, rbits, kw,   \
                   acc_two<TQ>());                                                                \
