@@ -510,6 +510,11 @@ def run_qr(args, cfg_name, comm):
                                    f"value counts column shards: {world} per column"}
                           if weak else {})},
             "graph": graph_used,
+            # how a row-sharded state sums s' per column: inside the LS launch by
+            # NVLink stores into the peers' exchange areas, or an NCCL all-reduce
+            "shard_sum": (None if comm is None else
+                          ("peer-memory exchange in the LS launch"
+                           if gstate.__dict__.get("_peer") is not None else "nccl all-reduce")),
             "hbm_gbs_whole_step": round(hbm_gbs, 1),
             "hbm_frac_whole_step": round(hbm_gbs / (peak * world), 4),
             # BASELINE.json quotes the nominal ~8 TB/s; the roofline uses the measured peak

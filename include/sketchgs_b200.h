@@ -49,6 +49,7 @@ extern "C" {
 #define SGS_ST_BREAKDOWN 1   /* reference: gram_schmidt.BreakdownError (gram_schmidt.py:323-326) */
 #define SGS_ST_RANK 2        /* reference: np.linalg.LinAlgError (gram_schmidt.py:186-189) */
 #define SGS_ST_CONVERGED 3   /* reference: gmres early exit est <= tol (krylov.py:300-301) */
+#define SGS_ST_TIMEOUT 4     /* a wait on another rank's published data gave up */
 /* (no code 4: a NaN r_ii flows through as in the reference, which has no
    non-finite guard - gram_schmidt.py:322-326 only compares r_ii <= tol) */
 
@@ -291,9 +292,36 @@ typedef struct sgs_ls_args {
                             GMRES step col_fin - 1 (as sgs_givens_step, same arithmetic) */
   double* giv_cs; double* giv_sn; double* giv_g; double* giv_T; long long giv_ldt;
   double* giv_hist; double giv_tol;  /* giv_tol < 0: no stop test */
+  const void* peer;      /* optional (NULL: off): device sgs_peer_desc (sgs_peer_desc_create) of a
+                            row-sharded state.  The finalize then sums s' across the ranks itself:
+                            each CTA reduces its rows of the local partials (s_partials), stores
+                            them into every rank's receive slots over NVLink, flags them, waits
+                            for every rank's flags and adds the ranks' rows in rank order - the
+                            k-vector all-reduce of sgs_partials_reduce + NCCL done inside the LS
+                            launch (fp64 fine dtype) */
 } sgs_ls_args;
 
 int64_t sgs_ls_scratch_elems(int k, int cap);
+
+/* ---- peer memory of a row-sharded state (one node, NVLink / NVSwitch) --------
+ * Replaces the per-column NCCL all-reduce of s' (the paper's distributed RGS,
+ * PAPER.md:255-261, absent from the reference) by stores into the peers'
+ * memory from the LS launch.  sgs_peer_alloc allocates this rank's exchange
+ * area (receive slots + flags, zeroed; size sgs_peer_bytes), sgs_peer_export /
+ * sgs_peer_import trade CUDA IPC handles (64 bytes) between the ranks (the
+ * caller moves them, e.g. all_gather_object), sgs_peer_desc_create builds the
+ * device descriptor the LS reads (area[q] = rank q's area as mapped here; the
+ * own area for q == rank).  sgs_peer_begin(desc) opens a factorisation
+ * (a new flag generation; enqueue it on every rank).  world <= 8. */
+int64_t sgs_peer_bytes(int world, int k, int cl);
+int sgs_peer_alloc(int64_t bytes, void** area);
+int sgs_peer_free(void* area);
+int sgs_peer_export(void* area, unsigned char* handle64);
+int sgs_peer_import(const unsigned char* handle64, void** area);
+int sgs_peer_unimport(void* area);
+int sgs_peer_desc_create(int world, int rank, int k, void* const* areas, void** desc);
+int sgs_peer_desc_free(void* desc);
+int sgs_peer_begin(void* desc, void* stream);
 int sgs_ls_cluster_size(int k);
 int sgs_ls_step(const sgs_ls_args* a, void* stream);
 

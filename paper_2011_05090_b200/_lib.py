@@ -26,6 +26,7 @@ ST_OK = 0
 ST_BREAKDOWN = 1
 ST_RANK = 2
 ST_CONVERGED = 3
+ST_TIMEOUT = 4
 
 
 class LsArgs(ctypes.Structure):
@@ -46,6 +47,7 @@ class LsArgs(ctypes.Structure):
         ("giv_on", c_int), ("giv_cs", c_void_p), ("giv_sn", c_void_p), ("giv_g", c_void_p),
         ("giv_T", c_void_p), ("giv_ldt", ctypes.c_longlong), ("giv_hist", c_void_p),
         ("giv_tol", c_double),
+        ("peer", c_void_p),
     ]
 
 
@@ -107,6 +109,15 @@ _SIGS = {
     "sgs_ls_scratch_elems": (c_int64, [c_int, c_int]),
     "sgs_ls_cluster_size": (c_int, [c_int]),
     "sgs_ls_step": (c_int, [POINTER(LsArgs), c_void_p]),
+    "sgs_peer_bytes": (c_int64, [c_int, c_int, c_int]),
+    "sgs_peer_alloc": (c_int, [c_int64, POINTER(c_void_p)]),
+    "sgs_peer_free": (c_int, [c_void_p]),
+    "sgs_peer_export": (c_int, [c_void_p, ctypes.c_char_p]),
+    "sgs_peer_import": (c_int, [ctypes.c_char_p, POINTER(c_void_p)]),
+    "sgs_peer_unimport": (c_int, [c_void_p]),
+    "sgs_peer_desc_create": (c_int, [c_int, c_int, c_int, POINTER(c_void_p), POINTER(c_void_p)]),
+    "sgs_peer_desc_free": (c_int, [c_void_p]),
+    "sgs_peer_begin": (c_int, [c_void_p, c_void_p]),
     "sgs_csr_spmv": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p,
                              c_void_p, c_void_p, c_void_p, c_void_p]),
     "sgs_norm2": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_void_p, c_void_p]),

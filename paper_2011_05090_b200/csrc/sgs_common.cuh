@@ -206,6 +206,24 @@ inline int check_ex(cudaError_t e, const char* what) {
 // (c1: 5800 -> 6014 columns/s on the same power-capped box class).
 constexpr int kTileGroup = 4;
 
+// Device descriptor of a row-sharded state's peer exchange (sgs_peer_*):
+// rank q's area holds, at fixed offsets, its generation counter, the receive
+// slots recv[parity][source rank][k] (fp64) and the flags
+// flags[parity][source rank][CTA of the LS cluster].
+constexpr int kPeerMaxWorld = 8;
+constexpr int kPeerMaxCl = 16;
+struct sgs_peer_desc_dev {
+  int world, rank, k, pad;
+  unsigned char* area[kPeerMaxWorld];
+};
+__host__ __device__ inline int64_t peer_recv_off() { return 256; }
+__host__ __device__ inline int64_t peer_flag_off(int world, int k) {
+  return 256 + ((int64_t)2 * world * k * 8 + 255) / 256 * 256;
+}
+__host__ __device__ inline int64_t peer_area_bytes(int world, int k) {
+  return peer_flag_off(world, k) + (int64_t)2 * world * kPeerMaxCl * 4;
+}
+
 // Canonical order for summing per-CTA partials (used by every consumer so
 // that the same vector reduced by different kernels gives the same bits):
 // eight interleaved ascending chains acc_g = sum_{p = g mod 8} x_p, then

@@ -492,6 +492,79 @@ __device__ __noinline__ void ls_reduce_parts(const double* parts, int nparts, in
   }
   __syncthreads();
 }
+// s' of a row-sharded state summed across the ranks inside the LS launch
+// (sgs_ls_args.peer): this CTA's rows of the local partials in the canonical
+// order (scale 1), stored into every rank's receive slots
+// recv[parity][this rank] over NVLink, flagged (release, system scope) with
+// the epoch (generation, column); then the CTA waits for the same rows of
+// every rank and adds them in rank order from 0.0.  Every rank therefore
+// holds bit-identical s' (the replicated LS needs no broadcast), and for one
+// rank it is the unsharded reduction's s' bit for bit.  Receive slots and
+// flags alternate by column parity: a rank can run at most one column ahead
+// of another (its next finalize waits for the other's flags).  Returns true
+// when the factorisation stopped (status) or the wait timed out.
+template <typename T>
+__device__ __noinline__ bool ls_peer_sum(const sgs_peer_desc_dev* d, const double* parts,
+                                         int nparts, int k, int ra, int nr, double scale, T* v,
+                                         double* red, int col, int cta, sgs_status* st) {
+  if constexpr (sizeof(T) != 8) {
+    return true;  // the host enables the exchange for an fp64 LS only
+  } else {
+    __shared__ int stop;
+    const int world = d->world, me = d->rank, par = col & 1;
+    ls_reduce_parts<T>(parts, nparts, k, ra, nr, 1.0, v, red);  // local rows, exact sums
+    const unsigned int gen =
+        *reinterpret_cast<volatile const unsigned int*>(d->area[me]);
+    const unsigned int epoch = gen * 8192u + (unsigned int)col;
+    for (int q = 0; q < world; ++q) {
+      double* dst = reinterpret_cast<double*>(d->area[q] + peer_recv_off()) +
+                    ((int64_t)par * world + me) * k + ra;
+      for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) dst[rr] = v[rr];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      stop = 0;
+      for (int q = 0; q < world; ++q) {
+        unsigned int* f = reinterpret_cast<unsigned int*>(d->area[q] + peer_flag_off(world, k)) +
+                          ((int64_t)par * world + me) * kPeerMaxCl + cta;
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+      }
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < world) {
+      const unsigned int* f = reinterpret_cast<const unsigned int*>(d->area[me] +
+                                                                    peer_flag_off(world, k)) +
+                              ((int64_t)par * world + threadIdx.x) * kPeerMaxCl + cta;
+      const unsigned long long t0 = gtimer();
+      for (;;) {
+        unsigned int x;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(x) : "l"(f) : "memory");
+        if (x == epoch) break;
+        if (*reinterpret_cast<volatile const int64_t*>(&st->code) != 0) { stop = 1; break; }
+        if (gtimer() - t0 > 4000000000ULL) {
+          atomicCAS(reinterpret_cast<unsigned long long*>(&st->code), 0ULL,
+                    (unsigned long long)SGS_ST_TIMEOUT);
+          stop = 1;
+          break;
+        }
+        __nanosleep(64);
+      }
+    }
+    __syncthreads();
+    if (stop) return true;
+    const double* rcv = reinterpret_cast<const double*>(d->area[me] + peer_recv_off()) +
+                        (int64_t)par * world * k + ra;
+    for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
+      double sacc = 0.0;
+      for (int q = 0; q < world; ++q) sacc += __ldcg(rcv + (int64_t)q * k + rr);
+      v[rr] = from_double<T>(scale * sacc);
+    }
+    __syncthreads();
+    return false;
+  }
+}
+
 // Two partial sets (s' and p' of a one-synchronisation launch) in one pass,
 // all loads of a row in flight together; each chain sums in ls_reduce_parts'
 // order, so the results are bit-identical to two separate calls.
@@ -810,6 +883,10 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     } else if (lag) {  // s' and p' together
       ls_reduce_parts2<T>(a.s_partials, a.s_nparts, a.s_scale, vs, a.p_partials, a.p_nparts,
                           a.p_scale, vp, k, ra, nr, dred);
+    } else if (a.peer != nullptr) {  // s' summed across the ranks here (row-sharded state)
+      if (ls_peer_sum<T>(static_cast<const sgs_peer_desc_dev*>(a.peer), a.s_partials, a.s_nparts,
+                         k, ra, nr, a.s_scale, vs, dred, i, rank, a.st))
+        return;  // uniform: every rank and CTA sees the same status / flags
     } else {
       ls_reduce_parts<T>(a.s_partials, a.s_nparts, k, ra, nr, a.s_scale, vs, dred);
     }
@@ -1233,6 +1310,8 @@ extern "C" int sgs_ls_step(const sgs_ls_args* a, void* stream) {
               "ls_step: fused solve must target the next column");
   SGS_REQUIRE(!a->p_lag || (a->do_finalize && a->do_solve && a->p_partials),
               "ls_step: p_lag needs a fused finalize + solve with p partials");
+  SGS_REQUIRE(!a->peer || (a->fine_dtype == SGS_F64 && !a->p_lag && ls_cluster_size_host(a->k) <= kPeerMaxCl),
+              "ls_step: the peer exchange needs an fp64 LS (no p_lag)");
   SGS_REQUIRE(!a->giv_on || (a->do_finalize && a->col_fin >= 1 && a->giv_cs && a->giv_sn &&
                              a->giv_g && a->giv_T && a->giv_hist && a->giv_ldt >= a->col_fin + 1),
               "ls_step: giv_on needs a finalize of column >= 1 and the Givens arrays");

@@ -27,7 +27,8 @@ class TorchComm:
         self.world = dist.get_world_size(group)
         # NCCL collectives are stream-ordered device work and can be captured
         # in a CUDA graph with the kernels around them; gloo runs on the host
-        self.capturable = dist.get_backend(group) == "nccl"
+        self.backend = dist.get_backend(group)
+        self.capturable = self.backend == "nccl"
 
     def allreduce_(self, t: torch.Tensor) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
@@ -54,6 +55,64 @@ class TorchComm:
             for r, c in enumerate(counts):
                 out[o:o + c].copy_(buf[r, :c])
                 o += c
+
+
+class PeerExchange:
+    """The peer-memory exchange area of a row-sharded RGS state (sgs_peer_*):
+    every rank allocates an area (receive slots + flags), exports its CUDA IPC
+    handle, gathers the others' (a host all_gather_object over the process
+    group) and maps them; the device descriptor lists the ranks' areas as seen
+    from this rank.  The LS launch then sums s' across the ranks by NVLink
+    stores into these areas instead of an NCCL all-reduce per column.  One
+    node only (IPC), world <= 8; the caller picks it for NCCL groups."""
+
+    def __init__(self, comm: TorchComm, k: int, cl: int):
+        import ctypes
+        from . import _lib
+        lib = _lib.load()
+        self.lib, self.world, self.rank = lib, comm.world, comm.rank
+        nbytes = int(lib.sgs_peer_bytes(comm.world, k, cl))
+        if nbytes <= 0:
+            raise ValueError(f"peer exchange: unsupported world={comm.world} / k={k} / cl={cl}")
+        area = ctypes.c_void_p()
+        _lib.check(lib.sgs_peer_alloc(nbytes, ctypes.byref(area)), "sgs_peer_alloc")
+        self.area = area.value
+        handle = ctypes.create_string_buffer(64)
+        _lib.check(lib.sgs_peer_export(self.area, handle), "sgs_peer_export")
+        handles = [None] * comm.world
+        dist.all_gather_object(handles, handle.raw, group=comm.group)
+        self.imported = []
+        areas = (ctypes.c_void_p * comm.world)()
+        for q, h in enumerate(handles):
+            if q == comm.rank:
+                areas[q] = self.area
+                continue
+            p = ctypes.c_void_p()
+            _lib.check(lib.sgs_peer_import(ctypes.create_string_buffer(h, 64), ctypes.byref(p)),
+                       "sgs_peer_import")
+            areas[q] = p.value
+            self.imported.append(p.value)
+        desc = ctypes.c_void_p()
+        _lib.check(lib.sgs_peer_desc_create(comm.world, comm.rank, k, areas, ctypes.byref(desc)),
+                   "sgs_peer_desc_create")
+        self.desc = desc.value
+
+    def begin(self, stream_ptr: int) -> None:
+        """Open a factorisation (next flag generation), stream-ordered."""
+        from . import _lib
+        _lib.check(self.lib.sgs_peer_begin(self.desc, stream_ptr), "sgs_peer_begin")
+
+    def close(self) -> None:
+        lib = self.lib
+        if getattr(self, "desc", None):
+            lib.sgs_peer_desc_free(self.desc)
+            self.desc = None
+        for p in getattr(self, "imported", []):
+            lib.sgs_peer_unimport(p)
+        self.imported = []
+        if getattr(self, "area", None):
+            lib.sgs_peer_free(self.area)
+            self.area = None
 
 
 def init_from_env(backend: str = "nccl") -> TorchComm | None:

@@ -298,7 +298,7 @@ class RgsState:
     # ---- kernels ---------------------------------------------------------------
     def _ls(self, *, fin: int | None = None, s_parts=None, s_nparts=0, s_scale=1.0,
             sol: int | None = None, p_parts=None, p_nparts=0, p_scale=1.0,
-            lag: bool = False, giv=None) -> None:
+            lag: bool = False, giv=None, peer: bool = False) -> None:
         a = self.__dict__.get("_ls_args")
         if a is None:
             a = self._ls_args = _lib.LsArgs()  # reused: the library copies it at launch
@@ -322,6 +322,7 @@ class RgsState:
             a.giv_cs, a.giv_sn, a.giv_g = cs.data_ptr(), sn.data_ptr(), g.data_ptr()
             a.giv_T, a.giv_ldt, a.giv_hist = T.data_ptr(), T.shape[1], hist.data_ptr()
             a.giv_tol = -1.0 if tol is None else float(tol)
+        a.peer = self._peer.desc if peer else None  # s' summed across ranks in the LS launch
         a.bf_ucrs = self.breakdown_factor * self.policy.u_crs
         a.S, a.P, a.R = self._S.data_ptr(), self._P.data_ptr(), self._R.data_ptr()
         a.Qs, a.Rinv, a.alpha = self._Qs.data_ptr(), self._Rinv.data_ptr(), self._alpha.data_ptr()
@@ -368,6 +369,15 @@ class RgsState:
         self.theta.partials_into(x_ptr, x_code, ldx, 1, out, n_local=self.n_local,
                                  row0=self.row0, status=self.status, **kw)
         return self._combine(out, self.nparts, kvec)
+
+    def _peer_ok(self) -> bool:
+        """The in-LS peer exchange of s' serves row-sharded fused SRHT states on
+        an NCCL group (one node) with an fp64 LS (SGS_PEER=0 keeps the
+        per-column NCCL all-reduce)."""
+        c = self.comm
+        return (_PEER and c is not None and getattr(c, "backend", None) == "nccl"
+                and getattr(c, "world", 1) <= 8 and self.fused and not self.phi_fused
+                and self.fdt == torch.float64)
 
     def _update(self, i: int, w_ptr: int, w_code: int, normalize_prev: bool) -> None:
         call("sgs_rgs_update", self._Q.data_ptr(), self.ccode, self.ldq, self.n_local, i,
@@ -499,6 +509,9 @@ class RgsState:
             raise BreakdownError(st["column"], st["r_ii"], st["tol"])
         if code == _lib.ST_RANK:
             raise np.linalg.LinAlgError("sketched basis numerically rank deficient")
+        if code == _lib.ST_TIMEOUT:
+            raise RuntimeError("the LS step timed out waiting for another rank's sketch "
+                               "(peer exchange; SGS_PEER=0 uses NCCL all-reduces)")
 
     # ---- streaming API -----------------------------------------------------------
     def _as_device_column(self, w) -> torch.Tensor:
@@ -683,6 +696,15 @@ class RgsState:
                     call("sgs_partials_reduce", kbp.data_ptr(), 1, kp_, nc, ph.scale, pdst,
                          self.fcode, kp_, self.status.ptr, sp)
             self._keep_phi = pparts
+        # row-sharded over NCCL: the LS launch sums s' across the ranks by
+        # NVLink stores into the peers' exchange areas (no all-reduce per column)
+        peer = self._peer_ok()
+        if peer:
+            if self.__dict__.get("_peer") is None:
+                from .distributed import PeerExchange
+                self._peer = PeerExchange(self.comm, self.k,
+                                          int(_lib.load().sgs_ls_cluster_size(self.k)))
+            self._peer.begin(stream_ptr())
         for i in range(m):
             sol = i + 1 if i + 1 < m else None
             if i == 0:
@@ -690,9 +712,10 @@ class RgsState:
                 phq = self._phi_q_parts(0)
                 self._ls(fin=0, sol=sol)
             else:
-                spp, snp, ssc = self._column(i, base + i * ldw * esz, wc, True, True)
+                spp, snp, ssc = self._column(i, base + i * ldw * esz, wc, True, True,
+                                             combine=not peer)
                 phq = self._phi_q_parts(i)
-                self._ls(fin=i, s_parts=spp, s_nparts=snp, s_scale=ssc, sol=sol)
+                self._ls(fin=i, s_parts=spp, s_nparts=snp, s_scale=ssc, sol=sol, peer=peer)
             self._phi_q_finish(i, phq)
         self._normalize(m - 1)
         self._keep = parts  # keep the chunk buffer alive for graph replays
@@ -873,6 +896,10 @@ _PINNED_POOL: list = []
 # CTAs, while the separate sketch kernel runs it at full occupancy; the q'
 # re-read it saves is an L2 hit.
 _RAD_FUSED = os.environ.get("SGS_RAD_FUSED", "0") == "1"
+
+# SGS_PEER=0: row-sharded states all-reduce s' with NCCL per column instead of
+# the peer-memory exchange inside the LS launch (A/B switch)
+_PEER = os.environ.get("SGS_PEER", "1") != "0"
 
 # SGS_PHI_FUSED=0 sketches Phi q' with its own launch (A/B and parity switch)
 _PHI_FUSED = os.environ.get("SGS_PHI_FUSED", "1") != "0"

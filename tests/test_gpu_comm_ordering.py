@@ -13,7 +13,10 @@ NCCL cannot run two ranks on one GPU, so two checks stand in for it:
   factors would differ from the unsharded run.
 * A real NCCL process group of world size 1 (spawned process): the NCCL
   collective code paths, eager and captured in a CUDA graph, must reproduce
-  the unsharded factorisation bit for bit.  With two or more GPUs a 2-rank
+  the unsharded factorisation bit for bit - with s' summed by the LS
+  launch's peer-memory exchange (CUDA IPC areas, release/acquire flags at
+  system scope; here the one rank is its own peer) and with the per-column
+  NCCL all-reduce (SGS_PEER=0).  With two or more GPUs a 2-rank
   NCCL run is checked against the gloo run (skipped on one GPU).
 """
 
@@ -130,6 +133,20 @@ def _nccl_worker(rank, world, port, backend, out):
             st.factorize_columns(Wd, n_loc, m)
         f = st.device_factors()
         res[graph] = tuple(t.cpu().numpy() for t in (f.Q, f.R, f.S, f.P))
+        if comm.capturable:  # NCCL: s' summed by the peer-memory exchange in the LS launch
+            assert st.__dict__.get("_peer") is not None
+    if comm.capturable:  # and with the per-column NCCL all-reduce instead (SGS_PEER=0)
+        from paper_2011_05090_b200 import gram_schmidt as gsm
+        old, gsm._PEER = gsm._PEER, False
+        try:
+            st = sg.RgsState(th, sg.MIXED32_64, capacity=m + 1, breakdown_factor=0.0, comm=comm,
+                             row0=row0, n_local=n_loc)
+            st.factorize_columns(Wd, n_loc, m)
+            assert st.__dict__.get("_peer") is None
+            f = st.device_factors()
+            res["nccl_allreduce"] = tuple(t.cpu().numpy() for t in (f.Q, f.R, f.S, f.P))
+        finally:
+            gsm._PEER = old
     # row-sharded RGMRES: halo exchange / all-gather over this backend
     N = 12
     rp, ci, va = convdiff3d(N)
@@ -156,9 +173,9 @@ def test_nccl_world1_eager_and_graph_match_unsharded(cuda):
     n, m, k = 3 * 4096 + 777, 40, 200
     th = sg.make_sketch(sg.SketchKind.PSRHT, k, n, 3)
     ref = _factor(make_w(n, m, 1e-6, 3, dtype=np.float32), th, sg.MIXED32_64)
-    for graph in (False, True):
-        for a, b in zip(ref, res[graph]):
-            assert np.array_equal(a, b), graph
+    for variant in (False, True, "nccl_allreduce"):  # peer exchange eager / graph, NCCL
+        for a, b in zip(ref, res[variant]):
+            assert np.array_equal(a, b), variant
     from paper_2011_05090_b200.workloads import convdiff3d, rhs_gaussian
     N = 12
     rp, ci, va = convdiff3d(N)
