@@ -381,6 +381,9 @@ def run_qr(args, cfg_name, comm):
     barrier()
     clk = clocks.stop()
     launches = _lib.launch_count() - lc0
+    shard_sum = (None if comm is None else
+                 ("peer-memory exchange in the LS launch"
+                  if gstate.__dict__.get("_peer") is not None else "nccl all-reduce"))
     if graph is not None:
         gstate.finish()  # raises if the replayed factorisation recorded a breakdown
         launches = graph_launches * args.steps
@@ -512,9 +515,7 @@ def run_qr(args, cfg_name, comm):
             "graph": graph_used,
             # how a row-sharded state sums s' per column: inside the LS launch by
             # NVLink stores into the peers' exchange areas, or an NCCL all-reduce
-            "shard_sum": (None if comm is None else
-                          ("peer-memory exchange in the LS launch"
-                           if gstate.__dict__.get("_peer") is not None else "nccl all-reduce")),
+            "shard_sum": shard_sum,
             "hbm_gbs_whole_step": round(hbm_gbs, 1),
             "hbm_frac_whole_step": round(hbm_gbs / (peak * world), 4),
             # BASELINE.json quotes the nominal ~8 TB/s; the roofline uses the measured peak

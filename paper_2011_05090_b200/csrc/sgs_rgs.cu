@@ -521,14 +521,21 @@ __device__ __noinline__ bool ls_peer_sum(const sgs_peer_desc_dev* d, const doubl
                     ((int64_t)par * world + me) * k + ra;
       for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) dst[rr] = v[rr];
     }
-    __threadfence_system();
-    __syncthreads();
+    __syncthreads();  // the CTA's rows are stored; thread 0 publishes them
     if (threadIdx.x == 0) {
       stop = 0;
+      // one fence for the CTA (cumulative over the barrier): system scope for
+      // peers on other GPUs, GPU scope when the only "peer" is this GPU (a
+      // system fence per thread measured ~8 % of a c1 step under PCIe traffic)
+      if (world > 1) __threadfence_system();
+      else __threadfence();
       for (int q = 0; q < world; ++q) {
         unsigned int* f = reinterpret_cast<unsigned int*>(d->area[q] + peer_flag_off(world, k)) +
                           ((int64_t)par * world + me) * kPeerMaxCl + cta;
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+        if (world > 1)
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+        else
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
       }
     }
     __syncthreads();

@@ -97,6 +97,20 @@ class PeerExchange:
                    "sgs_peer_desc_create")
         self.desc = desc.value
 
+    _cache: dict = {}
+
+    @classmethod
+    def get(cls, comm: TorchComm, k: int, cl: int) -> "PeerExchange":
+        """One exchange per (communicator, k, LS cluster size), reused by every
+        state on it (the IPC set-up is a host collective; factorisations on one
+        communicator run one at a time, each opening its own generation)."""
+        key = (id(comm.group) if comm.group is not None else None, comm.world, comm.rank, k, cl,
+               torch.cuda.current_device())
+        ex = cls._cache.get(key)
+        if ex is None:
+            ex = cls._cache[key] = cls(comm, k, cl)
+        return ex
+
     def begin(self, stream_ptr: int) -> None:
         """Open a factorisation (next flag generation), stream-ordered."""
         from . import _lib

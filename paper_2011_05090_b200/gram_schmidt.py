@@ -702,8 +702,8 @@ class RgsState:
         if peer:
             if self.__dict__.get("_peer") is None:
                 from .distributed import PeerExchange
-                self._peer = PeerExchange(self.comm, self.k,
-                                          int(_lib.load().sgs_ls_cluster_size(self.k)))
+                self._peer = PeerExchange.get(self.comm, self.k,
+                                              int(_lib.load().sgs_ls_cluster_size(self.k)))
             self._peer.begin(stream_ptr())
         for i in range(m):
             sol = i + 1 if i + 1 < m else None
@@ -823,6 +823,13 @@ class RgsState:
             with torch.cuda.stream(d2h):
                 Ph.copy_(self._P[:m], non_blocking=True)
 
+        peer = self._peer_ok()  # s' summed across ranks in the LS launch (as the device path)
+        if peer:
+            if self.__dict__.get("_peer") is None:
+                from .distributed import PeerExchange
+                self._peer = PeerExchange.get(self.comm, self.k,
+                                              int(_lib.load().sgs_ls_cluster_size(self.k)))
+            self._peer.begin(stream_ptr())
         sketch_chunk(0)
         if nchunks == 1:
             ship_p()
@@ -838,8 +845,9 @@ class RgsState:
                 self._column(0, base, wc, False, False)
                 self._ls(fin=0, sol=sol)
             else:
-                spp, snp, ssc = self._column(i, base + i * n * esz, wc, True, True)
-                self._ls(fin=i, s_parts=spp, s_nparts=snp, s_scale=ssc, sol=sol)
+                spp, snp, ssc = self._column(i, base + i * n * esz, wc, True, True,
+                                             combine=not peer)
+                self._ls(fin=i, s_parts=spp, s_nparts=snp, s_scale=ssc, sol=sol, peer=peer)
                 # columns < i are final once the column kernel i has normalised
                 # i-1; finer copies over the last columns keep the tail short
                 step = ship_chunk if i < m - self._e2e_tail else min(ship_chunk, 2)

@@ -147,6 +147,12 @@ def _nccl_worker(rank, world, port, backend, out):
             res["nccl_allreduce"] = tuple(t.cpu().numpy() for t in (f.Q, f.R, f.S, f.P))
         finally:
             gsm._PEER = old
+    # the end-to-end path (pinned host W, chunked H2D / compute / D2H) sharded
+    pin = torch.empty((m, n_loc), dtype=torch.float32, pin_memory=True)
+    pin.copy_(torch.from_numpy(np.ascontiguousarray(W.T)))
+    f, _ = sg.rgs_factorize(pin.numpy().T, th, sg.MIXED32_64, breakdown_factor=0.0, comm=comm,
+                            row0=row0, with_certificate=False)
+    res["pipelined"] = tuple(np.asarray(x) for x in (f.Q, f.R, f.S, f.P))
     # row-sharded RGMRES: halo exchange / all-gather over this backend
     N = 12
     rp, ci, va = convdiff3d(N)
@@ -173,7 +179,7 @@ def test_nccl_world1_eager_and_graph_match_unsharded(cuda):
     n, m, k = 3 * 4096 + 777, 40, 200
     th = sg.make_sketch(sg.SketchKind.PSRHT, k, n, 3)
     ref = _factor(make_w(n, m, 1e-6, 3, dtype=np.float32), th, sg.MIXED32_64)
-    for variant in (False, True, "nccl_allreduce"):  # peer exchange eager / graph, NCCL
+    for variant in (False, True, "nccl_allreduce", "pipelined"):  # peer eager/graph, NCCL, e2e
         for a, b in zip(ref, res[variant]):
             assert np.array_equal(a, b), variant
     from paper_2011_05090_b200.workloads import convdiff3d, rhs_gaussian
