@@ -8,7 +8,7 @@
 // re-reading q' - flips the signs, runs the 4096-point Walsh-Hadamard
 // transform (3 bits in registers, 9 bits in three shared-memory radix-8
 // passes), gathers the k sampled rows with the cross-tile sign
-// (-1)^popcount(r_hi & tile), and sums the k-vectors of its kTileGroup-CTA cluster
+// (-1)^popcount(r_hi & tile), and sums the k-vectors of its cluster (tile_group CTAs)
 // through distributed shared memory.  One partial k-vector per cluster is
 // written, exactly as sgs_srht_partials would for a one-tile-per-CTA grid.
 
@@ -26,7 +26,6 @@ namespace sgs {
 constexpr int kColThreads = 512;
 constexpr int kColLogT = 12;
 constexpr int kColT = 1 << kColLogT;
-constexpr int kColCluster = kTileGroup;  // tiles per partial (sgs_common.cuh)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -98,7 +97,7 @@ struct ColPhi {
   const int32_t* samples;     // (nblocks, kphi) block-local sample rows
   int k;
   int log2_block;
-  double* partials;           // one kphi-vector per kTileGroup-CTA cluster
+  double* partials;           // one kphi-vector per cluster (tile_group tiles)
 };
 
 template <typename TQ, typename TW, bool PHI>
@@ -365,23 +364,24 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
   }
   cl.sync();
   const int rank = (int)cl.block_rank();
-  const int j0 = (int)(((int64_t)rank * k) / kColCluster);
-  const int j1 = (int)(((int64_t)(rank + 1) * k) / kColCluster);
-  double* outp = partials + (int64_t)(blockIdx.x / kColCluster) * k;
+  const int G = (int)cl.num_blocks();  // tile_group(n): tiles per partial
+  const int j0 = (int)(((int64_t)rank * k) / G);
+  const int j1 = (int)(((int64_t)(rank + 1) * k) / G);
+  double* outp = partials + (int64_t)(blockIdx.x / G) * k;
   for (int j = j0 + tid; j < j1; j += blockDim.x) {
     double s = 0.0;
 #pragma unroll
-    for (int q = 0; q < kColCluster; ++q) s += cl.map_shared_rank(part, q)[j];
+    for (int q = 0; q < G; ++q) s += cl.map_shared_rank(part, q)[j];
     outp[j] = s;
   }
   if constexpr (PHI) {
-    const int p0 = (int)(((int64_t)rank * phi.k) / kColCluster);
-    const int p1 = (int)(((int64_t)(rank + 1) * phi.k) / kColCluster);
-    double* outq = phi.partials + (int64_t)(blockIdx.x / kColCluster) * phi.k;
+    const int p0 = (int)(((int64_t)rank * phi.k) / G);
+    const int p1 = (int)(((int64_t)(rank + 1) * phi.k) / G);
+    double* outq = phi.partials + (int64_t)(blockIdx.x / G) * phi.k;
     for (int j = p0 + tid; j < p1; j += blockDim.x) {
       double s = 0.0;
 #pragma unroll
-      for (int q = 0; q < kColCluster; ++q) s += cl.map_shared_rank(part2, q)[j];
+      for (int q = 0; q < G; ++q) s += cl.map_shared_rank(part2, q)[j];
       outq[j] = s;
     }
   }
@@ -391,7 +391,8 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
 
 static int64_t column_ctas(int64_t n_local) {
   const int64_t nt = (n_local + kColT - 1) / kColT;
-  return (nt + kColCluster - 1) / kColCluster * kColCluster;
+  const int G = tile_group(n_local);
+  return (nt + G - 1) / G * G;
 }
 
 // ===========================================================================
@@ -771,7 +772,7 @@ extern "C" int sgs_rgs_update_rademacher(void* Q, int q_dtype, int64_t ldq, int6
 }
 
 extern "C" int sgs_column_nparts(int64_t n_local) {
-  return n_local < 1 ? 0 : (int)(column_ctas(n_local) / kColCluster);
+  return n_local < 1 ? 0 : (int)(column_ctas(n_local) / tile_group(n_local));
 }
 
 static int update_srht_impl(void* Q, int q_dtype, int64_t ldq, int64_t n, int i, const void* w,
@@ -828,7 +829,7 @@ static int update_srht_impl(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
   do {                                                                                        \
     auto kern = use_phi ? rgs_column_kernel<TQ, TW, true> : rgs_column_kernel<TQ, TW, false>; \
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
-    err = launch_ex(kern, dim3((unsigned)nctas), dim3(kColThreads), smem, s, kColCluster,     \
+    err = launch_ex(kern, dim3((unsigned)nctas), dim3(kColThreads), smem, s, tile_group(n),   \
                     static_cast<TQ*>(Q), ldq, n, i, static_cast<const TW*>(w), w_div,        \
                     static_cast<const TQ*>(r_crs), normalize_prev, R, ldr, do_sketch, row0,  \
                     log2_block, sign_bits, samples, k, partials, st, debug_timeline(), pf,    \

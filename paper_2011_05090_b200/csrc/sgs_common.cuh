@@ -196,15 +196,23 @@ inline int check_ex(cudaError_t e, const char* what) {
   return check_launch(what);
 }
 
-// 4096-row SRHT tiles are summed in groups of kTileGroup consecutive tiles
-// into one partial k-vector: by one CTA in tile order (batches), or by a
-// cluster of kTileGroup CTAs through DSMEM in rank order (one column, and the
-// fused column kernel's epilogue) - the same bits either way.  Groups of 4
-// (was 8) make c1's column grid 62 clusters of 4 instead of 31 of 8: it then
-// leaves a GPC free, so the 16-CTA LS cluster of the column is resident from
-// the column kernel's start and its pre-wait part overlaps the Q stream
-// (c1: 5800 -> 6014 columns/s on the same power-capped box class).
-constexpr int kTileGroup = 4;
+// 4096-row SRHT tiles are summed in groups of tile_group(n_local) consecutive
+// tiles into one partial k-vector: by one CTA in tile order (batches), or by
+// a cluster of that many CTAs through DSMEM in rank order (one column, and
+// the fused column kernel's epilogue) - the same bits either way, and the same
+// group for every kernel that sketches a vector of that length.  Groups of 4
+// for grids of up to 256 tiles: c1's column grid is then 62 clusters of 4
+// instead of 31 of 8 and leaves a GPC free, so the 16-CTA LS cluster of the
+// column is resident from the column kernel's start and its pre-wait part
+// overlaps the Q stream (c1: 5800 -> 5928 columns/s on the same power-capped
+// box class).  Larger (multi-wave) grids keep groups of 8: half the partials
+// for the LS to reduce (c3's 512 tiles: the one-sync fp32 variant 3584 ->
+// 3675 Arnoldi steps/s).
+constexpr int kTileGroupMax = 8;
+__host__ __device__ inline int tile_group(int64_t n_local) {
+  const int64_t nt = (n_local + 4095) / 4096;
+  return nt <= 256 ? 4 : 8;
+}
 
 // Device descriptor of a row-sharded state's peer exchange (sgs_peer_*):
 // rank q's area holds, at fixed offsets, its generation counter, the receive

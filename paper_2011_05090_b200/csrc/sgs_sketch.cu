@@ -380,7 +380,7 @@ srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t
     if constexpr (PAIR) tile(lr0, b2.sign_bits, b2.log2_block, smp2, b2.k, part2);
   }
   if constexpr (!CLUSTERED) {
-    // kTileGroup tiles accumulated in tile order from 0.0: the cluster sum below, bit
+    // tiles_per_cta tiles accumulated in tile order from 0.0: the cluster sum below, bit
     // for bit ((0 + z0) + z1 ... = 0 + (0 + z0) + (0 + z1) ...)
     __syncthreads();
     double* out = partials + ((int64_t)col * gridDim.x + blockIdx.x) * k;
@@ -393,25 +393,26 @@ srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t
   } else {
     cg::cluster_group cl = cg::this_cluster();
     cl.sync();  // all k-vectors of the cluster are final
-    const int ngroups = gridDim.x / kTileGroup;
+    const int G = (int)cl.num_blocks();  // tile_group(n_local)
+    const int ngroups = gridDim.x / G;
     const int rank = (int)cl.block_rank();
-    const int j0 = (int)(((int64_t)rank * k) / kTileGroup);
-    const int j1 = (int)(((int64_t)(rank + 1) * k) / kTileGroup);
-    double* out = partials + ((int64_t)col * ngroups + blockIdx.x / kTileGroup) * k;
+    const int j0 = (int)(((int64_t)rank * k) / G);
+    const int j1 = (int)(((int64_t)(rank + 1) * k) / G);
+    double* out = partials + ((int64_t)col * ngroups + blockIdx.x / G) * k;
     for (int j = j0 + t; j < j1; j += kTileThreads) {
       double s = 0.0;
 #pragma unroll
-      for (int q = 0; q < kTileGroup; ++q) s += cl.map_shared_rank(part, q)[j];
+      for (int q = 0; q < G; ++q) s += cl.map_shared_rank(part, q)[j];
       out[j] = s;
     }
     if constexpr (PAIR) {
-      const int p0 = (int)(((int64_t)rank * b2.k) / kTileGroup);
-      const int p1 = (int)(((int64_t)(rank + 1) * b2.k) / kTileGroup);
-      double* out2 = b2.partials + ((int64_t)col * ngroups + blockIdx.x / kTileGroup) * b2.k;
+      const int p0 = (int)(((int64_t)rank * b2.k) / G);
+      const int p1 = (int)(((int64_t)(rank + 1) * b2.k) / G);
+      double* out2 = b2.partials + ((int64_t)col * ngroups + blockIdx.x / G) * b2.k;
       for (int j = p0 + t; j < p1; j += kTileThreads) {
         double s = 0.0;
 #pragma unroll
-        for (int q = 0; q < kTileGroup; ++q) s += cl.map_shared_rank(part2, q)[j];
+        for (int q = 0; q < G; ++q) s += cl.map_shared_rank(part2, q)[j];
         out2[j] = s;
       }
     }
@@ -428,7 +429,7 @@ static size_t srht_tile_smem(int k, int k2 = 0) {
 }
 
 // Partition of a column into tiles and partials.  4096-row tiles (the tile
-// kernel): one partial per kTileGroup consecutive tiles, *nctas = number of partials
+// kernel): one partial per tile_group(n_local) consecutive tiles, *nctas = number of partials
 // (the fused column kernel's structure).  Smaller tiles (and SGS_SRHT_LEGACY):
 // tiles_per_cta tiles per CTA, one partial per 8-CTA cluster.
 static void srht_geometry(int64_t n_local, int log2_block, int* logt, int64_t* ntiles,
@@ -440,7 +441,8 @@ static void srht_geometry(int64_t n_local, int log2_block, int* logt, int64_t* n
     *logt = lt;
     *ntiles = nt;
     *tpc = 1;
-    *nctas = (int)((nt + kTileGroup - 1) / kTileGroup);
+    const int G = tile_group(n_local);
+    *nctas = (int)((nt + G - 1) / G);
     return;
   }
   const int64_t per = (nt + kSrhtTargetCTAs - 1) / kSrhtTargetCTAs;
@@ -459,12 +461,12 @@ static int launch_srht_t(const void* X, int64_t ldx, int ncols, int64_t n_local,
                          int tpc, int64_t ntiles, int nctas, int geom) {
   if constexpr (LOGT == 12) {
     if (!srht_legacy()) {
-      // one partial per kTileGroup consecutive tiles (nctas = partials here): few
+      // one partial per G = tile_group(n_local) consecutive tiles (nctas = partials): few
       // columns -> one tile per CTA and a DSMEM cluster sum (parallelism);
-      // batches -> one CTA runs its kTileGroup tiles in order (no per-tile prologue
+      // batches -> one CTA runs its G tiles in order (no per-tile prologue
       // or cluster exchange).  Both give the same bits.
       const size_t sm = srht_tile_smem<TX>(k);
-      // geom 1: one CTA per kTileGroup tiles even for one column - a grid of ntiles/4
+      // geom 1: one CTA per G tiles even for one column - a grid of ntiles/G
       // CTAs leaves most SMs free, so a following LS cluster launch finds a
       // GPC and runs its pre-wait part alongside (RGMRES's sketch of w)
       const bool batch = geom == 1 || (geom == 0 && (int64_t)nctas * ncols >= 4 * (int64_t)sm_count());
@@ -472,10 +474,11 @@ static int launch_srht_t(const void* X, int64_t ldx, int ncols, int64_t n_local,
       if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                            cudaSharedmemCarveoutMaxShared);
-      const dim3 grid(batch ? nctas : nctas * kTileGroup, ncols);
-      return check_ex(launch_ex(kern, grid, dim3(kTileThreads), sm, s, batch ? 1 : kTileGroup,
+      const int G = tile_group(n_local);
+      const dim3 grid(batch ? nctas : nctas * G, ncols);
+      return check_ex(launch_ex(kern, grid, dim3(kTileThreads), sm, s, batch ? 1 : G,
                                 static_cast<const TX*>(X), ldx, n_local, row0, log2_block,
-                                sign_bits, samples, k, batch ? kTileGroup : 1, ntiles, partials,
+                                sign_bits, samples, k, batch ? G : 1, ntiles, partials,
                                 st, debug_timeline_row(), SrhtSecond{}),
                       "srht_tile_kernel");
     }
@@ -848,10 +851,11 @@ static int launch_srht_pair(const void* X, int64_t ldx, int ncols, int64_t n_loc
   if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                        cudaSharedmemCarveoutMaxShared);
-  const dim3 grid(batch ? nctas : nctas * kTileGroup, ncols);
-  return check_ex(launch_ex(kern, grid, dim3(kTileThreads), sm, s, batch ? 1 : kTileGroup,
+  const int G = tile_group(n_local);
+  const dim3 grid(batch ? nctas : nctas * G, ncols);
+  return check_ex(launch_ex(kern, grid, dim3(kTileThreads), sm, s, batch ? 1 : G,
                             static_cast<const TX*>(X), ldx, n_local, row0, log2_block, sign_bits,
-                            samples, k, batch ? kTileGroup : 1, ntiles, partials, st,
+                            samples, k, batch ? G : 1, ntiles, partials, st,
                             debug_timeline_row(), b2),
                   "srht_tile_kernel(pair)");
 }
