@@ -253,7 +253,16 @@ class RgsState:
         if self._cap:
             old = (self._Q, self._R, self._S, self._P, self._Qs, self._Rinv, self._alpha,
                    self._cap)
-        self._Q = torch.zeros((cap, self.ldq), dtype=self.cdt, device=dev)
+        # Q columns are written before they are read (q'_i by the column
+        # kernel i, in place): only the pad rows past n_local need zeros, and
+        # zeroing 2 GB at c1 cost 0.3 ms of every end-to-end call.
+        # SGS_DEBUG_POISON=1 fills Q with NaN instead (tests prove the claim).
+        if _POISON:
+            self._Q = torch.full((cap, self.ldq), float("nan"), dtype=self.cdt, device=dev)
+        else:
+            self._Q = torch.empty((cap, self.ldq), dtype=self.cdt, device=dev)
+        if self.ldq > self.n_local:
+            self._Q[:, self.n_local:].zero_()
         self._R = torch.zeros((cap, cap), dtype=torch.float64, device=dev)
         self._S = torch.zeros((cap, k), dtype=self.fdt, device=dev)
         self._P = torch.zeros((cap, k), dtype=self.fdt, device=dev)
@@ -345,6 +354,13 @@ class RgsState:
     _e2e_late = (192, 64)  # pipelined path: (column from which chunks grow, late chunk cap)
     _e2e_ship = 8          # pipelined path: Q columns per D2H copy
     _e2e_tail = 32         # pipelined path: last columns shipped two at a time
+    _e2e_side = os.environ.get("SGS_E2E_SIDE", "1") != "0"  # pipelined path: side-stream sketches
+    _e2e_ship_far = 32     # side-stream path: Q columns per copy between chunk boundaries
+    _e2e_ahead = 4         # pipelined path: W chunks enqueued ahead of the column loop
+    # side-stream path: no Q copies before this column - both directions at
+    # once run at ~48 GB/s each against ~55 GB/s for H2D alone, and the early
+    # columns are bound by W's arrival
+    _e2e_ship_from = 192
 
     def _trace_ptr(self, col):
         t = self._trace
@@ -739,10 +755,12 @@ class RgsState:
     def factorize_host_pipelined(self, Wh: np.ndarray, m: int, chunk: int = 8) -> QrFactors:
         """End-to-end factorisation of a pinned, column-major host W (n x m,
         Fortran order): W streams to the GPU in column chunks on one copy
-        stream while the compute stream sketches each chunk as it lands and
-        starts the column loop; finished Q columns stream back to a pinned host
-        buffer on a second copy stream.  Returns host factors (Q is a view of
-        pinned memory)."""
+        stream, a side stream sketches each chunk as it lands (P = Theta W),
+        and the compute stream runs the column loop, waiting on a chunk's
+        sketch only before the LS launch that first reads it; finished Q
+        columns stream back to a pinned host buffer on a second copy stream.
+        Returns host factors (Q is a view of pinned memory).  Schedule knobs:
+        the ``_e2e_*`` class attributes."""
         if self.m != 0:
             raise RuntimeError("factorize_host_pipelined needs a fresh state")
         n, k = self.n_local, self.k
@@ -766,22 +784,31 @@ class RgsState:
             # cost as much as 64)
             bounds = list(range(0, m, 64)) + [m]
             c0 = m
-        while c0 < m:
-            c0 = min(m, c0 + min(sz, chunk if c0 < late else late_chunk))
+        while c0 < m:  # 2, 4, ..., chunk; past `late` doubling again up to late_chunk
+            step = min(sz, chunk if c0 < late else late_chunk)
+            c0 = min(m, c0 + step)
             bounds.append(c0)
-            sz *= 2
+            sz = 2 * step
         nchunks = len(bounds) - 1
         chunk_of = np.zeros(m + 1, dtype=np.int64)
         for c in range(nchunks):
             chunk_of[bounds[c]:bounds[c + 1]] = c
+        # Copies and side-stream sketches are enqueued a few chunks ahead of
+        # the column loop rather than all up front: ~40 host calls each would
+        # hold back column 0 by ~1.3 ms of host time, while the host stays well
+        # ahead of the device once the loop runs.
         landed = []
-        with torch.cuda.stream(h2d):
-            for c in range(nchunks):
-                c0, c1 = bounds[c], bounds[c + 1]
-                Wd[c0:c1].copy_(Wt[c0:c1], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(h2d)
-                landed.append(ev)
+
+        def copy_until(c_end):
+            with torch.cuda.stream(h2d):
+                while len(landed) < min(nchunks, c_end):
+                    c0, c1 = bounds[len(landed)], bounds[len(landed) + 1]
+                    Wd[c0:c1].copy_(Wt[c0:c1], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(h2d)
+                    landed.append(ev)
+
+        copy_until(self._e2e_ahead)
         Qh, Qarr = _pinned_buffer((m, n), self.cdt)
         wc, esz, base = _lib.dtype_code(dt), Wd.element_size(), Wd.data_ptr()
         pmax = max(chunk, self._e2e_late[1])
@@ -791,8 +818,17 @@ class RgsState:
         kbuf = (torch.empty((pmax, k), dtype=torch.float64, device=self.device)
                 if self.comm is not None else None)
 
+        # Unsharded states sketch each chunk on a side stream as soon as it
+        # lands, so the compute stream only waits on an event (one broken PDL
+        # edge, before the LS that first reads the chunk's P columns) instead
+        # of running the sketch between an LS and the next column kernel.
+        side = self.comm is None and self._e2e_side
+        sk = torch.cuda.Stream() if side else None
+        sketched = []
+
         def sketch_chunk(c):
-            comp.wait_event(landed[c])
+            copy_until(c + self._e2e_ahead)
+            torch.cuda.current_stream().wait_event(landed[c])
             c0, c1 = bounds[c], bounds[c + 1]
             self.theta.partials_into(base + c0 * n * esz, wc, n, c1 - c0, parts,
                                      n_local=n, row0=self.row0, status=self.status)
@@ -818,7 +854,7 @@ class RgsState:
 
         def ship_p():  # P is final once the last chunk is sketched
             ev = torch.cuda.Event()
-            ev.record(comp)
+            ev.record(sk if side else comp)
             d2h.wait_event(ev)
             with torch.cuda.stream(d2h):
                 Ph.copy_(self._P[:m], non_blocking=True)
@@ -830,28 +866,58 @@ class RgsState:
                 self._peer = PeerExchange.get(self.comm, self.k,
                                               int(_lib.load().sgs_ls_cluster_size(self.k)))
             self._peer.begin(stream_ptr())
-        sketch_chunk(0)
-        if nchunks == 1:
-            ship_p()
+        def sketch_until(c_end):
+            with torch.cuda.stream(sk):
+                while len(sketched) < min(nchunks, c_end):
+                    sketch_chunk(len(sketched))
+                    ev = torch.cuda.Event()
+                    ev.record(sk)
+                    sketched.append(ev)
+                    if len(sketched) == nchunks:
+                        ship_p()
+
+        if side:
+            sk.wait_stream(comp)  # status reset and state set-up
+            sketch_until(2)
+        else:
+            sketch_chunk(0)
+            if nchunks == 1:
+                ship_p()
         shipped, ship_chunk = 0, self._e2e_ship
         for i in range(m):
             nxt = i + 1
-            if nxt < m and bounds[chunk_of[nxt]] == nxt:
+            new_chunk = nxt < m and bounds[chunk_of[nxt]] == nxt
+            if i == 0 and side:
+                comp.wait_event(sketched[0])
+            if new_chunk and not side:
                 sketch_chunk(int(chunk_of[nxt]))
                 if int(chunk_of[nxt]) == nchunks - 1:
                     ship_p()
             sol = nxt if nxt < m else None
             if i == 0:
                 self._column(0, base, wc, False, False)
+                if new_chunk and side:
+                    sketch_until(int(chunk_of[nxt]) + 2)
+                    comp.wait_event(sketched[int(chunk_of[nxt])])
                 self._ls(fin=0, sol=sol)
             else:
                 spp, snp, ssc = self._column(i, base + i * n * esz, wc, True, True,
                                              combine=not peer)
-                self._ls(fin=i, s_parts=spp, s_nparts=snp, s_scale=ssc, sol=sol, peer=peer)
                 # columns < i are final once the column kernel i has normalised
-                # i-1; finer copies over the last columns keep the tail short
+                # i-1; finer copies over the last columns keep the tail short.
+                # On the side-stream path the copies start where the chunk wait
+                # already breaks the PDL chain (an event record breaks it too).
                 step = ship_chunk if i < m - self._e2e_tail else min(ship_chunk, 2)
-                if i - shipped >= step:
+                if side:
+                    if new_chunk:
+                        sketch_until(int(chunk_of[nxt]) + 2)
+                        comp.wait_event(sketched[int(chunk_of[nxt])])
+                    if i >= self._e2e_ship_from and i - shipped >= (
+                            step if new_chunk or i >= m - self._e2e_tail else self._e2e_ship_far):
+                        ship(shipped, i)
+                        shipped = i
+                self._ls(fin=i, s_parts=spp, s_nparts=snp, s_scale=ssc, sol=sol, peer=peer)
+                if not side and i - shipped >= step:
                     ship(shipped, shipped + step)
                     shipped += step
         self._normalize(m - 1)
@@ -868,6 +934,8 @@ class RgsState:
             Rh.copy_(self._R[:m, :m], non_blocking=True)
             Sh.copy_(self._S[:m], non_blocking=True)
         comp.wait_stream(d2h)
+        if side:
+            comp.wait_stream(sk)
         st = self._sync_status()
         if st["code"]:
             self._raise_status(st)
@@ -904,6 +972,9 @@ _PINNED_POOL: list = []
 # CTAs, while the separate sketch kernel runs it at full occupancy; the q'
 # re-read it saves is an L2 hit.
 _RAD_FUSED = os.environ.get("SGS_RAD_FUSED", "0") == "1"
+
+# SGS_DEBUG_POISON=1: fill new Q storage with NaN (uninitialised-read check)
+_POISON = os.environ.get("SGS_DEBUG_POISON", "0") == "1"
 
 # SGS_PEER=0: row-sharded states all-reduce s' with NCCL per column instead of
 # the peer-memory exchange inside the LS launch (A/B switch)
@@ -1071,7 +1142,7 @@ def sketched_lsq(S_prev, p, solver: LsqSolver = HOUSEHOLDER_QR):
     st.breakdown_factor = 0.0  # tol = 0: only an exactly zero column "breaks down"
     st.cdt = st.fdt = fdt
     st.ccode = st.fcode = _lib.dtype_code(fdt)
-    st.ldq = 32
+    st.ldq = st.n_local = 32
     with torch.cuda.device(dev):
         st.status = _lib.Status(dev)
         st._alloc(i + 2)

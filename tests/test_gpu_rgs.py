@@ -192,8 +192,18 @@ def test_device_factors_and_certificates(cuda):
     assert cert.passes_gate()
 
 
-def test_pinned_host_pipeline_matches_device_path(cuda):
+@pytest.mark.parametrize("knobs", [
+    {},
+    # every schedule branch at m = 80: late chunks doubling, Q copies from
+    # column 40, far copies, the two-column tail; and the in-stream sketches
+    {"_e2e_late": (24, 32), "_e2e_ship_from": 40, "_e2e_ship_far": 12, "_e2e_tail": 10,
+     "_e2e_ahead": 2},
+    {"_e2e_side": False, "_e2e_late": (24, 32)},
+])
+def test_pinned_host_pipeline_matches_device_path(cuda, monkeypatch, knobs):
     # the end-to-end path (chunked H2D / compute / D2H overlap) gives the same bits
+    for key, val in knobs.items():
+        monkeypatch.setattr(sg.RgsState, key, val)
     n, m, k = 200_000, 80, 300
     W = make_w(n, m, 1e-8, 21, dtype=np.float32)
     pin = torch.empty((m, n), dtype=torch.float32, pin_memory=True)
