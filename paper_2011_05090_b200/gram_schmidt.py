@@ -760,7 +760,7 @@ class RgsState:
         sketch only before the LS launch that first reads it; finished Q
         columns stream back to a pinned host buffer on a second copy stream.
         Returns host factors (Q is a view of pinned memory).  Schedule knobs:
-        the ``_e2e_*`` class attributes (DESIGN.md section 9)."""
+        the ``_e2e_*`` class attributes (DESIGN.md section 5)."""
         if self.m != 0:
             raise RuntimeError("factorize_host_pipelined needs a fresh state")
         n, k = self.n_local, self.k
