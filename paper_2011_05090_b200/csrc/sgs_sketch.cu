@@ -421,6 +421,168 @@ srht_tile_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t
   }
 }
 
+// Batches of columns (one CTA per tile_group consecutive tiles of a column, no
+// cluster): 256 threads per 4096-row tile, 16 values per thread, three
+// register phases of four butterfly levels - bits 6..9 | 10, 11, 0, 1 | 2..5,
+// the level order of srht_tile_kernel and of the column kernel's epilogue, so
+// the partials are the same bits - with two exchanges through a padded tile
+// (element e in slot e + e / 16: the three phases' accesses are all
+// conflict-free, and every per-register slot offset is a compile-time
+// immediate).  Against the 64-thread kernel's 64 values per thread: 80
+// registers instead of 228, so 3 CTAs of 8 warps per SM instead of 4 of 2
+// warps, and other warps' FP64 adds cover the exchange and load latencies.
+// The next tile's values and sign words are loaded during the current one.
+constexpr int kT3Threads = 256;
+constexpr int kT3Buf = 4096 + 256;  // t3idx(4096)
+__device__ __forceinline__ int t3idx(int e) { return e + (e >> 4); }
+
+template <typename TX, int KQ>
+__global__ void __launch_bounds__(kT3Threads, sizeof(TX) == 4 && KQ <= 8 ? 3 : 2)
+srht_tile3_kernel(const TX* __restrict__ X, int64_t ldx, int64_t n_local, int64_t row0,
+                  int log2_block, const uint32_t* __restrict__ sign_bits,
+                  const int32_t* __restrict__ samples, int k, int tiles_per_cta, int64_t ntiles,
+                  double* __restrict__ partials, const sgs_status* st, unsigned long long* tl) {
+  constexpr int LOGT = 12, T = 1 << LOGT;
+  extern __shared__ double smem[];
+  double* buf = smem;                                              // kT3Buf entries
+  double* part = smem + kT3Buf;                                    // k entries
+  int32_t* smp = reinterpret_cast<int32_t*>(part + k);             // k entries
+  uint32_t* sgn = reinterpret_cast<uint32_t*>(smp + k + (k & 1));  // 2 x 128 sign words
+  const int t = threadIdx.x;
+  SGS_DCHECK(dyn_smem_offset(sgn + 256, smem) <= dyn_smem_bytes());
+  const int col = blockIdx.y;
+  const TX* x = X + (int64_t)col * ldx;
+  const int64_t t0 = (int64_t)blockIdx.x * tiles_per_cta;
+  const int64_t t1 = min(t0 + tiles_per_cta, ntiles);
+  const int64_t bmask = (int64_t(1) << log2_block) - 1;
+  // the k-vector: entries t + 256 q in registers (KQ >= k / 256), else in
+  // shared memory
+  double acc[KQ > 0 ? KQ : 1];
+#pragma unroll
+  for (int q = 0; q < (KQ > 0 ? KQ : 1); ++q) acc[q] = 0.0;
+  if constexpr (KQ == 0)
+    for (int j = t; j < k; j += kT3Threads) part[j] = 0.0;
+  int64_t cur_blk = -1;
+  if (t0 < t1) {  // the operator does not depend on the predecessor
+    cur_blk = (row0 + t0 * T) >> log2_block;
+    const int32_t* sb = samples + cur_blk * (int64_t)k;
+    for (int j = t; j < k; j += kT3Threads) smp[j] = __ldg(sb + j);
+  }
+  pdl_enter();
+  if (status_stopped(st)) return;
+  if (tl && t == 0) atomicMin(tl + 12, gtimer());
+  // phase A: register r holds element ea + 64 r (bits 0..5 = t & 63,
+  // bits 6..9 = r, bits 10..11 = t >> 6): coalesced loads; slot base + 68 r
+  const int ea = (t & 63) | ((t >> 6) << 10);
+  double* const pa = buf + t3idx(ea);
+  // phase B: register bits 0..3 = element bits 10, 11, 0, 1, thread = bits
+  // 2..9: slot base + (r >> 2) + 1088 (r & 3)
+  double* const pb = buf + t3idx(t << 2);
+  // phase C: register bits 0..3 = element bits 2..5, thread = bits 0, 1, 6..11:
+  // slot base + 4 r + (r >> 2)
+  double* const pc = buf + t3idx((t & 3) | ((t >> 2) << 6));
+  const uint32_t* const sgw = sgn + (ea >> 5);  // + 2 r (+ 128 on odd tiles)
+  TX nx[16];
+  uint32_t ns = ~0u;
+  auto load_next = [&](int64_t lr0) {
+    if (lr0 + T <= n_local) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) nx[r] = __ldg(x + lr0 + ea + 64 * r);
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const int64_t lr = lr0 + ea + 64 * r;
+        nx[r] = lr < n_local ? __ldg(x + lr) : TX(0);
+      }
+    }
+    if (t < T / 32)  // word t of the tile covers rows lr0 + 32 t .. + 31
+      ns = (lr0 + 32 * (int64_t)t < n_local) ? __ldg(sign_bits + (lr0 >> 5) + t) : ~0u;
+  };
+  if (t0 < t1) load_next(t0 * T);
+  for (int64_t ti = t0; ti < t1; ++ti) {
+    const int64_t lr0 = ti * T;
+    const int64_t g0 = row0 + lr0;
+    const int64_t blk = g0 >> log2_block;
+    const int64_t h = (g0 & bmask) >> LOGT;
+    const int odd = 128 * (int)((ti - t0) & 1);
+    if (t < T / 32) sgn[odd + t] = ns;
+    double v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = (double)nx[r];
+    if (ti + 1 < t1) load_next(lr0 + T);  // in flight during this tile
+    __syncthreads();  // sign words visible; the previous tile's gather is done with buf and smp
+    if (blk != cur_blk) {
+      const int32_t* sb = samples + blk * (int64_t)k;
+      for (int j = t; j < k; j += kT3Threads) smp[j] = __ldg(sb + j);
+      cur_blk = blk;
+    }
+    // element ea + 64 r: sign word (ea >> 5) + 2 r, bit t & 31 (warp-uniform word)
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      if (((sgw[odd + 2 * r] >> (t & 31)) & 1u) == 0u) v[r] = -v[r];
+    fwht_reg<4>(v);  // bits 6..9
+#pragma unroll
+    for (int r = 0; r < 16; ++r) pa[68 * r] = v[r];
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = pb[(r >> 2) + 1088 * (r & 3)];
+    fwht_reg<4>(v);  // bits 10, 11, 0, 1
+    // each thread re-writes exactly the slots it read: no barrier in between
+#pragma unroll
+    for (int r = 0; r < 16; ++r) pb[(r >> 2) + 1088 * (r & 3)] = v[r];
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = pc[4 * r + (r >> 2)];
+    fwht_reg<4>(v);  // bits 2..5
+#pragma unroll
+    for (int r = 0; r < 16; ++r) pc[4 * r + (r >> 2)] = v[r];
+    __syncthreads();
+    if constexpr (KQ > 0) {
+#pragma unroll
+      for (int q = 0; q < KQ; ++q) {
+        const int j = t + kT3Threads * q;
+        if (j < k) {
+          const int32_t r = smp[j];
+          SGS_DCHECK(r >= 0 && (int64_t)r < (int64_t(1) << log2_block));
+          const double z = buf[t3idx(r & (T - 1))];
+          const int64_t rh = (int64_t)(r >> LOGT);
+          acc[q] += (__popcll(rh & h) & 1) ? -z : z;
+        }
+      }
+    } else {
+      for (int j = t; j < k; j += kT3Threads) {
+        const int32_t r = smp[j];
+        SGS_DCHECK(r >= 0 && (int64_t)r < (int64_t(1) << log2_block));
+        const double z = buf[t3idx(r & (T - 1))];
+        const int64_t rh = (int64_t)(r >> LOGT);
+        part[j] += (__popcll(rh & h) & 1) ? -z : z;
+      }
+    }
+  }
+  double* out = partials + ((int64_t)col * gridDim.x + blockIdx.x) * k;
+  if constexpr (KQ > 0) {
+#pragma unroll
+    for (int q = 0; q < KQ; ++q) {
+      const int j = t + kT3Threads * q;
+      if (j < k) out[j] = acc[q];
+    }
+  } else {
+    __syncthreads();
+    for (int j = t; j < k; j += kT3Threads) out[j] = part[j];
+  }
+  if (tl && t == 0) atomicMax(tl + 13, gtimer());
+}
+
+// SGS_SRHT_TILE64=1: batches through the 64-thread srht_tile_kernel (A/B
+// switch; the default is srht_tile3_kernel)
+static bool srht_tile64() {
+  static const bool v = [] {
+    const char* e = getenv("SGS_SRHT_TILE64");
+    return e && atoi(e) != 0;
+  }();
+  return v;
+}
+
 template <typename TX>
 static size_t srht_tile_smem(int k, int k2 = 0) {
   return (size_t)(kTileBuf + k) * sizeof(double) + (size_t)(k + (k & 1)) * sizeof(int32_t) +
@@ -470,11 +632,28 @@ static int launch_srht_t(const void* X, int64_t ldx, int ncols, int64_t n_local,
       // CTAs leaves most SMs free, so a following LS cluster launch finds a
       // GPC and runs its pre-wait part alongside (RGMRES's sketch of w)
       const bool batch = geom == 1 || (geom == 0 && (int64_t)nctas * ncols >= 4 * (int64_t)sm_count());
+      const int G = tile_group(n_local);
+      if (batch && !srht_tile64()) {
+        const size_t sm3 = (size_t)(kT3Buf + k) * sizeof(double) +
+                           (size_t)(k + (k & 1)) * sizeof(int32_t) + 256 * sizeof(uint32_t);
+        // the k-vector in registers up to k = 2048 (8 per thread), then in
+        // shared memory
+        auto k3 = k <= 4 * kT3Threads   ? srht_tile3_kernel<TX, 4>
+                  : k <= 8 * kT3Threads ? srht_tile3_kernel<TX, 8>
+                                        : srht_tile3_kernel<TX, 0>;
+        if (sm3 > 48 * 1024) cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
+        cudaFuncSetAttribute(k3, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+        return check_ex(launch_ex(k3, dim3(nctas, ncols), dim3(kT3Threads), sm3, s, 1,
+                                  static_cast<const TX*>(X), ldx, n_local, row0, log2_block,
+                                  sign_bits, samples, k, G, ntiles, partials, st,
+                                  debug_timeline_row()),
+                        "srht_tile3_kernel");
+      }
       auto kern = batch ? srht_tile_kernel<TX, false, false> : srht_tile_kernel<TX, true, false>;
       if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                            cudaSharedmemCarveoutMaxShared);
-      const int G = tile_group(n_local);
       const dim3 grid(batch ? nctas : nctas * G, ncols);
       return check_ex(launch_ex(kern, grid, dim3(kTileThreads), sm, s, batch ? 1 : G,
                                 static_cast<const TX*>(X), ldx, n_local, row0, log2_block,

@@ -179,10 +179,12 @@ def test_column_kernel_sketch_equals_stand_alone_sketch(cuda, dt, n, kind):
 
 @pytest.mark.parametrize("dt", [torch.float32, torch.float64])
 def test_batched_tile_sketch_equals_per_column(cuda, dt):
-    """Batches of many columns run the SRHT tile kernel one CTA per 8 tiles
-    (tiles in order, no cluster); single columns run one tile per CTA with a
-    DSMEM cluster sum.  Same partial structure and order: apply_block over 24
-    columns of c1's shape equals 24 apply() calls bit for bit."""
+    """Batches of many columns run srht_tile3_kernel: one 256-thread CTA per
+    tile group, tiles in order, three register phases of the same butterfly
+    levels in the same order; single columns run the 64-thread tile kernel,
+    one tile per CTA with a DSMEM cluster sum.  Same partial structure and
+    order: apply_block over 24 columns of c1's shape equals 24 apply() calls
+    bit for bit."""
     n, k, m = 1_000_000, 1500, 24
     th = sg.make_sketch(sg.SketchKind.PSRHT, k, n, 2)
     g = torch.Generator(device="cuda").manual_seed(5)
