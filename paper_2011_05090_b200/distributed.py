@@ -67,48 +67,79 @@ class PeerExchange:
     node only (IPC), world <= 8; the caller picks it for NCCL groups."""
 
     def __init__(self, comm: TorchComm, k: int, cl: int):
+        """Collective over ``comm`` (every rank must call it).  Each step that
+        can fail locally (allocation, export, import on a rank that is not on
+        this node or lacks IPC) is caught, so every rank still reaches the
+        host collectives; ``self.ok`` is this rank's outcome."""
         import ctypes
+        import socket
         from . import _lib
         lib = _lib.load()
         self.lib, self.world, self.rank = lib, comm.world, comm.rank
-        nbytes = int(lib.sgs_peer_bytes(comm.world, k, cl))
-        if nbytes <= 0:
-            raise ValueError(f"peer exchange: unsupported world={comm.world} / k={k} / cl={cl}")
-        area = ctypes.c_void_p()
-        _lib.check(lib.sgs_peer_alloc(nbytes, ctypes.byref(area)), "sgs_peer_alloc")
-        self.area = area.value
-        handle = ctypes.create_string_buffer(64)
-        _lib.check(lib.sgs_peer_export(self.area, handle), "sgs_peer_export")
-        handles = [None] * comm.world
-        dist.all_gather_object(handles, handle.raw, group=comm.group)
-        self.imported = []
-        areas = (ctypes.c_void_p * comm.world)()
-        for q, h in enumerate(handles):
-            if q == comm.rank:
-                areas[q] = self.area
-                continue
-            p = ctypes.c_void_p()
-            _lib.check(lib.sgs_peer_import(ctypes.create_string_buffer(h, 64), ctypes.byref(p)),
-                       "sgs_peer_import")
-            areas[q] = p.value
-            self.imported.append(p.value)
-        desc = ctypes.c_void_p()
-        _lib.check(lib.sgs_peer_desc_create(comm.world, comm.rank, k, areas, ctypes.byref(desc)),
-                   "sgs_peer_desc_create")
-        self.desc = desc.value
+        self.area, self.desc, self.imported, self.ok, self.error = None, None, [], False, None
+        handle = None
+        try:
+            nbytes = int(lib.sgs_peer_bytes(comm.world, k, cl))
+            if nbytes <= 0:
+                raise ValueError(f"unsupported world={comm.world} / k={k} / cl={cl}")
+            area = ctypes.c_void_p()
+            _lib.check(lib.sgs_peer_alloc(nbytes, ctypes.byref(area)), "sgs_peer_alloc")
+            self.area = area.value
+            hb = ctypes.create_string_buffer(64)
+            _lib.check(lib.sgs_peer_export(self.area, hb), "sgs_peer_export")
+            handle = hb.raw
+        except Exception as e:  # reported through the agreement below
+            self.error = e
+        entries = [None] * comm.world
+        dist.all_gather_object(entries, (socket.gethostname(), handle), group=comm.group)
+        if self.error is None and len({h for h, _ in entries}) != 1:
+            self.error = RuntimeError("ranks on more than one host (CUDA IPC is per node)")
+        if self.error is None and any(hd is None for _, hd in entries):
+            self.error = RuntimeError("another rank could not export its area")
+        if self.error is None:
+            try:
+                areas = (ctypes.c_void_p * comm.world)()
+                for q, (_, hd) in enumerate(entries):
+                    if q == comm.rank:
+                        areas[q] = self.area
+                        continue
+                    p = ctypes.c_void_p()
+                    _lib.check(lib.sgs_peer_import(ctypes.create_string_buffer(hd, 64),
+                                                   ctypes.byref(p)), "sgs_peer_import")
+                    areas[q] = p.value
+                    self.imported.append(p.value)
+                desc = ctypes.c_void_p()
+                _lib.check(lib.sgs_peer_desc_create(comm.world, comm.rank, k, areas,
+                                                    ctypes.byref(desc)), "sgs_peer_desc_create")
+                self.desc = desc.value
+                self.ok = True
+            except Exception as e:
+                self.error = e
 
     _cache: dict = {}
 
     @classmethod
-    def get(cls, comm: TorchComm, k: int, cl: int) -> "PeerExchange":
+    def get(cls, comm: TorchComm, k: int, cl: int) -> "PeerExchange | None":
         """One exchange per (communicator, k, LS cluster size), reused by every
         state on it (the IPC set-up is a host collective; factorisations on one
-        communicator run one at a time, each opening its own generation)."""
+        communicator run one at a time, each opening its own generation).
+        None - on every rank alike - when any rank could not set it up: the
+        caller then sums s' with the NCCL all-reduce."""
         key = (id(comm.group) if comm.group is not None else None, comm.world, comm.rank, k, cl,
-               torch.cuda.current_device())
-        ex = cls._cache.get(key)
-        if ex is None:
-            ex = cls._cache[key] = cls(comm, k, cl)
+               torch.cuda.current_device() if torch.cuda.is_available() else -1)
+        if key in cls._cache:
+            return cls._cache[key]
+        ex = cls(comm, k, cl)
+        dev = "cuda" if dist.get_backend(comm.group) == "nccl" else "cpu"
+        flag = torch.tensor([1 if ex.ok else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=comm.group)
+        if int(flag.item()) == 0:
+            import warnings
+            warnings.warn(f"peer-memory exchange unavailable ({ex.error or 'on another rank'}); "
+                          "s' is summed with an NCCL all-reduce per column")
+            ex.close()
+            ex = None
+        cls._cache[key] = ex
         return ex
 
     def begin(self, stream_ptr: int) -> None:

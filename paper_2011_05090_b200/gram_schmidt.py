@@ -395,6 +395,21 @@ class RgsState:
                 and getattr(c, "world", 1) <= 8 and self.fused and not self.phi_fused
                 and self.fdt == torch.float64)
 
+    def _peer_begin(self) -> bool:
+        """Set up (first call, collective) and open the peer exchange for one
+        factorisation; False when it does not apply or is unavailable on some
+        rank (then every rank uses the NCCL all-reduce)."""
+        if not self._peer_ok():
+            return False
+        if "_peer" not in self.__dict__:
+            from .distributed import PeerExchange
+            self._peer = PeerExchange.get(self.comm, self.k,
+                                          int(_lib.load().sgs_ls_cluster_size(self.k)))
+        if self._peer is None:
+            return False
+        self._peer.begin(stream_ptr())
+        return True
+
     def _update(self, i: int, w_ptr: int, w_code: int, normalize_prev: bool) -> None:
         call("sgs_rgs_update", self._Q.data_ptr(), self.ccode, self.ldq, self.n_local, i,
              w_ptr, w_code, self._rc.data_ptr(), 1 if normalize_prev else 0,
@@ -714,13 +729,7 @@ class RgsState:
             self._keep_phi = pparts
         # row-sharded over NCCL: the LS launch sums s' across the ranks by
         # NVLink stores into the peers' exchange areas (no all-reduce per column)
-        peer = self._peer_ok()
-        if peer:
-            if self.__dict__.get("_peer") is None:
-                from .distributed import PeerExchange
-                self._peer = PeerExchange.get(self.comm, self.k,
-                                              int(_lib.load().sgs_ls_cluster_size(self.k)))
-            self._peer.begin(stream_ptr())
+        peer = self._peer_begin()
         for i in range(m):
             sol = i + 1 if i + 1 < m else None
             if i == 0:
@@ -859,13 +868,7 @@ class RgsState:
             with torch.cuda.stream(d2h):
                 Ph.copy_(self._P[:m], non_blocking=True)
 
-        peer = self._peer_ok()  # s' summed across ranks in the LS launch (as the device path)
-        if peer:
-            if self.__dict__.get("_peer") is None:
-                from .distributed import PeerExchange
-                self._peer = PeerExchange.get(self.comm, self.k,
-                                              int(_lib.load().sgs_ls_cluster_size(self.k)))
-            self._peer.begin(stream_ptr())
+        peer = self._peer_begin()  # s' summed across ranks in the LS launch (as the device path)
         def sketch_until(c_end):
             with torch.cuda.stream(sk):
                 while len(sketched) < min(nchunks, c_end):

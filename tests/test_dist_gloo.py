@@ -154,3 +154,85 @@ def test_halo_exchange_in_a_subgroup():
         assert full_ok
     assert (out[1][1], out[1][2]) == (0, 2049)
     assert (out[2][1], out[2][2]) == (2047, 4097)
+
+
+class _FakePeerLib:
+    """sgs_peer_* stand-ins that succeed (a rank whose IPC set-up works)."""
+
+    def __init__(self):
+        self.freed = []
+
+    def sgs_peer_bytes(self, world, k, cl):
+        return 4096
+
+    def sgs_peer_alloc(self, nbytes, out):
+        out._obj.value = 0x1000
+        return 0
+
+    def sgs_peer_export(self, area, buf):
+        buf.raw = b"h" * 64
+        return 0
+
+    def sgs_peer_import(self, buf, out):
+        out._obj.value = 0x2000
+        return 0
+
+    def sgs_peer_desc_create(self, world, rank, k, areas, out):
+        out._obj.value = 0x3000
+        return 0
+
+    def sgs_peer_desc_free(self, d):
+        self.freed.append("desc")
+        return 0
+
+    def sgs_peer_unimport(self, p):
+        self.freed.append("import")
+        return 0
+
+    def sgs_peer_free(self, p):
+        self.freed.append("area")
+        return 0
+
+
+def _peer_worker(rank, world, port, out, fake_ranks):
+    import warnings
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2011_05090_b200 import _lib
+    from paper_2011_05090_b200.distributed import PeerExchange
+    fake = _FakePeerLib()
+    if rank in fake_ranks:
+        _lib.load = lambda: fake
+    with warnings.catch_warnings(record=True) as caught:
+        warnings.simplefilter("always")
+        ex = PeerExchange.get(TorchComm(), 64, 16)
+        again = PeerExchange.get(TorchComm(), 64, 16)  # cached outcome, no collective
+    out[rank] = (ex is None, again is None, [str(w.message) for w in caught],
+                 None if ex is None else (ex.ok, ex.desc), fake.freed)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fake_ranks", [(), (1,), (0, 1)])
+def test_peer_exchange_setup_is_agreed_across_ranks(fake_ranks):
+    """The peer-memory exchange is set up collectively: a rank whose
+    allocation, export or import fails still joins the host collectives, and
+    the ranks agree (MIN of their outcomes) - all use the exchange or all fall
+    back to the NCCL all-reduce, never a mix that would leave one rank
+    spinning on flags the others never write.  Here the real library fails
+    without a GPU; fake_ranks succeed through stand-ins."""
+    world = 2
+    port = _free_port()
+    out = mp.Manager().dict()
+    mp.spawn(_peer_worker, args=(world, port, out, fake_ranks), nprocs=world, join=True)
+    if len(fake_ranks) == world:
+        for r in range(world):
+            none, again, warns, state, freed = out[r]
+            assert not none and not again and state == (True, 0x3000) and not warns
+    else:
+        for r in range(world):
+            none, again, warns, state, freed = out[r]
+            assert none and again
+            assert any("peer-memory exchange unavailable" in w for w in warns)
+            if r in fake_ranks:  # its own area is freed; it never imported the
+                assert freed == ["area"]  # failed rank's (missing) handle
