@@ -479,9 +479,12 @@ def run_qr(args, cfg_name, comm):
         barrier()
         t0 = time.perf_counter()
         ne = max(1, min(args.steps, 3))
+        calls_ms = []
         for _ in range(ne):
             f = None
+            tc = time.perf_counter()
             f, _ = e2e_call()
+            calls_ms.append(round(1e3 * (time.perf_counter() - tc), 2))
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) / ne
         if comm:
@@ -491,7 +494,7 @@ def run_qr(args, cfg_name, comm):
         fb = np.dtype(pol.fine_dtype).itemsize
         e2e = {"value": units / dt, "unit": "columns/s", "h2d_bytes_per_step": n * m * bq,
                "d2h_bytes_per_step": n * m * bq + world * (m * m * 8 + 2 * k * m * fb),
-               "ms_per_step": 1e3 * dt,
+               "ms_per_step": 1e3 * dt, "calls_ms": calls_ms,
                "path": "rgs_factorize(pinned host W shard) -> host Q, R, S, P"}
         del pin, Wh, f
 
