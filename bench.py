@@ -752,8 +752,11 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="N >= 4: skip the c4 line")
+    ap.add_argument("--no-c2", action="store_true",
+                    help="default N = 1 run: skip the c2 strong-scaling point (results.c2_strong_n1)")
     args = ap.parse_args()
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    defaulted = args.config is None
     if args.config is None:
         # N = 1: BASELINE configs[1] (the metric's config); N > 1: configs[2],
         # the row-sharded c2, strong-scaled with the same Theta at every N
@@ -783,6 +786,25 @@ def main():
             line["results"] = {"c4": {k_: l4.get(k_) for k_ in (
                 "value", "unit", "ms_per_step", "steps", "warmup", "config", "hbm_gbs_whole_step",
                 "hbm_frac_whole_step", "roofline", "gpu_launches", "graph", "unavailable")}}
+    if (defaulted and world == 1 and not args.no_c2 and args.columns is None
+            and line is not None):
+        # the N = 1 point of the c2 strong-scaling curve that the N > 1 runs
+        # print (their default): same workload, same Theta, one GPU (W and Q
+        # are 67 GB each); fewer timed steps, no e2e / CPU legs
+        import copy
+        import torch
+        torch.cuda.empty_cache()
+        a2 = copy.copy(args)
+        a2.steps, a2.warmup, a2.no_e2e, a2.no_cpu = min(args.steps, 2), 1, True, True
+        try:
+            l2 = run_qr(a2, "c2", None)
+        except Exception as e:  # the c1 line stands on its own
+            l2 = {"unavailable": f"{type(e).__name__}: {e}"[:200]}
+        if l2 is not None:
+            line["results"] = {"c2_strong_n1": {k_: l2.get(k_) for k_ in (
+                "value", "unit", "ms_per_step", "steps", "warmup", "config",
+                "hbm_gbs_whole_step", "hbm_frac_whole_step", "roofline", "gpu_launches", "graph",
+                "clocks", "unavailable") if k_ in l2}}
     if line is not None:
         print(json.dumps(line), flush=True)
     if comm:

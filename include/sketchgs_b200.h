@@ -336,6 +336,25 @@ int sgs_csr_spmv(int64_t n, const int32_t* row_ptr, const int32_t* col_idx,
                  const double* alpha, double* y, const sgs_status* st,
                  void* stream);
 
+/* The Arnoldi step's w = A v (krylov.py:81-83, 276) and its sketch Theta w
+ * (gram_schmidt.py:297, sketch.py:90-109) in one launch, for an SRHT on
+ * 4096-row tiles (P-SRHT or block-SRHT, log2_block >= 12, k <= 2048): y as
+ * sgs_csr_spmv, and the partials of Theta y exactly as sgs_srht_partials
+ * writes them for one column of n rows (same bits; sgs_srht_nparts(n,
+ * log2_block) partials of k).  row0: global row of local row 0 (tile
+ * aligned); sign_bits: the sign words of the local rows.  Scratch: tilevec
+ * (sgs_spmv_srht_tilevec_elems doubles) and counters
+ * (sgs_spmv_srht_counter_elems u64, zero before the first call, never reset
+ * after; one stream at a time). */
+int sgs_csr_spmv_srht(int64_t n, const int32_t* row_ptr, const int32_t* col_idx,
+                      const double* vals, const void* x, int x_dtype, const double* xdiv,
+                      const double* alpha, double* y, int64_t row0, int log2_block,
+                      const uint32_t* sign_bits, const int32_t* samples, int k,
+                      double* tilevec, unsigned long long* counters, double* partials,
+                      const sgs_status* st, void* stream);
+int64_t sgs_spmv_srht_tilevec_elems(int64_t n, int k);
+int64_t sgs_spmv_srht_counter_elems(int64_t n);
+
 /* deterministic ||x||_2 (fp64 or fp32 input, fp64 result on device) */
 int sgs_norm2(const void* x, int x_dtype, int64_t n, double* out, double* work,
               void* stream);

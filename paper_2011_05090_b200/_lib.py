@@ -120,6 +120,12 @@ _SIGS = {
     "sgs_peer_begin": (c_int, [c_void_p, c_void_p]),
     "sgs_csr_spmv": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p,
                              c_void_p, c_void_p, c_void_p, c_void_p]),
+    "sgs_csr_spmv_srht": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
+                                  c_void_p, c_void_p, c_void_p, c_int64, c_int, c_void_p,
+                                  c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
+                                  c_void_p]),
+    "sgs_spmv_srht_tilevec_elems": (c_int64, [c_int64, c_int]),
+    "sgs_spmv_srht_counter_elems": (c_int64, [c_int64]),
     "sgs_norm2": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_void_p, c_void_p]),
     "sgs_norm2_work_elems": (c_int64, [c_int64]),
     "sgs_scale": (c_int, [c_void_p, c_double, c_void_p, c_int, c_void_p, c_int64, c_void_p]),

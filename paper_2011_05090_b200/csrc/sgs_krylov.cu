@@ -5,6 +5,7 @@
 
 #include <cstdlib>
 #include "sgs_common.cuh"
+#include "sgs_fwht.cuh"
 
 namespace sgs {
 
@@ -85,16 +86,19 @@ __device__ __forceinline__ double sp_xval(const TX* __restrict__ x, int c, const
   else return (double)xr / dv;
 }
 
+// The rows of one CTA (kSpRows) of y = (A x) / alpha, staged through svals /
+// sci / mbar (shared memory).  Returns true when the status block stopped the
+// launch (nothing written).
 template <typename TX>
-__global__ void __launch_bounds__(kSpThreads)
-csr_spmv_staged_kernel(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                       const double* __restrict__ vals, const TX* __restrict__ x,
-                       const double* __restrict__ xdiv, const double* __restrict__ alpha,
-                       double* __restrict__ y, const sgs_status* st, unsigned long long* tl,
-                       int allow_stage) {
-  __shared__ __align__(16) double svals[kSpCap + 2];
-  __shared__ __align__(16) int32_t sci[kSpCap + 4];
-  __shared__ __align__(8) uint64_t mbar;
+__device__ __forceinline__ bool spmv_block(int64_t n, const int32_t* __restrict__ rp,
+                                           const int32_t* __restrict__ ci,
+                                           const double* __restrict__ vals,
+                                           const TX* __restrict__ x,
+                                           const double* __restrict__ xdiv,
+                                           const double* __restrict__ alpha,
+                                           double* __restrict__ y, const sgs_status* st,
+                                           unsigned long long* tl, int allow_stage,
+                                           double* svals, int32_t* sci, uint64_t* mbar) {
   const int64_t r0 = (int64_t)blockIdx.x * kSpRows;
   const int64_t r1 = min(n, r0 + kSpRows);
   const int b = __ldg(rp + r0), e = __ldg(rp + r1), nnz = __ldg(rp + n);
@@ -112,21 +116,21 @@ csr_spmv_staged_kernel(int64_t n, const int32_t* __restrict__ rp, const int32_t*
     re[h] = r < r1 ? __ldg(rp + r + 1) : 0;
   }
   if (staged && threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sp_smem_u32(&mbar)) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sp_smem_u32(mbar)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     const uint32_t bci = (uint32_t)(e_ci - b_ci) * 4u, bv = (uint32_t)(e_v - b_v) * 8u;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sp_smem_u32(&mbar)),
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sp_smem_u32(mbar)),
                  "r"(bci + bv) : "memory");
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
         " [%0], [%1], %2, [%3], %4;" ::"r"(sp_smem_u32(sci)), "l"(ci + b_ci), "r"(bci),
-        "r"(sp_smem_u32(&mbar)), "l"(pol) : "memory");
+        "r"(sp_smem_u32(mbar)), "l"(pol) : "memory");
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
         " [%0], [%1], %2, [%3], %4;" ::"r"(sp_smem_u32(svals)), "l"(vals + b_v), "r"(bv),
-        "r"(sp_smem_u32(&mbar)), "l"(pol) : "memory");
+        "r"(sp_smem_u32(mbar)), "l"(pol) : "memory");
   }
   __syncthreads();
   pdl_enter();
@@ -135,16 +139,16 @@ csr_spmv_staged_kernel(int64_t n, const int32_t* __restrict__ rp, const int32_t*
     if (staged) {  // drain the copies before the shared memory goes away
       asm volatile(
           "{\n\t.reg .pred p;\nW0_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
-          "@!p bra W0_%=;\n}" ::"r"(sp_smem_u32(&mbar)) : "memory");
+          "@!p bra W0_%=;\n}" ::"r"(sp_smem_u32(mbar)) : "memory");
     }
-    return;
+    return true;
   }
   const double dv = xdiv ? __ldg(xdiv) : 1.0;
   const double ia = alpha ? __ldg(alpha) : 1.0;
   if (staged) {
     asm volatile(
         "{\n\t.reg .pred p;\nW1_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
-        "@!p bra W1_%=;\n}" ::"r"(sp_smem_u32(&mbar)) : "memory");
+        "@!p bra W1_%=;\n}" ::"r"(sp_smem_u32(mbar)) : "memory");
   }
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -165,6 +169,174 @@ csr_spmv_staged_kernel(int64_t n, const int32_t* __restrict__ rp, const int32_t*
   if (tl) {
     __syncthreads();
     if (threadIdx.x == 0) atomicMax(tl + 10, gtimer());
+  }
+  return false;
+}
+
+template <typename TX>
+__global__ void __launch_bounds__(kSpThreads)
+csr_spmv_staged_kernel(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                       const double* __restrict__ vals, const TX* __restrict__ x,
+                       const double* __restrict__ xdiv, const double* __restrict__ alpha,
+                       double* __restrict__ y, const sgs_status* st, unsigned long long* tl,
+                       int allow_stage) {
+  __shared__ __align__(16) double svals[kSpCap + 2];
+  __shared__ __align__(16) int32_t sci[kSpCap + 4];
+  __shared__ __align__(8) uint64_t mbar;
+  spmv_block<TX>(n, rp, ci, vals, x, xdiv, alpha, y, st, tl, allow_stage, svals, sci, &mbar);
+}
+
+// ---------------------------------------------------------------------------
+// SpMV with the SRHT of its output fused in (RGMRES's w = A q and p = Theta w,
+// one launch instead of two and no HBM re-read of w).  The CTAs are the plain
+// staged SpMV's (kSpRows rows each, kSpPerTile per 4096-row SRHT tile).  A CTA
+// publishes its rows of w (barrier, one device-scope fence, a per-tile
+// counter); the CTA that completes a tile transforms it from L2 with the
+// 256-thread three-phase register FWHT of srht_tile3_kernel (levels 6..9 |
+// 10, 11, 0, 1 | 2..5, the level order of every SRHT kernel here), gathers
+// the tile's k sampled rows into a tile vector (0.0 + (+-z), as one tile of
+// the clustered tile kernel) and bumps a per-group counter; the CTA that
+// completes a group of tile_group(n) tiles sums their tile vectors in tile
+// order from 0.0 - the DSMEM cluster sum of srht_tile_kernel - into the
+// group's partial.  So the partials are the stand-alone sketch's bit for bit.
+// The counters are monotonic (every CTA counts, also when the status block
+// stopped the launch), so they never need a reset.
+constexpr int kSpTile = 4096;
+constexpr int kSpPerTile = kSpTile / kSpRows;  // CTAs per SRHT tile
+constexpr int kSpT3Buf = 4096 + 256;           // padded tile: slot e + e / 16
+__device__ __forceinline__ int sp_t3idx(int e) { return e + (e >> 4); }
+
+struct SpmvSrht {
+  int64_t row0;               // global row of local row 0 (shard offset)
+  int log2_block;             // SRHT block (>= 12)
+  const uint32_t* sign_bits;  // sign word of local rows 32 w .. 32 w + 31 at [w]
+  const int32_t* samples;     // k sample rows per block
+  int k;
+  int G;                      // tiles per partial: tile_group(n)
+  double* tilevec;            // ntiles x k scratch
+  unsigned long long* counters;  // ntiles tile counters, then ngroups group counters
+  double* partials;           // ngroups x k
+};
+
+template <typename TX, int KQ>
+__global__ void __launch_bounds__(kSpThreads, 5)  // 5 CTAs per SM, as the plain SpMV
+csr_spmv_srht_kernel(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                     const double* __restrict__ vals, const TX* __restrict__ x,
+                     const double* __restrict__ xdiv, const double* __restrict__ alpha,
+                     double* __restrict__ y, const sgs_status* st, unsigned long long* tl,
+                     int allow_stage, SpmvSrht sk) {
+  extern __shared__ __align__(16) unsigned char sp_dyn[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ int s_last;
+  double* svals = reinterpret_cast<double*>(sp_dyn);
+  int32_t* sci = reinterpret_cast<int32_t*>(sp_dyn + (size_t)(kSpCap + 2) * 8);
+  const bool stop = spmv_block<TX>(n, rp, ci, vals, x, xdiv, alpha, y, st, tl, allow_stage,
+                                   svals, sci, &mbar);
+  const int t = threadIdx.x;
+  const int64_t tile = (int64_t)blockIdx.x / kSpPerTile;
+  const int64_t ntiles = (n + kSpTile - 1) / kSpTile;
+  const int64_t lr0 = tile * kSpTile;
+  // ---- tile completion: this CTA's rows of w are published
+  __syncthreads();  // every row of the CTA stored; the staging buffers are free
+  if (t == 0) {
+    __threadfence();
+    const unsigned long long per =
+        (unsigned long long)((min(n, lr0 + kSpTile) - lr0 + kSpRows - 1) / kSpRows);
+    const unsigned long long old = atomicAdd(sk.counters + tile, 1ull);
+    s_last = ((old + 1) % per) == 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();  // the other CTAs' rows of this tile
+  if (tl && t == 0) atomicMin(tl + 12, gtimer());
+  // shared memory reused: the padded tile, 128 sign words, the k samples
+  double* buf = svals;
+  uint32_t* sgn = reinterpret_cast<uint32_t*>(sp_dyn + (size_t)kSpT3Buf * 8);
+  int32_t* smp = reinterpret_cast<int32_t*>(sgn + 128);
+  SGS_DCHECK(dyn_smem_offset(smp + sk.k, sp_dyn) <= dyn_smem_bytes());
+  if (!stop) {
+    constexpr int LOGT = 12;
+    const int64_t g0 = sk.row0 + lr0;
+    const int64_t blk = g0 >> sk.log2_block;
+    const int64_t h = (g0 & ((int64_t(1) << sk.log2_block) - 1)) >> LOGT;
+    const int ea = (t & 63) | ((t >> 6) << 10);
+    double v[16];
+    if (lr0 + kSpTile <= n) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) v[r] = __ldcg(y + lr0 + ea + 64 * r);
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const int64_t lr = lr0 + ea + 64 * r;
+        v[r] = lr < n ? __ldcg(y + lr) : 0.0;
+      }
+    }
+    if (t < kSpTile / 32)
+      sgn[t] = (lr0 + 32 * (int64_t)t < n) ? __ldg(sk.sign_bits + (lr0 >> 5) + t) : ~0u;
+    const int32_t* sb = sk.samples + blk * (int64_t)sk.k;
+    for (int j = t; j < sk.k; j += kSpThreads) smp[j] = __ldg(sb + j);
+    __syncthreads();
+    const uint32_t* sgw = sgn + (ea >> 5);
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      if (((sgw[2 * r] >> (t & 31)) & 1u) == 0u) v[r] = -v[r];
+    fwht_reg<4>(v);  // bits 6..9
+    double* const pa = buf + sp_t3idx(ea);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) pa[68 * r] = v[r];
+    __syncthreads();
+    double* const pb = buf + sp_t3idx(t << 2);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = pb[(r >> 2) + 1088 * (r & 3)];
+    fwht_reg<4>(v);  // bits 10, 11, 0, 1
+#pragma unroll
+    for (int r = 0; r < 16; ++r) pb[(r >> 2) + 1088 * (r & 3)] = v[r];
+    __syncthreads();
+    double* const pc = buf + sp_t3idx((t & 3) | ((t >> 2) << 6));
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = pc[4 * r + (r >> 2)];
+    fwht_reg<4>(v);  // bits 2..5
+#pragma unroll
+    for (int r = 0; r < 16; ++r) pc[4 * r + (r >> 2)] = v[r];
+    __syncthreads();
+    double* tv = sk.tilevec + tile * (int64_t)sk.k;
+#pragma unroll
+    for (int q = 0; q < KQ; ++q) {
+      const int j = t + kSpThreads * q;
+      if (j < sk.k) {
+        const int32_t r = smp[j];
+        SGS_DCHECK(r >= 0 && (int64_t)r < (int64_t(1) << sk.log2_block));
+        const double z = buf[sp_t3idx(r & (kSpTile - 1))];
+        const int64_t rh = (int64_t)(r >> LOGT);
+        tv[j] = 0.0 + ((__popcll(rh & h) & 1) ? -z : z);
+      }
+    }
+  }
+  // ---- group completion
+  __syncthreads();
+  const int64_t grp = tile / sk.G;
+  const int64_t ngroups = (ntiles + sk.G - 1) / sk.G;
+  if (t == 0) {
+    __threadfence();
+    const unsigned long long per = (unsigned long long)min((int64_t)sk.G, ntiles - grp * sk.G);
+    const unsigned long long old = atomicAdd(sk.counters + ntiles + grp, 1ull);
+    s_last = ((old + 1) % per) == 0;
+  }
+  __syncthreads();
+  if (!s_last || stop) return;
+  __threadfence();
+  const int64_t gt0 = grp * sk.G;
+  const int nt = (int)min((int64_t)sk.G, ntiles - gt0);
+  double* out = sk.partials + grp * (int64_t)sk.k;
+  for (int j = t; j < sk.k; j += kSpThreads) {
+    double acc = 0.0;
+    for (int q = 0; q < nt; ++q) acc += __ldcg(sk.tilevec + (gt0 + q) * (int64_t)sk.k + j);
+    out[j] = acc;
+  }
+  (void)ngroups;
+  if (tl) {
+    __syncthreads();
+    if (t == 0) atomicMax(tl + 13, gtimer());
   }
 }
 
@@ -272,7 +444,43 @@ __device__ __forceinline__ void givens_update(const double* __restrict__ R, int6
     const double beta = R[0];
     if (i == 0) g[0] = beta;
     double carry = h[0];
-    for (int j = 0; j < i; ++j) {
+    // the dependent chain runs from registers: 8 rotations and h entries are
+    // loaded one chunk ahead (a chunk writes h[j..j+7] and the next reads
+    // h[j+9..j+16]), so no shared-memory latency sits on the carry
+    constexpr int kU = 8;
+    const int nfull = i / kU * kU;
+    double cc[kU], ss[kU], hh[kU];
+    if (nfull > 0) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        cc[u] = c_s[u];
+        ss[u] = s_s[u];
+        hh[u] = h[u + 1];
+      }
+    }
+    for (int j = 0; j < nfull; j += kU) {
+      double nc[kU], ns[kU], nh[kU], ho[kU];
+      const bool more = j + kU < nfull;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        nc[u] = more ? c_s[j + kU + u] : 0.0;
+        ns[u] = more ? s_s[j + kU + u] : 0.0;
+        nh[u] = more ? h[j + kU + u + 1] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        ho[u] = __dadd_rn(__dmul_rn(cc[u], carry), __dmul_rn(ss[u], hh[u]));
+        carry = __dadd_rn(__dmul_rn(-ss[u], carry), __dmul_rn(cc[u], hh[u]));
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        h[j + u] = ho[u];
+        cc[u] = nc[u];
+        ss[u] = ns[u];
+        hh[u] = nh[u];
+      }
+    }
+    for (int j = nfull; j < i; ++j) {
       const double c = c_s[j], s = s_s[j], hn = h[j + 1];
       h[j] = __dadd_rn(__dmul_rn(c, carry), __dmul_rn(s, hn));
       carry = __dadd_rn(__dmul_rn(-s, carry), __dmul_rn(c, hn));
@@ -414,6 +622,66 @@ extern "C" int sgs_csr_spmv(int64_t n, const int32_t* row_ptr, const int32_t* co
                             1, n, row_ptr, col_idx, vals, static_cast<const double*>(x), xdiv,
                             alpha, y, st, debug_timeline_row(), stage),
                   "csr_spmv_staged_kernel");
+}
+
+// Scratch of sgs_csr_spmv_srht for n local rows and k sample rows: tile
+// vectors (doubles) and counters (u64, zeroed once by the caller).
+extern "C" int64_t sgs_spmv_srht_tilevec_elems(int64_t n, int k) {
+  return n < 1 || k < 1 ? 0 : (n + kSpTile - 1) / kSpTile * (int64_t)k;
+}
+extern "C" int64_t sgs_spmv_srht_counter_elems(int64_t n) {
+  if (n < 1) return 0;
+  const int64_t nt = (n + kSpTile - 1) / kSpTile;
+  const int G = tile_group(n);
+  return nt + (nt + G - 1) / G;
+}
+
+extern "C" int sgs_csr_spmv_srht(int64_t n, const int32_t* row_ptr, const int32_t* col_idx,
+                                 const double* vals, const void* x, int x_dtype,
+                                 const double* xdiv, const double* alpha, double* y, int64_t row0,
+                                 int log2_block, const uint32_t* sign_bits,
+                                 const int32_t* samples, int k, double* tilevec,
+                                 unsigned long long* counters, double* partials,
+                                 const sgs_status* st, void* stream) {
+  SGS_REQUIRE(n >= 1 && row_ptr && col_idx && vals && x && y, "spmv_srht: bad args");
+  SGS_REQUIRE(sign_bits && samples && tilevec && counters && partials && k >= 1 &&
+                  k <= 8 * kSpThreads && log2_block >= 12 && log2_block <= 40 && row0 >= 0 &&
+                  row0 % kSpTile == 0,
+              "spmv_srht: bad sketch args (k <= %d, 4096-row tiles, tile-aligned row0)",
+              8 * kSpThreads);
+  const int stage = ((uintptr_t)col_idx & 15) == 0 && ((uintptr_t)vals & 15) == 0;
+  cudaStream_t s = as_stream(stream);
+  const unsigned blocks = (unsigned)((n + kSpRows - 1) / kSpRows);
+  SpmvSrht sk;
+  sk.row0 = row0;
+  sk.log2_block = log2_block;
+  sk.sign_bits = sign_bits;
+  sk.samples = samples;
+  sk.k = k;
+  sk.G = tile_group(n);
+  sk.tilevec = tilevec;
+  sk.counters = counters;
+  sk.partials = partials;
+  const size_t a = (size_t)(kSpCap + 2) * 8 + (size_t)(kSpCap + 4) * 4;
+  const size_t b = (size_t)kSpT3Buf * 8 + 128 * 4 + (size_t)k * 4;
+  const size_t smem = a > b ? a : b;
+#define SGS_SPSR_LAUNCH(TX, KQ)                                                              \
+  do {                                                                                       \
+    auto kern = csr_spmv_srht_kernel<TX, KQ>;                                                \
+    if (smem > 48 * 1024)                                                                    \
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
+    return check_ex(launch_ex(kern, dim3(blocks), dim3(kSpThreads), smem, s, 1, n, row_ptr,  \
+                              col_idx, vals, static_cast<const TX*>(x), xdiv, alpha, y, st,  \
+                              debug_timeline_row(), stage, sk),                              \
+                    "csr_spmv_srht_kernel");                                                 \
+  } while (0)
+  if (x_dtype == SGS_F32) {
+    if (k <= 4 * kSpThreads) SGS_SPSR_LAUNCH(float, 4);
+    SGS_SPSR_LAUNCH(float, 8);
+  }
+  if (k <= 4 * kSpThreads) SGS_SPSR_LAUNCH(double, 4);
+  SGS_SPSR_LAUNCH(double, 8);
+#undef SGS_SPSR_LAUNCH
 }
 
 extern "C" int64_t sgs_norm2_work_elems(int64_t n) { (void)n; return kNormBlocks; }

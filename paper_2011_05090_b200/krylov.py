@@ -26,6 +26,7 @@ from ._lib import call, stream_ptr
 from .gram_schmidt import (BREAKDOWN_FACTOR, HOUSEHOLDER_QR, GsVariant, LazyFactors, LsqSolver,
                            QrFactors, RgsState)
 from .precision import MIXED32_64, PrecisionPolicy
+from .sketch import SketchKind
 
 # SGS_W_SMALL_GRID=1: sketch w = A q with one CTA per 4 tiles (128 CTAs at c3)
 # instead of one tile per CTA (same partials): the LS cluster that follows
@@ -33,6 +34,14 @@ from .precision import MIXED32_64, PrecisionPolicy
 # 8.6 -> 0.8 us), but one fp64 column on 64 CTAs takes 46 us instead of 9
 # (c3 fp32 basis, one-sync: 3686 -> 3310 steps/s).  Off by default.
 _W_SMALL_GRID = os.environ.get("SGS_W_SMALL_GRID", "0") == "1"
+
+# SGS_SPMV_SRHT=1: the SRHT of w fused into the SpMV (sgs_csr_spmv_srht: the
+# CTA completing a 4096-row tile transforms it from L2, bit-identical
+# partials).  Off by default: measured slower at c3 - the per-CTA publication
+# (fence + tile counter) and the tile transforms inside the SpMV grid cost
+# 46.7 - 35.0 us of SpMV time against the 9.6 us launch they replace (one-sync
+# fp32 basis 3763 -> 3628 Arnoldi steps/s, profiles/r02g_spmv_srht_ab.json).
+_SPMV_SRHT = os.environ.get("SGS_SPMV_SRHT", "0") == "1"
 
 __all__ = ["SparseMatrix", "Ilu0Preconditioner", "ilu0", "arnoldi", "gmres", "gmres_restarted",
            "ArnoldiDecomposition", "GmresResult", "RestartedResult"]
@@ -525,11 +534,59 @@ class _ArnoldiEngine:
         self.hist = torch.zeros(m + 1, dtype=torch.float64, device=dev)
         self.norm_flag = torch.full((1,), -1, dtype=torch.int32, device=dev)
         self._owed = None  # step whose Givens update rides on the next step's head
+        self._spsr = self._spmv_srht_scratch()
         if self.lagged:
             self._kv2 = (torch.empty(2 * st.k, dtype=torch.float64, device=dev)
                          if dist is not None else None)
             if not self.fused:
                 self._wdiv = torch.empty(self.n_loc, dtype=torch.float64, device=dev)
+
+    def _spmv_srht_scratch(self):
+        """Scratch of the fused SpMV + SRHT launch (tile vectors, monotonic
+        counters), or None when the step takes two launches: a preconditioner
+        (w = A M^-1 q), a sketch other than 4096-row-tile SRHT, k > 2048, or
+        the generic (unfused) engine."""
+        st = self.state
+        th = st.theta
+        if not (_SPMV_SRHT and not _W_SMALL_GRID and self.fused and self.M is None
+                and th.kind in (SketchKind.PSRHT, SketchKind.BLOCK_SRHT)
+                and th.log2_block >= 12 and st.k <= 2048 and st.row0 % 4096 == 0):
+            return None
+        lib = _lib.load()
+        ntv = int(lib.sgs_spmv_srht_tilevec_elems(self.n_loc, st.k))
+        nct = int(lib.sgs_spmv_srht_counter_elems(self.n_loc))
+        if ntv <= 0 or nct <= 0:
+            return None
+        dev = st.device
+        return (torch.empty(ntv, dtype=torch.float64, device=dev),
+                torch.zeros(nct, dtype=torch.int64, device=dev))
+
+    def _matvec_sketch(self, i: int, alpha) -> None:
+        """w = (A q_i) / alpha into ws.w (q_i as stored, this rank's rows) and
+        the SRHT partials of w into the state's p partials (st.nparts of
+        them): one fused launch when possible, else the SpMV and the
+        stand-alone sketch."""
+        st, ws = self.state, self.ws
+        if self._spsr is None:
+            self._matvec(i, ws.w, alpha, st.status)
+            st.theta.partials_into(ws.w.data_ptr(), _lib.SGS_F64, self.n_loc, 1, st._parts_p,
+                                   n_local=self.n_loc, row0=st.row0, status=st.status,
+                                   small_grid=_W_SMALL_GRID)
+            return
+        tv, cnt = self._spsr
+        th = st.theta
+        d = th.device_data(ws.w.device)
+        if self.dist is None:
+            rp, ci, va = self.A.device_arrays(ws.w.device)
+            nrows, xp = self.A.n, st._qcol_ptr(i)
+        else:
+            xw, blk = self.dist.window(st._Q[i, :self.n_loc])
+            rp, ci, va, nrows, xp = blk.rp, blk.ci, blk.va, blk.n_rows, xw.data_ptr()
+        call("sgs_csr_spmv_srht", nrows, rp.data_ptr(), ci.data_ptr(), va.data_ptr(), xp,
+             st.ccode, None, alpha.data_ptr() if alpha is not None else None, ws.w.data_ptr(),
+             st.row0, th.log2_block, d["bits"].data_ptr() + (st.row0 // 32) * 4,
+             d["samples"].data_ptr(), st.k, tv.data_ptr(), cnt.data_ptr(),
+             st._parts_p.data_ptr(), st.status.ptr, stream_ptr())
 
     def _matvec(self, i: int, out: torch.Tensor, alpha, status) -> None:
         """out = (A M^{-1} q_i) / alpha over this rank's rows."""
@@ -552,16 +609,8 @@ class _ArnoldiEngine:
         """w = A M^{-1} q'_c (/ alpha) from the unnormalised column c, its sketch
         p', and the LS launch finalizing c and solving c + 1 (p = p' / r_cc).
         ``s_raw``: raw partials of s'_c (None for c = 0: s'_0 = p_0)."""
-        st, ws = self.state, self.ws
-        if self.dist is None:
-            _eff_matvec_into(self.A, self.M, ws, st._qcol_ptr(c), st.ccode, ws.w, alpha=alpha,
-                             status=st.status)
-        else:
-            xw, blk = self.dist.window(st._Q[c, :self.n_loc])
-            blk.spmv_into(xw.data_ptr(), st.ccode, ws.w, alpha=alpha, status=st.status)
-        st.theta.partials_into(ws.w.data_ptr(), _lib.SGS_F64, self.n_loc, 1, st._parts_p,
-                               n_local=self.n_loc, row0=st.row0, status=st.status,
-                               small_grid=_W_SMALL_GRID)
+        st = self.state
+        self._matvec_sketch(c, alpha)
         p_raw = (st._parts_p.data_ptr(), st.nparts, st.theta.scale)
         if self.dist is not None:  # one all-reduce of [s'; p'] (2k)
             k, kv = st.k, self._kv2
@@ -657,10 +706,8 @@ class _ArnoldiEngine:
                  self.sn.data_ptr(), self.g.data_ptr(), self.T.data_ptr(), self.T.shape[1],
                  self.hist.data_ptr(), -1.0 if tol is None else float(tol), st.status.ptr,
                  stream_ptr())
-            self._matvec(i, ws.w, alpha, st.status)
-            pp, pn, ps = st._sketch_parts(ws.w.data_ptr(), _lib.SGS_F64, self.n_loc,
-                                          st._parts_p, getattr(st, "_kvec_p", None),
-                                          small_grid=_W_SMALL_GRID)
+            self._matvec_sketch(i, alpha)
+            pp, pn, ps = st._combine(st._parts_p, st.nparts, getattr(st, "_kvec_p", None))
             st._phi_w(i + 1, ws.w.data_ptr(), _lib.SGS_F64, self.n_loc)
             st._ls(sol=i + 1, p_parts=pp, p_nparts=pn, p_scale=ps)
             sp, sn, ss = st._column(i + 1, ws.w.data_ptr(), _lib.SGS_F64, False, True)
