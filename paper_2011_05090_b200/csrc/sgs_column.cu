@@ -57,15 +57,31 @@ __device__ __forceinline__ void l2_prefetch(const void* src, uint32_t bytes) {
 }
 
 // L2 prefetch budget (bytes) of the SRHT column kernel's pre-wait prologue:
-// about what one LS launch's latency lets HBM move (SGS_COL_PF_MB overrides;
-// measured at c1: 48 MB 5777, 64 MB 5820, 72 MB 5831, 80 MB 5841, 88 MB 5818,
-// 96 MB 5807 columns/s.  The dense ring kernel measured slower with it at c0.)
+// about what one LS launch's latency lets HBM move (SGS_COL_PF_MB overrides).
+// Issued all at once (one bulk prefetch per thread) the optimum measured at c1
+// was 80 MB (48 MB 5777, 64 MB 5820, 80 MB 5841, 96 MB 5807 columns/s): the
+// burst of every tile queues up in front of the LS launch's own L2 round trips.
+// Paced (col_pf_pace below) a larger budget pays: means of two 20-step runs at
+// c1, columns/s - 80 MB burst 5986, 96 MB / 400 cycles 6046, 104 MB / 300-500
+// cycles 6045-6054, 112 MB / 400 6035, 120 MB / 800 5814
+// (profiles/r02i_prefetch_pacing.txt).  The dense ring kernel measured slower
+// with a prefetch at c0.
 static long col_pf_bytes() {
   static const long b = [] {
     const char* e = getenv("SGS_COL_PF_MB");
-    return (e ? atol(e) : 80L) << 20;
+    return (e ? atol(e) : 104L) << 20;
   }();
   return b;
+}
+
+// Cycles between a tile's successive L2 prefetches (SGS_COL_PF_PACE; 0 = all
+// at once, one per thread).
+static int col_pf_pace() {
+  static const int p = [] {
+    const char* e = getenv("SGS_COL_PF_PACE");
+    return e ? atoi(e) : 400;
+  }();
+  return p;
 }
 
 // Ring depth: two CTAs per SM (<= 64 registers, __launch_bounds__ below), with
@@ -109,7 +125,7 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
                   int log2_block, const uint32_t* __restrict__ sign_bits,
                   const int32_t* __restrict__ samples, int k, double* __restrict__ partials,
                   const sgs_status* st, unsigned long long* tl, int pf_cols, int nstages,
-                  int two, ColPhi phi) {
+                  int two, ColPhi phi, int pf_pace, int pf_wave) {
   cg::cluster_group cl = cg::this_cluster();
   if (tl && threadIdx.x == 0) atomicMin(tl + (int64_t)i * 16 + 0, gtimer());
   constexpr int V = VecT<TQ>::N;                  // rows per vector (4 fp32, 2 fp64)
@@ -166,7 +182,7 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
       tma_load_1d(ring + (size_t)j * kColT, Q + (int64_t)j * ldq + lr0, bytes, &mbar[j], policy);
   // The predecessor LS launch keeps HBM idle while it solves: pull the next
   // pf_cols columns of this tile into L2 meanwhile (one bulk prefetch per thread).
-  if (active && tid >= 32 && tid - 32 < pf_cols && S + tid - 32 < nplain)
+  if (pf_pace == 0 && active && tid >= 32 && tid - 32 < pf_cols && S + tid - 32 < nplain)
     l2_prefetch(Q + (int64_t)(S + tid - 32) * ldq + lr0, bytes);
   int64_t rows[NH];
 #pragma unroll
@@ -179,6 +195,28 @@ rgs_column_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i,
 #pragma unroll
       for (int v = 0; v < V; ++v)
         wv[hh][v] = (rows[hh] + v < n) ? cvt<TQ>(__ldcs(w + rows[hh] + v)) : TQ(0);
+  }
+  if (pf_pace > 0 && pf_cols > 0 && (tid >> 5) >= 1 && (tid >> 5) <= 2) {
+    // paced variant: warp 1 issues this tile's prefetches one every pf_pace
+    // cycles, so the burst of all tiles does not queue up in front of the LS
+    // launch's own L2 round trips.  Grids of more than one wave (pf_wave > 0:
+    // CTAs below pf_wave are resident before the wait, the others start after
+    // it and just stream): warp 2 of a first-wave CTA prefetches for the tile
+    // pf_wave further on.
+    const bool second = (tid >> 5) == 2;
+    const int64_t t = (int64_t)blockIdx.x + (second ? pf_wave : 0);
+    const int64_t tr0 = t * kColT;
+    bool ok = second ? (pf_wave > 0 && t < (int64_t)gridDim.x && tr0 < n) : active;
+    if (pf_wave > 0 && (int)blockIdx.x >= pf_wave) ok = false;
+    if (ok) {
+      const uint32_t tb =
+          (uint32_t)(((size_t)min((int64_t)kColT, n - tr0) * sizeof(TQ) + 15) / 16 * 16);
+      const long long t0 = clock64();
+      for (int c = 0; c < pf_cols && S + c < nplain; ++c) {
+        while (clock64() - t0 < (long long)c * pf_pace) {}
+        if ((tid & 31) == (c & 31)) l2_prefetch(Q + (int64_t)(S + c) * ldq + tr0, tb);
+      }
+    }
   }
   pdl_enter();
   if (w_div != nullptr) {
@@ -818,11 +856,27 @@ static int update_srht_impl(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
   const size_t smem = ring_of(nst) + rest;
   SGS_REQUIRE(smem <= 227 * 1024, "update_srht: i=%d k=%d needs %zu bytes of shared memory", i,
               k, smem);
-  // L2 prefetch of the columns behind the ring prologue, spread over the tiles
-  // (single-wave grids only: later waves start after the wait and just stream)
-  const int pf = nctas > 2 * 148 ? 0
-                                  : (int)std::min<int64_t>(kColThreads - 32,
-                                                           col_pf_bytes() / (nctas * kColT * esz));
+  // L2 prefetch of the columns behind the ring prologue, spread over the tiles.
+  // A grid of one wave prefetches per tile; a larger one (c3: 512 tiles) only
+  // with the paced variant, whose first-wave CTAs (taken as 2 per SM on the SMs
+  // the LS cluster leaves free) also cover the tiles of the next wave.  The
+  // pace is scaled so that the whole grid issues bytes at c1's rate.
+  // Measured at c3 (512 tiles; Arnoldi steps/s with / without): f64 2078 / 2001,
+  // fp32 basis 3443 / 3496, one-sync 2138 / 2152 and 3620 / 3751 - no gain, so
+  // multi-wave grids prefetch only with SGS_COL_PF_MULTI=1.
+  static const bool pf_multi = [] {
+    const char* e = getenv("SGS_COL_PF_MULTI");
+    return e && atoi(e) != 0;
+  }();
+  const int pace0 = col_pf_pace();
+  const int64_t wave = 2 * (148 - 16);
+  const bool multi = nctas > 2 * 148;
+  int pf = (multi && (!pf_multi || pace0 == 0 || nctas > 2 * wave))
+               ? 0
+               : (int)std::min<int64_t>(kColThreads - 32, col_pf_bytes() / (nctas * kColT * esz));
+  const int pf_wave = multi ? (int)wave : 0;
+  const int pace = (int)std::min<int64_t>(
+      1 << 20, (int64_t)pace0 * nctas * esz / (248 * 4) + (pace0 > 0 ? 1 : 0));
   cudaError_t err = cudaSuccess;
   const ColPhi phi{phi_sign_bits, phi_samples, use_phi ? kphi : 0, phi_log2_block, phi_partials};
 #define SGS_COL(TQ, TW)                                                                       \
@@ -833,7 +887,7 @@ static int update_srht_impl(void* Q, int q_dtype, int64_t ldq, int64_t n, int i,
                     static_cast<TQ*>(Q), ldq, n, i, static_cast<const TW*>(w), w_div,        \
                     static_cast<const TQ*>(r_crs), normalize_prev, R, ldr, do_sketch, row0,  \
                     log2_block, sign_bits, samples, k, partials, st, debug_timeline(), pf,    \
-                    nst, acc_two<TQ>(), phi);                                                 \
+                    nst, acc_two<TQ>(), phi, pace, pf_wave);                                  \
   } while (0)
   if (q_dtype == SGS_F32 && w_dtype == SGS_F32) SGS_COL(float, float);
   else if (q_dtype == SGS_F32 && w_dtype == SGS_F64) SGS_COL(float, double);

@@ -254,8 +254,12 @@ struct ColSrc {
 // flight), lanes stride the rows, one transposed butterfly for the 8 sums.
 template <typename T, int NV>
 __device__ __noinline__ void ls_coldot(ColSrc<T> M, int nr, int j0, int j1, const T* v0,
-                                       const T* v1, T* __restrict__ o0, T* __restrict__ o1) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+                                       const T* v1, T* __restrict__ o0, T* __restrict__ o1,
+                                       int w0 = 0, int nw = kLsWarps) {
+  // warps [w0, w0 + nw) share the columns (which warp takes a column does not
+  // change its sum); the others return at once
+  const int lane = threadIdx.x & 31, warp = (int)(threadIdx.x >> 5) - w0;
+  if (warp < 0) return;
   for (int rc = 0; rc < nr; rc += kLsChunk) {  // rows in chunks of 128 (4 per lane)
     const int rn = min(kLsChunk, nr - rc);
     T x0[4], x1[4];
@@ -265,7 +269,7 @@ __device__ __noinline__ void ls_coldot(ColSrc<T> M, int nr, int j0, int j1, cons
       x0[q] = (lane + 32 * q < rn) ? v0[rr] : T(0);
       x1[q] = (NV > 1 && lane + 32 * q < rn) ? v1[rr] : T(0);
     }
-    for (int jb = j0 + warp * kLsCpw; jb < j1; jb += kLsWarps * kLsCpw) {
+    for (int jb = j0 + warp * kLsCpw; jb < j1; jb += nw * kLsCpw) {
       T mv[kLsCpw][4];
 #pragma unroll
       for (int u = 0; u < kLsCpw; ++u) {
@@ -621,6 +625,51 @@ __device__ __noinline__ void ls_reduce_parts2(const double* pa, int na, double s
   __syncthreads();
 }
 
+// block_sum / block_sum2 (sgs_common.cuh) for the LS kernel's fixed 16 warps:
+// the same shuffle tree and the same ascending warp order, with the 16 warp
+// sums loaded together instead of one dependent shared-memory load per term.
+template <typename T>
+__device__ __forceinline__ T ls_block_sum(T v, T* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  T r[kLsWarps];
+#pragma unroll
+  for (int w = 0; w < kLsWarps; ++w) r[w] = red[w];
+  T t = T(0);
+#pragma unroll
+  for (int w = 0; w < kLsWarps; ++w) t += r[w];
+  return t;
+}
+template <typename T>
+__device__ __forceinline__ void ls_block_sum2(T& a, T& b, T* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  __syncthreads();
+  if (lane == 0) {
+    red[warp] = a;
+    red[kLsWarps + warp] = b;
+  }
+  __syncthreads();
+  T ra[kLsWarps], rb[kLsWarps];
+#pragma unroll
+  for (int w = 0; w < kLsWarps; ++w) {
+    ra[w] = red[w];
+    rb[w] = red[kLsWarps + w];
+  }
+  T ta = T(0), tb = T(0);
+#pragma unroll
+  for (int w = 0; w < kLsWarps; ++w) {
+    ta += ra[w];
+    tb += rb[w];
+  }
+  a = ta;
+  b = tb;
+}
+
 // Cluster sum of one scalar per CTA from slots[q*stride] (ascending q).
 template <typename T>
 __device__ __forceinline__ T ls_slot_sum(const T* slots, int64_t stride, int CL) {
@@ -869,7 +918,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     const int64_t pi = (int64_t)a.col_fin * k + ra;
     T l1 = T(0);
     for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) l1 = fma(P[pi + rr], P[pi + rr], l1);
-    l1 = block_sum(l1, red);
+    l1 = ls_block_sum(l1, red);
     if (threadIdx.x == 0) bc[6] = l1;
   }
   SGS_TR(1);
@@ -901,18 +950,48 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     SGS_TR(3);
     // ---- exchange #1: ||s'||^2, ||p_i||^2, T^T s' --------------------------------
     const bool defer = a.t_pend != nullptr;
+    if (nr <= 128) {
+      // Up to 128 rows per CTA (k <= 2048 on 16 CTAs): warp 0 alone forms the
+      // two sums while warps 1..15 start on the column dots - no block
+      // barrier in this phase.  Lane l holds the values threads l, l + 32,
+      // l + 64, l + 96 would in the block-wide sum, each group of 32 goes
+      // through the same shuffle tree, and the four warp sums are added in
+      // warp order from 0: block_sum's result bit for bit (its other twelve
+      // terms are +0).
+      if (threadIdx.x < 32) {
+        T l0 = T(0), l2 = T(0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int rr = (int)threadIdx.x + 32 * q;
+          const T sv = rr < nr ? vs[rr] : T(0);
+          T a0 = fma(sv, sv, T(0));
+          T a2 = (defer && fused && rr < nr) ? fma(sv, vp[rr], T(0)) : T(0);  // s'^T p_{i+1}
+          a0 = warp_sum(a0);
+          a2 = warp_sum(a2);
+          l0 += a0;
+          l2 += a2;
+        }
+        if (threadIdx.x == 0) { myA[0] = l0; myA[1] = bc[6]; myA[2] = l2; }  // bc[6]: ||p_i||^2
+      }
+      SGS_TR(14);
+      if (nq > 0) {
+        if (lag) ls_coldot<T, 2>(TS, nr, 0, nq, vs, vp, myA + 8, myA + 8 + cap, 1, kLsWarps - 1);
+        else ls_coldot<T, 1>(TS, nr, 0, nq, vs, nullptr, myA + 8, nullptr, 1, kLsWarps - 1);
+      }
+    } else {
     T l0 = T(0), l2 = T(0);
     for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
       l0 = fma(vs[rr], vs[rr], l0);
       if (defer && fused) l2 = fma(vs[rr], vp[rr], l2);  // s'^T p_{i+1}
     }
-    if (defer && fused) block_sum2(l0, l2, red);
-    else l0 = block_sum(l0, red);
+    if (defer && fused) ls_block_sum2(l0, l2, red);
+    else l0 = ls_block_sum(l0, red);
     if (threadIdx.x == 0) { myA[0] = l0; myA[1] = bc[6]; myA[2] = l2; }  // bc[6]: ||p_i||^2
     SGS_TR(14);
     if (nq > 0) {
       if (lag) ls_coldot<T, 2>(TS, nr, 0, nq, vs, vp, myA + 8, myA + 8 + cap);  // + T^T p'
       else ls_coldot<T, 1>(TS, nr, 0, nq, vs, nullptr, myA + 8, nullptr);
+    }
     }
     SGS_TR(15);  // thread 0's share of the column dots done
     xsync();
@@ -958,12 +1037,19 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
       vs[rr] = sv;
       S[(int64_t)i * k + ra + rr] = sv;
     }
+    // the fast path's two sums ride along: a thread squares the c1 entries it
+    // has just scaled, in the order of the separate pass it replaces
+    T acc_c = T(0), acc_p = T(0);
     for (int j = threadIdx.x; j < nq; j += blockDim.x) {
       const T cj = c1[j] / rT;       // (Qs^T s)_j
       c1[j] = cj;
       c2[j] = cj / to[j];            // coefficient on the unnormalised column T_j (to = alpha)
+      if (defer) {
+        acc_c = fma(cj, cj, acc_c);
+        if (fused) acc_p = fma(cj, zc[j], acc_p);
+      }
     }
-    __syncthreads();
+    if (!defer) __syncthreads();     // (block_sum's barriers publish c1 / c2 otherwise)
     SGS_TR(6);
     // Fast path: Q_s = T diag(1/alpha) is orthonormal, so ||t||^2 = ||s||^2 -
     // sum_j c1_j^2 and t^T p = s^T p - sum_j c1_j zc_j (zc = Q_s^T p from before
@@ -975,13 +1061,8 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     bool explicit_t = true;
     T tt = T(0);
     if (defer) {
-      T acc_c = T(0), acc_p = T(0);
-      for (int j = threadIdx.x; j < nq; j += blockDim.x) {
-        acc_c = fma(c1[j], c1[j], acc_c);
-        if (fused) acc_p = fma(c1[j], zc[j], acc_p);
-      }
-      if (fused) block_sum2(acc_c, acc_p, red);  // one barrier pair, block_sum's order
-      else acc_c = block_sum(acc_c, red);
+      if (fused) ls_block_sum2(acc_c, acc_p, red);  // one barrier pair, block_sum's order
+      else acc_c = ls_block_sum(acc_c, red);
       const T ss0 = bc[0] / (rT * rT);
       const T tt_est = ss0 - acc_c;
       if (nq == 0 || tt_est >= T(0.5) * ss0) {
@@ -1011,7 +1092,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) Tm[(int64_t)i * k + ra + rr] = vt[rr];
     T lt = T(0);
     for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) lt = fma(vt[rr], vt[rr], lt);
-    lt = block_sum(lt, red);  // its __syncthreads also publishes the T_i stores in the CTA
+    lt = ls_block_sum(lt, red);  // its __syncthreads also publishes the T_i stores in the CTA
     if (threadIdx.x == 0) myB[0] = lt;
     const ColSrc<T> TG{sq, RM, 0, Tm + ra, (int64_t)k};
     if (fused) ls_coldot<T, 1>(TG, nr, i, i + 1, vp, nullptr, myB + 1 - i, nullptr);
@@ -1043,7 +1124,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
       }
       T l2 = T(0);
       for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) l2 = fma(vt[rr], vt[rr], l2);
-      l2 = block_sum(l2, red);
+      l2 = ls_block_sum(l2, red);
       if (threadIdx.x == 0) myR[0] = l2;
       if (fused) ls_coldot<T, 1>(TG, nr, i, i + 1, vp, nullptr, myR + 1 - i, nullptr);
       xsync();
@@ -1143,7 +1224,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
         const T* sprime = static_cast<const T*>(a.t_coef) + cap;
         T l2 = T(0);
         for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) l2 = fma(__ldcg(sprime + ra + rr), vp[rr], l2);
-        l2 = block_sum(l2, red);
+        l2 = ls_block_sum(l2, red);
         if (threadIdx.x == 0) myA[2] = l2;
       }
       ls_coldot<T, 1>(TS, nr, 0, c, vp, nullptr, myA + 8 + cap, nullptr);
@@ -1157,7 +1238,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
       if (idz) {
         T acc_p = T(0);
         for (int j = threadIdx.x; j < c - 1; j += blockDim.x) acc_p = fma(c1[j], zc[j], acc_p);
-        acc_p = block_sum(acc_p, red);
+        acc_p = ls_block_sum(acc_p, red);
         const T rTn = (T)R[(int64_t)(c - 1) * cap + (c - 1)];
         zl = (bc[2] / rTn - acc_p) / __ldcg(AL + (c - 1));
       } else {
