@@ -64,8 +64,9 @@ __device__ __forceinline__ void l2_prefetch(const void* src, uint32_t bytes) {
 // Paced (col_pf_pace below) a larger budget pays: means of two 20-step runs at
 // c1, columns/s - 80 MB burst 5986, 96 MB / 400 cycles 6046, 104 MB / 300-500
 // cycles 6045-6054, 112 MB / 400 6035, 120 MB / 800 5814
-// (profiles/r02i_prefetch_pacing.txt).  The dense ring kernel measured slower
-// with a prefetch at c0.
+// (profiles/r02i_prefetch_pacing.txt).  An evict-first policy on the prefetched
+// lines changed nothing (6045 vs 6092 without, LS post-wait time the same).  The
+// dense ring kernel measured slower with a prefetch at c0.
 static long col_pf_bytes() {
   static const long b = [] {
     const char* e = getenv("SGS_COL_PF_MB");
