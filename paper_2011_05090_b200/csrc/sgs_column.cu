@@ -66,7 +66,7 @@ __device__ __forceinline__ void l2_prefetch(const void* src, uint32_t bytes) {
 // cycles 6045-6054, 112 MB / 400 6035, 120 MB / 800 5814
 // (profiles/r02i_prefetch_pacing.txt).  An evict-first policy on the prefetched
 // lines changed nothing (6045 vs 6092 without, LS post-wait time the same).  The
-// dense ring kernel measured slower with a prefetch at c0.
+// dense ring kernel has its own paced prefetch (launch_dense_ring).
 static long col_pf_bytes() {
   static const long b = [] {
     const char* e = getenv("SGS_COL_PF_MB");
@@ -468,7 +468,8 @@ dense_ring_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
                   const TQ* __restrict__ rc, int normalize_prev, const double* __restrict__ R,
                   int64_t ldr, int do_sketch, const double* __restrict__ thetaT, int64_t ldt,
                   int k, double* __restrict__ partials, int64_t chunk, int stage_bytes,
-                  const sgs_status* st, const uint32_t* __restrict__ rbits, int kw, int two) {
+                  const sgs_status* st, const uint32_t* __restrict__ rbits, int kw, int two,
+                  int pf_stages, int pf_pace) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* ring = smem_raw;  // kDcStages x stage_bytes
   double* xq = reinterpret_cast<double*>(smem_raw + (size_t)kDcStages * stage_bytes);  // chunk
@@ -532,6 +533,25 @@ dense_ring_kernel(TQ* __restrict__ Q, int64_t ldq, int64_t n, int i, const TW* _
   for (int u = 0; u < kDcMaxRPT; ++u) {
     const int lr = tid + u * T;
     wv[u] = lr < nr ? cvt<TQ>(__ldcs(w + r0 + lr)) : TQ(0);
+  }
+  // The predecessor LS launch leaves HBM idle: warp 1 pulls the next pf_stages
+  // ring stages (the rest of Q[:, :nplain], then this chunk's first rows of
+  // Theta^T - the order they are streamed in) into L2, one stage every pf_pace
+  // cycles so that the burst does not queue up in front of the LS round trips.
+  if (pf_stages > 0 && (tid >> 5) == 1) {
+    const int lane = tid & 31;
+    const long long t0 = clock64();
+    for (int c = 0; c < pf_stages && kDcStages + c < ntot; ++c) {
+      const int t = kDcStages + c;
+      while (clock64() - t0 < (long long)c * pf_pace) {}
+      if (t < n1) {
+        const int j0 = t * G, j1 = min(nplain, j0 + G);
+        for (int j = j0 + lane; j < j1; j += 32) l2_prefetch(Q + (int64_t)j * ldq + r0, segb);
+      } else if (lane == 0) {
+        const int rr0 = (t - n1) * Rr, rr1 = min(nr, rr0 + Rr);
+        l2_prefetch(thetaT + (r0 + rr0) * ldt, (uint32_t)(rr1 - rr0) * rowb);
+      }
+    }
   }
   pdl_enter();
   if (status_stopped(st)) {  // uniform; drain the prologue before leaving
@@ -731,6 +751,18 @@ static int launch_dense_ring(void* Q, int64_t ldq, int64_t n, int i, const void*
     set_error("dense column: k=%d / i=%d need %zu bytes of shared memory", k, i, smem);
     return SGS_EINVAL;
   }
+  // pre-wait L2 prefetch (SGS_DENSE_PF_MB total over the grid, 0 = off), paced
+  // at the SRHT column kernel's byte rate.  c0, columns/s, two 20-step runs
+  // each: off 9123 / 9129, 48 MB 9106 / 9106, 80 MB 9179 / 9166, 104 MB 9168 /
+  // 9158, 128 MB 9113 / 9136; the Rademacher variant (Q only) does not move
+  // (12 245 at 0, 48 and 104 MB).
+  static const long dpf_mb = [] {
+    const char* e = getenv("SGS_DENSE_PF_MB");
+    return e ? atol(e) : 80L;
+  }();
+  const int pf_stages = (int)std::min<int64_t>(4096, (dpf_mb << 20) / ((int64_t)np * stage_bytes));
+  const int pf_pace = (int)std::min<int64_t>(
+      1 << 20, (int64_t)col_pf_pace() * np * stage_bytes / (248 * 16384) + 1);
   cudaError_t e;
 #define SGS_DR(QPV)                                                                              \
   do {                                                                                           \
@@ -740,7 +772,7 @@ static int launch_dense_ring(void* Q, int64_t ldq, int64_t n, int i, const void*
     e = launch_ex(kern, dim3(np), dim3(threads), smem, s, dr_cluster(), static_cast<TQ*>(Q), ldq, n, i, \
                   static_cast<const TW*>(w), static_cast<const TQ*>(r_crs), normalize_prev, R,   \
                   ldr, do_sketch, thetaT, ldt, k, partials, chunk, stage_bytes, st, rbits, kw,   \
-                  acc_two<TQ>());                                                                \
+                  acc_two<TQ>(), pf_stages, pf_pace);                                            \
   } while (0)
   if (qp <= 1) SGS_DR(1);
   else if (qp <= 2) SGS_DR(2);
