@@ -186,7 +186,12 @@ __global__ void transpose_kernel(const T* __restrict__ src, int64_t lds, T* __re
 constexpr int kLsThreads = 512;
 constexpr int kLsWarps = kLsThreads / 32;
 constexpr int kLsMaxCluster = 16;
-constexpr int kLsRowsPerCta = 96;
+// Rows of the k-vectors per CTA: the cluster is ceil(k / 64) CTAs, at most 16
+// (SGS_LS_ROWS overrides).  Measured at k = 600 (c0 columns/s; c3 one-sync fp32
+// Arnoldi steps/s): 96 rows (7 CTAs) 9172 / 3763, 64 (10 CTAs) 9290 / 3782, 48
+// (13) 9299 / 3693, 38 (16) 9322 / 3661 - a larger cluster shortens the LS
+// launch but takes SMs from the column grid it overlaps with.
+constexpr int kLsRowsPerCta = 64;
 constexpr int kLsChunk = 128;  // rows / outputs per pass of the 2-D helpers (4 per lane)
 constexpr int kLsCpw = 8;      // columns in flight per warp
 
@@ -200,7 +205,12 @@ static int ls_cluster_size_host(int k) {
     if (v > kLsMaxCluster) v = kLsMaxCluster;
     g_ls_max_cluster = v;
   }
-  int cl = (k + kLsRowsPerCta - 1) / kLsRowsPerCta;
+  static const int rows_per_cta = [] {
+    const char* e = getenv("SGS_LS_ROWS");
+    const int v = e ? atoi(e) : kLsRowsPerCta;
+    return v >= 8 ? v : kLsRowsPerCta;
+  }();
+  int cl = (k + rows_per_cta - 1) / rows_per_cta;
   if (cl < 1) cl = 1;
   if (cl > g_ls_max_cluster) cl = g_ls_max_cluster;
   return cl;
