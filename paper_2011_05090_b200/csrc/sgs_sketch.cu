@@ -1075,26 +1075,36 @@ int dense_nparts_of(int64_t n) { return dense_nparts_host(n); }
 // ---------------------------------------------------------------------------
 // Gaussian P = Theta W on the fp64 tensor cores (mma.sync m8n8k4 f64: the DMMA
 // SASS op).  The contraction over the n rows is split into nsub sub-chunks
-// (chunk_begin over gaussian_nsub(n) <= 296 of them, a multiple of 8); each
+// (chunk_begin over gaussian_nsub(n) <= 152 of them, a multiple of 8); each
 // CTA owns one sub-chunk and a (j, c) output tile, and its per-output chain
 // is a sequence of DMMAs over ascending 4-row k-steps (the chunk's last step
 // zero-padded).  The 8 CTAs of a cluster are 8 consecutive sub-chunks: they
 // sum their tiles through distributed shared memory in rank order, so one
-// partial per 8 sub-chunks goes to HBM (c0: 37 x k per column instead of
-// 296 x k).  apply() (one column) runs the same kernel with an 8-column tile:
+// partial per 8 sub-chunks goes to HBM (c0: 19 x k per column instead of
+// the DFMA GEMM's 296 x k).  apply() (one column) runs the same kernel with an 8-column tile:
 // every output element is the same chain of the same operands, so
 // apply_block is bit-identical to apply whatever the tile shape.
 //
 // Fragments (PTX m8n8k4 .f64, lane l): A[l/4][l%4] = Theta^T[r + l%4][j + l/4],
 // B[l%4][l/4] = W[r + l%4][c + l/4], D[l/4][2 (l%4) + {0,1}].
-constexpr int kMmaStageRows = 16;
-constexpr int kMmaStages = 3;
-constexpr int kMmaMaxSub = 296;
+// Rows per ring stage x stages, per tile shape (SR, NS below): a block barrier
+// per stage, so the 300-column batch runs 32-row stages (c0 P batch 1.742 ->
+// 1.650 ms against 16 x 3), the one-column apply keeps 16 x 3 (109 us; 140 us
+// with 32 x 2).  The k-steps of a chain are the same 4-row steps either way.
+// Sub-chunks of the contraction (c0, 300 columns, P batch ms / apply us per
+// column: 296 1.838 / 112, 152 1.742 / 109, 104 1.732 / 123, 72 1.726 / 107,
+// 40 1.781 / 129; profiles/r02k_dmma_subchunks.txt).
+constexpr int kMmaMaxSub = 152;
 
 static int gaussian_nsub(int64_t n) {
   int64_t p = (n + 31) / 32;
   p = (p + kSrhtCluster - 1) / kSrhtCluster * kSrhtCluster;
-  if (p > kMmaMaxSub) p = kMmaMaxSub;
+  static const int max_sub = [] {  // SGS_MMA_MAXSUB (a multiple of 8): experiment override
+    const char* e = getenv("SGS_MMA_MAXSUB");
+    const int v = e ? atoi(e) / kSrhtCluster * kSrhtCluster : kMmaMaxSub;
+    return v >= kSrhtCluster ? v : kMmaMaxSub;
+  }();
+  if (p > max_sub) p = max_sub;
   return (int)p;
 }
 
@@ -1112,12 +1122,13 @@ struct MmaTile {
   static constexpr int kBS = kC + 4;         // of a k-step fall in distinct banks
 };
 
-template <typename TX, int WJ, int WC, int TJ, int TC>
+template <typename TX, int WJ, int WC, int TJ, int TC, int SR, int NS>
 __global__ void __launch_bounds__(32 * WJ * WC)
 dense_mma_kernel(const double* __restrict__ thetaT, int64_t ldt, int k, const TX* __restrict__ X,
                  int64_t ldx, int ncols, int64_t n, int nsub, double* __restrict__ partials,
                  const sgs_status* st) {
   using G = MmaTile<WJ, WC, TJ, TC>;
+  constexpr int kMmaStageRows = SR, kMmaStages = NS;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char mma_raw[];
   SGS_DCHECK((size_t)G::kJ * G::kC * sizeof(double) <= dyn_smem_bytes());
@@ -1214,18 +1225,19 @@ dense_mma_kernel(const double* __restrict__ thetaT, int64_t ldt, int k, const TX
   cl.sync();  // the tile stays readable until every CTA of the cluster is done
 }
 
-template <typename TX, int WJ, int WC, int TJ, int TC>
+template <typename TX, int WJ, int WC, int TJ, int TC, int SR, int NS>
 static int launch_dense_mma_t(const double* thetaT, int64_t ldt, int k, const TX* X, int64_t ldx,
                               int ncols, int64_t n, double* partials, const sgs_status* st,
                               cudaStream_t s) {
   using G = MmaTile<WJ, WC, TJ, TC>;
+  constexpr int kMmaStageRows = SR, kMmaStages = NS;
   const int nsub = gaussian_nsub(n);
   const size_t stage = (size_t)kMmaStageRows * G::kAS * sizeof(double) +
                        (size_t)kMmaStageRows * G::kBS * sizeof(TX);
   size_t smem = kMmaStages * stage;
   const size_t otile = (size_t)G::kJ * G::kC * sizeof(double);
   if (otile > smem) smem = otile;
-  auto kern = dense_mma_kernel<TX, WJ, WC, TJ, TC>;
+  auto kern = dense_mma_kernel<TX, WJ, WC, TJ, TC, SR, NS>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid(nsub, (k + G::kJ - 1) / G::kJ, (ncols + G::kC - 1) / G::kC);
   return check_ex(launch_ex(kern, grid, dim3(G::kThreads), smem, s, kSrhtCluster, thetaT, ldt, k,
@@ -1239,8 +1251,8 @@ static int launch_dense_mma(const double* thetaT, int64_t ldt, int k, const void
                             cudaStream_t s) {
   const TX* x = static_cast<const TX*>(X);
   if (ncols <= 8)  // apply(): 256 (j) x 8 (c) tiles, 8 warps along j
-    return launch_dense_mma_t<TX, 8, 1, 4, 1>(thetaT, ldt, k, x, ldx, ncols, n, partials, st, s);
-  return launch_dense_mma_t<TX, 4, 2, 4, 4>(thetaT, ldt, k, x, ldx, ncols, n, partials, st, s);
+    return launch_dense_mma_t<TX, 8, 1, 4, 1, 16, 3>(thetaT, ldt, k, x, ldx, ncols, n, partials, st, s);
+  return launch_dense_mma_t<TX, 4, 2, 4, 4, 32, 2>(thetaT, ldt, k, x, ldx, ncols, n, partials, st, s);
 }
 
 // SGS_DENSE_LEGACY=1: the DFMA GEMV / split-K GEMM with 296 partials (A/B)
