@@ -444,7 +444,15 @@ def run_qr(args, cfg_name, comm):
                     cfg["kind"], "rgs_column_kernel (update + SRHT epilogue)"),
                 "peak_source": peak_kind,
                 "share_of_step": round(tot_ms / ms, 4),
-                "launches": len(evs), "avg_launch_us": round(1e3 * tot_ms / len(evs), 2)}
+                "launches": len(evs), "avg_launch_us": round(1e3 * tot_ms / len(evs), 2),
+                # Under programmatic dependent launch the events bracket a launch
+                # from its predecessor's end: the column kernel's pre-wait prologue
+                # (ring prologue + its paced L2 prefetch, ~100 MB of the next
+                # columns) overlaps the predecessor LS launch and is not in the
+                # duration, so the per-launch figure can exceed the copy peak;
+                # hbm_frac_whole_step is the fraction with nothing excluded.
+                "note": "launch durations exclude the pre-wait L2 prefetch that overlaps the "
+                        "predecessor LS launch; hbm_frac_whole_step excludes nothing"}
 
     # ---- e2e through the public API (pinned host W -> factors on the host)
     e2e = None
