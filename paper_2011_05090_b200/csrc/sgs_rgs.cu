@@ -778,7 +778,10 @@ __device__ __noinline__ void ls_givens_chain(const double* rc, const double* cs,
   if (lane == 0) Tc[gi] = carry;
 }
 
-template <typename T>
+// PLAIN: a launch without the one-synchronisation p' partials, the peer
+// exchange and the Givens chain (plain RGS-QR on one GPU); those branches are
+// compiled out, which shortens the code the post-wait path steps through.
+template <typename T, bool PLAIN>
 __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
@@ -792,7 +795,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   const bool fused = a.do_finalize && a.do_solve;
   // one-synchronisation Arnoldi: p'_{i+1} = Theta A q'_i
   // arrives as partials with s'_i, and p_{i+1} = p'_{i+1} / r_ii
-  const bool lag = fused && a.p_lag && a.p_partials != nullptr;
+  const bool lag = !PLAIN && fused && a.p_lag && a.p_partials != nullptr;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LsSmem<T> L(smem_raw, RM, cap);
@@ -858,7 +861,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   // runs the same chain from shuffled operands (same operations as
   // givens_update).  The carry waits in T[gi, gi] for thread 0 (bar.syncs
   // between), which overwrites it with the new rotation.
-  const int gi = (a.giv_on && a.do_finalize) ? a.col_fin - 1 : -1;
+  const int gi = (!PLAIN && a.giv_on && a.do_finalize) ? a.col_fin - 1 : -1;
   const bool giv_warp = gi >= 0 && rank == 0 && code0 == 0 && (threadIdx.x >> 5) == (int)(blockDim.x >> 5) - 1;
   if (giv_warp) ls_givens_chain(R + (int64_t)a.col_fin * cap, a.giv_cs, a.giv_sn,
                                  a.giv_T + (int64_t)gi * a.giv_ldt, gi, dred);
@@ -949,7 +952,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     } else if (lag) {  // s' and p' together
       ls_reduce_parts2<T>(a.s_partials, a.s_nparts, a.s_scale, vs, a.p_partials, a.p_nparts,
                           a.p_scale, vp, k, ra, nr, dred);
-    } else if (a.peer != nullptr) {  // s' summed across the ranks here (row-sharded state)
+    } else if (!PLAIN && a.peer != nullptr) {  // s' summed across the ranks here (row-sharded state)
       if (ls_peer_sum<T>(static_cast<const sgs_peer_desc_dev*>(a.peer), a.s_partials, a.s_nparts,
                          k, ra, nr, a.s_scale, vs, dred, i, rank, a.st))
         return;  // uniform: every rank and CTA sees the same status / flags
@@ -1298,7 +1301,12 @@ static int launch_ls(const sgs_ls_args* a, cudaStream_t s) {
     const int col = a->do_finalize ? a->col_fin : a->col_sol;
     aa.timeline = tlb ? tlb + (int64_t)col * 16 + (a->do_finalize ? 0 : 3) : nullptr;
   }
-  auto kern = ls_step_kernel<T>;
+  static const bool plain_ok = [] {  // SGS_LS_PLAIN=0: always the full variant (A/B)
+    const char* e = getenv("SGS_LS_PLAIN");
+    return !(e && atoi(e) == 0);
+  }();
+  const bool plain = plain_ok && !(a->p_lag && a->p_partials) && a->peer == nullptr && !a->giv_on;
+  auto kern = plain ? ls_step_kernel<T, true> : ls_step_kernel<T, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (CL > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return check_ex(launch_ex(kern, dim3(CL), dim3(kLsThreads), smem, s, CL, aa), "ls_step_kernel");
