@@ -778,10 +778,11 @@ __device__ __noinline__ void ls_givens_chain(const double* rc, const double* cs,
   if (lane == 0) Tc[gi] = carry;
 }
 
+// FUSED / PLAIN select compiled-out variants of the same code.
 // PLAIN: a launch without the one-synchronisation p' partials, the peer
 // exchange and the Givens chain (plain RGS-QR on one GPU); those branches are
 // compiled out, which shortens the code the post-wait path steps through.
-template <typename T, bool PLAIN>
+template <typename T, bool PLAIN, bool FUSED>
 __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
@@ -792,7 +793,9 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   const int rb = ((rank + 1) * k) / CL;
   const int nr = rb - ra;
   const int RM = (k + CL - 1) / CL;
-  const bool fused = a.do_finalize && a.do_solve;
+  // FUSED: the launch is known to finalize column i and solve for i + 1
+  const bool do_fin = FUSED || a.do_finalize, do_sol = FUSED || a.do_solve;
+  const bool fused = FUSED || (do_fin && do_sol);
   // one-synchronisation Arnoldi: p'_{i+1} = Theta A q'_i
   // arrives as partials with s'_i, and p_{i+1} = p'_{i+1} / r_ii
   const bool lag = !PLAIN && fused && a.p_lag && a.p_partials != nullptr;
@@ -802,8 +805,8 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   // fixed arrays + the cache of ncache columns of T fit; the row slice fits RM
   SGS_DCHECK(CL >= 1 && CL <= kLsMaxCluster && nr >= 0 && nr <= RM);
   SGS_DCHECK(L.bytes + (size_t)a.cache_cols * RM * sizeof(T) <= dyn_smem_bytes());
-  SGS_DCHECK(!a.do_finalize || (a.col_fin >= 0 && a.col_fin < cap));
-  SGS_DCHECK(!a.do_solve || (a.col_sol >= 1 && a.col_sol < cap));
+  SGS_DCHECK(!do_fin || (a.col_fin >= 0 && a.col_fin < cap));
+  SGS_DCHECK(!do_sol || (a.col_sol >= 1 && a.col_sol < cap));
   T* vs = L.vs;    // RM   s' -> s (own rows)
   T* vt = L.vt;    // RM   t
   T* vp = L.vp;    // RM   p
@@ -832,7 +835,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   T* Tm = static_cast<T*>(a.Qs);  // unnormalised T
   T* Rinv = static_cast<T*>(a.Rinv);
   double* R = a.R;
-  long long* trc = (rank == 0 && threadIdx.x == 0) ? a.trace : nullptr;
+  long long* trc = (!FUSED && rank == 0 && threadIdx.x == 0) ? a.trace : nullptr;
 #define SGS_TR(ix) \
   do {             \
     if (trc) trc[ix] = clock64(); \
@@ -849,7 +852,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   // CTA's rows of T and, in the fused QR path, the whole solve except the last
   // column's term run while the predecessor column kernel is still streaming Q.
   SGS_TR(0);
-  if (a.timeline && rank == 0 && threadIdx.x == 0) a.timeline[6] = gtimer();
+  if (!FUSED && a.timeline && rank == 0 && threadIdx.x == 0) a.timeline[6] = gtimer();
   const int64_t code0 = *reinterpret_cast<volatile const int64_t*>(&a.st->code);
   double dmax = a.st->diag_max, dmin = a.st->diag_min;
   // Progressive Givens update of GMRES step gi = col_fin - 1 (krylov.py:282-301),
@@ -861,7 +864,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   // runs the same chain from shuffled operands (same operations as
   // givens_update).  The carry waits in T[gi, gi] for thread 0 (bar.syncs
   // between), which overwrites it with the new rotation.
-  const int gi = (!PLAIN && a.giv_on && a.do_finalize) ? a.col_fin - 1 : -1;
+  const int gi = (!PLAIN && a.giv_on && do_fin) ? a.col_fin - 1 : -1;
   const bool giv_warp = gi >= 0 && rank == 0 && code0 == 0 && (threadIdx.x >> 5) == (int)(blockDim.x >> 5) - 1;
   if (giv_warp) ls_givens_chain(R + (int64_t)a.col_fin * cap, a.giv_cs, a.giv_sn,
                                  a.giv_T + (int64_t)gi * a.giv_ldt, gi, dred);
@@ -874,7 +877,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   // the fast path (its c1 / s' are in t_coef) - kept when [0] is cleared
   const int pend = a.t_pend ? *reinterpret_cast<volatile const int*>(a.t_pend) : -1;
   const int last_fast = a.t_pend ? *reinterpret_cast<volatile const int*>(a.t_pend + 1) : -1;
-  const int ncols_t = a.do_finalize ? a.col_fin : a.col_sol;  // columns of T in use
+  const int ncols_t = do_fin ? a.col_fin : a.col_sol;  // columns of T in use
   const int ncache = min(ncols_t, a.cache_cols);
   if (!giv_warp) {  // warp per column, 4 columns x 3 row groups of loads in flight per lane
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -903,14 +906,14 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   // a solve-only launch whose newest column was finalized on the fast path
   // evaluates z by the identity below and needs that column's c1 (even when
   // an earlier launch - e.g. a push that broke down - already formed T)
-  const bool need_c1 = !a.do_finalize && a.do_solve && last_fast >= 0 && last_fast == a.col_sol - 1;
+  const bool need_c1 = !do_fin && do_sol && last_fast >= 0 && last_fast == a.col_sol - 1;
   if ((pend >= 0 || need_c1) && code0 == 0)
     ls_deferred_column<T>(static_cast<const T*>(a.t_coef), pend, pend >= 0 ? pend : last_fast, AL,
                           S, Tm, TS, sq, RM, ncache, k, ra, nr, c1, c2, vt, tmp, red);
   __syncthreads();
   SGS_TR(12);
   int s0 = 0, s1 = 0;  // output slice of the solve: [0, c) for c = col_sol
-  if (a.do_solve) slice(a.col_sol, s0, s1);
+  if (do_sol) slice(a.col_sol, s0, s1);
   if (fused && !lag && code0 == 0) {
     const int i = a.col_fin;  // solve for c = i + 1 uses T[:, :i] now, T[:, i] later
     for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vp[rr] = P[(int64_t)(i + 1) * k + ra + rr];
@@ -927,7 +930,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
       __syncthreads();
     }
   }
-  if (a.do_finalize && code0 == 0) {  // ||p_i||^2 over this CTA's rows: P is an input
+  if (do_fin && code0 == 0) {  // ||p_i||^2 over this CTA's rows: P is an input
     const int64_t pi = (int64_t)a.col_fin * k + ra;
     T l1 = T(0);
     for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) l1 = fma(P[pi + rr], P[pi + rr], l1);
@@ -935,7 +938,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     if (threadIdx.x == 0) bc[6] = l1;
   }
   SGS_TR(1);
-  unsigned long long* tl = a.timeline;
+  unsigned long long* tl = FUSED ? nullptr : a.timeline;  // no stamps in the FUSED variant
   if (tl && rank == 0 && threadIdx.x == 0) tl[3] = gtimer();
   pdl_enter();
   if (tl && rank == 0 && threadIdx.x == 0) tl[4] = gtimer();
@@ -943,7 +946,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   if (code0 != 0) return;  // uniform: nobody writes st before a cluster barrier
 
   T tp = T(0), alpha = T(0);
-  if (a.do_finalize) {
+  if (do_fin) {
     const int i = a.col_fin;
     const int nq = i;
     if (i == 0) {
@@ -1016,7 +1019,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     SGS_TR(5);
     const double r_ii = (double)sqrt(bc[0]);
     const double tol = a.bf_ucrs * (double)sqrt(bc[1]);
-    if (r_ii <= tol) {  // NaN compares false and propagates, as in numpy (gram_schmidt.py:325)
+    if (__builtin_expect(r_ii <= tol, 0)) {  // NaN compares false and propagates, as in numpy (gram_schmidt.py:325)
       if (rank == 0 && threadIdx.x == 0) {
         a.st->code = SGS_ST_BREAKDOWN;
         a.st->column = i + 1;
@@ -1092,7 +1095,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
         }
       }
     }
-    if (explicit_t) {
+    if (__builtin_expect(explicit_t, 0)) {
     if (nq > 0) {
       ls_rows_gemv<T>(TS, nr, nq, c2, tmp, red);
       for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) vt[rr] = vs[rr] - tmp[rr];
@@ -1205,7 +1208,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     SGS_TR(8);
   }
 
-  if (a.do_solve) {
+  if (do_sol) {
     const int c = a.col_sol;  // r = R_S^{-1}[:c,:c] z, z = Qs[:, :c]^T p
     // rank check of the sketched basis (gram_schmidt.py:186-189)
     if (dmin < 1e-8 * fmax(dmax, 1.0)) {
@@ -1243,7 +1246,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
       ls_coldot<T, 1>(TS, nr, 0, c, vp, nullptr, myA + 8 + cap, nullptr);
       xsync();
       // every CTA has read t_pend (pre-wait) and formed its rows of it
-      if (!a.do_finalize && a.t_pend != nullptr && rank == 0 && threadIdx.x == 0) a.t_pend[0] = -1;
+      if (!do_fin && a.t_pend != nullptr && rank == 0 && threadIdx.x == 0) a.t_pend[0] = -1;
       ls_gather<T>(XA + 8 + cap, sA, CL, 0, c, AL, zc);
       if (idz && threadIdx.x == 0) bc[2] = ls_slot_sum(XA + 2, sA, CL);
       __syncthreads();
@@ -1301,12 +1304,17 @@ static int launch_ls(const sgs_ls_args* a, cudaStream_t s) {
     const int col = a->do_finalize ? a->col_fin : a->col_sol;
     aa.timeline = tlb ? tlb + (int64_t)col * 16 + (a->do_finalize ? 0 : 3) : nullptr;
   }
-  static const bool plain_ok = [] {  // SGS_LS_PLAIN=0: always the full variant (A/B)
+  // SGS_LS_PLAIN=0: always the full variant; 1: no FUSED variant (A/B)
+  static const int plain_lvl = [] {
     const char* e = getenv("SGS_LS_PLAIN");
-    return !(e && atoi(e) == 0);
+    return e ? atoi(e) : 2;
   }();
-  const bool plain = plain_ok && !(a->p_lag && a->p_partials) && a->peer == nullptr && !a->giv_on;
-  auto kern = plain ? ls_step_kernel<T, true> : ls_step_kernel<T, false>;
+  const bool plain =
+      plain_lvl >= 1 && !(a->p_lag && a->p_partials) && a->peer == nullptr && !a->giv_on;
+  const bool fusedl = plain_lvl >= 2 && a->do_finalize && a->do_solve && a->trace == nullptr &&
+                      aa.timeline == nullptr;
+  auto kern = plain ? (fusedl ? ls_step_kernel<T, true, true> : ls_step_kernel<T, true, false>)
+                    : (fusedl ? ls_step_kernel<T, false, true> : ls_step_kernel<T, false, false>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (CL > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return check_ex(launch_ex(kern, dim3(CL), dim3(kLsThreads), smem, s, CL, aa), "ls_step_kernel");
