@@ -49,8 +49,8 @@ def test_pure_host_queries_without_gpu():
     assert lib.sgs_srht_nparts(1_000_000, 20) == lib.sgs_srht_nparts(1_000_000, 20) > 0
     assert lib.sgs_srht_nparts(24, 5) == 1
     assert lib.sgs_dense_nparts(100_000) == 296
-    # Gaussian: 296 DMMA sub-chunks summed in clusters of 8 -> 37 partials
-    assert lib.sgs_gaussian_nparts(100_000) == 37
+    # Gaussian: 152 DMMA sub-chunks summed in clusters of 8 -> 19 partials
+    assert lib.sgs_gaussian_nparts(100_000) == 19
     assert lib.sgs_gaussian_nparts(50) == 1
     assert 1 <= lib.sgs_ls_cluster_size(1500) <= 16
     assert lib.sgs_ls_scratch_elems(1500, 501) > 0
