@@ -53,6 +53,9 @@ def test_pure_host_queries_without_gpu():
     assert lib.sgs_gaussian_nparts(100_000) == 19
     assert lib.sgs_gaussian_nparts(50) == 1
     assert 1 <= lib.sgs_ls_cluster_size(1500) <= 16
+    if "SGS_LS_ROWS" not in os.environ and "SGS_LS_MAX_CLUSTER" not in os.environ:
+        # ceil(k / 64) CTAs, at most 16 (the non-portable cluster limit)
+        assert [lib.sgs_ls_cluster_size(k) for k in (1, 64, 65, 600, 1500, 3000)] == [1, 1, 2, 10, 16, 16]
     assert lib.sgs_ls_scratch_elems(1500, 501) > 0
 
 
