@@ -778,11 +778,11 @@ __device__ __noinline__ void ls_givens_chain(const double* rc, const double* cs,
   if (lane == 0) Tc[gi] = carry;
 }
 
-// FUSED / PLAIN select compiled-out variants of the same code.
+// PLAIN / MODE select compiled-out variants of the same code.
 // PLAIN: a launch without the one-synchronisation p' partials, the peer
 // exchange and the Givens chain (plain RGS-QR on one GPU); those branches are
 // compiled out, which shortens the code the post-wait path steps through.
-template <typename T, bool PLAIN, bool FUSED>
+template <typename T, bool PLAIN, int MODE>
 __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
@@ -793,9 +793,12 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   const int rb = ((rank + 1) * k) / CL;
   const int nr = rb - ra;
   const int RM = (k + CL - 1) / CL;
-  // FUSED: the launch is known to finalize column i and solve for i + 1
-  const bool do_fin = FUSED || a.do_finalize, do_sol = FUSED || a.do_solve;
-  const bool fused = FUSED || (do_fin && do_sol);
+  // MODE 1: the launch is known to finalize column i and solve for i + 1
+  // (fused); 2: finalize only; 3: solve only; 0: whatever the arguments say
+  constexpr bool SPEC = MODE != 0;  // a specialised variant: no stamps
+  const bool do_fin = MODE == 1 || MODE == 2 || (MODE == 0 && a.do_finalize);
+  const bool do_sol = MODE == 1 || MODE == 3 || (MODE == 0 && a.do_solve);
+  const bool fused = do_fin && do_sol;
   // one-synchronisation Arnoldi: p'_{i+1} = Theta A q'_i
   // arrives as partials with s'_i, and p_{i+1} = p'_{i+1} / r_ii
   const bool lag = !PLAIN && fused && a.p_lag && a.p_partials != nullptr;
@@ -835,7 +838,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   T* Tm = static_cast<T*>(a.Qs);  // unnormalised T
   T* Rinv = static_cast<T*>(a.Rinv);
   double* R = a.R;
-  long long* trc = (!FUSED && rank == 0 && threadIdx.x == 0) ? a.trace : nullptr;
+  long long* trc = (!SPEC && rank == 0 && threadIdx.x == 0) ? a.trace : nullptr;
 #define SGS_TR(ix) \
   do {             \
     if (trc) trc[ix] = clock64(); \
@@ -852,7 +855,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
   // CTA's rows of T and, in the fused QR path, the whole solve except the last
   // column's term run while the predecessor column kernel is still streaming Q.
   SGS_TR(0);
-  if (!FUSED && a.timeline && rank == 0 && threadIdx.x == 0) a.timeline[6] = gtimer();
+  if (!SPEC && a.timeline && rank == 0 && threadIdx.x == 0) a.timeline[6] = gtimer();
   const int64_t code0 = *reinterpret_cast<volatile const int64_t*>(&a.st->code);
   double dmax = a.st->diag_max, dmin = a.st->diag_min;
   // Progressive Givens update of GMRES step gi = col_fin - 1 (krylov.py:282-301),
@@ -938,7 +941,7 @@ __global__ void __launch_bounds__(kLsThreads, 1) ls_step_kernel(sgs_ls_args a) {
     if (threadIdx.x == 0) bc[6] = l1;
   }
   SGS_TR(1);
-  unsigned long long* tl = FUSED ? nullptr : a.timeline;  // no stamps in the FUSED variant
+  unsigned long long* tl = SPEC ? nullptr : a.timeline;  // no stamps in the specialised variants
   if (tl && rank == 0 && threadIdx.x == 0) tl[3] = gtimer();
   pdl_enter();
   if (tl && rank == 0 && threadIdx.x == 0) tl[4] = gtimer();
@@ -1304,17 +1307,22 @@ static int launch_ls(const sgs_ls_args* a, cudaStream_t s) {
     const int col = a->do_finalize ? a->col_fin : a->col_sol;
     aa.timeline = tlb ? tlb + (int64_t)col * 16 + (a->do_finalize ? 0 : 3) : nullptr;
   }
-  // SGS_LS_PLAIN=0: always the full variant; 1: no FUSED variant (A/B)
+  // SGS_LS_PLAIN=0: always the full variant; 1: PLAIN but no MODE variants (A/B)
   static const int plain_lvl = [] {
     const char* e = getenv("SGS_LS_PLAIN");
     return e ? atoi(e) : 2;
   }();
   const bool plain =
       plain_lvl >= 1 && !(a->p_lag && a->p_partials) && a->peer == nullptr && !a->giv_on;
-  const bool fusedl = plain_lvl >= 2 && a->do_finalize && a->do_solve && a->trace == nullptr &&
-                      aa.timeline == nullptr;
-  auto kern = plain ? (fusedl ? ls_step_kernel<T, true, true> : ls_step_kernel<T, true, false>)
-                    : (fusedl ? ls_step_kernel<T, false, true> : ls_step_kernel<T, false, false>);
+  const bool spec = plain_lvl >= 2 && a->trace == nullptr && aa.timeline == nullptr;
+  const int mode = !spec ? 0 : (a->do_finalize && a->do_solve) ? 1 : a->do_finalize ? 2 : 3;
+  void (*kern)(sgs_ls_args) = nullptr;
+#define SGS_LS_PICK(P)                                                        \
+  kern = mode == 1 ? ls_step_kernel<T, P, 1> : mode == 2 ? ls_step_kernel<T, P, 2> \
+       : mode == 3 ? ls_step_kernel<T, P, 3> : ls_step_kernel<T, P, 0>
+  if (plain) SGS_LS_PICK(true);
+  else SGS_LS_PICK(false);
+#undef SGS_LS_PICK
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (CL > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return check_ex(launch_ex(kern, dim3(CL), dim3(kLsThreads), smem, s, CL, aa), "ls_step_kernel");

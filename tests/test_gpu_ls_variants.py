@@ -1,10 +1,11 @@
 """The LS kernel's compiled-out variants and the column kernels' prefetch
 switches must not change a bit of the factors.
 
-`ls_step_kernel<T, PLAIN, FUSED>` (csrc/sgs_rgs.cu) is the same code with the
-one-synchronisation / peer / Givens branches (PLAIN) and the unfused branches
-and stamps (FUSED) compiled out; which one runs is a per-launch choice
-(SGS_LS_PLAIN=0: always the full kernel, 1: PLAIN only).  The column kernels'
+`ls_step_kernel<T, PLAIN, MODE>` (csrc/sgs_rgs.cu) is the same code with the
+one-synchronisation / peer / Givens branches compiled out (PLAIN) and the
+launch mode fixed at compile time (MODE: fused, finalize-only, solve-only; no
+stamps); which one runs is a per-launch choice (SGS_LS_PLAIN=0: always the
+full kernel, 1: PLAIN only, default: all specialisations).  The column kernels'
 pre-wait L2 prefetch (SGS_COL_PF_MB / SGS_DENSE_PF_MB = 0: off, SGS_COL_PF_PACE
 = 0: one burst) only moves bytes.  The switches are read once per process, so
 each setting runs tools/ls_variant_probe.py in a fresh process; the probe
@@ -34,6 +35,6 @@ def test_ls_variants_and_prefetch_switches_are_bit_identical(cuda):
     base = _probe()
     assert len(base) == 8
     assert _probe(SGS_LS_PLAIN="0") == base          # full kernel everywhere
-    assert _probe(SGS_LS_PLAIN="1") == base          # PLAIN without FUSED
+    assert _probe(SGS_LS_PLAIN="1") == base          # PLAIN without the MODE variants
     assert _probe(SGS_COL_PF_MB="0", SGS_DENSE_PF_MB="0") == base   # no prefetch
     assert _probe(SGS_COL_PF_PACE="0") == base       # burst prefetch
